@@ -1,0 +1,173 @@
+/*
+ * sspd_cuda.h -- the drop-in boundary: a C ABI over the B200 (sm_100a)
+ * implementation of the sliding super point detector hot path
+ * (arXiv 1803.11036; reference /root/reference/proj).
+ *
+ * Plain pointers and sizes only; no C++ or torch types.  The C++ API in
+ * include/sspd/ (the reference's public headers, re-implemented in
+ * paper_1803_11036_b200/csrc/host/) sits on top of these entry points, and so
+ * do the Python bindings (paper_1803_11036_b200/_cabi.py) and any other
+ * FFI.  Each entry point names the reference interface it
+ * replaces (file:line, relative to /root/reference/proj).
+ *
+ * Representation.  The grid holds one u32 "slice stamp" per recorder instead
+ * of the reference's u16 distance.  A per-grid counter `now` starts at 65535
+ * and advance_slot increments it; stamp 0 means never seen.  The reference's
+ * distance of a recorder is min(now - stamp, 0xFFFF), bit-exactly, so
+ * advance_slot is O(1), union-min merge is element-wise max of stamps and
+ * paper-max merge is element-wise min.  Touches are first recorded in a
+ * per-slot bitmap (1 bit per recorder) and folded into the stamps by an
+ * ordered pass before anything reads the grid; see DESIGN.md.
+ *
+ * Errors.  Every call returns an sspd_status; sspd_last_error() gives the
+ * message of the last failure on the calling thread, worded like the
+ * reference's exception text so the C++ shim can rethrow the same exception
+ * types with the same what().
+ *
+ * Threading.  Calls on one grid are serialised by a per-grid mutex, so
+ * concurrent scan callers (the reference's SCAN phase contract,
+ * rsea.hpp:49-51) remain legal.  Work is queued on the grid's CUDA stream;
+ * calls that return host data synchronise that stream.
+ */
+#ifndef SSPD_CUDA_H
+#define SSPD_CUDA_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  SSPD_OK = 0,
+  SSPD_INVALID_ARGUMENT = 1,  /* std::invalid_argument in the reference */
+  SSPD_OUT_OF_RANGE = 2,      /* std::out_of_range */
+  SSPD_CANDIDATE_OVERFLOW = 3,/* sspd::CandidateOverflow (rsea.hpp:38-43) */
+  SSPD_CUDA_ERROR = 4,        /* device failure -> std::runtime_error */
+  SSPD_NO_DEVICE = 5          /* no usable sm_100 device: fail loudly */
+} sspd_status;
+
+typedef enum { SSPD_UNION_MIN = 0, SSPD_PAPER_MAX = 1 } sspd_merge_policy; /* snapshot.hpp:11-14 */
+
+typedef struct sspd_grid sspd_grid;
+
+/* One reported host: the reference's Detection (rsea.hpp:25-28) plus the
+ * integer in-window count the estimate was computed from. */
+typedef struct {
+  uint32_t cip;
+  uint32_t r_k;
+  double estimate;
+} sspd_detection;
+
+/* ---- library ---- */
+int sspd_abi_version(void);
+const char* sspd_last_error(void);
+/* Number of visible devices this library can run on (sm_100). */
+sspd_status sspd_device_count(int* n);
+
+/* ---- grid lifetime: Rsea::Rsea (rsea.hpp:54; rsea.cpp:18-27) ---- */
+/* Validates like validate_config(cfg, eta, 1, 1.0) (hashing.cpp:63-87) and
+ * fails with "Rsea: <first diagnostic>".  All recorders start never-seen. */
+sspd_status sspd_grid_create(int device, uint32_t q, uint32_t r, uint32_t delta,
+                             uint64_t seed, uint32_t eta, sspd_grid** out);
+/* Copy constructor (Rsea is copyable: snapshot.cpp:127, pipeline.cpp:39):
+ * device-to-device copy onto `device` (-1 = the source's device). */
+sspd_status sspd_grid_clone(const sspd_grid* src, int device, sspd_grid** out);
+sspd_status sspd_grid_destroy(sspd_grid* g);
+/* Geometry and state: recorder_count (rsea.hpp:59), device, now. */
+sspd_status sspd_grid_info(const sspd_grid* g, uint64_t* recorders, int* device,
+                           uint32_t* now);
+/* Queue the grid's work on an external cudaStream_t (NULL = the grid's own). */
+sspd_status sspd_grid_set_stream(sspd_grid* g, void* cuda_stream);
+sspd_status sspd_grid_synchronize(sspd_grid* g);
+
+/* ---- SCAN phase ---- */
+/* Rsea::scan_batch / Rsea::update (rsea.hpp:71-75; rsea.cpp:29-53).  `pairs`
+ * holds n (cip, oip) u32 pairs interleaved (the IpPair layout, rsea.hpp:14-17).
+ * pairs_on_device != 0: device pointer on the grid's device, consumed in place;
+ * otherwise a host pointer, copied in chunks (async when pinned).  Order- and
+ * batch-invariant like the reference. */
+sspd_status sspd_scan(sspd_grid* g, const uint32_t* pairs, uint64_t n, int pairs_on_device);
+
+/* ---- QUIESCENT phase ---- */
+/* Rsea::advance_slot (rsea.cpp:55-63): O(1), `slots` times. */
+sspd_status sspd_advance(sspd_grid* g, uint32_t slots);
+
+/* Rsea::cells() as distances (rsea.hpp:61-68): recorders [offset, offset+count)
+ * in (row, column, bucket) order, as the reference's u16 values. */
+sspd_status sspd_get_distances(sspd_grid* g, uint16_t* host_out, uint64_t offset,
+                               uint64_t count);
+/* Writes through a mutable cells() span (import_snapshot, snapshot.cpp:95-111). */
+sspd_status sspd_put_distances(sspd_grid* g, const uint16_t* host_in, uint64_t offset,
+                               uint64_t count);
+
+/* rec::active_count over every estimator (estimator.hpp:26-31): R_k per cell,
+ * r*2^q values in (row, column) order. */
+sspd_status sspd_active_counts(sspd_grid* g, uint32_t k, uint32_t* host_out);
+
+/* Rsea::hot_sets (rsea.cpp:65-84) with the integer cutoff
+ * hot_cutoff(eta, theta) computed by the caller (estimator.cpp:32-36).
+ * cols_out: capacity r*2^q, rows concatenated, columns ascending;
+ * row_counts: r entries. */
+sspd_status sspd_hot_sets(sspd_grid* g, uint32_t k, uint64_t cutoff, uint32_t* cols_out,
+                          uint32_t* row_counts);
+
+/* Rsea::finalize_candidate (rsea.cpp:86-108) over n tuples of r columns
+ * (host memory).  accepted[i] = 1 when tuple i is accepted, with cip/r_k
+ * filled.  The estimate is estimate_cardinality(eta, r_k) on the host. */
+sspd_status sspd_finalize(sspd_grid* g, const uint32_t* tuples, uint64_t n, uint32_t k,
+                          uint64_t cutoff, uint8_t* accepted, uint32_t* cips,
+                          uint32_t* r_ks);
+
+/* Rsea::reconstruct_leveled (rsea.cpp:168-255): hot cells, level-2 triples,
+ * levels 3..r-1, finalize, dedup by cip (larger estimate kept) sorted by cip.
+ * Fails with SSPD_CANDIDATE_OVERFLOW and *ovf_level / *ovf_count set exactly
+ * as CandidateOverflow(level, count, cap) would be.  Writes at most out_cap
+ * detections; *n_out is the full count.  The same cip set as
+ * reconstruct_recursive (rsea.cpp:126-166), which has no cap (pass
+ * cap = UINT64_MAX). */
+sspd_status sspd_reconstruct(sspd_grid* g, uint32_t k, uint64_t cutoff, uint64_t cap,
+                             sspd_detection* out, uint64_t out_cap, uint64_t* n_out,
+                             uint32_t* ovf_level, uint64_t* ovf_count);
+
+/* merge_rseas (snapshot.hpp:54; snapshot.cpp:117-142): element-wise combine
+ * of n grids into `out` (which may alias grids[0] for an in-place merge).
+ * Grids must share (seed, q, r, delta, eta) -- else SSPD_INVALID_ARGUMENT with
+ * the reference's message -- and are brought to a common `now`.  Grids on other
+ * devices are read directly over NVLink (peer access). */
+sspd_status sspd_merge(const sspd_grid* const* grids, uint64_t n, int policy,
+                       sspd_grid* out);
+
+/* Rsea::operator== (rsea.hpp:100-102): same distances everywhere. */
+sspd_status sspd_equal(sspd_grid* a, sspd_grid* b, int* equal);
+
+/* ---- window tracking (B200-native extension) ---- */
+/* Maintain per-cell in-window counts incrementally for windows up to k_max
+ * slots, so hot_sets / reconstruct at k <= k_max skip the full-grid count
+ * pass.  0 disables.  Results are identical either way. */
+sspd_status sspd_track_window(sspd_grid* g, uint32_t k_max);
+
+/* ---- raw device views, for torch.distributed / NCCL plumbing ---- */
+/* Device pointer to the u32 stamp array (recorders words) after folding any
+ * pending touches.  Stamps are < 2^31, so an int32 view reduces identically. */
+sspd_status sspd_grid_stamps(sspd_grid* g, uint32_t** dev_stamps, uint64_t* words);
+/* Device pointer to this slot's touched bitmap (ceil(recorders/32) words)
+ * without folding it, for an OR-merge across routers; after the caller has
+ * OR-reduced it in place, sspd_commit folds it into the stamps. */
+sspd_status sspd_grid_touched(sspd_grid* g, uint32_t** dev_bits, uint64_t* words);
+sspd_status sspd_commit(sspd_grid* g);
+
+/* Per-kernel timing of the last call on this grid (CUDA events on the grid's
+ * stream), for bench.py's roofline: name -> milliseconds, launches. */
+sspd_status sspd_profile_enable(sspd_grid* g, int on);
+sspd_status sspd_profile_read(sspd_grid* g, const char* kernel, double* total_ms,
+                              uint64_t* launches, uint64_t* units);
+sspd_status sspd_profile_reset(sspd_grid* g);
+/* Total kernels this library has launched (all grids, since load). */
+uint64_t sspd_launch_count(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SSPD_CUDA_H */

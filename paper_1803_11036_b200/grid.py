@@ -1,0 +1,272 @@
+"""Python mirror of the reference's Rsea / merge_rseas surface over the C ABI.
+
+Method names and argument meanings follow include/sspd/rsea.hpp and
+snapshot.hpp of the reference (rsea.hpp:52-114, snapshot.hpp:54), so the
+parity tests read like the reference's own tests.  All work runs in the CUDA
+library (lib/libsspd_cuda.so); the only host arithmetic is the reference's
+double-precision hot_cutoff / estimate_cardinality formulas
+(estimator.cpp:25-36), which the reports need bit-identical.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import math
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _cabi
+from ._cabi import CandidateOverflow, check, load
+
+BASE_NOW = 65535
+
+
+@dataclass(frozen=True)
+class Detection:
+    cip: int
+    estimate: float
+    r_k: int
+
+
+def hot_cutoff(eta: int, theta: float) -> int:
+    """ceil(eta * (1 - e^(-theta/eta))) -- estimator.cpp:32-36."""
+    deta = float(eta)
+    return int(math.ceil(deta * (1.0 - math.exp(-theta / deta))))
+
+
+def estimate_cardinality(eta: int, r_k: int) -> float:
+    """-eta * ln(z0/eta), eta*ln(eta) when z0 == 0 -- estimator.cpp:25-30."""
+    z0 = eta - r_k
+    deta = float(eta)
+    if z0 == 0:
+        return deta * math.log(deta)
+    return -deta * math.log(float(z0) / deta)
+
+
+def device_count() -> int:
+    n = C.c_int()
+    check(load().sspd_device_count(C.byref(n)))
+    return n.value
+
+
+def _u32(a):
+    return a.ctypes.data_as(_cabi.u32p)
+
+
+class Grid:
+    """An RSEA grid resident on one B200 (Rsea, rsea.hpp:52-114)."""
+
+    def __init__(self, q: int = 14, r: int = 5, delta: int = 6, seed: int = 0,
+                 eta: int = 2048, device: int = 0, _handle=None):
+        self._L = load()
+        self.q, self.r, self.delta, self.seed, self.eta = q, r, delta, seed, eta
+        if _handle is None:
+            h = C.c_void_p()
+            check(self._L.sspd_grid_create(device, q, r, delta, seed, eta, C.byref(h)))
+            _handle = h
+        self._h = _handle
+        self.candidate_cap = 1 << 24
+
+    def close(self):
+        if getattr(self, "_h", None):
+            self._L.sspd_grid_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    # -- geometry ------------------------------------------------------------
+    @property
+    def columns(self) -> int:
+        return 1 << self.q
+
+    def recorder_count(self) -> int:
+        n = C.c_uint64()
+        check(self._L.sspd_grid_info(self._h, C.byref(n), None, None))
+        return n.value
+
+    @property
+    def now(self) -> int:
+        v = C.c_uint32()
+        check(self._L.sspd_grid_info(self._h, None, None, C.byref(v)))
+        return v.value
+
+    @property
+    def device(self) -> int:
+        d = C.c_int()
+        check(self._L.sspd_grid_info(self._h, None, C.byref(d), None))
+        return d.value
+
+    def copy(self, device: int = -1) -> "Grid":
+        h = C.c_void_p()
+        check(self._L.sspd_grid_clone(self._h, device, C.byref(h)))
+        g = Grid(self.q, self.r, self.delta, self.seed, self.eta, _handle=h)
+        g.candidate_cap = self.candidate_cap
+        return g
+
+    # -- SCAN ------------------------------------------------------------------
+    def update(self, cip: int, oip: int):
+        self.scan_batch(np.array([[cip, oip]], dtype=np.uint32))
+
+    def scan_batch(self, pairs, workers: int = 1):
+        """pairs: (n,2) uint32 host array, or a CUDA tensor/array exposing
+        __cuda_array_interface__ / data_ptr() on this grid's device."""
+        if workers == 0:
+            raise _cabi.InvalidArgument("scan_batch: workers == 0")
+        if hasattr(pairs, "data_ptr") and getattr(pairs, "is_cuda", False):
+            n = pairs.numel() // 2
+            check(self._L.sspd_scan(self._h, C.c_void_p(pairs.data_ptr()), n, 1))
+            return
+        p = np.ascontiguousarray(pairs, dtype=np.uint32).reshape(-1, 2)
+        if p.shape[0] == 0:
+            return
+        check(self._L.sspd_scan(self._h, p.ctypes.data_as(C.c_void_p), p.shape[0], 0))
+
+    def scan_device(self, dev_ptr: int, n_pairs: int):
+        check(self._L.sspd_scan(self._h, C.c_void_p(dev_ptr), n_pairs, 1))
+
+    # -- QUIESCENT ---------------------------------------------------------
+    def advance_slot(self, workers: int = 1, slots: int = 1):
+        if workers == 0:
+            raise _cabi.InvalidArgument("advance_slot: workers == 0")
+        check(self._L.sspd_advance(self._h, slots))
+
+    def cells(self) -> np.ndarray:
+        """Host copy of all recorders as the reference's u16 distances."""
+        n = self.recorder_count()
+        out = np.empty(n, dtype=np.uint16)
+        check(self._L.sspd_get_distances(self._h, out.ctypes.data_as(_cabi.u16p), 0, n))
+        return out
+
+    def set_cells(self, values: np.ndarray, offset: int = 0):
+        v = np.ascontiguousarray(values, dtype=np.uint16).ravel()
+        check(self._L.sspd_put_distances(self._h, v.ctypes.data_as(_cabi.u16p), offset, v.size))
+
+    def estimator(self, row: int, col: int) -> np.ndarray:
+        off = ((row << self.q) + col) * self.eta
+        out = np.empty(self.eta, dtype=np.uint16)
+        check(self._L.sspd_get_distances(self._h, out.ctypes.data_as(_cabi.u16p), off, self.eta))
+        return out
+
+    def active_counts(self, k: int) -> np.ndarray:
+        out = np.empty(self.r << self.q, dtype=np.uint32)
+        check(self._L.sspd_active_counts(self._h, k, _u32(out)))
+        return out
+
+    def hot_sets(self, k: int, theta: float) -> list[np.ndarray]:
+        cols = np.empty(self.r << self.q, dtype=np.uint32)
+        counts = np.empty(self.r, dtype=np.uint32)
+        check(self._L.sspd_hot_sets(self._h, k, hot_cutoff(self.eta, theta), _u32(cols),
+                                    _u32(counts)))
+        out, s = [], 0
+        for c in counts:
+            out.append(cols[s:s + int(c)].copy())
+            s += int(c)
+        return out
+
+    def finalize_candidates(self, tuples, k: int, theta: float):
+        t = np.ascontiguousarray(tuples, dtype=np.uint32).reshape(-1, self.r)
+        n = t.shape[0]
+        acc = np.zeros(n, dtype=np.uint8)
+        cips = np.zeros(n, dtype=np.uint32)
+        rks = np.zeros(n, dtype=np.uint32)
+        check(self._L.sspd_finalize(self._h, _u32(t), n, k, hot_cutoff(self.eta, theta),
+                                    acc.ctypes.data_as(_cabi.u8p), _u32(cips), _u32(rks)))
+        return [Detection(int(cips[i]), estimate_cardinality(self.eta, int(rks[i])), int(rks[i]))
+                if acc[i] else None for i in range(n)]
+
+    def finalize_candidate(self, cols, k: int, theta: float):
+        return self.finalize_candidates(np.asarray(cols).reshape(1, -1), k, theta)[0]
+
+    def _reconstruct(self, k: int, theta: float, cap: int) -> list[Detection]:
+        out_cap = 1 << 16
+        while True:
+            buf = (_cabi.Detection_t * out_cap)()
+            n = C.c_uint64()
+            lvl = C.c_uint32()
+            cnt = C.c_uint64()
+            st = self._L.sspd_reconstruct(self._h, k, hot_cutoff(self.eta, theta), cap, buf,
+                                          out_cap, C.byref(n), C.byref(lvl), C.byref(cnt))
+            if st == _cabi.SSPD_CANDIDATE_OVERFLOW:
+                raise CandidateOverflow(self._L.sspd_last_error().decode(), lvl.value, cnt.value)
+            check(st)
+            if n.value <= out_cap:
+                return [Detection(buf[i].cip, buf[i].estimate, buf[i].r_k) for i in range(n.value)]
+            out_cap = n.value
+
+    def reconstruct_leveled(self, k: int, theta: float, workers: int = 1) -> list[Detection]:
+        """Rsea::reconstruct_leveled (rsea.cpp:168-255)."""
+        if workers == 0:
+            raise _cabi.InvalidArgument("reconstruct_leveled: workers == 0")
+        return self._reconstruct(k, theta, self.candidate_cap)
+
+    def reconstruct_recursive(self, k: int, theta: float) -> list[Detection]:
+        """Rsea::reconstruct_recursive (rsea.cpp:126-166): no candidate cap."""
+        return self._reconstruct(k, theta, (1 << 64) - 1)
+
+    def track_window(self, k_max: int):
+        check(self._L.sspd_track_window(self._h, k_max))
+
+    def stamps_ptr(self) -> tuple[int, int]:
+        p = C.c_void_p()
+        n = C.c_uint64()
+        check(self._L.sspd_grid_stamps(self._h, C.byref(p), C.byref(n)))
+        return p.value, n.value
+
+    def touched_ptr(self) -> tuple[int, int]:
+        p = C.c_void_p()
+        n = C.c_uint64()
+        check(self._L.sspd_grid_touched(self._h, C.byref(p), C.byref(n)))
+        return p.value, n.value
+
+    def commit(self):
+        check(self._L.sspd_commit(self._h))
+
+    def synchronize(self):
+        check(self._L.sspd_grid_synchronize(self._h))
+
+    def set_stream(self, stream_ptr: int | None):
+        check(self._L.sspd_grid_set_stream(self._h, C.c_void_p(stream_ptr or 0)))
+
+    # profiling -----------------------------------------------------------
+    def profile(self, on: bool = True):
+        check(self._L.sspd_profile_enable(self._h, int(on)))
+
+    def profile_reset(self):
+        check(self._L.sspd_profile_reset(self._h))
+
+    def profile_read(self, kernel: str | None = None) -> tuple[float, int, int]:
+        ms = C.c_double()
+        n = C.c_uint64()
+        u = C.c_uint64()
+        check(self._L.sspd_profile_read(self._h, kernel.encode() if kernel else None,
+                                        C.byref(ms), C.byref(n), C.byref(u)))
+        return ms.value, n.value, u.value
+
+    def __eq__(self, other: "Grid") -> bool:
+        e = C.c_int()
+        check(self._L.sspd_equal(self._h, other._h, C.byref(e)))
+        return bool(e.value)
+
+
+def merge_rseas(grids: list[Grid], policy: int = _cabi.UNION_MIN, out: Grid | None = None,
+                device: int | None = None) -> Grid:
+    """merge_rseas (snapshot.hpp:54): a new grid (or `out`) holding the
+    element-wise union-min / paper-max of the inputs."""
+    if not grids:
+        raise _cabi.InvalidArgument("merge_rseas: empty set")
+    g0 = grids[0]
+    if out is None:
+        out = Grid(g0.q, g0.r, g0.delta, g0.seed, g0.eta,
+                   device=g0.device if device is None else device)
+        out.candidate_cap = g0.candidate_cap
+    arr = (C.c_void_p * len(grids))(*[g._h for g in grids])
+    check(load().sspd_merge(arr, len(grids), policy, out._h))
+    return out
+
+
+def launch_count() -> int:
+    return int(load().sspd_launch_count())
