@@ -16,7 +16,7 @@ pytestmark = pytest.mark.gpu
 
 DESK = dict(q=10, r=5, delta=8, eta=256)       # desk_preset (pipeline.cpp:7-14)
 PAPER = dict(q=14, r=5, delta=6, eta=2048)     # RunConfig defaults (pipeline.hpp:16-26)
-ODD = dict(q=12, r=6, delta=4, eta=1000)       # non-power-of-two eta: u64 % eta path
+ODD = dict(q=12, r=7, delta=4, eta=1000)       # non-power-of-two eta: u64 % eta path
 WIDE = dict(q=16, r=8, delta=6, eta=64)        # (r-2)*delta >= 32: masked shifts
 
 
