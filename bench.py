@@ -1,0 +1,413 @@
+#!/usr/bin/env python
+"""Throughput of the sliding super point detector hot path on B200.
+
+One step = one time slice (slot) of BASELINE.json's config C2: scan the slot's
+pairs into the RSEA grid, fold the slot's touches into the stamps, find hot
+estimators, reconstruct the super points (levels 2..r-1 + finalize, reports
+back on the host), advance the slot.  At N GPUs each GPU is one edge router
+scanning its own shard of the slot (weak scaling) and the routers merge by
+union-min (OR of the slot's touched bitmaps, see paper_1803_11036_b200/dist.py)
+before reconstruction.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                  [--config c2|c1] [--no-cpu-baseline]
+
+Prints ONE JSON line (rank 0).  `--impl reference` times the reference's own
+CPU implementation (oracle/_ref, compiled from /root/reference/proj) on the
+same workload on this host's cores.
+"""
+from __future__ import annotations
+
+import argparse
+import ctypes as C
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+CONFIGS = {
+    # BASELINE.json configs[1]: single router, 1B-packet Zipf trace with injected
+    # scanner / DDoS super points, full-HBM estimator table.
+    "c2": dict(workload="C2: 1 router/GPU, 1e9-pair Zipf(1.1) trace (10 slots x 1e8 pairs) with "
+                        "100 scanners + 10 DDoS victims at 4*theta injected, full-HBM table "
+                        "q16 r5 delta6 eta65536 (80 GiB u32 stamps)",
+               q=16, r=5, delta=6, eta=1 << 16, seed=0x5eed, k=5, theta=1024.0,
+               pairs_per_slot=100_000_000, trace_slots=10, hosts=1 << 21, pool=16, zipf=1.1,
+               n_super=110, fanout=4096),
+    # configs[0]: the reference's CPU-runnable case (reference default geometry).
+    "c1": dict(workload="C1: 1 router/GPU, uniform (cip,oip) pairs, 10 slots x 1e6 pairs + 20 "
+                        "planted supers x 2048 per slot, reference default table q14 r5 delta6 "
+                        "eta2048", q=14, r=5, delta=6, eta=2048, seed=0x5eed, k=5, theta=1024.0,
+               pairs_per_slot=1_000_000, trace_slots=10, hosts=1, pool=0, zipf=1.1,
+               n_super=20, fanout=2048),
+}
+
+PKT_BYTES = 800  # the paper's Gb/s convention
+
+
+def env_int(name, default):
+    v = os.environ.get(name)
+    return int(v) if v not in (None, "") else default
+
+
+class SynthParams(C.Structure):
+    _fields_ = [("seed", C.c_uint64), ("hosts", C.c_uint32), ("pool", C.c_uint32),
+                ("n_super", C.c_uint32), ("super_fanout", C.c_uint32),
+                ("pairs_per_slot", C.c_uint64), ("shard", C.c_uint32), ("n_shards", C.c_uint32)]
+
+
+def synth_params(cfg, rank, world):
+    return SynthParams(cfg["seed"] ^ 0xC2C2, cfg["hosts"], cfg["pool"], cfg["n_super"],
+                       cfg["fanout"], cfg["pairs_per_slot"] * world, rank, world)
+
+
+def zipf_cdf(L, cfg):
+    cdf = np.empty(cfg["hosts"], dtype=np.uint64)
+    assert L.sspd_synth_zipf_cdf(cfg["hosts"], cfg["zipf"], cdf.ctypes.data) == 0
+    return cdf
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    def __init__(self, device: int):
+        self.device = device
+        self.proc = None
+        self.path = os.path.join(ROOT, "gpurun_out", f"clocks_dev{device}.csv")
+
+    def __enter__(self):
+        os.makedirs(os.path.dirname(self.path), exist_ok=True)
+        q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+             "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+        try:
+            self.f = open(self.path, "w")
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.device), f"--query-gpu={q}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=self.f, stderr=subprocess.DEVNULL)
+        except Exception:
+            self.proc = None
+        return self
+
+    def __exit__(self, *a):
+        if self.proc:
+            time.sleep(0.25)
+            self.proc.terminate()
+            self.proc.wait()
+            self.f.close()
+
+    def summary(self):
+        if not self.proc:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        with open(self.path) as f:
+            for line in f:
+                parts = [x.strip() for x in line.split(",")]
+                if len(parts) < 9:
+                    continue
+                try:
+                    sm.append(float(parts[1]))
+                    mx = float(parts[2])
+                except ValueError:
+                    continue
+                for nm, v in zip(names, parts[5:9]):
+                    if v.lower() == "active":
+                        reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ---------------------------------------------------------------------------
+# Reference arm / cpu baseline: the compiled reference on host cores.
+
+def run_reference(cfg, steps, warmup, pairs_cap, time_budget_s):
+    """Reference Rsea at the same geometry: per step one slot of the same
+    trace through scan_batch (alpha=32768 batches, pipeline.cpp:58-63),
+    reconstruct_leveled and advance_slot, workers = all host cores."""
+    from oracle import oracle as O
+    import paper_1803_11036_b200 as P
+
+    L = P.load()
+    workers = os.cpu_count() or 1
+    t0 = time.time()
+    g = O.RefGrid(cfg["q"], cfg["r"], cfg["delta"], cfg["seed"], cfg["eta"])
+    t_init = time.time() - t0
+    cdf = zipf_cdf(L, cfg)
+    sp = synth_params(cfg, 0, 1)
+    n = min(cfg["pairs_per_slot"], pairs_cap)
+    buf = np.empty((n, 2), dtype=np.uint32)
+    times, scan_t, rec_t, adv_t, n_rep = [], [], [], [], []
+    budget_hit = False
+    for i in range(warmup + steps):
+        assert L.sspd_synth_host(C.byref(sp), cdf.ctypes.data, i % cfg["trace_slots"], 0, n,
+                                 buf.ctypes.data) == 0
+        a = time.perf_counter()
+        g.scan_alpha(buf, workers)
+        b = time.perf_counter()
+        rep = g.reconstruct(cfg["k"], cfg["theta"], workers=workers)
+        c = time.perf_counter()
+        g.advance(workers)
+        d = time.perf_counter()
+        if i >= warmup:
+            times.append(d - a)
+            scan_t.append(b - a)
+            rec_t.append(c - b)
+            adv_t.append(d - c)
+            n_rep.append(len(rep))
+        if time.time() - t0 > time_budget_s and len(times) >= 1:
+            budget_hit = True
+            break
+    mean = sum(times) / len(times)
+    return {
+        "value": n / mean / 1e6, "steps_timed": len(times), "pairs_per_step": n,
+        "workers": workers, "init_s": t_init, "scan_ms": 1e3 * statistics.mean(scan_t),
+        "reconstruct_ms": 1e3 * statistics.mean(rec_t), "advance_ms": 1e3 * statistics.mean(adv_t),
+        "step_ms": 1e3 * mean, "reports": n_rep[-1] if n_rep else 0, "budget_hit": budget_hit,
+    }
+
+
+# ---------------------------------------------------------------------------
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="c2", choices=sorted(CONFIGS))
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--ref-pairs", type=int, default=100_000_000,
+                    help="pairs per reference step (bounded sample of the slot)")
+    args = ap.parse_args()
+    cfg = CONFIGS[args.config]
+    rank = env_int("RANK", 0)
+    world = env_int("WORLD_SIZE", 1)
+    local = env_int("LOCAL_RANK", 0)
+    unit = "Mpackets/s"
+    metric = "scan+reconstruct throughput, Mpackets/s (Gb/s at 800 B/pkt in gbps_800B)"
+
+    if args.impl == "reference":
+        if rank != 0:
+            return
+        r = run_reference(cfg, args.steps, args.warmup, args.ref_pairs, time_budget_s=240)
+        line = {
+            "impl": "reference", "metric": metric, "value": round(r["value"], 3), "unit": unit,
+            "n_gpus": args.gpus, "steps": r["steps_timed"], "warmup": args.warmup,
+            "ms_per_step": round(r["step_ms"], 3), "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "u32/u16 integer", "data": "synthetic",
+            "config": {"workload": cfg["workload"], "sample": f"{r['pairs_per_step']} pairs per step",
+                       "parallelism": "host OpenMP"},
+            "gbps_800B": round(r["value"] * 1e6 * PKT_BYTES * 8 / 1e9, 3),
+            "reconstruct_ms": round(r["reconstruct_ms"], 3),
+            "phases_ms": {"scan": round(r["scan_ms"], 3), "reconstruct": round(r["reconstruct_ms"], 3),
+                          "advance": round(r["advance_ms"], 3)},
+            "cpu_baseline": {"value": round(r["value"], 3), "unit": unit, "cores": r["workers"],
+                             "kind": "reference",
+                             "sample": f"{r['steps_timed']} slots x {r['pairs_per_step']} pairs of "
+                                       f"the {args.config} trace, reference grid at full geometry"},
+            "e2e": {"value": round(r["value"], 3), "unit": unit, "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0},
+        }
+        print(json.dumps(line), flush=True)
+        return
+
+    import torch
+    import torch.distributed as dist
+
+    import paper_1803_11036_b200 as P
+    from paper_1803_11036_b200 import dist as PD
+
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
+    torch.cuda.set_device(local)
+    dev = local
+    L = P.load()
+    stream = torch.cuda.current_stream()
+
+    # --- setup (untimed): grid, trace resident in HBM, pinned host copy ------
+    g = P.Grid(cfg["q"], cfg["r"], cfg["delta"], cfg["seed"], cfg["eta"], device=dev)
+    g.set_stream(stream.cuda_stream)
+    g.track_window(cfg["k"])
+    cdf = torch.from_numpy(zipf_cdf(L, cfg).view(np.int64)).to(f"cuda:{dev}")
+    sp = synth_params(cfg, rank, world)
+    n_local = cfg["pairs_per_slot"]
+    S = cfg["trace_slots"]
+    trace = torch.empty((S, n_local, 2), dtype=torch.int32, device=f"cuda:{dev}")
+    for s in range(S):
+        P._cabi.check(L.sspd_synth_device(dev, C.byref(sp), C.c_void_p(cdf.data_ptr()), s, 0,
+                                          n_local, C.c_void_p(trace[s].data_ptr()),
+                                          C.c_void_p(stream.cuda_stream)))
+    torch.cuda.synchronize()
+    host_trace = None
+    if not args.no_e2e:
+        host_trace = torch.empty((S, n_local, 2), dtype=torch.int32, pin_memory=True)
+        host_trace.copy_(trace)
+        torch.cuda.synchronize()
+
+    k, theta = cfg["k"], cfg["theta"]
+    rec_ms = []
+
+    def step(i, from_host=False):
+        s = i % S
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e2 = torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        if from_host:
+            g.scan_host_ptr(host_trace[s].data_ptr(), n_local)
+        else:
+            g.scan_device(trace[s].data_ptr(), n_local)
+        if world > 1:
+            PD.merge_touched(g)
+        e1.record(stream)
+        rep = g.reconstruct_leveled(k, theta)
+        e2.record(stream)
+        g.advance_slot()
+        return rep, (e1, e2)
+
+    def timed_loop(n_steps, start, from_host):
+        marks = []
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        ev_a = torch.cuda.Event(enable_timing=True)
+        ev_b = torch.cuda.Event(enable_timing=True)
+        ev_a.record(stream)
+        reps = None
+        for i in range(n_steps):
+            reps, m = step(start + i, from_host)
+            marks.append(m)
+        ev_b.record(stream)
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        ms = ev_a.elapsed_time(ev_b)
+        recon = [a.elapsed_time(b) for a, b in marks]
+        if world > 1:
+            t = torch.tensor([ms], device=f"cuda:{dev}")
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            ms = float(t.item())
+        return ms, recon, reps
+
+    for i in range(args.warmup):
+        step(i)
+    slot = args.warmup
+
+    # --- device-resident timed region --------------------------------------
+    g.profile(True)
+    g.profile_reset()
+    launches0 = P.launch_count()
+    with ClockSampler(dev) as clk:
+        ms, recon, reps = timed_loop(args.steps, slot, False)
+    launches = P.launch_count() - launches0
+    slot += args.steps
+    prof = {}
+    for name in ("scan", "commit", "hist_counts", "count", "hot_compact", "level2", "level_ext",
+                 "finalize", "merge"):
+        t, n, u = g.profile_read(name)
+        if n:
+            prof[name] = {"ms": t, "launches": n, "units": u}
+    g.profile(False)
+    g.profile_reset()
+    total_pairs = n_local * args.steps * world
+    value = total_pairs / (ms / 1e3) / 1e6
+
+    # --- e2e through the public API with host buffers ----------------------
+    e2e = None
+    if host_trace is not None:
+        for i in range(2):
+            step(slot + i, True)
+        slot += 2
+        g.io_bytes(reset=True)
+        ms_e, _, _ = timed_loop(args.steps, slot, True)
+        h2d, d2h = g.io_bytes(reset=True)
+        slot += args.steps
+        e2e = {"value": round(total_pairs / (ms_e / 1e3) / 1e6, 3), "unit": unit,
+               "h2d_bytes_per_step": h2d // args.steps, "d2h_bytes_per_step": d2h // args.steps,
+               "ms_per_step": round(ms_e / args.steps, 3)}
+
+    if rank != 0:
+        if world > 1:
+            dist.barrier()
+            dist.destroy_process_group()
+        return
+
+    # --- roofline of the dominant kernel --------------------------------------
+    peaks = {}
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            peaks = json.load(f)
+    except Exception:
+        pass
+    hbm = peaks.get("hbm_gbs", 6650.0)
+    dom = max(prof, key=lambda x: prof[x]["ms"]) if prof else None
+    r = cfg["r"]
+    roof = None
+    if dom:
+        d = prof[dom]
+        per_launch_ms = d["ms"] / d["launches"]
+        units_per_launch = d["units"] / d["launches"]
+        bytes_per_unit = {"scan": 8 + r * 32,                       # 168 B/pkt at r=5
+                          "count": cfg["eta"] * 4,                  # one estimator of u32 stamps
+                          "commit": 8 / 32 * 32,                    # bitmap word read+clear per 32 rec
+                          "merge": 4 * 2}.get(dom)
+        if bytes_per_unit is not None:
+            achieved = bytes_per_unit * units_per_launch / (per_launch_ms / 1e3) / 1e9
+            roof = {"kernel": dom, "bound": "hbm", "achieved": round(achieved, 1), "peak": hbm,
+                    "unit": "GB/s", "frac": round(achieved / hbm, 4), "traffic": None,
+                    "bytes_per_unit": bytes_per_unit, "units_per_launch": units_per_launch,
+                    "launch_ms": round(per_launch_ms, 4),
+                    "peak_source": "MEASURED_PEAKS.json hbm_gbs" if "hbm_gbs" in peaks else "fallback"}
+    kernels_share = {k2: round(v["ms"] / ms, 4) for k2, v in prof.items()}
+
+    # --- CPU baseline: the compiled reference on this host ---------------------
+    cpu = None
+    if world == 1 and not args.no_cpu_baseline:
+        try:
+            rr = run_reference(cfg, steps=1, warmup=1, pairs_cap=args.ref_pairs, time_budget_s=150)
+            cpu = {"value": round(rr["value"], 3), "unit": unit, "cores": rr["workers"],
+                   "kind": "reference",
+                   "sample": f"{rr['steps_timed']} slot(s) x {rr['pairs_per_step']} pairs of the "
+                             f"same trace after 1 warm-up slot; scan_batch alpha=32768 + "
+                             f"reconstruct_leveled + advance_slot, full-size grid in host RAM",
+                   "step_ms": round(rr["step_ms"], 1), "reconstruct_ms": round(rr["reconstruct_ms"], 1)}
+        except Exception as e:  # report, do not hide
+            cpu = {"value": None, "unit": unit, "cores": os.cpu_count(), "kind": "reference",
+                   "sample": f"failed: {type(e).__name__}: {e}"}
+
+    line = {
+        "metric": metric, "value": round(value, 3), "unit": unit, "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms / args.steps, 3),
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u32",
+        "data": "synthetic",
+        "config": {"workload": cfg["workload"], "pairs_per_step_per_gpu": n_local,
+                   "window_k": k, "theta": theta, "merge": "union-min (OR of touched bitmaps)",
+                   "parallelism": f"{world} routers, one per GPU",
+                   "l2": "inputs larger than L2 (800 MB per slot)"},
+        "gbps_800B": round(value * 1e6 * PKT_BYTES * 8 / 1e9, 1),
+        "reconstruct_ms": round(statistics.mean(recon), 3),
+        "reports_last_step": len(reps) if reps is not None else None,
+        "kernels_share": kernels_share,
+        "roofline": roof,
+        "cpu_baseline": cpu,
+        "e2e": e2e,
+        "gpu_launches": launches,
+        "clocks": clk.summary(),
+    }
+    print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -158,12 +158,40 @@ sspd_status sspd_grid_stamps(sspd_grid* g, uint32_t** dev_stamps, uint64_t* word
 sspd_status sspd_grid_touched(sspd_grid* g, uint32_t** dev_bits, uint64_t* words);
 sspd_status sspd_commit(sspd_grid* g);
 
+/* ---- synthetic traces (shape of synth_trace,
+ * workload.cpp:215-300), bit-identical on host and device ---- */
+/* Parameters: see paper_1803_11036_b200/csrc/synth.h (sspd_synth_params). */
+typedef struct {
+  uint64_t seed;
+  uint32_t hosts;
+  uint32_t pool;
+  uint32_t n_super;
+  uint32_t super_fanout;
+  uint64_t pairs_per_slot;
+  uint32_t shard;
+  uint32_t n_shards;
+} sspd_synth_params_t;
+/* Integer Zipf CDF over `hosts` ranks (hosts+0 entries, last = 2^63). */
+sspd_status sspd_synth_zipf_cdf(uint32_t hosts, double exponent, uint64_t* cdf_out);
+/* n pairs of slot `slot` starting at local index j0, into host memory
+ * (all host cores) or device memory (cdf must then be a device pointer). */
+sspd_status sspd_synth_host(const sspd_synth_params_t* p, const uint64_t* cdf, uint64_t slot,
+                            uint64_t j0, uint64_t n, uint32_t* pairs_out);
+sspd_status sspd_synth_device(int device, const sspd_synth_params_t* p, const uint64_t* dev_cdf,
+                              uint64_t slot, uint64_t j0, uint64_t n, uint32_t* dev_pairs_out,
+                              void* cuda_stream);
+/* Distinct super point cips injected by the generator (ground truth for
+ * the injected set). */
+uint32_t sspd_synth_super_cip(const sspd_synth_params_t* p, uint32_t i);
+
 /* Per-kernel timing of the last call on this grid (CUDA events on the grid's
  * stream), for bench.py's roofline: name -> milliseconds, launches. */
 sspd_status sspd_profile_enable(sspd_grid* g, int on);
 sspd_status sspd_profile_read(sspd_grid* g, const char* kernel, double* total_ms,
                               uint64_t* launches, uint64_t* units);
 sspd_status sspd_profile_reset(sspd_grid* g);
+/* Host<->device bytes this grid's calls have copied (e2e accounting). */
+sspd_status sspd_grid_io_bytes(sspd_grid* g, uint64_t* h2d, uint64_t* d2h, int reset);
 /* Total kernels this library has launched (all grids, since load). */
 uint64_t sspd_launch_count(void);
 

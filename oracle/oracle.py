@@ -390,6 +390,7 @@ def ref():
         L.ref_update.argtypes = [C.c_void_p, C.c_uint32, C.c_uint32]
         L.ref_scan.argtypes = [C.c_void_p, u32p, C.c_size_t, C.c_uint]
         L.ref_advance.argtypes = [C.c_void_p, C.c_uint]
+        L.ref_scan_alpha.argtypes = [C.c_void_p, C.c_void_p, C.c_size_t, C.c_uint, C.c_size_t]
         L.ref_get_cells.argtypes = [C.c_void_p, u16p]
         L.ref_set_cells.argtypes = [C.c_void_p, u16p]
         L.ref_hot_sets.restype = C.c_size_t
@@ -442,6 +443,11 @@ class RefGrid:
 
     def advance(self, workers: int = 1):
         ref().ref_advance(self._h, workers)
+
+    def scan_alpha(self, pairs: np.ndarray, workers: int, alpha: int = 1 << 15):
+        """scan in the pipeline's alpha-sized batches (pipeline.cpp:58-63)."""
+        p = np.ascontiguousarray(pairs, dtype=np.uint32).reshape(-1, 2)
+        ref().ref_scan_alpha(self._h, p.ctypes.data, p.shape[0], workers, alpha)
 
     def cells(self) -> np.ndarray:
         out = np.empty(ref().ref_grid_size(self._h), dtype=np.uint16)

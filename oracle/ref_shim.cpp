@@ -5,6 +5,7 @@
 // cpu_baseline legs.  Built into oracle/_ref/libsspd_ref.so; this file is
 // ours, the reference sources are compiled where they lie.
 #include <cstdint>
+#include <algorithm>
 #include <cstring>
 #include <exception>
 #include <new>
@@ -95,6 +96,13 @@ void ref_scan(void* g, const uint32_t* pairs, size_t n, unsigned workers) {
   static_assert(sizeof(IpPair) == 8);
   static_cast<Rsea*>(g)->scan_batch(
       std::span<const IpPair>(reinterpret_cast<const IpPair*>(pairs), n), workers);
+}
+// The reference pipeline's alpha-sized scan_batch calls (pipeline.cpp:58-63).
+void ref_scan_alpha(void* g, const uint32_t* pairs, size_t n, unsigned workers, size_t alpha) {
+  auto* rs = static_cast<Rsea*>(g);
+  const auto* p = reinterpret_cast<const IpPair*>(pairs);
+  for (size_t i = 0; i < n; i += alpha)
+    rs->scan_batch(std::span<const IpPair>(p + i, std::min(alpha, n - i)), workers);
 }
 void ref_advance(void* g, unsigned workers) { static_cast<Rsea*>(g)->advance_slot(workers); }
 void ref_get_cells(void* g, uint16_t* out) {

@@ -66,6 +66,13 @@ SIGNATURES = {
     "sspd_profile_read": (C.c_int, [grid_p, C.c_char_p, C.POINTER(C.c_double), u64p, u64p]),
     "sspd_profile_reset": (C.c_int, [grid_p]),
     "sspd_launch_count": (C.c_uint64, []),
+    "sspd_grid_io_bytes": (C.c_int, [grid_p, u64p, u64p, C.c_int]),
+    "sspd_synth_zipf_cdf": (C.c_int, [C.c_uint32, C.c_double, C.c_void_p]),
+    "sspd_synth_host": (C.c_int, [C.c_void_p, C.c_void_p, C.c_uint64, C.c_uint64, C.c_uint64,
+                                  C.c_void_p]),
+    "sspd_synth_device": (C.c_int, [C.c_int, C.c_void_p, C.c_void_p, C.c_uint64, C.c_uint64,
+                                    C.c_uint64, C.c_void_p, C.c_void_p]),
+    "sspd_synth_super_cip": (C.c_uint32, [C.c_void_p, C.c_uint32]),
 }
 
 _lib = None

@@ -17,6 +17,9 @@
 
 #include "../../include/sspd_cuda.h"
 #include "kernels.cuh"
+#include "synth.h"
+
+#include <omp.h>
 
 using namespace sspd_dev;
 
@@ -133,6 +136,7 @@ struct sspd_grid {
   void* pinned_small = nullptr;  // 4 KB pinned scratch for counters
   bool profiling = false;
   std::vector<ProfRec> prof;
+  uint64_t h2d_bytes = 0, d2h_bytes = 0;  // host<->device traffic, for e2e accounting
   std::mutex mu;
 };
 
@@ -266,6 +270,7 @@ sspd_status hot_locked(sspd_grid* g, uint32_t k, uint64_t cutoff, std::vector<ui
   if (s) return s;
   host_rowcnt.resize(g->r);
   CU(cudaMemcpyAsync(host_rowcnt.data(), g->hot_rowcnt.p, g->r * 4, cudaMemcpyDeviceToHost, g->stream));
+  g->d2h_bytes += (g->r * 4);
   CU(cudaStreamSynchronize(g->stream));
   return SSPD_OK;
 }
@@ -299,6 +304,7 @@ sspd_status finalize_dev(sspd_grid* g, const uint32_t* d_tuples, uint64_t n, uin
   }
   unsigned long long cnt = 0;
   CU(cudaMemcpyAsync(&cnt, counter, 8, cudaMemcpyDeviceToHost, g->stream));
+  g->d2h_bytes += (8);
   CU(cudaStreamSynchronize(g->stream));
   if (idx) {
     idx->resize(cnt);
@@ -306,8 +312,11 @@ sspd_status finalize_dev(sspd_grid* g, const uint32_t* d_tuples, uint64_t n, uin
     rks->resize(cnt);
     if (cnt) {
       CU(cudaMemcpyAsync(idx->data(), o_idx, cnt * 4, cudaMemcpyDeviceToHost, g->stream));
+  g->d2h_bytes += (cnt * 4);
       CU(cudaMemcpyAsync(cips->data(), o_cip, cnt * 4, cudaMemcpyDeviceToHost, g->stream));
+  g->d2h_bytes += (cnt * 4);
       CU(cudaMemcpyAsync(rks->data(), o_rk, cnt * 4, cudaMemcpyDeviceToHost, g->stream));
+  g->d2h_bytes += (cnt * 4);
       CU(cudaStreamSynchronize(g->stream));
     }
   }
@@ -532,6 +541,7 @@ sspd_status sspd_scan(sspd_grid* g, const uint32_t* pairs, uint64_t n, int pairs
     const uint64_t cnt = std::min(chunk_pairs, n - done);
     CU(cudaStreamWaitEvent(g->copy_stream, g->ev_used[buf], 0));
     CU(cudaMemcpyAsync(g->stage[buf].p, pairs + 2 * done, cnt * 8, cudaMemcpyHostToDevice, g->copy_stream));
+  g->h2d_bytes += (cnt * 8);
     CU(cudaEventRecord(g->ev_copy[buf], g->copy_stream));
     CU(cudaStreamWaitEvent(g->stream, g->ev_copy[buf], 0));
     launch(g->stage[buf].as<uint32_t>(), cnt);
@@ -587,6 +597,7 @@ sspd_status sspd_get_distances(sspd_grid* g, uint16_t* host_out, uint64_t offset
           g->stamps + offset + done, cnt, g->now, g->misc.as<uint16_t>());
     }
     CU(cudaMemcpyAsync(host_out + done, g->misc.p, cnt * 2, cudaMemcpyDeviceToHost, g->stream));
+  g->d2h_bytes += (cnt * 2);
     CU(cudaStreamSynchronize(g->stream));
     done += cnt;
   }
@@ -606,6 +617,7 @@ sspd_status sspd_put_distances(sspd_grid* g, const uint16_t* host_in, uint64_t o
   for (uint64_t done = 0; done < count;) {
     const uint64_t cnt = std::min(chunk, count - done);
     CU(cudaMemcpyAsync(g->misc.p, host_in + done, cnt * 2, cudaMemcpyHostToDevice, g->stream));
+  g->h2d_bytes += (cnt * 2);
     {
       Prof p(g, "from_distance", cnt);
       dist_to_stamps_kernel<<<grid_blocks(g, cnt, 256, 8), 256, 0, g->stream>>>(
@@ -625,6 +637,7 @@ sspd_status sspd_active_counts(sspd_grid* g, uint32_t k, uint32_t* host_out) {
   sspd_status s = counts_locked(g, k);
   if (s) return s;
   CU(cudaMemcpyAsync(host_out, g->counts.p, (size_t)g->geo.ncells * 4, cudaMemcpyDeviceToHost, g->stream));
+  g->d2h_bytes += ((size_t)g->geo.ncells * 4);
   CU(cudaStreamSynchronize(g->stream));
   return SSPD_OK;
 }
@@ -645,6 +658,7 @@ sspd_status sspd_hot_sets(sspd_grid* g, uint32_t k, uint64_t cutoff, uint32_t* c
                          cudaMemcpyDeviceToHost, g->stream));
     pos += rc[row];
   }
+  g->d2h_bytes += pos * 4;
   CU(cudaStreamSynchronize(g->stream));
   return SSPD_OK;
 }
@@ -659,10 +673,12 @@ sspd_status sspd_finalize(sspd_grid* g, const uint32_t* tuples, uint64_t n, uint
   if (g->tupA.ensure(n * g->r * 4) != cudaSuccess || g->misc.ensure(n) != cudaSuccess)
     return fail(SSPD_CUDA_ERROR, "CUDA error: out of memory (finalize)");
   CU(cudaMemcpyAsync(g->tupA.p, tuples, n * g->r * 4, cudaMemcpyHostToDevice, g->stream));
+  g->h2d_bytes += (n * g->r * 4);
   std::vector<uint32_t> idx, c, rk;
   s = finalize_dev(g, g->tupA.as<uint32_t>(), n, k, cutoff, g->misc.as<uint8_t>(), &idx, &c, &rk);
   if (s) return s;
   CU(cudaMemcpyAsync(accepted, g->misc.p, n, cudaMemcpyDeviceToHost, g->stream));
+  g->d2h_bytes += (n);
   CU(cudaStreamSynchronize(g->stream));
   for (size_t i = 0; i < idx.size(); ++i) {
     cips[idx[i]] = c[i];
@@ -706,6 +722,7 @@ sspd_status sspd_reconstruct(sspd_grid* g, uint32_t k, uint64_t cutoff, uint64_t
       sspd_status e = check_launch();
       if (e) return e;
       CU(cudaMemcpyAsync(counter, d_counter, 8, cudaMemcpyDeviceToHost, g->stream));
+  g->d2h_bytes += (8);
       CU(cudaStreamSynchronize(g->stream));
       count = *counter;
       if (count <= cap_tuples || count > cap) return SSPD_OK;
@@ -822,6 +839,7 @@ sspd_status sspd_merge(const sspd_grid* const* grids_c, uint64_t n, int policy, 
   DevBuf tmp;
   if (tmp.ensure(sbytes) != cudaSuccess) return fail(SSPD_CUDA_ERROR, "CUDA error: out of memory (merge)");
   CU(cudaMemcpyAsync(tmp.p, srcs.data(), sbytes, cudaMemcpyHostToDevice, out->stream));
+  out->h2d_bytes += (sbytes);
   {
     Prof p(out, "merge", out->geo.n_rec * n);
     merge_kernel<<<grid_blocks(out, out->geo.n_rec, 256, 8), 256, 0, out->stream>>>(
@@ -864,6 +882,7 @@ sspd_status sspd_equal(sspd_grid* a, sspd_grid* b, int* equal) {
         a->stamps, a->now, b->stamps, b->now, a->geo.n_rec, a->misc.as<int>());
   }
   CU(cudaMemcpyAsync(flag, a->misc.p, 4, cudaMemcpyDeviceToHost, a->stream));
+  a->d2h_bytes += (4);
   CU(cudaStreamSynchronize(a->stream));
   *equal = *flag ? 0 : 1;
   return check_launch();
@@ -916,6 +935,14 @@ sspd_status sspd_grid_touched(sspd_grid* g, uint32_t** dev_bits, uint64_t* words
   return SSPD_OK;
 }
 
+sspd_status sspd_grid_io_bytes(sspd_grid* g, uint64_t* h2d, uint64_t* d2h, int reset) {
+  std::lock_guard<std::mutex> lk(g->mu);
+  if (h2d) *h2d = g->h2d_bytes;
+  if (d2h) *d2h = g->d2h_bytes;
+  if (reset) g->h2d_bytes = g->d2h_bytes = 0;
+  return SSPD_OK;
+}
+
 sspd_status sspd_profile_enable(sspd_grid* g, int on) {
   std::lock_guard<std::mutex> lk(g->mu);
   g->profiling = on != 0;
@@ -953,6 +980,66 @@ sspd_status sspd_profile_read(sspd_grid* g, const char* kernel, double* total_ms
   if (launches) *launches = cnt;
   if (units) *units = u;
   return SSPD_OK;
+}
+
+static_assert(sizeof(sspd_synth_params_t) == sizeof(sspd_synth_params), "synth params layout");
+
+__global__ void synth_kernel(sspd_synth_params p, const uint64_t* __restrict__ cdf, uint64_t slot,
+                             uint64_t j0, uint64_t n, uint2* __restrict__ out) {
+  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (uint64_t)gridDim.x * blockDim.x) {
+    uint32_t c, o;
+    sspd_synth_pair(&p, cdf, slot, j0 + i, &c, &o);
+    out[i] = make_uint2(c, o);
+  }
+}
+
+sspd_status sspd_synth_zipf_cdf(uint32_t hosts, double exponent, uint64_t* cdf_out) {
+  if (hosts == 0) return fail(SSPD_INVALID_ARGUMENT, "synth: hosts == 0");
+  std::vector<double> acc(hosts);
+  double s = 0;
+  for (uint32_t i = 0; i < hosts; ++i) {
+    s += std::pow(static_cast<double>(i + 1), -exponent);
+    acc[i] = s;
+  }
+  const double scale = 9223372036854775808.0;  // 2^63
+  for (uint32_t i = 0; i < hosts; ++i) {
+    const double v = acc[i] / s * scale;
+    cdf_out[i] = v >= scale ? (1ull << 63) : static_cast<uint64_t>(v);
+  }
+  cdf_out[hosts - 1] = 1ull << 63;
+  return SSPD_OK;
+}
+
+static bool synth_ok(const sspd_synth_params_t* p) {
+  return p && p->hosts && p->n_shards && p->shard < p->n_shards &&
+         (p->n_super == 0 || p->super_fanout);
+}
+
+sspd_status sspd_synth_host(const sspd_synth_params_t* p, const uint64_t* cdf, uint64_t slot, uint64_t j0,
+                            uint64_t n, uint32_t* pairs_out) {
+  if (!synth_ok(p)) return fail(SSPD_INVALID_ARGUMENT, "synth: bad parameters");
+  const auto* q = reinterpret_cast<const sspd_synth_params*>(p);
+#pragma omp parallel for schedule(static)
+  for (long long i = 0; i < (long long)n; ++i)
+    sspd_synth_pair(q, cdf, slot, j0 + (uint64_t)i, &pairs_out[2 * i], &pairs_out[2 * i + 1]);
+  return SSPD_OK;
+}
+
+sspd_status sspd_synth_device(int device, const sspd_synth_params_t* p, const uint64_t* dev_cdf, uint64_t slot,
+                              uint64_t j0, uint64_t n, uint32_t* dev_pairs_out, void* cuda_stream) {
+  if (!synth_ok(p)) return fail(SSPD_INVALID_ARGUMENT, "synth: bad parameters");
+  DeviceGuard dg(device);
+  const auto q = *reinterpret_cast<const sspd_synth_params*>(p);
+  const unsigned blocks = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>((n + 255) / 256, 148ull * 16));
+  g_launches.fetch_add(1, std::memory_order_relaxed);
+  synth_kernel<<<blocks, 256, 0, static_cast<cudaStream_t>(cuda_stream)>>>(q, dev_cdf, slot, j0, n,
+                                                                           reinterpret_cast<uint2*>(dev_pairs_out));
+  return check_launch();
+}
+
+uint32_t sspd_synth_super_cip(const sspd_synth_params_t* p, uint32_t i) {
+  return sspd_super_cip(reinterpret_cast<const sspd_synth_params*>(p), i);
 }
 
 }  // extern "C"

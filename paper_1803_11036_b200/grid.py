@@ -125,6 +125,16 @@ class Grid:
             return
         check(self._L.sspd_scan(self._h, p.ctypes.data_as(C.c_void_p), p.shape[0], 0))
 
+    def scan_host_ptr(self, host_ptr: int, n_pairs: int):
+        """Host (ideally pinned) buffer of n (cip, oip) pairs; copied in chunks."""
+        check(self._L.sspd_scan(self._h, C.c_void_p(host_ptr), n_pairs, 0))
+
+    def io_bytes(self, reset: bool = False) -> tuple[int, int]:
+        a = C.c_uint64()
+        b = C.c_uint64()
+        check(self._L.sspd_grid_io_bytes(self._h, C.byref(a), C.byref(b), int(reset)))
+        return a.value, b.value
+
     def scan_device(self, dev_ptr: int, n_pairs: int):
         check(self._L.sspd_scan(self._h, C.c_void_p(dev_ptr), n_pairs, 1))
 
