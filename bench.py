@@ -185,6 +185,8 @@ def main():
     ap.add_argument("--config", default="c2", choices=sorted(CONFIGS))
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--scan-mode", default="auto", choices=["auto", "bitmap", "direct"])
+    ap.add_argument("--filter", type=int, default=-1, help="L1 duplicate probe 0/1 (-1 = default)")
     ap.add_argument("--ref-pairs", type=int, default=100_000_000,
                     help="pairs per reference step (bounded sample of the slot)")
     args = ap.parse_args()
@@ -231,12 +233,19 @@ def main():
     torch.cuda.set_device(local)
     dev = local
     L = P.load()
-    stream = torch.cuda.current_stream()
+    # One non-default stream carries every kernel of the grid, the NCCL
+    # collectives and the timing events (torch's default stream is the legacy
+    # NULL stream, which the grid's stream would not be ordered with).
+    stream = torch.cuda.Stream(device=dev)
+    torch.cuda.set_stream(stream)
 
     # --- setup (untimed): grid, trace resident in HBM, pinned host copy ------
     g = P.Grid(cfg["q"], cfg["r"], cfg["delta"], cfg["seed"], cfg["eta"], device=dev)
     g.set_stream(stream.cuda_stream)
+    g.scan_mode({"auto": -1, "bitmap": 0, "direct": 1}[args.scan_mode], args.filter)
     g.track_window(cfg["k"])
+    if world > 1:
+        PD.prepare(g)
     cdf = torch.from_numpy(zipf_cdf(L, cfg).view(np.int64)).to(f"cuda:{dev}")
     sp = synth_params(cfg, rank, world)
     n_local = cfg["pairs_per_slot"]

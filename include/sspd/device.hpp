@@ -1,0 +1,13 @@
+// sspd/device.hpp -- B200 extension of the sspd API: which GPU new grids
+// live on.  Grids are created on the calling thread's current sspd device
+// (default: $SSPD_DEVICE, else 0).  There is no CPU fallback: constructing a
+// grid without a usable sm_100 device throws std::runtime_error.
+#pragma once
+
+namespace sspd {
+
+void set_device(int device);
+int current_device();
+int device_count();
+
+}  // namespace sspd

@@ -157,6 +157,13 @@ sspd_status sspd_grid_stamps(sspd_grid* g, uint32_t** dev_stamps, uint64_t* word
  * OR-reduced it in place, sspd_commit folds it into the stamps. */
 sspd_status sspd_grid_touched(sspd_grid* g, uint32_t** dev_bits, uint64_t* words);
 sspd_status sspd_commit(sspd_grid* g);
+/* Record each slot's touched bitmap even when scanning in direct mode, so
+ * routers can OR-merge it (union-min exchange). */
+sspd_status sspd_set_exchange(sspd_grid* g, int on);
+/* Scan strategy: mode 0 = deferred bitmap, 1 = direct stamping, -1 = keep
+ * (default: bitmap while it fits in L2); filter 0/1 = L1 duplicate probe,
+ * -1 = keep.  Results are identical in every mode. */
+sspd_status sspd_scan_mode(sspd_grid* g, int mode, int filter);
 
 /* ---- synthetic traces (shape of synth_trace,
  * workload.cpp:215-300), bit-identical on host and device ---- */

@@ -244,7 +244,11 @@ class OracleGrid:
         return self._g.eta
 
     def cells(self) -> np.ndarray:
-        """Live numpy view of the recorder array (writes go to the grid)."""
+        """Copy of the recorder array."""
+        return self.cells_view().copy()
+
+    def cells_view(self) -> np.ndarray:
+        """Live view of the recorder array; valid while this grid is alive."""
         return np.ctypeslib.as_array(self._g.cells, shape=(self._g.n,))
 
     def copy(self) -> "OracleGrid":

@@ -88,115 +88,215 @@ __device__ __forceinline__ uint2 ld_stream_u2(const void* p) {
 }
 
 // ---------------------------------------------------------------------------
-// SCAN: Rsea::update over a batch (rsea.cpp:29-53), recording touches in the
-// per-slot bitmap.  The bitmap is 1/32 of the stamp grid; when it fits in L2
-// (reference geometry: 20 MiB) every touch is an L2-resident red.or.
+// SCAN: Rsea::update over a batch (rsea.cpp:29-53).  Two modes:
 //
+//  * bitmap (deferred): each touch sets its recorder's bit in the per-slot
+//    touched bitmap with red.or; commit_kernel folds the bitmap into the
+//    stamps before anything reads them.  When the bitmap fits in L2 (the
+//    reference geometry: 20 MiB for 640 MiB of stamps) every touch is an
+//    L2-resident atomic and the stamp grid is written once, in address order.
+//  * direct: each touch stamps its recorder in place (atomicMax(now) when the
+//    window ring is tracked -- the old stamp says which ring entry to move the
+//    bucket from -- else red.max).  Used when the bitmap itself would not fit
+//    in L2, where streaming it in the commit would cost more than it saves.
+//
+// FILTER: probe the target word through L1 first and skip the atomic when the
+// touch is already recorded (bit set / stamp == now).  Both only move one way
+// during a scan, so a stale L1 line can cost a redundant atomic but never
+// lose one; with Zipf traffic most packets repeat a pair seen this slot.
 // H1MODE 0: eta a power of two <= 2^32, H1 needs only its low 32 bits.
 // H1MODE 1: general eta, full 64-bit tabulation value % eta (hashing.hpp:58).
-template <int H1MODE>
-__global__ void __launch_bounds__(256) scan_bitmap_kernel(const uint32_t* __restrict__ pairs,
-                                                          uint64_t n, const HashTabs* __restrict__ tabs,
-                                                          Geo geo, uint32_t* __restrict__ touched) {
-  __shared__ uint16_t s_row0[4][256];
-  __shared__ uint64_t s_h1[4][256];  // low 32 bits used in mode 0
+
+struct ScanTables {
+  uint16_t row0[4][256];
+  uint64_t h1[4][256];  // low 32 bits used in H1MODE 0
+};
+
+__device__ __forceinline__ void load_scan_tables(ScanTables& t, const HashTabs* __restrict__ tabs) {
   for (int i = threadIdx.x; i < 1024; i += blockDim.x) {
-    s_row0[i >> 8][i & 255] = (uint16_t)tabs->row0[i >> 8][i & 255];
-    s_h1[i >> 8][i & 255] = tabs->h1[i >> 8][i & 255];
+    t.row0[i >> 8][i & 255] = (uint16_t)tabs->row0[i >> 8][i & 255];
+    t.h1[i >> 8][i & 255] = tabs->h1[i >> 8][i & 255];
   }
   __syncthreads();
-  const uint32_t* s_h1_lo = reinterpret_cast<const uint32_t*>(&s_h1[0][0]);
+}
 
-  auto touch = [&](uint32_t cip, uint32_t oip) {
-    uint32_t bucket;
-    if (H1MODE == 0) {
-      // low words of the u64 entries (little endian): index 2*i
-      uint32_t h = s_h1_lo[2 * (0 * 256 + (oip & 0xff))] ^ s_h1_lo[2 * (1 * 256 + ((oip >> 8) & 0xff))] ^
-                   s_h1_lo[2 * (2 * 256 + ((oip >> 16) & 0xff))] ^ s_h1_lo[2 * (3 * 256 + (oip >> 24))];
-      bucket = h & (geo.eta - 1u);
-    } else {
-      uint64_t h = s_h1[0][oip & 0xff] ^ s_h1[1][(oip >> 8) & 0xff] ^ s_h1[2][(oip >> 16) & 0xff] ^
-                   s_h1[3][oip >> 24];
-      bucket = (uint32_t)(h % geo.eta);
-    }
-    const uint32_t col0 = ((uint32_t)s_row0[0][cip & 0xff] ^ s_row0[1][(cip >> 8) & 0xff] ^
-                           s_row0[2][(cip >> 16) & 0xff] ^ s_row0[3][cip >> 24]) &
-                          geo.col_mask;
-    // row 0
-    uint64_t idx = (uint64_t)col0 * geo.eta + bucket;
-    red_or(touched + (idx >> 5), 1u << (idx & 31));
-    for (uint32_t row = 1; row < geo.r; ++row) {
-      const uint32_t col = (shr32(cip, (row - 1) * geo.delta) ^ col0) & geo.col_mask;
-      idx = ((uint64_t)row << geo.q | col) * geo.eta + bucket;
-      red_or(touched + (idx >> 5), 1u << (idx & 31));
-    }
-  };
+// Bucket of oip and row-0 column of cip (hash_opposite, hashing.hpp:56-59;
+// rsea.cpp:31-32).
+template <int H1MODE>
+__device__ __forceinline__ void hash_pair(const ScanTables& t, const Geo& geo, uint32_t cip, uint32_t oip,
+                                          uint32_t& bucket, uint32_t& col0) {
+  if (H1MODE == 0) {
+    const uint32_t* lo = reinterpret_cast<const uint32_t*>(&t.h1[0][0]);
+    const uint32_t h = lo[2 * (0 * 256 + (oip & 0xff))] ^ lo[2 * (1 * 256 + ((oip >> 8) & 0xff))] ^
+                       lo[2 * (2 * 256 + ((oip >> 16) & 0xff))] ^ lo[2 * (3 * 256 + (oip >> 24))];
+    bucket = h & (geo.eta - 1u);
+  } else {
+    const uint64_t h = t.h1[0][oip & 0xff] ^ t.h1[1][(oip >> 8) & 0xff] ^ t.h1[2][(oip >> 16) & 0xff] ^
+                       t.h1[3][oip >> 24];
+    bucket = (uint32_t)(h % geo.eta);
+  }
+  col0 = ((uint32_t)t.row0[0][cip & 0xff] ^ t.row0[1][(cip >> 8) & 0xff] ^ t.row0[2][(cip >> 16) & 0xff] ^
+          t.row0[3][cip >> 24]) &
+         geo.col_mask;
+}
 
+// Column of row `row` (rhfg_from_row0, hashing.hpp:68-71).
+__device__ __forceinline__ uint32_t row_col(const Geo& geo, uint32_t row, uint32_t cip, uint32_t col0) {
+  return row == 0 ? col0 : (shr32(cip, (row - 1) * geo.delta) ^ col0) & geo.col_mask;
+}
+
+// Stream the pairs: two pairs per 16-byte load, two loads in flight.
+template <class F>
+__device__ __forceinline__ void for_each_pair(const uint32_t* __restrict__ pairs, uint64_t n, F&& f) {
   const uint64_t tid = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
   const uint64_t nthreads = (uint64_t)gridDim.x * blockDim.x;
-  const bool aligned16 = ((reinterpret_cast<uintptr_t>(pairs) & 15u) == 0);
-  if (aligned16) {
-    // Two pairs per 16-byte load; two loads in flight per thread.
+  if ((reinterpret_cast<uintptr_t>(pairs) & 15u) == 0) {
     const uint64_t nquads = n >> 1;
     uint64_t i = tid;
     for (; i + nthreads < nquads; i += 2 * nthreads) {
       const uint4 a = ld_stream_u4(pairs + 4 * i);
       const uint4 b = ld_stream_u4(pairs + 4 * (i + nthreads));
-      touch(a.x, a.y);
-      touch(a.z, a.w);
-      touch(b.x, b.y);
-      touch(b.z, b.w);
+      f(a.x, a.y);
+      f(a.z, a.w);
+      f(b.x, b.y);
+      f(b.z, b.w);
     }
     for (; i < nquads; i += nthreads) {
       const uint4 a = ld_stream_u4(pairs + 4 * i);
-      touch(a.x, a.y);
-      touch(a.z, a.w);
+      f(a.x, a.y);
+      f(a.z, a.w);
     }
-    if ((n & 1) && tid == 0) touch(pairs[2 * (n - 1)], pairs[2 * (n - 1) + 1]);
+    if ((n & 1) && tid == 0) f(pairs[2 * (n - 1)], pairs[2 * (n - 1) + 1]);
   } else {
-    for (uint64_t i = tid; i < n; i += nthreads) touch(pairs[2 * i], pairs[2 * i + 1]);
+    for (uint64_t i = tid; i < n; i += nthreads) f(pairs[2 * i], pairs[2 * i + 1]);
   }
+}
+
+template <int H1MODE, int FILTER>
+__global__ void __launch_bounds__(256) scan_bitmap_kernel(const uint32_t* __restrict__ pairs,
+                                                          uint64_t n, const HashTabs* __restrict__ tabs,
+                                                          Geo geo, uint32_t* __restrict__ touched) {
+  __shared__ ScanTables t;
+  load_scan_tables(t, tabs);
+  for_each_pair(pairs, n, [&](uint32_t cip, uint32_t oip) {
+    uint32_t bucket, col0;
+    hash_pair<H1MODE>(t, geo, cip, oip, bucket, col0);
+    // rows in groups of 4: the L1 probes of a group are issued together
+    for (uint32_t r0 = 0; r0 < geo.r; r0 += 4) {
+      uint64_t w[4];
+      uint32_t bit[4], cur[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const uint32_t row = r0 + u;
+        const uint64_t idx = ((uint64_t)row << geo.q | row_col(geo, row, cip, col0)) * geo.eta + bucket;
+        w[u] = idx >> 5;
+        bit[u] = 1u << (idx & 31);
+        cur[u] = (row < geo.r) ? (FILTER ? __ldca(touched + w[u]) : 0u) : bit[u];
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+        if (!(cur[u] & bit[u])) red_or(touched + w[u], bit[u]);
+    }
+  });
+}
+
+// HIST: maintain the window ring (K slots) from the old stamps.
+// BITS: also record touches in the bitmap (the union-min exchange of a
+//       multi-router slot, paper_1803_11036_b200/dist.py).
+template <int H1MODE, int FILTER, int HIST, int BITS>
+__global__ void __launch_bounds__(256) scan_direct_kernel(const uint32_t* __restrict__ pairs, uint64_t n,
+                                                          const HashTabs* __restrict__ tabs, Geo geo,
+                                                          uint32_t* __restrict__ stamps, uint32_t now,
+                                                          uint32_t* __restrict__ hist, uint32_t K,
+                                                          uint32_t* __restrict__ touched) {
+  __shared__ ScanTables t;
+  load_scan_tables(t, tabs);
+  const uint32_t now_slot = HIST ? now % K : 0;
+  for_each_pair(pairs, n, [&](uint32_t cip, uint32_t oip) {
+    uint32_t bucket, col0;
+    hash_pair<H1MODE>(t, geo, cip, oip, bucket, col0);
+    for (uint32_t r0 = 0; r0 < geo.r; r0 += 4) {
+      uint64_t idx[4];
+      uint32_t cell[4], cur[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const uint32_t row = r0 + u;
+        cell[u] = row << geo.q | row_col(geo, row, cip, col0);
+        idx[u] = (uint64_t)cell[u] * geo.eta + bucket;
+        cur[u] = (row < geo.r) ? (FILTER ? __ldca(stamps + idx[u]) : 0u) : now;
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        if (cur[u] == now) continue;
+        if (HIST) {
+          const uint32_t old = atomicMax(stamps + idx[u], now);
+          if (old < now) {
+            atomicAdd(hist + (uint64_t)now_slot * geo.ncells + cell[u], 1u);
+            if (old + K > now) atomicSub(hist + (uint64_t)(old % K) * geo.ncells + cell[u], 1u);
+          }
+        } else {
+          asm volatile("red.relaxed.gpu.global.max.u32 [%0], %1;" ::"l"(stamps + idx[u]), "r"(now) : "memory");
+        }
+        if (BITS) red_or(touched + (idx[u] >> 5), 1u << (idx[u] & 31));
+      }
+    }
+  });
 }
 
 // ---------------------------------------------------------------------------
 // COMMIT: fold this slot's touched bitmap into the stamps (stamp = now) and,
 // when a window of K slots is tracked, move each first-touched bucket's count
 // from the ring entry of its previous stamp to the entry of `now`.  Clears
-// the bitmap.  One warp covers 32 consecutive bitmap words (1024 recorders);
-// for each non-zero word the lanes update the 32 recorders of that word, so
-// the stamp writes of a warp land in one 128-byte line, in address order.
+// the bitmap.  Each thread takes 4 bitmap words (128 recorders) per 16-byte
+// load, skips empty groups, and walks its set bits; the stamp accesses of a
+// warp stay within 16 KiB of address space, in order, so DRAM sees an ordered
+// sparse stream rather than random scatter.
+__device__ __forceinline__ void commit_word(uint32_t bits, uint64_t rec0, uint32_t* __restrict__ stamps,
+                                            uint64_t n_rec, uint32_t now, uint32_t* __restrict__ hist,
+                                            uint32_t K, uint32_t now_slot, uint32_t ncells, const Div40& by_eta) {
+  while (bits) {
+    const uint32_t b = __ffs(bits) - 1;
+    bits &= bits - 1;
+    const uint64_t rec = rec0 + b;
+    if (rec >= n_rec) break;
+    if (hist) {
+      const uint32_t old = stamps[rec];
+      if (old != now) {
+        stamps[rec] = now;
+        const uint32_t cell = (uint32_t)by_eta.div(rec);
+        atomicAdd(hist + (uint64_t)now_slot * ncells + cell, 1u);
+        if (old + K > now) atomicSub(hist + (uint64_t)(old % K) * ncells + cell, 1u);
+      }
+    } else {
+      stamps[rec] = now;  // idempotent: a recorder touched this slot reads `now`
+    }
+  }
+}
+
 __global__ void __launch_bounds__(256) commit_kernel(uint32_t* __restrict__ touched, uint64_t nwords,
                                                      uint32_t* __restrict__ stamps, uint64_t n_rec,
                                                      uint32_t now, uint32_t* __restrict__ hist,
                                                      uint32_t K, uint32_t ncells, Div40 by_eta) {
-  const uint32_t lane = threadIdx.x & 31;
-  const uint64_t warp = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  const uint64_t nwarps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+  const uint64_t tid = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const uint64_t nthreads = (uint64_t)gridDim.x * blockDim.x;
   const uint32_t now_slot = K ? now % K : 0;
-  for (uint64_t base = warp * 32; base < nwords; base += nwarps * 32) {
-    const uint64_t my = base + lane;
-    uint32_t w = my < nwords ? touched[my] : 0u;
-    uint32_t nz = __ballot_sync(0xffffffffu, w != 0);
-    if (w) touched[my] = 0u;
-    while (nz) {
-      const int src = __ffs(nz) - 1;
-      nz &= nz - 1;
-      const uint32_t word = __shfl_sync(0xffffffffu, w, src);
-      const uint64_t rec = (base + src) * 32 + lane;
-      if ((word >> lane) & 1u) {
-        if (rec < n_rec) {
-          const uint32_t old = stamps[rec];
-          if (old != now) {
-            stamps[rec] = now;
-            if (hist) {
-              const uint32_t cell = (uint32_t)by_eta.div(rec);
-              atomicAdd(hist + (uint64_t)now_slot * ncells + cell, 1u);
-              if (old + K > now) atomicSub(hist + (uint64_t)(old % K) * ncells + cell, 1u);
-            }
-          }
-        }
-      }
-    }
+  const uint64_t nvec = nwords >> 2;
+  uint4* tv = reinterpret_cast<uint4*>(touched);
+  for (uint64_t v = tid; v < nvec; v += nthreads) {
+    const uint4 w = tv[v];
+    if ((w.x | w.y | w.z | w.w) == 0) continue;
+    tv[v] = make_uint4(0, 0, 0, 0);
+    const uint64_t rec0 = v * 128;
+    commit_word(w.x, rec0, stamps, n_rec, now, hist, K, now_slot, ncells, by_eta);
+    commit_word(w.y, rec0 + 32, stamps, n_rec, now, hist, K, now_slot, ncells, by_eta);
+    commit_word(w.z, rec0 + 64, stamps, n_rec, now, hist, K, now_slot, ncells, by_eta);
+    commit_word(w.w, rec0 + 96, stamps, n_rec, now, hist, K, now_slot, ncells, by_eta);
+  }
+  for (uint64_t wi = nvec * 4 + tid; wi < nwords; wi += nthreads) {
+    const uint32_t w = touched[wi];
+    if (!w) continue;
+    touched[wi] = 0;
+    commit_word(w, wi * 32, stamps, n_rec, now, hist, K, now_slot, ncells, by_eta);
   }
 }
 
@@ -319,7 +419,18 @@ __global__ void __launch_bounds__(1024) hot_compact_kernel(const uint32_t* __res
 // c & low_mask == ((t0 ^ t[m-1]) >> delta) ^ (t0 & low_mask): the matching
 // columns are exactly the set bits of that key's row segment in hotT.  Every
 // survivor is counted (64-bit, exact even past the cap, as CandidateOverflow
-// reports it) and written while it fits the buffer.
+// reports it) and written while it fits the buffer.  Sizes come from device
+// memory (row counts, previous level's count), so a whole reconstruction is
+// queued without host round trips; a level whose input was truncated (count
+// above the buffer) does nothing and the host re-runs with larger buffers.
+
+// Device-side bookkeeping of one reconstruction, copied back in one piece.
+struct ReconMeta {
+  uint32_t rowcnt[64];             // hot columns per row
+  unsigned long long level[64];    // survivors per level (index = level)
+  unsigned long long surv;         // tuples passing the address checks
+  unsigned long long pad[3];
+};
 
 __device__ __forceinline__ uint64_t warp_reserve(uint32_t mine, unsigned long long* counter,
                                                  uint32_t lane) {
@@ -344,12 +455,14 @@ __device__ __forceinline__ uint32_t seg_popc(const uint32_t* seg, uint32_t words
 }
 
 // Level 2: (c0, c1) over HSE(0) x HSE(1); c2 from row 2's segment.
-__global__ void __launch_bounds__(256) level2_kernel(const uint32_t* __restrict__ H0, uint32_t n0,
-                                                     const uint32_t* __restrict__ H1, uint32_t n1,
-                                                     const uint32_t* __restrict__ T2, uint32_t wpk,
-                                                     Geo geo, uint32_t* __restrict__ out,
-                                                     uint64_t out_cap,
-                                                     unsigned long long* __restrict__ counter) {
+__global__ void __launch_bounds__(256) level2_kernel(const uint32_t* __restrict__ cols, uint32_t ncol,
+                                                     const uint32_t* __restrict__ T2, uint32_t wpk, Geo geo,
+                                                     uint32_t* __restrict__ out, uint64_t out_cap,
+                                                     ReconMeta* __restrict__ meta) {
+  const uint32_t n0 = meta->rowcnt[0], n1 = meta->rowcnt[1];
+  const uint32_t* H0 = cols;
+  const uint32_t* H1 = cols + ncol;
+  unsigned long long* counter = &meta->level[2];
   const uint32_t lane = threadIdx.x & 31;
   const uint64_t total = (uint64_t)n0 * n1;
   const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
@@ -387,11 +500,13 @@ __global__ void __launch_bounds__(256) level2_kernel(const uint32_t* __restrict_
 }
 
 // Levels 3..r-1: extend m-tuples by row m.
-__global__ void __launch_bounds__(256) level_ext_kernel(const uint32_t* __restrict__ in, uint64_t n_in,
+__global__ void __launch_bounds__(256) level_ext_kernel(const uint32_t* __restrict__ in, uint64_t in_cap,
                                                         uint32_t m, const uint32_t* __restrict__ Tm,
                                                         uint32_t wpk, Geo geo, uint32_t* __restrict__ out,
-                                                        uint64_t out_cap,
-                                                        unsigned long long* __restrict__ counter) {
+                                                        uint64_t out_cap, ReconMeta* __restrict__ meta) {
+  const uint64_t n_in = meta->level[m - 1];
+  if (n_in > in_cap) return;  // input truncated: the host re-runs with larger buffers
+  unsigned long long* counter = &meta->level[m];
   const uint32_t lane = threadIdx.x & 31;
   const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
   const uint32_t kbits = geo.q - geo.delta;
@@ -426,71 +541,108 @@ __global__ void __launch_bounds__(256) level_ext_kernel(const uint32_t* __restri
 }
 
 // ---------------------------------------------------------------------------
-// FINALIZE (rsea.cpp:86-108), one warp per r-tuple.  The address checks
-// (assemble_ip, hashing.cpp:45-61, then the row-0 re-hash) need no memory and
-// run first; surviving tuples intersect their r estimators (max distance ==
-// min stamp) and count in-window buckets.  The accept set equals the
+// FINALIZE (rsea.cpp:86-108) in two kernels.  The accept set equals the
 // reference's, which tests R_k first: the three tests are a conjunction.
-__global__ void __launch_bounds__(256) finalize_kernel(const uint32_t* __restrict__ tuples, uint64_t n,
-                                                       const uint32_t* __restrict__ stamps,
-                                                       const HashTabs* __restrict__ tabs, Geo geo,
-                                                       uint32_t thr, uint64_t cutoff,
-                                                       uint32_t* __restrict__ out_idx,
-                                                       uint32_t* __restrict__ out_cip,
-                                                       uint32_t* __restrict__ out_rk,
-                                                       unsigned long long* __restrict__ counter,
-                                                       uint8_t* __restrict__ accepted) {
+//
+// (1) address checks, one thread per r-tuple: assemble_ip (hashing.cpp:45-61)
+//     then the row-0 re-hash; survivors are compacted.
+__global__ void __launch_bounds__(256) finalize_check_kernel(const uint32_t* __restrict__ tuples,
+                                                             uint64_t in_cap, const HashTabs* __restrict__ tabs,
+                                                             Geo geo, ReconMeta* __restrict__ meta,
+                                                             uint32_t* __restrict__ surv_idx,
+                                                             uint32_t* __restrict__ surv_cip) {
   __shared__ uint16_t s_row0[4][256];
   for (int i = threadIdx.x; i < 1024; i += blockDim.x)
     s_row0[i >> 8][i & 255] = (uint16_t)tabs->row0[i >> 8][i & 255];
   __syncthreads();
+  const uint64_t n = meta->level[geo.r - 1];
+  if (n > in_cap) return;
   const uint32_t lane = threadIdx.x & 31;
-  const uint64_t warp = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  const uint64_t nwarps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
-  for (uint64_t t = warp; t < n; t += nwarps) {
-    const uint32_t* cols = tuples + t * geo.r;
-    // assemble_ip over blocks B(i) = c0 ^ ci, i = 1..r-1 (lane-parallel)
-    const uint32_t c0 = cols[0];
-    uint64_t part = 0;
-    for (uint32_t j = lane; j + 1 < geo.r; j += 32) {
-      const uint32_t b = c0 ^ cols[j + 1];
-      part |= (uint64_t)b << ((j * geo.delta) & 63u);
-    }
-#pragma unroll
-    for (int o = 16; o; o >>= 1) part |= __shfl_xor_sync(0xffffffffu, part, o);
-    const uint32_t ip = (uint32_t)part;
-    bool ok = true;
-    for (uint32_t j = lane; j + 1 < geo.r; j += 32) {
-      const uint32_t b = c0 ^ cols[j + 1];
-      if ((shr32(ip, j * geo.delta) & geo.col_mask) != b) ok = false;
-    }
-    ok = __all_sync(0xffffffffu, ok);
-    if (ok) {
-      const uint32_t h0 = ((uint32_t)s_row0[0][ip & 0xff] ^ s_row0[1][(ip >> 8) & 0xff] ^
-                           s_row0[2][(ip >> 16) & 0xff] ^ s_row0[3][ip >> 24]) &
-                          geo.col_mask;
-      ok = (h0 == c0);
-    }
-    uint32_t rk = 0;
-    if (ok) {
-      for (uint32_t b = lane; b < geo.eta; b += 32) {
-        uint32_t m = 0xffffffffu;
-        for (uint32_t row = 0; row < geo.r; ++row) {
-          const uint32_t s = stamps[((uint64_t)row << geo.q | cols[row]) * geo.eta + b];
-          m = s < m ? s : m;
-        }
-        rk += m > thr;
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  for (uint64_t base = (uint64_t)blockIdx.x * blockDim.x; base < n; base += stride) {
+    const uint64_t t = base + threadIdx.x;
+    bool ok = false;
+    uint32_t ip = 0;
+    if (t < n) {
+      const uint32_t* cols = tuples + t * geo.r;
+      const uint32_t c0 = cols[0];
+      uint64_t acc = 0;
+      for (uint32_t j = 0; j + 1 < geo.r; ++j) acc |= (uint64_t)(c0 ^ cols[j + 1]) << ((j * geo.delta) & 63u);
+      ip = (uint32_t)acc;
+      ok = true;
+      for (uint32_t j = 0; j + 1 < geo.r; ++j)
+        if ((shr32(ip, j * geo.delta) & geo.col_mask) != (c0 ^ cols[j + 1])) ok = false;
+      if (ok) {
+        const uint32_t h0 = ((uint32_t)s_row0[0][ip & 0xff] ^ s_row0[1][(ip >> 8) & 0xff] ^
+                             s_row0[2][(ip >> 16) & 0xff] ^ s_row0[3][ip >> 24]) &
+                            geo.col_mask;
+        ok = (h0 == c0);
       }
-#pragma unroll
-      for (int o = 16; o; o >>= 1) rk += __shfl_xor_sync(0xffffffffu, rk, o);
-      ok = rk >= cutoff;
     }
-    if (accepted && lane == 0) accepted[t] = ok ? 1 : 0;
-    if (ok && lane == 0) {
-      const unsigned long long pos = atomicAdd(counter, 1ull);
-      out_idx[pos] = (uint32_t)t;
-      out_cip[pos] = ip;
-      out_rk[pos] = rk;
+    const uint64_t pos = warp_reserve(ok ? 1u : 0u, &meta->surv, lane);
+    if (ok) {
+      surv_idx[pos] = (uint32_t)t;
+      surv_cip[pos] = ip;
+    }
+  }
+}
+
+// (2) in-window count of the intersected estimator (max distance == min
+//     stamp over the r rows), spread over CTAs: work item = (survivor, chunk
+//     of 1024 buckets), 16-byte loads, one atomicAdd per CTA.
+//     kmode: 0 -> stamp > thr, 1 -> nothing active (k == 0), 2 -> all (k > 65535).
+__global__ void __launch_bounds__(256) finalize_count_kernel(const uint32_t* __restrict__ tuples,
+                                                             const uint32_t* __restrict__ stamps, Geo geo,
+                                                             uint32_t thr, int kmode,
+                                                             const ReconMeta* __restrict__ meta,
+                                                             const uint32_t* __restrict__ surv_idx,
+                                                             uint32_t* __restrict__ surv_rk) {
+  constexpr uint32_t kChunk = 1024;
+  const uint64_t n_surv = meta->surv;
+  const uint32_t chunks = (geo.eta + kChunk - 1) / kChunk;
+  __shared__ uint32_t s_cols[64];
+  __shared__ uint32_t s_red[8];
+  const bool vec = (geo.eta & 3u) == 0;
+  for (uint64_t item = blockIdx.x; item < n_surv * chunks; item += gridDim.x) {
+    const uint64_t sidx = item / chunks;
+    const uint32_t c0 = (uint32_t)(item % chunks) * kChunk;
+    const uint32_t c1 = min(c0 + kChunk, geo.eta);
+    __syncthreads();
+    if (threadIdx.x < geo.r) s_cols[threadIdx.x] = tuples[(uint64_t)surv_idx[sidx] * geo.r + threadIdx.x];
+    __syncthreads();
+    uint32_t cnt = 0;
+    if (kmode == 0) {
+      if (vec) {
+        for (uint32_t b = c0 + 4 * threadIdx.x; b < c1; b += 4 * blockDim.x) {
+          uint4 m = make_uint4(0xffffffffu, 0xffffffffu, 0xffffffffu, 0xffffffffu);
+          for (uint32_t row = 0; row < geo.r; ++row) {
+            const uint4 v = ld_stream_u4(stamps + ((uint64_t)row << geo.q | s_cols[row]) * geo.eta + b);
+            m.x = min(m.x, v.x);
+            m.y = min(m.y, v.y);
+            m.z = min(m.z, v.z);
+            m.w = min(m.w, v.w);
+          }
+          cnt += (m.x > thr) + (m.y > thr) + (m.z > thr) + (m.w > thr);
+        }
+      } else {
+        for (uint32_t b = c0 + threadIdx.x; b < c1; b += blockDim.x) {
+          uint32_t m = 0xffffffffu;
+          for (uint32_t row = 0; row < geo.r; ++row)
+            m = min(m, stamps[((uint64_t)row << geo.q | s_cols[row]) * geo.eta + b]);
+          cnt += m > thr;
+        }
+      }
+    } else if (kmode == 2) {
+      for (uint32_t b = c0 + threadIdx.x; b < c1; b += blockDim.x) ++cnt;
+    }
+#pragma unroll
+    for (int o = 16; o; o >>= 1) cnt += __shfl_xor_sync(0xffffffffu, cnt, o);
+    if ((threadIdx.x & 31) == 0) s_red[threadIdx.x >> 5] = cnt;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      uint32_t t = 0;
+      for (uint32_t w = 0; w < blockDim.x / 32; ++w) t += s_red[w];
+      if (t) atomicAdd(surv_rk + sidx, t);
     }
   }
 }

@@ -9,6 +9,7 @@
 #include <atomic>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <mutex>
@@ -132,7 +133,13 @@ struct sspd_grid {
   cudaStream_t copy_stream = nullptr;
   cudaEvent_t ev_copy[2] = {nullptr, nullptr}, ev_used[2] = {nullptr, nullptr};
   DevBuf stage[2];       // host pair staging
-  DevBuf counts, hot_cols, hot_rowcnt, hotT, tupA, tupB, fin, misc;
+  DevBuf counts, hot_cols, hot_rowcnt, hotT, tupA, tupB, misc;
+  DevBuf meta, surv;            // reconstruction bookkeeping, survivors
+  ReconMeta* meta_host = nullptr;  // pinned mirror of meta
+  uint64_t cap_alloc = 0;       // tuples per candidate buffer
+  int scan_filter = 1;          // L1 duplicate filter in the scan (SSPD_SCAN_FILTER=0 disables)
+  bool scan_direct = false;     // stamp in place instead of the deferred bitmap (auto by size)
+  bool record_touched = false;  // direct mode: also record the slot's bitmap (multi-router merge)
   void* pinned_small = nullptr;  // 4 KB pinned scratch for counters
   bool profiling = false;
   std::vector<ProfRec> prof;
@@ -226,7 +233,13 @@ sspd_status counts_locked(sspd_grid* g, uint32_t k) {
   if (s) return s;
   if (g->counts.ensure((size_t)g->geo.ncells * 4) != cudaSuccess)
     return fail(SSPD_CUDA_ERROR, "CUDA error: out of memory (counts)");
-  if (g->K && k <= g->K) {
+  if (k == 0 || k > 0xFFFFu) {
+    // distance < 0 never holds; distance < k > 65535 always holds (estimator.hpp:26-31)
+    const unsigned blocks = grid_blocks(g, g->geo.ncells, 256, 4);
+    Prof p(g, "fill", g->geo.ncells);
+    fill_u32_kernel<<<blocks, 256, 0, g->stream>>>(g->counts.as<uint32_t>(), g->geo.ncells,
+                                                   k == 0 ? 0u : g->eta);
+  } else if (g->K && k <= g->K) {
     s = hist_rebuild_locked(g);
     if (s) return s;
     const unsigned blocks = grid_blocks(g, g->geo.ncells, 256, 4);
@@ -249,7 +262,8 @@ uint32_t words_per_key(const sspd_grid* g) {
 
 // Hot compaction into g->hot_cols / hot_rowcnt / hotT (device); row counts
 // copied to host_rowcnt (synchronises).
-sspd_status hot_locked(sspd_grid* g, uint32_t k, uint64_t cutoff, std::vector<uint32_t>& host_rowcnt) {
+sspd_status hot_locked(sspd_grid* g, uint32_t k, uint64_t cutoff, std::vector<uint32_t>* host_rowcnt,
+                       uint32_t* d_rowcnt) {
   sspd_status s = counts_locked(g, k);
   if (s) return s;
   const uint32_t ncol = 1u << g->q;
@@ -258,20 +272,22 @@ sspd_status hot_locked(sspd_grid* g, uint32_t k, uint64_t cutoff, std::vector<ui
   if (g->hot_cols.ensure((size_t)g->r * ncol * 4) != cudaSuccess ||
       g->hot_rowcnt.ensure((size_t)g->r * 4) != cudaSuccess || g->hotT.ensure(t_words * 4) != cudaSuccess)
     return fail(SSPD_CUDA_ERROR, "CUDA error: out of memory (hot sets)");
+  if (!d_rowcnt) d_rowcnt = g->hot_rowcnt.as<uint32_t>();
   CU(cudaMemsetAsync(g->hotT.p, 0, t_words * 4, g->stream));
   {
     Prof p(g, "hot_compact", g->geo.ncells);
     hot_compact_kernel<<<g->r, 1024, 0, g->stream>>>(g->counts.as<uint32_t>(), g->geo, cutoff,
-                                                     g->hot_cols.as<uint32_t>(),
-                                                     g->hot_rowcnt.as<uint32_t>(), g->hotT.as<uint32_t>(),
-                                                     wpk);
+                                                     g->hot_cols.as<uint32_t>(), d_rowcnt,
+                                                     g->hotT.as<uint32_t>(), wpk);
   }
   s = check_launch();
   if (s) return s;
-  host_rowcnt.resize(g->r);
-  CU(cudaMemcpyAsync(host_rowcnt.data(), g->hot_rowcnt.p, g->r * 4, cudaMemcpyDeviceToHost, g->stream));
-  g->d2h_bytes += (g->r * 4);
-  CU(cudaStreamSynchronize(g->stream));
+  if (host_rowcnt) {
+    host_rowcnt->resize(g->r);
+    CU(cudaMemcpyAsync(host_rowcnt->data(), d_rowcnt, g->r * 4, cudaMemcpyDeviceToHost, g->stream));
+    g->d2h_bytes += g->r * 4;
+    CU(cudaStreamSynchronize(g->stream));
+  }
   return SSPD_OK;
 }
 
@@ -283,44 +299,37 @@ double estimate(uint64_t eta, uint64_t r_k) {
   return -deta * std::log(static_cast<double>(z0) / deta);
 }
 
-sspd_status finalize_dev(sspd_grid* g, const uint32_t* d_tuples, uint64_t n, uint32_t k, uint64_t cutoff,
-                         uint8_t* d_accepted, std::vector<uint32_t>* idx, std::vector<uint32_t>* cips,
-                         std::vector<uint32_t>* rks) {
-  // fin buffer: counter (8B) + 3 arrays of n u32
-  const size_t bytes = 256 + (size_t)std::max<uint64_t>(n, 1) * 12;
-  if (g->fin.ensure(bytes) != cudaSuccess) return fail(SSPD_CUDA_ERROR, "CUDA error: out of memory (finalize)");
-  auto* counter = reinterpret_cast<unsigned long long*>(g->fin.p);
-  uint32_t* o_idx = reinterpret_cast<uint32_t*>(static_cast<char*>(g->fin.p) + 256);
-  uint32_t* o_cip = o_idx + n;
-  uint32_t* o_rk = o_cip + n;
-  CU(cudaMemsetAsync(counter, 0, 8, g->stream));
-  if (n) {
-    const unsigned blocks = grid_blocks(g, n * 32, 256, 8);
-    Prof p(g, "finalize", n);
-    finalize_kernel<<<blocks, 256, 0, g->stream>>>(d_tuples, n, g->stamps, g->d_tabs, g->geo, g->now - k,
-                                                   cutoff, o_idx, o_cip, o_rk, counter, d_accepted);
-    sspd_status s = check_launch();
-    if (s) return s;
-  }
-  unsigned long long cnt = 0;
-  CU(cudaMemcpyAsync(&cnt, counter, 8, cudaMemcpyDeviceToHost, g->stream));
-  g->d2h_bytes += (8);
-  CU(cudaStreamSynchronize(g->stream));
-  if (idx) {
-    idx->resize(cnt);
-    cips->resize(cnt);
-    rks->resize(cnt);
-    if (cnt) {
-      CU(cudaMemcpyAsync(idx->data(), o_idx, cnt * 4, cudaMemcpyDeviceToHost, g->stream));
-  g->d2h_bytes += (cnt * 4);
-      CU(cudaMemcpyAsync(cips->data(), o_cip, cnt * 4, cudaMemcpyDeviceToHost, g->stream));
-  g->d2h_bytes += (cnt * 4);
-      CU(cudaMemcpyAsync(rks->data(), o_rk, cnt * 4, cudaMemcpyDeviceToHost, g->stream));
-  g->d2h_bytes += (cnt * 4);
-      CU(cudaStreamSynchronize(g->stream));
-    }
-  }
+int kmode_of(uint32_t k) { return k == 0 ? 1 : (k > 0xFFFFu ? 2 : 0); }
+
+// Survivor buffers for up to n tuples.
+sspd_status ensure_surv(sspd_grid* g, uint64_t n) {
+  if (g->surv.ensure((size_t)std::max<uint64_t>(n, 1) * 12) != cudaSuccess)
+    return fail(SSPD_CUDA_ERROR, "CUDA error: out of memory (finalize)");
   return SSPD_OK;
+}
+
+// Queue finalize_check + finalize_count over the r-tuples in `tuples`, their
+// count taken from meta->level[r-1] (device).
+sspd_status queue_finalize(sspd_grid* g, const uint32_t* tuples, uint64_t in_cap, uint32_t k) {
+  uint32_t* s_idx = g->surv.as<uint32_t>();
+  uint32_t* s_cip = s_idx + in_cap;
+  uint32_t* s_rk = s_cip + in_cap;
+  ReconMeta* meta = g->meta.as<ReconMeta>();
+  {
+    Prof p(g, "finalize_check", in_cap);
+    finalize_check_kernel<<<grid_blocks(g, in_cap, 256, 8), 256, 0, g->stream>>>(tuples, in_cap, g->d_tabs,
+                                                                                   g->geo, meta, s_idx, s_cip);
+  }
+  sspd_status s = check_launch();
+  if (s) return s;
+  CU(cudaMemsetAsync(s_rk, 0, (size_t)std::max<uint64_t>(in_cap, 1) * 4, g->stream));
+  {
+    const uint32_t chunks = (g->eta + 1023) / 1024;
+    Prof p(g, "finalize", in_cap * chunks);
+    finalize_count_kernel<<<(unsigned)sm_count(g->device) * 8, 256, 0, g->stream>>>(
+        tuples, g->stamps, g->geo, g->now - (k <= 0xFFFFu ? k : 0u), kmode_of(k), meta, s_idx, s_rk);
+  }
+  return check_launch();
 }
 
 bool compatible(const sspd_grid* a, const sspd_grid* b) {
@@ -385,6 +394,14 @@ sspd_status sspd_grid_create(int device, uint32_t q, uint32_t r, uint32_t delta,
   g->geo.ncells = r << q;
   g->geo.n_rec = (uint64_t)g->geo.ncells * eta;
   g->by_eta = Div40::make(eta);
+  if (const char* f = std::getenv("SSPD_SCAN_FILTER")) g->scan_filter = std::atoi(f) != 0;
+  // Deferred bitmap by default: measured faster than direct stamping at both
+  // the reference geometry and the full-HBM one (profiles/r01_ab_scan_modes.txt).
+  g->scan_direct = false;
+  if (const char* m = std::getenv("SSPD_SCAN_MODE")) {
+    if (!std::strcmp(m, "bitmap")) g->scan_direct = false;
+    if (!std::strcmp(m, "direct")) g->scan_direct = true;
+  }
   g->n_words = (g->geo.n_rec + 31) / 32;
   auto cleanup = [&](const std::string& why) {
     sspd_grid_destroy(g);
@@ -407,7 +424,10 @@ sspd_status sspd_grid_create(int device, uint32_t q, uint32_t r, uint32_t delta,
     return cleanup("CUDA error: out of memory allocating the touched bitmap");
   }
   if (cudaMalloc(&g->d_tabs, sizeof(HashTabs)) != cudaSuccess) return cleanup("CUDA error: tables");
-  if (cudaMallocHost(&g->pinned_small, 4096) != cudaSuccess) return cleanup("CUDA error: pinned scratch");
+  if (cudaMallocHost(&g->pinned_small, 4096) != cudaSuccess ||
+      cudaMallocHost(&g->meta_host, sizeof(ReconMeta)) != cudaSuccess ||
+      g->meta.ensure(sizeof(ReconMeta)) != cudaSuccess)
+    return cleanup("CUDA error: pinned scratch");
   HashTabs h = make_tabs(seed);
   if (cudaMemcpyAsync(g->d_tabs, &h, sizeof h, cudaMemcpyHostToDevice, g->stream) != cudaSuccess)
     return cleanup("CUDA error: table upload");
@@ -431,8 +451,9 @@ sspd_status sspd_grid_destroy(sspd_grid* g) {
     cudaFree(g->hist);
     cudaFree(g->d_tabs);
     if (g->pinned_small) cudaFreeHost(g->pinned_small);
+    if (g->meta_host) cudaFreeHost(g->meta_host);
     for (DevBuf* b : {&g->stage[0], &g->stage[1], &g->counts, &g->hot_cols, &g->hot_rowcnt, &g->hotT,
-                      &g->tupA, &g->tupB, &g->fin, &g->misc})
+                      &g->tupA, &g->tupB, &g->misc, &g->meta, &g->surv})
       b->release();
     for (auto& r : g->prof) {
       cudaEventDestroy(r.a);
@@ -511,16 +532,42 @@ sspd_status sspd_scan(sspd_grid* g, const uint32_t* pairs, uint64_t n, int pairs
   if (!pairs) return fail(SSPD_INVALID_ARGUMENT, "scan_batch: null pairs");
   std::lock_guard<std::mutex> lk(g->mu);
   DeviceGuard dg(g->device);
-  const bool pow2 = (g->eta & (g->eta - 1)) == 0;
+  const bool pow2 = (g->eta & (g->eta - 1)) == 0 && g->eta <= (1u << 31);
+  const bool direct = g->scan_direct;
+  const bool hist = direct && g->K && g->hist_valid;
+  const bool bits = direct && g->record_touched;
   auto launch = [&](const uint32_t* dp, uint64_t cnt) {
     const unsigned blocks = grid_blocks(g, (cnt + 3) / 4, 256, 8);
     Prof p(g, "scan", cnt);
-    if (pow2)
-      scan_bitmap_kernel<0><<<blocks, 256, 0, g->stream>>>(dp, cnt, g->d_tabs, g->geo, g->touched);
-    else
-      scan_bitmap_kernel<1><<<blocks, 256, 0, g->stream>>>(dp, cnt, g->d_tabs, g->geo, g->touched);
+    const int F = g->scan_filter;
+#define SSPD_DIRECT(H1, FI, HI, BI)                                                                 \
+  scan_direct_kernel<H1, FI, HI, BI><<<blocks, 256, 0, g->stream>>>(dp, cnt, g->d_tabs, g->geo, g->stamps, \
+                                                                    g->now, g->hist, g->K, g->touched)
+    if (!direct) {
+      if (pow2 && F) scan_bitmap_kernel<0, 1><<<blocks, 256, 0, g->stream>>>(dp, cnt, g->d_tabs, g->geo, g->touched);
+      else if (pow2) scan_bitmap_kernel<0, 0><<<blocks, 256, 0, g->stream>>>(dp, cnt, g->d_tabs, g->geo, g->touched);
+      else if (F) scan_bitmap_kernel<1, 1><<<blocks, 256, 0, g->stream>>>(dp, cnt, g->d_tabs, g->geo, g->touched);
+      else scan_bitmap_kernel<1, 0><<<blocks, 256, 0, g->stream>>>(dp, cnt, g->d_tabs, g->geo, g->touched);
+    } else if (pow2) {
+      if (F && hist && bits) SSPD_DIRECT(0, 1, 1, 1);
+      else if (F && hist) SSPD_DIRECT(0, 1, 1, 0);
+      else if (F && bits) SSPD_DIRECT(0, 1, 0, 1);
+      else if (F) SSPD_DIRECT(0, 1, 0, 0);
+      else if (hist && bits) SSPD_DIRECT(0, 0, 1, 1);
+      else if (hist) SSPD_DIRECT(0, 0, 1, 0);
+      else if (bits) SSPD_DIRECT(0, 0, 0, 1);
+      else SSPD_DIRECT(0, 0, 0, 0);
+    } else {
+      if (hist && bits) SSPD_DIRECT(1, 1, 1, 1);
+      else if (hist) SSPD_DIRECT(1, 1, 1, 0);
+      else if (bits) SSPD_DIRECT(1, 1, 0, 1);
+      else SSPD_DIRECT(1, 1, 0, 0);
+    }
+#undef SSPD_DIRECT
   };
-  g->pending = true;
+  // Direct scans stamp in place; only recorded bits (multi-router) or a
+  // stale window ring leave work for the commit.
+  if (!direct || bits) g->pending = true;
   if (pairs_on_device) {
     launch(pairs, n);
     return check_launch();
@@ -631,7 +678,6 @@ sspd_status sspd_put_distances(sspd_grid* g, const uint16_t* host_in, uint64_t o
 }
 
 sspd_status sspd_active_counts(sspd_grid* g, uint32_t k, uint32_t* host_out) {
-  if (k < 1 || k > 65534) return fail(SSPD_OUT_OF_RANGE, "active_count: k must be in [1, 65534]");
   std::lock_guard<std::mutex> lk(g->mu);
   DeviceGuard dg(g->device);
   sspd_status s = counts_locked(g, k);
@@ -643,11 +689,10 @@ sspd_status sspd_active_counts(sspd_grid* g, uint32_t k, uint32_t* host_out) {
 }
 
 sspd_status sspd_hot_sets(sspd_grid* g, uint32_t k, uint64_t cutoff, uint32_t* cols_out, uint32_t* row_counts) {
-  if (k < 1 || k > 65534) return fail(SSPD_OUT_OF_RANGE, "active_count: k must be in [1, 65534]");
   std::lock_guard<std::mutex> lk(g->mu);
   DeviceGuard dg(g->device);
   std::vector<uint32_t> rc;
-  sspd_status s = hot_locked(g, k, cutoff, rc);
+  sspd_status s = hot_locked(g, k, cutoff, &rc, nullptr);
   if (s) return s;
   const uint32_t ncol = 1u << g->q;
   uint64_t pos = 0;
@@ -670,131 +715,148 @@ sspd_status sspd_finalize(sspd_grid* g, const uint32_t* tuples, uint64_t n, uint
   sspd_status s = commit_locked(g);
   if (s) return s;
   if (n == 0) return SSPD_OK;
-  if (g->tupA.ensure(n * g->r * 4) != cudaSuccess || g->misc.ensure(n) != cudaSuccess)
-    return fail(SSPD_CUDA_ERROR, "CUDA error: out of memory (finalize)");
-  CU(cudaMemcpyAsync(g->tupA.p, tuples, n * g->r * 4, cudaMemcpyHostToDevice, g->stream));
-  g->h2d_bytes += (n * g->r * 4);
-  std::vector<uint32_t> idx, c, rk;
-  s = finalize_dev(g, g->tupA.as<uint32_t>(), n, k, cutoff, g->misc.as<uint8_t>(), &idx, &c, &rk);
+  if (g->tupA.ensure(n * g->r * 4) != cudaSuccess) return fail(SSPD_CUDA_ERROR, "CUDA error: out of memory");
+  s = ensure_surv(g, n);
   if (s) return s;
-  CU(cudaMemcpyAsync(accepted, g->misc.p, n, cudaMemcpyDeviceToHost, g->stream));
-  g->d2h_bytes += (n);
+  CU(cudaMemcpyAsync(g->tupA.p, tuples, n * g->r * 4, cudaMemcpyHostToDevice, g->stream));
+  g->h2d_bytes += n * g->r * 4;
+  std::memset(g->meta_host, 0, sizeof(ReconMeta));
+  g->meta_host->level[g->r - 1] = n;
+  CU(cudaMemcpyAsync(g->meta.p, g->meta_host, sizeof(ReconMeta), cudaMemcpyHostToDevice, g->stream));
+  s = queue_finalize(g, g->tupA.as<uint32_t>(), n, k);
+  if (s) return s;
+  CU(cudaMemcpyAsync(g->meta_host, g->meta.p, sizeof(ReconMeta), cudaMemcpyDeviceToHost, g->stream));
   CU(cudaStreamSynchronize(g->stream));
-  for (size_t i = 0; i < idx.size(); ++i) {
-    cips[idx[i]] = c[i];
-    r_ks[idx[i]] = rk[i];
+  const uint64_t ns = g->meta_host->surv;
+  std::vector<uint32_t> buf(ns * 3 + 1);
+  const uint32_t* s_idx = g->surv.as<uint32_t>();
+  if (ns) {
+    CU(cudaMemcpyAsync(buf.data(), s_idx, ns * 4, cudaMemcpyDeviceToHost, g->stream));
+    CU(cudaMemcpyAsync(buf.data() + ns, s_idx + n, ns * 4, cudaMemcpyDeviceToHost, g->stream));
+    CU(cudaMemcpyAsync(buf.data() + 2 * ns, s_idx + 2 * n, ns * 4, cudaMemcpyDeviceToHost, g->stream));
+    CU(cudaStreamSynchronize(g->stream));
+  }
+  g->d2h_bytes += sizeof(ReconMeta) + ns * 12;
+  std::memset(accepted, 0, n);
+  for (uint64_t i = 0; i < ns; ++i) {
+    const uint32_t t = buf[i], rk = buf[2 * ns + i];
+    if (rk >= cutoff) {
+      accepted[t] = 1;
+      cips[t] = buf[ns + i];
+      r_ks[t] = rk;
+    }
   }
   return SSPD_OK;
 }
 
 sspd_status sspd_reconstruct(sspd_grid* g, uint32_t k, uint64_t cutoff, uint64_t cap, sspd_detection* out,
                              uint64_t out_cap, uint64_t* n_out, uint32_t* ovf_level, uint64_t* ovf_count) {
-  if (k < 1 || k > 65534) return fail(SSPD_OUT_OF_RANGE, "active_count: k must be in [1, 65534]");
   std::lock_guard<std::mutex> lk(g->mu);
   DeviceGuard dg(g->device);
   *n_out = 0;
-  std::vector<uint32_t> rc;
-  sspd_status s = hot_locked(g, k, cutoff, rc);
-  if (s) return s;
-  for (uint32_t row = 0; row < g->r; ++row)
-    if (rc[row] == 0) return SSPD_OK;  // rsea.cpp:173-174
+  if (g->r > 64) return fail(SSPD_INVALID_ARGUMENT, "reconstruct: r > 64 unsupported");
   const uint32_t ncol = 1u << g->q;
   const uint32_t wpk = words_per_key(g);
   const uint64_t t_stride = (uint64_t)wpk << (g->q - g->delta);
-  const uint32_t* cols = g->hot_cols.as<uint32_t>();
-  const uint32_t* T = g->hotT.as<uint32_t>();
-  auto* counter = static_cast<unsigned long long*>(g->pinned_small);  // host copy target
-  unsigned long long* d_counter = nullptr;
-  if (g->fin.ensure(256) != cudaSuccess) return fail(SSPD_CUDA_ERROR, "CUDA error: out of memory");
-  // a dedicated 8-byte device counter lives at the end of the misc buffer
-  if (g->misc.ensure(std::max<size_t>(g->misc.bytes, 64)) != cudaSuccess)
-    return fail(SSPD_CUDA_ERROR, "CUDA error: out of memory");
-  d_counter = reinterpret_cast<unsigned long long*>(g->misc.p);
-
-  // Run one level with growing output capacity; returns survivor count.
-  auto run_level = [&](uint32_t m_out, auto&& launch, DevBuf& dst, uint64_t& count) -> sspd_status {
-    uint64_t cap_tuples = std::min<uint64_t>(std::max<uint64_t>(dst.bytes / (m_out * 4), 1u << 16), cap);
-    for (int attempt = 0; attempt < 2; ++attempt) {
-      if (dst.ensure(std::max<uint64_t>(cap_tuples, 1) * m_out * 4) != cudaSuccess)
-        return fail(SSPD_CUDA_ERROR, "CUDA error: out of memory (candidate buffer)");
-      CU(cudaMemsetAsync(d_counter, 0, 8, g->stream));
-      launch(dst.as<uint32_t>(), cap_tuples);
-      sspd_status e = check_launch();
-      if (e) return e;
-      CU(cudaMemcpyAsync(counter, d_counter, 8, cudaMemcpyDeviceToHost, g->stream));
-  g->d2h_bytes += (8);
+  ReconMeta* meta = g->meta.as<ReconMeta>();
+  ReconMeta* mh = g->meta_host;
+  if (g->cap_alloc == 0) g->cap_alloc = std::min<uint64_t>(cap, 1u << 20);
+  // Everything below is queued without host round trips; one synchronisation
+  // at the end reads the row counts, per-level counts and survivors.
+  for (int attempt = 0;; ++attempt) {
+    const uint64_t C = std::max<uint64_t>(g->cap_alloc, 1);
+    if (g->tupA.ensure(C * g->r * 4) != cudaSuccess || g->tupB.ensure(C * g->r * 4) != cudaSuccess)
+      return fail(SSPD_CUDA_ERROR, "CUDA error: out of memory (candidate buffer)");
+    sspd_status s = ensure_surv(g, C);
+    if (s) return s;
+    CU(cudaMemsetAsync(meta, 0, sizeof(ReconMeta), g->stream));
+    s = hot_locked(g, k, cutoff, nullptr, meta->rowcnt);
+    if (s) return s;
+    const uint32_t* cols = g->hot_cols.as<uint32_t>();
+    const uint32_t* T = g->hotT.as<uint32_t>();
+    const unsigned blocks = (unsigned)sm_count(g->device) * 8;
+    {
+      Prof p(g, "level2", 0);
+      level2_kernel<<<blocks, 256, 0, g->stream>>>(cols, ncol, T + 2 * t_stride, wpk, g->geo, g->tupA.as<uint32_t>(),
+                                                   C, meta);
+    }
+    s = check_launch();
+    if (s) return s;
+    DevBuf* rd = &g->tupA;
+    DevBuf* wr = &g->tupB;
+    for (uint32_t row = 3; row < g->r; ++row) {
+      {
+        Prof p(g, "level_ext", 0);
+        level_ext_kernel<<<blocks, 256, 0, g->stream>>>(rd->as<uint32_t>(), C, row, T + (uint64_t)row * t_stride,
+                                                        wpk, g->geo, wr->as<uint32_t>(), C, meta);
+      }
+      s = check_launch();
+      if (s) return s;
+      std::swap(rd, wr);
+    }
+    s = queue_finalize(g, rd->as<uint32_t>(), C, k);
+    if (s) return s;
+    // Survivors are few (true super points plus hash-consistent impostors):
+    // copy a fixed prefix in the same batch.
+    const uint64_t pre = std::min<uint64_t>(C, 4096);
+    uint32_t* s_idx = g->surv.as<uint32_t>();
+    uint32_t* hbuf = static_cast<uint32_t*>(g->pinned_small);  // 4 KB: 2 x 512 entries
+    const uint64_t pre_small = std::min<uint64_t>(pre, 512);
+    CU(cudaMemcpyAsync(mh, meta, sizeof(ReconMeta), cudaMemcpyDeviceToHost, g->stream));
+    CU(cudaMemcpyAsync(hbuf, s_idx + C, pre_small * 4, cudaMemcpyDeviceToHost, g->stream));
+    CU(cudaMemcpyAsync(hbuf + 512, s_idx + 2 * C, pre_small * 4, cudaMemcpyDeviceToHost, g->stream));
+    CU(cudaStreamSynchronize(g->stream));
+    g->d2h_bytes += sizeof(ReconMeta) + pre_small * 8;
+    for (uint32_t row = 0; row < g->r; ++row)
+      if (mh->rowcnt[row] == 0) return SSPD_OK;  // rsea.cpp:173-174
+    // Overflow is decided level by level, as the reference does (rsea.cpp:206-216);
+    // a level whose count exceeds our buffer but not the cap forces a re-run.
+    uint64_t need = 0;
+    bool truncated = false;
+    for (uint32_t lvl = 2; lvl < g->r && !truncated; ++lvl) {
+      const uint64_t cnt = mh->level[lvl];
+      if (cnt > cap) {
+        *ovf_level = lvl;
+        *ovf_count = cnt;
+        return fail(SSPD_CANDIDATE_OVERFLOW, "candidate buffer cap exceeded at level " + std::to_string(lvl) +
+                                                 ": " + std::to_string(cnt) + " tuples, cap " + std::to_string(cap));
+      }
+      if (cnt > C) {
+        need = cnt;
+        truncated = true;
+      }
+    }
+    if (truncated) {
+      g->cap_alloc = need;
+      if (attempt > 8) return fail(SSPD_CUDA_ERROR, "reconstruct: candidate buffer did not converge");
+      continue;
+    }
+    const uint64_t ns = mh->surv;
+    std::vector<uint32_t> cip(ns), rk(ns);
+    if (ns <= pre_small) {
+      std::memcpy(cip.data(), hbuf, ns * 4);
+      std::memcpy(rk.data(), hbuf + 512, ns * 4);
+    } else {
+      CU(cudaMemcpyAsync(cip.data(), s_idx + C, ns * 4, cudaMemcpyDeviceToHost, g->stream));
+      CU(cudaMemcpyAsync(rk.data(), s_idx + 2 * C, ns * 4, cudaMemcpyDeviceToHost, g->stream));
       CU(cudaStreamSynchronize(g->stream));
-      count = *counter;
-      if (count <= cap_tuples || count > cap) return SSPD_OK;
-      cap_tuples = count;  // grow and recompute (count <= cap here)
+      g->d2h_bytes += ns * 8;
+    }
+    // dedup_report (rsea.cpp:112-122): by cip, larger estimate kept, sorted by cip.
+    std::map<uint32_t, uint32_t> best;
+    for (uint64_t i = 0; i < ns; ++i) {
+      if (rk[i] < cutoff) continue;
+      auto it = best.emplace(cip[i], rk[i]);
+      if (!it.second && rk[i] > it.first->second) it.first->second = rk[i];
+    }
+    *n_out = best.size();
+    uint64_t w = 0;
+    for (const auto& [c, r_k] : best) {
+      if (w < out_cap) out[w] = sspd_detection{c, r_k, estimate(g->eta, r_k)};
+      ++w;
     }
     return SSPD_OK;
-  };
-
-  // Level 2 (rsea.cpp:179-201).
-  uint64_t n_t = 0;
-  {
-    const uint64_t pairs = (uint64_t)rc[0] * rc[1];
-    s = run_level(
-        3,
-        [&](uint32_t* dst, uint64_t dcap) {
-          const unsigned blocks = grid_blocks(g, pairs, 256, 8);
-          Prof p(g, "level2", pairs);
-          level2_kernel<<<blocks, 256, 0, g->stream>>>(cols, rc[0], cols + ncol, rc[1], T + 2 * t_stride, wpk,
-                                                       g->geo, dst, dcap, d_counter);
-        },
-        g->tupA, n_t);
-    if (s) return s;
-    if (n_t > cap) {
-      *ovf_level = 2;
-      *ovf_count = n_t;
-      return fail(SSPD_CANDIDATE_OVERFLOW, "candidate buffer cap exceeded at level 2: " + std::to_string(n_t) +
-                                               " tuples, cap " + std::to_string(cap));
-    }
   }
-  DevBuf* rd = &g->tupA;
-  DevBuf* wr = &g->tupB;
-  for (uint32_t row = 3; row < g->r; ++row) {
-    const uint32_t m = row;  // tuple length before extension
-    uint64_t n_next = 0;
-    const uint32_t* in = rd->as<uint32_t>();
-    const uint64_t n_in = n_t;
-    s = run_level(
-        m + 1,
-        [&](uint32_t* dst, uint64_t dcap) {
-          if (!n_in) return;
-          const unsigned blocks = grid_blocks(g, n_in, 256, 8);
-          Prof p(g, "level_ext", n_in);
-          level_ext_kernel<<<blocks, 256, 0, g->stream>>>(in, n_in, m, T + (uint64_t)row * t_stride, wpk, g->geo,
-                                                          dst, dcap, d_counter);
-        },
-        *wr, n_next);
-    if (s) return s;
-    if (n_next > cap) {
-      *ovf_level = row;
-      *ovf_count = n_next;
-      return fail(SSPD_CANDIDATE_OVERFLOW, "candidate buffer cap exceeded at level " + std::to_string(row) + ": " +
-                                               std::to_string(n_next) + " tuples, cap " + std::to_string(cap));
-    }
-    n_t = n_next;
-    std::swap(rd, wr);
-  }
-  // Finalization + dedup (rsea.cpp:239-254, 112-122).
-  std::vector<uint32_t> idx, cip, rk;
-  s = finalize_dev(g, rd->as<uint32_t>(), n_t, k, cutoff, nullptr, &idx, &cip, &rk);
-  if (s) return s;
-  std::map<uint32_t, uint32_t> best;  // cip -> max r_k (estimate is monotone in r_k)
-  for (size_t i = 0; i < cip.size(); ++i) {
-    auto it = best.emplace(cip[i], rk[i]);
-    if (!it.second && rk[i] > it.first->second) it.first->second = rk[i];
-  }
-  *n_out = best.size();
-  uint64_t w = 0;
-  for (const auto& [c, r_k] : best) {
-    if (w < out_cap) out[w] = sspd_detection{c, r_k, estimate(g->eta, r_k)};
-    ++w;
-  }
-  return SSPD_OK;
 }
 
 sspd_status sspd_merge(const sspd_grid* const* grids_c, uint64_t n, int policy, sspd_grid* out) {
@@ -923,6 +985,23 @@ sspd_status sspd_grid_stamps(sspd_grid* g, uint32_t** dev_stamps, uint64_t* word
   // the caller may rewrite stamps (e.g. an in-place NCCL max); the ring is
   // rebuilt from them on next use
   g->hist_valid = false;
+  return SSPD_OK;
+}
+
+sspd_status sspd_set_exchange(sspd_grid* g, int on) {
+  std::lock_guard<std::mutex> lk(g->mu);
+  g->record_touched = on != 0;
+  return SSPD_OK;
+}
+
+sspd_status sspd_scan_mode(sspd_grid* g, int mode, int filter) {
+  std::lock_guard<std::mutex> lk(g->mu);
+  DeviceGuard dg(g->device);
+  sspd_status s = commit_locked(g);
+  if (s) return s;
+  if (mode == 0) g->scan_direct = false;
+  if (mode == 1) g->scan_direct = true;
+  if (filter >= 0) g->scan_filter = filter != 0;
   return SSPD_OK;
 }
 

@@ -23,36 +23,29 @@ import torch.distributed as dist
 def or_allreduce_(t: torch.Tensor, group=None) -> torch.Tensor:
     """In-place bitwise-OR all-reduce of an int32 tensor (NCCL has no OR op).
 
-    NCCL: reduce-scatter by all_to_all + local OR, then all-gather -- the
-    2(N-1)/N volume of a ring all-reduce.  gloo (CPU tests): all_gather + OR.
+    Reduce-scatter by all_to_all + a local OR of the received chunks, then
+    all-gather: the 2(N-1)/N per-rank volume of a ring all-reduce.  The same
+    code runs on NCCL (GPU) and gloo (the CPU tests).
     """
     world = dist.get_world_size(group)
     if world == 1:
         return t
     flat = t.view(-1)
-    if dist.get_backend(group) == "nccl":
-        n = flat.numel()
-        per = (n + world - 1) // world
-        padded = flat
-        if per * world != n:
-            padded = torch.zeros(per * world, dtype=flat.dtype, device=flat.device)
-            padded[:n].copy_(flat)
-        recv = torch.empty_like(padded)
-        dist.all_to_all_single(recv, padded, group=group)
-        chunks = recv.view(world, per)
-        mine = chunks[0].clone()
-        for i in range(1, world):
-            mine.bitwise_or_(chunks[i])
-        out = torch.empty_like(padded)
-        dist.all_gather_into_tensor(out, mine, group=group)
-        flat.copy_(out[:n])
-    else:
-        parts = [torch.empty_like(flat) for _ in range(world)]
-        dist.all_gather(parts, flat, group=group)
-        acc = parts[0].clone()
-        for p in parts[1:]:
-            acc.bitwise_or_(p)
-        flat.copy_(acc)
+    n = flat.numel()
+    per = (n + world - 1) // world
+    padded = flat
+    if per * world != n:
+        padded = torch.zeros(per * world, dtype=flat.dtype, device=flat.device)
+        padded[:n].copy_(flat)
+    recv = torch.empty_like(padded)
+    dist.all_to_all_single(recv, padded, group=group)
+    chunks = recv.view(world, per)
+    mine = chunks[0].clone()
+    for i in range(1, world):
+        mine.bitwise_or_(chunks[i])
+    out = torch.empty_like(padded)
+    dist.all_gather_into_tensor(out, mine, group=group)
+    flat.copy_(out[:n])
     return t
 
 
@@ -67,6 +60,11 @@ class _CudaArray:
 def device_view(ptr: int, n_words: int, device: int) -> torch.Tensor:
     with torch.cuda.device(device):
         return torch.as_tensor(_CudaArray(ptr, n_words), device=f"cuda:{device}")
+
+
+def prepare(grid):
+    """Make the grid record each slot's touched bitmap (needed in direct mode)."""
+    grid.set_exchange(True)
 
 
 def merge_touched(grid, group=None):

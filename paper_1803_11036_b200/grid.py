@@ -232,6 +232,13 @@ class Grid:
         check(self._L.sspd_grid_touched(self._h, C.byref(p), C.byref(n)))
         return p.value, n.value
 
+    def set_exchange(self, on: bool = True):
+        check(self._L.sspd_set_exchange(self._h, int(on)))
+
+    def scan_mode(self, mode: int = -1, filter: int = -1):
+        """mode 0 = deferred bitmap, 1 = direct; filter 0/1 (-1 keeps)."""
+        check(self._L.sspd_scan_mode(self._h, mode, filter))
+
     def commit(self):
         check(self._L.sspd_commit(self._h))
 

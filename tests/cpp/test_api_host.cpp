@@ -1,0 +1,264 @@
+// Host-only parts of the drop-in C++ API (no GPU needed): hashing, estimator
+// helpers, the work split and the workload utilities.  Cases follow the
+// reference suites (proj/tests/test_hashing.cpp, test_estimator.cpp,
+// test_workload.cpp, acceptance.cpp:353-383); with HAVE_REF the synthetic
+// generator is also checked record-for-record against the compiled reference.
+#include <cmath>
+#include <random>
+#include <set>
+#include <sstream>
+
+#include "check.hpp"
+#include "sspd/estimator.hpp"
+#include "sspd/hashing.hpp"
+#include "sspd/split.hpp"
+#include "sspd/workload.hpp"
+#ifdef HAVE_REF
+#include "ref_abi.hpp"
+#endif
+
+using namespace sspd;
+
+namespace {
+const RhfgConfig kPaper{14, 5, 6, 0x1234abcdULL};
+const RhfgConfig kDesk{10, 5, 8, 0x1234abcdULL};
+uint32_t slice(uint32_t cip, uint32_t i, const RhfgConfig& c) {
+  return (cip >> ((i - 1) * c.delta)) & c.column_mask();
+}
+}  // namespace
+
+TEST_CASE("survey anchors of the reference hashing") {
+  HashSeeds s(0x5eed);
+  CHECK(s.h1_raw(0x08080808) == 0x48d9a5b7829ca305ULL);
+  CHECK(s.row0_raw(0xC0A80101) == 0x3a77151ffcf0dfdbULL);
+  CHECK(hash_opposite(s, 0x08080808, 2048) == 773);
+  CHECK(hash_opposite(s, 0x08080808, 256) == 5);
+  const RhfgConfig c{14, 5, 6, 0x5eed};
+  const uint32_t want[5] = {8155, 7898, 16351, 5467, 12273};
+  for (uint32_t i = 0; i < 5; ++i) CHECK(rhfg(s, i, 0xC0A80101, c) == want[i]);
+}
+
+TEST_CASE("hash_opposite determinism and eta=1") {
+  HashSeeds a(42), b(42), c(43);
+  CHECK(hash_opposite(a, 0xdeadbeef, 1) == 0);
+  CHECK(hash_opposite(a, 12345, 2048) == hash_opposite(b, 12345, 2048));
+  bool diff = false;
+  for (uint32_t x = 0; x < 64; ++x) diff |= hash_opposite(a, x, 2048) != hash_opposite(c, x, 2048);
+  CHECK(diff);
+}
+
+TEST_CASE("rhfg rows, recover_block, blocks_consistent") {
+  HashSeeds s(kPaper.seed);
+  const uint32_t c0 = rhfg(s, 0, 0, kPaper);
+  for (uint32_t i = 1; i < kPaper.r; ++i) CHECK(rhfg(s, i, 0, kPaper) == c0);
+  CHECK(rhfg(s, 1, 0xffffffff, kPaper) == ((0x3fffu ^ rhfg(s, 0, 0xffffffff, kPaper)) & 0x3fff));
+  CHECK_THROWS_AS(rhfg(s, kPaper.r, 1, kPaper), std::out_of_range);
+  std::mt19937_64 rng(5);
+  for (const RhfgConfig& cfg : {kPaper, kDesk}) {
+    HashSeeds hs(cfg.seed);
+    for (int t = 0; t < 20000; ++t) {
+      const uint32_t cip = static_cast<uint32_t>(rng());
+      const uint32_t col0 = rhfg(hs, 0, cip, cfg);
+      for (uint32_t i = 1; i < cfg.r; ++i) REQUIRE(recover_block(col0, rhfg(hs, i, cip, cfg)) == slice(cip, i, cfg));
+    }
+  }
+  CHECK(blocks_consistent(0, 0, kPaper));
+  CHECK_FALSE(blocks_consistent(0x3f00, 0x0001, kPaper));
+}
+
+TEST_CASE("assemble_ip round trips and rejections") {
+  std::vector<uint32_t> zeros(kPaper.r - 1, 0);
+  CHECK(assemble_ip(zeros, kPaper) == 0u);
+  std::mt19937_64 rng(7);
+  for (const RhfgConfig& cfg : {kPaper, kDesk}) {
+    HashSeeds hs(cfg.seed);
+    for (int t = 0; t < 20000; ++t) {
+      const uint32_t cip = static_cast<uint32_t>(rng());
+      std::vector<uint32_t> b;
+      const uint32_t col0 = rhfg(hs, 0, cip, cfg);
+      for (uint32_t i = 1; i < cfg.r; ++i) b.push_back(recover_block(col0, rhfg(hs, i, cip, cfg)));
+      REQUIRE(assemble_ip(b, cfg) == cip);
+    }
+  }
+  std::vector<uint32_t> blocks(kDesk.r - 1, 0);
+  blocks.back() = 1u << (kDesk.q - 1);
+  CHECK_FALSE(assemble_ip(blocks, kDesk).has_value());
+  CHECK_THROWS_AS(assemble_ip(std::vector<uint32_t>(2, 0), kDesk), std::invalid_argument);
+}
+
+TEST_CASE("validate_config diagnostics") {
+  CHECK(validate_config(RhfgConfig{14, 5, 6, 0}, 2048, 300, 1024).empty());
+  auto p = validate_config(RhfgConfig{8, 5, 6, 0}, 2048, 300, 1024);
+  REQUIRE(!p.empty());
+  CHECK(p.front().find("coverage") != std::string::npos);
+  CHECK(validate_config(RhfgConfig{17, 5, 6, 0}, 2048, 300, 1024).front() == "q must be in [1, 16], got 17");
+  CHECK(validate_config(RhfgConfig{14, 5, 6, 0}, 1, 300, 1024).front() == "eta must be >= 2, got 1");
+  CHECK(validate_config(RhfgConfig{14, 5, 6, 0}, 2048, 0, 1024).front() == "k must be in [1, 65534], got 0");
+}
+
+TEST_CASE("estimator helpers") {
+  SlidingEstimator se(8);
+  for (Recorder v : se.recorders()) CHECK(v == kNeverSeen);
+  se.touch(3);
+  CHECK(se.recorders()[3] == 0);
+  se.advance();
+  CHECK(se.recorders()[3] == 1);
+  CHECK(se.active_count(1) == 0);
+  CHECK(se.active_count(2) == 1);
+  CHECK_THROWS_AS(se.active_count(0), std::out_of_range);
+  CHECK_THROWS_AS(se.touch(8), std::out_of_range);
+  CHECK_THROWS_AS(SlidingEstimator(1), std::invalid_argument);
+  SlidingEstimator sat(2);
+  sat.touch(0);
+  for (int i = 0; i < 65534; ++i) sat.advance();
+  CHECK(sat.recorders()[0] == 65534);
+  sat.advance();
+  CHECK(sat.recorders()[0] == 65535);
+  CHECK(hot_cutoff(2048, 1024) == 806);
+  CHECK(hot_cutoff(256, 128) == 101);
+  CHECK(std::fabs(estimate_cardinality(2048, 806) - 1024.0) < 1.0);
+  CHECK(estimate_cardinality(2048, 2048) == 2048.0 * std::log(2048.0));
+  SlidingEstimator a(4), b(4);
+  a.touch(0);
+  b.touch(1);
+  b.touch(0);
+  b.advance();
+  CHECK(merge_min({a, b}).recorders()[0] == 0);
+  CHECK(intersect_max({a, b}).recorders()[0] == 1);
+  CHECK(intersect_max({a, b}).recorders()[1] == kNeverSeen);
+  CHECK_THROWS_AS(merge_min({}), std::invalid_argument);
+  CHECK_THROWS_AS(merge_min({SlidingEstimator(4), SlidingEstimator(5)}), std::invalid_argument);
+}
+
+TEST_CASE("worker_ranges U/V/W split") {
+  const auto r = worker_ranges(10, 4);
+  REQUIRE(r.size() == 4);
+  CHECK((r[0] == std::pair<std::size_t, std::size_t>{0, 3}));
+  CHECK((r[1] == std::pair<std::size_t, std::size_t>{3, 6}));
+  CHECK((r[2] == std::pair<std::size_t, std::size_t>{6, 8}));
+  CHECK((r[3] == std::pair<std::size_t, std::size_t>{8, 10}));
+  CHECK(worker_ranges(5, 0).empty());
+  std::mt19937_64 rng(110);
+  for (int t = 0; t < 50; ++t) {
+    const std::size_t q = rng() % 100000;
+    const unsigned v = 1 + rng() % 64;
+    const auto rr = worker_ranges(q, v);
+    std::size_t lo = 0;
+    for (unsigned i = 0; i < v; ++i) {
+      CHECK(rr[i].first == lo);
+      CHECK(rr[i].second - rr[i].first == q / v + (i < q % v ? 1 : 0));
+      lo = rr[i].second;
+    }
+    CHECK(lo == q);
+  }
+}
+
+TEST_CASE("ipv4 parsing and formatting") {
+  CHECK(parse_ipv4("192.168.1.1") == 0xC0A80101u);
+  CHECK(parse_ipv4("3232235777") == 0xC0A80101u);
+  CHECK(format_ipv4(0xC0A80101u) == "192.168.1.1");
+  CHECK_THROWS_AS(parse_ipv4("1.2.3"), std::invalid_argument);
+  CHECK_THROWS_AS(parse_ipv4("1.2.3.256"), std::invalid_argument);
+  CHECK_THROWS_AS(parse_ipv4("4294967296"), std::invalid_argument);
+}
+
+TEST_CASE("trace I/O round trips and errors") {
+  std::vector<TraceRecord> recs{{0, 1, 2}, {0, 0xC0A80101u, 0x08080808u}, {5, 7, 9}};
+  for (TraceFormat f : {TraceFormat::kBinary, TraceFormat::kText}) {
+    std::stringstream ss;
+    write_trace(recs, ss, f);
+    CHECK(read_trace(ss, f) == recs);
+  }
+  std::stringstream empty;
+  CHECK(read_trace(empty, TraceFormat::kBinary).empty());
+  std::stringstream bad("XXXX\x01\0\0\0", std::ios::in | std::ios::binary);
+  CHECK_THROWS_WITH_SUBSTR(read_trace(bad, TraceFormat::kBinary), "bad magic");
+  std::stringstream regress("5,1.2.3.4,5.6.7.8\n4,1.2.3.4,5.6.7.8\n");
+  CHECK_THROWS_WITH_SUBSTR(read_trace(regress, TraceFormat::kText), "timestamp regression at record 1");
+  std::stringstream malformed("1,2\n");
+  CHECK_THROWS_WITH_SUBSTR(read_trace(malformed, TraceFormat::kText), "malformed line 1");
+  std::stringstream trunc;
+  write_trace(recs, trunc, TraceFormat::kBinary);
+  std::string t = trunc.str();
+  t.pop_back();
+  std::stringstream tr(t);
+  CHECK_THROWS_WITH_SUBSTR(read_trace(tr, TraceFormat::kBinary), "truncated record at position 2");
+}
+
+TEST_CASE("orientation by core-network prefixes") {
+  CnetSpec cnet({"10.0.0.0/8", "192.168.0.0/16"});
+  CHECK(cnet.contains(0x0A010203));
+  CHECK_FALSE(cnet.contains(0x0B000000));
+  auto o = orient_pair(0x08080808, 0x0A000001, cnet);
+  REQUIRE(o.has_value());
+  CHECK(o->first == 0x0A000001u);
+  CHECK_FALSE(orient_pair(0x0A000001, 0x0A000002, cnet).has_value());
+  CHECK_THROWS_AS(CnetSpec({}), std::invalid_argument);
+  CHECK_THROWS_AS(CnetSpec({"10.0.0.0"}), std::invalid_argument);
+}
+
+TEST_CASE("exact counts and synthetic truth") {
+  WindowConfig win;
+  win.k = 3;
+  SynthSpec spec;
+  spec.slots = 6;
+  spec.planted.push_back({0x0A000001, 50, 1, 3});
+  spec.background_hosts = 100;
+  spec.pairs_per_slot = 300;
+  spec.max_distinct_per_host = 8;
+  const SynthResult res = synth_trace(spec, 9, win);
+  const GroundTruth gt = exact_counts(res.trace, win);
+  REQUIRE(gt.slots.size() == res.truth.slots.size());
+  for (std::size_t s = 0; s < gt.slots.size(); ++s) CHECK(gt.slots[s] == res.truth.slots[s]);
+  CHECK(gt.slots[1].at(0x0A000001) == 50);
+  CHECK(gt.slots[5].at(0x0A000001) == 50);  // window 3..5 still holds slot 3
+  SynthSpec none;
+  none.slots = 0;
+  CHECK_THROWS_AS(synth_trace(none, 1, win), std::invalid_argument);
+  std::istringstream in("slots 4\nbackground hosts=10 pairs-per-slot=5\nsuper cip=10.0.0.1 count=7 from=1 to=2\n");
+  const SynthSpec p = parse_synth_spec(in);
+  CHECK(p.slots == 4);
+  CHECK(p.background_hosts == 10);
+  REQUIRE(p.planted.size() == 1);
+  CHECK(p.planted[0].count == 7);
+  std::istringstream bad("bogus\n");
+  CHECK_THROWS_WITH_SUBSTR(parse_synth_spec(bad), "synth spec line 1: unknown stanza: bogus");
+}
+
+TEST_CASE("evaluate normalises by true super points") {
+  std::unordered_map<uint32_t, uint32_t> truth{{1, 10}, {2, 3}, {3, 20}};
+  auto r = evaluate({1, 2}, truth, 10);
+  CHECK(r.fpr == 0.5);
+  CHECK(r.fnr == 0.5);
+  CHECK(r.tfr == 1.0);
+  auto d = evaluate({5}, {{1, 1}}, 10);
+  CHECK(d.degenerate);
+  CHECK(d.fpr == 1.0);
+}
+
+#ifdef HAVE_REF
+TEST_CASE("synth_trace equals the reference generator record for record") {
+  for (uint64_t seed : {77ull, 104ull, 107ull}) {
+    SynthSpec spec;
+    spec.slots = 5;
+    for (uint32_t i = 0; i < 3; ++i) spec.planted.push_back({0x0A000000 + i, 200, 0, 4});
+    spec.background_hosts = 500;
+    spec.pairs_per_slot = 700;
+    spec.max_distinct_per_host = 8;
+    WindowConfig win;
+    win.k = 5;
+    const auto ours = synth_trace(spec, seed, win).trace;
+    std::vector<uint32_t> planted;
+    for (const auto& p : spec.planted) planted.insert(planted.end(), {p.cip, p.count, p.slot_lo, p.slot_hi});
+    const size_t n = ref_synth_trace(planted.data(), spec.planted.size(), 500, 1.1, 700, 8, 5, seed, 1.0, 5, 0,
+                                     nullptr, 0);
+    std::vector<uint32_t> recs(3 * n);
+    ref_synth_trace(planted.data(), spec.planted.size(), 500, 1.1, 700, 8, 5, seed, 1.0, 5, 0, recs.data(), n);
+    REQUIRE(ours.size() == n);
+    for (size_t i = 0; i < n; ++i)
+      REQUIRE((ours[i] == TraceRecord{recs[3 * i], recs[3 * i + 1], recs[3 * i + 2]}));
+  }
+}
+#endif
+
+CHECK_MAIN

@@ -30,9 +30,15 @@ def dets_equal(a, b):
     return [(d.cip, d.estimate) for d in a] == [(d.cip, d.estimate) for d in b]
 
 
+MODES = [(0, 1), (0, 0), (1, 1), (1, 0)]  # (direct, filter)
+MODE_IDS = ["bitmap+filter", "bitmap", "direct+filter", "direct"]
+
+
+@pytest.mark.parametrize("mode", MODES, ids=MODE_IDS)
 @pytest.mark.parametrize("geo", [DESK, PAPER, ODD, WIDE], ids=["desk", "paper", "odd_eta", "wide_r"])
-def test_scan_advance_bit_exact(gpu, geo):
+def test_scan_advance_bit_exact(gpu, geo, mode):
     g, o = make_pair(gpu, geo, 0x5eed)
+    g.scan_mode(*mode)
     rng = O.Mt64(7)
     for step in range(4):
         p = rng.pairs(50_000 if geo is not PAPER else 100_000)
@@ -271,9 +277,11 @@ def test_cells_roundtrip_and_import(gpu):
     assert np.array_equal(h.active_counts(8), o.active_counts(8))
 
 
-def test_window_tracking_matches_full_count(gpu):
+@pytest.mark.parametrize("mode", MODES, ids=MODE_IDS)
+def test_window_tracking_matches_full_count(gpu, mode):
     """The incremental in-window ring gives the same counts and reports."""
     g, o = make_pair(gpu, DESK, 0x107)
+    g.scan_mode(*mode)
     g.track_window(5)
     rng = O.Mt64(8)
     for s in range(12):
@@ -300,5 +308,8 @@ def test_invalid_config_messages(gpu):
     with pytest.raises(gpu.InvalidArgument, match="eta must be >= 2"):
         gpu.Grid(q=14, r=5, delta=6, eta=1)
     g = gpu.Grid(**DESK)
-    with pytest.raises(gpu.OutOfRange):
-        g.active_counts(0)
+    g.update(1, 2)
+    # rec::active_count does not validate k (estimator.hpp:26-31): v < 0 never
+    # holds, v < k > 65535 always holds
+    assert int(g.active_counts(0).max()) == 0
+    assert int(g.active_counts(70000).min()) == 256
