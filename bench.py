@@ -185,7 +185,7 @@ def main():
     ap.add_argument("--config", default="c2", choices=sorted(CONFIGS))
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
-    ap.add_argument("--scan-mode", default="auto", choices=["auto", "bitmap", "direct"])
+    ap.add_argument("--scan-mode", default="auto", choices=["auto", "bitmap", "direct", "dedup"])
     ap.add_argument("--filter", type=int, default=-1, help="L1 duplicate probe 0/1 (-1 = default)")
     ap.add_argument("--ref-pairs", type=int, default=100_000_000,
                     help="pairs per reference step (bounded sample of the slot)")
@@ -242,7 +242,7 @@ def main():
     # --- setup (untimed): grid, trace resident in HBM, pinned host copy ------
     g = P.Grid(cfg["q"], cfg["r"], cfg["delta"], cfg["seed"], cfg["eta"], device=dev)
     g.set_stream(stream.cuda_stream)
-    g.scan_mode({"auto": -1, "bitmap": 0, "direct": 1}[args.scan_mode], args.filter)
+    g.scan_mode({"auto": -1, "bitmap": 0, "direct": 1, "dedup": 2}[args.scan_mode], args.filter)
     g.track_window(cfg["k"])
     if world > 1:
         PD.prepare(g)

@@ -160,9 +160,10 @@ sspd_status sspd_commit(sspd_grid* g);
 /* Record each slot's touched bitmap even when scanning in direct mode, so
  * routers can OR-merge it (union-min exchange). */
 sspd_status sspd_set_exchange(sspd_grid* g, int on);
-/* Scan strategy: mode 0 = deferred bitmap, 1 = direct stamping, -1 = keep
- * (default: bitmap while it fits in L2); filter 0/1 = L1 duplicate probe,
- * -1 = keep.  Results are identical in every mode. */
+/* Scan strategy: mode 0 = deferred bitmap, 1 = direct stamping, -1 = auto
+ * (direct for host pairs, which are PCIe-bound, bitmap for device pairs);
+ * filter 0/1 = L1 duplicate probe, -1 = keep.  Results are identical in
+ * every mode, and modes may be mixed within a slot. */
 sspd_status sspd_scan_mode(sspd_grid* g, int mode, int filter);
 
 /* ---- synthetic traces (shape of synth_trace,

@@ -243,6 +243,67 @@ __global__ void __launch_bounds__(256) scan_direct_kernel(const uint32_t* __rest
   });
 }
 
+// DEDUP (direct stamping behind a per-slot pair set): a pair that repeats
+// within the slot touches the same r recorders again, so only the first
+// occurrence needs the random-access work.  The set is an open-addressed
+// table of exact 64-bit (cip, oip) keys sized to stay L2-resident; a probe
+// reads through L1 first (hot pairs hit there once inserted), and insertion
+// is an atomicCAS.  Every miss path -- probe limit reached, table full, the
+// one key equal to the empty marker -- falls back to "new pair", which is
+// only ever redundant work, never a lost touch.  New pairs stamp their r
+// recorders like scan_direct_kernel.
+constexpr uint64_t kEmptyKey = ~0ull;
+constexpr int kProbeLimit = 8;
+
+__device__ __forceinline__ bool pair_is_new(unsigned long long* __restrict__ table, uint64_t mask,
+                                            uint64_t key) {
+  if (key == kEmptyKey) return true;
+  uint64_t h = key * 0x9e3779b97f4a7c15ull;
+  h ^= h >> 29;
+  for (int i = 0; i < kProbeLimit; ++i) {
+    const uint64_t slot = (h + i) & mask;
+    const unsigned long long v = __ldca(table + slot);
+    if (v == key) return false;
+    if (v == kEmptyKey) {
+      const unsigned long long old = atomicCAS(table + slot, kEmptyKey, key);
+      if (old == kEmptyKey) return true;
+      if (old == key) return false;
+    }
+  }
+  return true;
+}
+
+template <int H1MODE, int HIST, int BITS>
+__global__ void __launch_bounds__(256) scan_dedup_kernel(const uint32_t* __restrict__ pairs, uint64_t n,
+                                                         const HashTabs* __restrict__ tabs, Geo geo,
+                                                         unsigned long long* __restrict__ table,
+                                                         uint64_t table_mask, uint32_t* __restrict__ stamps,
+                                                         uint32_t now, uint32_t* __restrict__ hist, uint32_t K,
+                                                         uint32_t* __restrict__ touched) {
+  __shared__ ScanTables t;
+  load_scan_tables(t, tabs);
+  const uint32_t now_slot = HIST ? now % K : 0;
+  for_each_pair(pairs, n, [&](uint32_t cip, uint32_t oip) {
+    if (!pair_is_new(table, table_mask, (uint64_t)cip << 32 | oip)) return;
+    uint32_t bucket, col0;
+    hash_pair<H1MODE>(t, geo, cip, oip, bucket, col0);
+    for (uint32_t row = 0; row < geo.r; ++row) {
+      const uint32_t cell = row << geo.q | row_col(geo, row, cip, col0);
+      const uint64_t idx = (uint64_t)cell * geo.eta + bucket;
+      if (HIST) {
+        const uint32_t old = atomicMax(stamps + idx, now);
+        if (old < now) {
+          atomicAdd(hist + (uint64_t)now_slot * geo.ncells + cell, 1u);
+          if (old + K > now) atomicSub(hist + (uint64_t)(old % K) * geo.ncells + cell, 1u);
+        }
+      } else {
+        asm volatile("red.relaxed.gpu.global.max.u32 [%0], %1;" ::"l"(stamps + idx), "r"(now) : "memory");
+      }
+      if (BITS) red_or(touched + (idx >> 5), 1u << (idx & 31));
+    }
+  });
+}
+
 // ---------------------------------------------------------------------------
 // COMMIT: fold this slot's touched bitmap into the stamps (stamp = now) and,
 // when a window of K slots is tracked, move each first-touched bucket's count

@@ -138,7 +138,10 @@ struct sspd_grid {
   ReconMeta* meta_host = nullptr;  // pinned mirror of meta
   uint64_t cap_alloc = 0;       // tuples per candidate buffer
   int scan_filter = 1;          // L1 duplicate filter in the scan (SSPD_SCAN_FILTER=0 disables)
-  bool scan_direct = false;     // stamp in place instead of the deferred bitmap (auto by size)
+  int scan_mode = -1;           // 0 bitmap, 1 direct, 2 dedup, -1 auto
+  DevBuf pairset;               // dedup mode: per-slot set of seen (cip, oip) pairs
+  uint64_t pairset_mask = 0;
+  bool pairset_dirty = false;   // holds keys from the current slot
   bool record_touched = false;  // direct mode: also record the slot's bitmap (multi-router merge)
   void* pinned_small = nullptr;  // 4 KB pinned scratch for counters
   bool profiling = false;
@@ -213,6 +216,15 @@ sspd_status commit_locked(sspd_grid* g) {
   }
   g->pending = false;  // a stale window ring is rebuilt on demand
   return check_launch();
+}
+
+// The pair set may only skip a pair whose recorders still read `now`; any
+// write to the stamps other than a scan invalidates it.
+sspd_status pairset_reset_locked(sspd_grid* g) {
+  if (!g->pairset_dirty) return SSPD_OK;
+  CU(cudaMemsetAsync(g->pairset.p, 0xff, (g->pairset_mask + 1) * 8, g->stream));
+  g->pairset_dirty = false;
+  return SSPD_OK;
 }
 
 sspd_status hist_rebuild_locked(sspd_grid* g) {
@@ -395,12 +407,12 @@ sspd_status sspd_grid_create(int device, uint32_t q, uint32_t r, uint32_t delta,
   g->geo.n_rec = (uint64_t)g->geo.ncells * eta;
   g->by_eta = Div40::make(eta);
   if (const char* f = std::getenv("SSPD_SCAN_FILTER")) g->scan_filter = std::atoi(f) != 0;
-  // Deferred bitmap by default: measured faster than direct stamping at both
-  // the reference geometry and the full-HBM one (profiles/r01_ab_scan_modes.txt).
-  g->scan_direct = false;
+  // Device-resident pairs: deferred bitmap, measured faster than direct
+  // stamping at both geometries (profiles/r01_ab_scan_modes.txt).
   if (const char* m = std::getenv("SSPD_SCAN_MODE")) {
-    if (!std::strcmp(m, "bitmap")) g->scan_direct = false;
-    if (!std::strcmp(m, "direct")) g->scan_direct = true;
+    if (!std::strcmp(m, "bitmap")) g->scan_mode = 0;
+    if (!std::strcmp(m, "direct")) g->scan_mode = 1;
+    if (!std::strcmp(m, "dedup")) g->scan_mode = 2;
   }
   g->n_words = (g->geo.n_rec + 31) / 32;
   auto cleanup = [&](const std::string& why) {
@@ -453,7 +465,7 @@ sspd_status sspd_grid_destroy(sspd_grid* g) {
     if (g->pinned_small) cudaFreeHost(g->pinned_small);
     if (g->meta_host) cudaFreeHost(g->meta_host);
     for (DevBuf* b : {&g->stage[0], &g->stage[1], &g->counts, &g->hot_cols, &g->hot_rowcnt, &g->hotT,
-                      &g->tupA, &g->tupB, &g->misc, &g->meta, &g->surv})
+                      &g->tupA, &g->tupB, &g->misc, &g->meta, &g->surv, &g->pairset})
       b->release();
     for (auto& r : g->prof) {
       cudaEventDestroy(r.a);
@@ -533,9 +545,27 @@ sspd_status sspd_scan(sspd_grid* g, const uint32_t* pairs, uint64_t n, int pairs
   std::lock_guard<std::mutex> lk(g->mu);
   DeviceGuard dg(g->device);
   const bool pow2 = (g->eta & (g->eta - 1)) == 0 && g->eta <= (1u << 31);
-  const bool direct = g->scan_direct;
-  const bool hist = direct && g->K && g->hist_valid;
-  const bool bits = direct && g->record_touched;
+  // auto: pairs streamed from the host are PCIe-bound, so stamp them in place
+  // while the copies run (nothing left to fold after the last chunk);
+  // device-resident pairs use the deferred bitmap, which is faster in HBM.
+  // auto: pairs streamed from the host are PCIe-bound, so stamp them in place
+  // while the copies run (nothing left to fold after the last chunk); device
+  // pairs use the deferred bitmap while it is L2-resident, else the pair set.
+  int mode = g->scan_mode;
+  if (mode < 0) mode = !pairs_on_device ? (g->n_words * 4 > (48ull << 20) ? 2 : 1)
+                                        : (g->n_words * 4 > (48ull << 20) ? 2 : 0);
+  const bool direct = mode == 1;
+  const bool dedup = mode == 2;
+  const bool hist = (direct || dedup) && g->K && g->hist_valid;
+  const bool bits = (direct || dedup) && g->record_touched;
+  if (dedup && !g->pairset.p) {
+    // 8 B per key, power of two, at most 64 MiB: stays L2-resident (126 MB L2)
+    const uint64_t entries = 8ull << 20;
+    if (g->pairset.ensure(entries * 8) != cudaSuccess)
+      return fail(SSPD_CUDA_ERROR, "CUDA error: out of memory (pair set)");
+    g->pairset_mask = entries - 1;
+    CU(cudaMemsetAsync(g->pairset.p, 0xff, entries * 8, g->stream));
+  }
   auto launch = [&](const uint32_t* dp, uint64_t cnt) {
     const unsigned blocks = grid_blocks(g, (cnt + 3) / 4, 256, 8);
     Prof p(g, "scan", cnt);
@@ -543,7 +573,22 @@ sspd_status sspd_scan(sspd_grid* g, const uint32_t* pairs, uint64_t n, int pairs
 #define SSPD_DIRECT(H1, FI, HI, BI)                                                                 \
   scan_direct_kernel<H1, FI, HI, BI><<<blocks, 256, 0, g->stream>>>(dp, cnt, g->d_tabs, g->geo, g->stamps, \
                                                                     g->now, g->hist, g->K, g->touched)
-    if (!direct) {
+    if (dedup) {
+      auto* tb = g->pairset.as<unsigned long long>();
+#define SSPD_DEDUP(H1, HI, BI)                                                                          \
+  scan_dedup_kernel<H1, HI, BI><<<blocks, 256, 0, g->stream>>>(dp, cnt, g->d_tabs, g->geo, tb, g->pairset_mask, \
+                                                               g->stamps, g->now, g->hist, g->K, g->touched)
+      if (pow2 && hist && bits) SSPD_DEDUP(0, 1, 1);
+      else if (pow2 && hist) SSPD_DEDUP(0, 1, 0);
+      else if (pow2 && bits) SSPD_DEDUP(0, 0, 1);
+      else if (pow2) SSPD_DEDUP(0, 0, 0);
+      else if (hist && bits) SSPD_DEDUP(1, 1, 1);
+      else if (hist) SSPD_DEDUP(1, 1, 0);
+      else if (bits) SSPD_DEDUP(1, 0, 1);
+      else SSPD_DEDUP(1, 0, 0);
+#undef SSPD_DEDUP
+      g->pairset_dirty = true;
+    } else if (!direct) {
       if (pow2 && F) scan_bitmap_kernel<0, 1><<<blocks, 256, 0, g->stream>>>(dp, cnt, g->d_tabs, g->geo, g->touched);
       else if (pow2) scan_bitmap_kernel<0, 0><<<blocks, 256, 0, g->stream>>>(dp, cnt, g->d_tabs, g->geo, g->touched);
       else if (F) scan_bitmap_kernel<1, 1><<<blocks, 256, 0, g->stream>>>(dp, cnt, g->d_tabs, g->geo, g->touched);
@@ -567,14 +612,14 @@ sspd_status sspd_scan(sspd_grid* g, const uint32_t* pairs, uint64_t n, int pairs
   };
   // Direct scans stamp in place; only recorded bits (multi-router) or a
   // stale window ring leave work for the commit.
-  if (!direct || bits) g->pending = true;
+  if (!(direct || dedup) || bits) g->pending = true;
   if (pairs_on_device) {
     launch(pairs, n);
     return check_launch();
   }
   // Host pairs: double-buffered chunks; the copy stream fills one staging
   // buffer while the scan consumes the other.
-  const uint64_t chunk = 8ull << 20;  // pairs per chunk (64 MiB)
+  const uint64_t chunk = 4ull << 20;  // pairs per chunk (32 MiB): small first-copy latency
   const uint64_t chunk_pairs = std::min<uint64_t>(chunk, n);
   for (int i = 0; i < 2; ++i)
     if (g->stage[i].ensure(chunk_pairs * 8) != cudaSuccess)
@@ -613,6 +658,8 @@ sspd_status sspd_advance(sspd_grid* g, uint32_t slots) {
   std::lock_guard<std::mutex> lk(g->mu);
   DeviceGuard dg(g->device);
   sspd_status s = commit_locked(g);
+  if (s) return s;
+  s = pairset_reset_locked(g);  // the pair set only deduplicates within a slot
   if (s) return s;
   for (uint32_t i = 0; i < slots; ++i) {
     if (g->now >= 0x7fffffffu) return fail(SSPD_OUT_OF_RANGE, "advance_slot: slice counter exhausted");
@@ -657,6 +704,8 @@ sspd_status sspd_put_distances(sspd_grid* g, const uint16_t* host_in, uint64_t o
   std::lock_guard<std::mutex> lk(g->mu);
   DeviceGuard dg(g->device);
   sspd_status s = commit_locked(g);
+  if (s) return s;
+  s = pairset_reset_locked(g);
   if (s) return s;
   const uint64_t chunk = 32ull << 20;
   if (g->misc.ensure(std::min(chunk, std::max<uint64_t>(count, 1)) * 2) != cudaSuccess)
@@ -886,6 +935,10 @@ sspd_status sspd_merge(const sspd_grid* const* grids_c, uint64_t n, int policy, 
     sspd_status s = commit_locked(out);
     if (s) return s;
   }
+  {
+    sspd_status s = pairset_reset_locked(out);
+    if (s) return s;
+  }
   // Peer access for inputs on other devices (NVLink loads in merge_kernel).
   std::vector<MergeSrc> srcs(n);
   for (uint64_t i = 0; i < n; ++i) {
@@ -979,6 +1032,8 @@ sspd_status sspd_grid_stamps(sspd_grid* g, uint32_t** dev_stamps, uint64_t* word
   DeviceGuard dg(g->device);
   sspd_status s = commit_locked(g);
   if (s) return s;
+  s = pairset_reset_locked(g);
+  if (s) return s;
   CU(cudaStreamSynchronize(g->stream));
   *dev_stamps = g->stamps;
   *words = g->geo.n_rec;
@@ -999,8 +1054,7 @@ sspd_status sspd_scan_mode(sspd_grid* g, int mode, int filter) {
   DeviceGuard dg(g->device);
   sspd_status s = commit_locked(g);
   if (s) return s;
-  if (mode == 0) g->scan_direct = false;
-  if (mode == 1) g->scan_direct = true;
+  if (mode >= -1 && mode <= 2) g->scan_mode = mode;
   if (filter >= 0) g->scan_filter = filter != 0;
   return SSPD_OK;
 }

@@ -236,7 +236,7 @@ class Grid:
         check(self._L.sspd_set_exchange(self._h, int(on)))
 
     def scan_mode(self, mode: int = -1, filter: int = -1):
-        """mode 0 = deferred bitmap, 1 = direct; filter 0/1 (-1 keeps)."""
+        """mode 0 = deferred bitmap, 1 = direct, -1 = auto; filter 0/1 (-1 keeps)."""
         check(self._L.sspd_scan_mode(self._h, mode, filter))
 
     def commit(self):
