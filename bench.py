@@ -276,7 +276,7 @@ def main():
         else:
             g.scan_device(trace[s].data_ptr(), n_local)
         if world > 1:
-            PD.merge_touched(g)
+            PD.merge(g)
         e1.record(stream)
         rep = g.reconstruct_leveled(k, theta)
         e2.record(stream)
@@ -399,7 +399,8 @@ def main():
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u32",
         "data": "synthetic",
         "config": {"workload": cfg["workload"], "pairs_per_step_per_gpu": n_local,
-                   "window_k": k, "theta": theta, "merge": "union-min (OR of touched bitmaps)",
+                   "window_k": k, "theta": theta,
+                   "merge": "union-min: all-gather of each router's distinct pairs per slot",
                    "parallelism": f"{world} routers, one per GPU",
                    "l2": "inputs larger than L2 (800 MB per slot)"},
         "gbps_800B": round(value * 1e6 * PKT_BYTES * 8 / 1e9, 1),

@@ -157,9 +157,14 @@ sspd_status sspd_grid_stamps(sspd_grid* g, uint32_t** dev_stamps, uint64_t* word
  * OR-reduced it in place, sspd_commit folds it into the stamps. */
 sspd_status sspd_grid_touched(sspd_grid* g, uint32_t** dev_bits, uint64_t* words);
 sspd_status sspd_commit(sspd_grid* g);
-/* Record each slot's touched bitmap even when scanning in direct mode, so
- * routers can OR-merge it (union-min exchange). */
-sspd_status sspd_set_exchange(sspd_grid* g, int on);
+/* Union-min exchange between routers.  mode 1: record each slot's touched
+ * bitmap (OR-merge it, then sspd_commit).  mode 2: list each slot's distinct
+ * (cip, oip) pairs (scans then always use the pair set); routers all-gather
+ * the lists and scan each other's.  0: off. */
+sspd_status sspd_set_exchange(sspd_grid* g, int mode);
+/* This slot's distinct pairs (exchange mode 2): device pointer to `count`
+ * interleaved (cip, oip) pairs, valid until the next advance. */
+sspd_status sspd_grid_new_pairs(sspd_grid* g, uint32_t** dev_pairs, uint64_t* count);
 /* Scan strategy: mode 0 = deferred bitmap, 1 = direct stamping, -1 = auto
  * (direct for host pairs, which are PCIe-bound, bitmap for device pairs);
  * filter 0/1 = L1 duplicate probe, -1 = keep.  Results are identical in

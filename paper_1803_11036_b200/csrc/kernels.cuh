@@ -273,18 +273,36 @@ __device__ __forceinline__ bool pair_is_new(unsigned long long* __restrict__ tab
   return true;
 }
 
-template <int H1MODE, int HIST, int BITS>
+// EXPORT: append each new pair to `out_pairs` (the slot's distinct pairs,
+// exchanged between routers instead of a bitmap; paper_1803_11036_b200/dist.py).
+template <int H1MODE, int HIST, int BITS, int EXPORT>
 __global__ void __launch_bounds__(256) scan_dedup_kernel(const uint32_t* __restrict__ pairs, uint64_t n,
                                                          const HashTabs* __restrict__ tabs, Geo geo,
                                                          unsigned long long* __restrict__ table,
                                                          uint64_t table_mask, uint32_t* __restrict__ stamps,
                                                          uint32_t now, uint32_t* __restrict__ hist, uint32_t K,
-                                                         uint32_t* __restrict__ touched) {
+                                                         uint32_t* __restrict__ touched,
+                                                         uint2* __restrict__ out_pairs,
+                                                         unsigned long long* __restrict__ out_count) {
   __shared__ ScanTables t;
   load_scan_tables(t, tabs);
   const uint32_t now_slot = HIST ? now % K : 0;
+  const uint32_t lane = threadIdx.x & 31;
   for_each_pair(pairs, n, [&](uint32_t cip, uint32_t oip) {
-    if (!pair_is_new(table, table_mask, (uint64_t)cip << 32 | oip)) return;
+    const bool fresh = pair_is_new(table, table_mask, (uint64_t)cip << 32 | oip);
+    if (EXPORT) {
+      // warp-aggregated append over the lanes present here
+      const unsigned m = __activemask();
+      const unsigned b = __ballot_sync(m, fresh);
+      if (b) {
+        const int leader = __ffs(b) - 1;
+        unsigned long long base = 0;
+        if ((int)lane == leader) base = atomicAdd(out_count, (unsigned long long)__popc(b));
+        base = __shfl_sync(m, base, leader);
+        if (fresh) out_pairs[base + __popc(b & ((1u << lane) - 1u))] = make_uint2(cip, oip);
+      }
+    }
+    if (!fresh) return;
     uint32_t bucket, col0;
     hash_pair<H1MODE>(t, geo, cip, oip, bucket, col0);
     for (uint32_t row = 0; row < geo.r; ++row) {

@@ -142,7 +142,11 @@ struct sspd_grid {
   DevBuf pairset;               // dedup mode: per-slot set of seen (cip, oip) pairs
   uint64_t pairset_mask = 0;
   bool pairset_dirty = false;   // holds keys from the current slot
-  bool record_touched = false;  // direct mode: also record the slot's bitmap (multi-router merge)
+  bool record_touched = false;  // direct/dedup: also record the slot's bitmap (multi-router merge)
+  bool export_pairs = false;    // dedup: also list the slot's distinct pairs (multi-router merge)
+  DevBuf newpairs;              // this slot's distinct pairs (export_pairs)
+  DevBuf newpairs_count;        // u64 on device
+  uint64_t scanned_in_slot = 0; // pairs scanned since the last advance (list capacity bound)
   void* pinned_small = nullptr;  // 4 KB pinned scratch for counters
   bool profiling = false;
   std::vector<ProfRec> prof;
@@ -465,7 +469,8 @@ sspd_status sspd_grid_destroy(sspd_grid* g) {
     if (g->pinned_small) cudaFreeHost(g->pinned_small);
     if (g->meta_host) cudaFreeHost(g->meta_host);
     for (DevBuf* b : {&g->stage[0], &g->stage[1], &g->counts, &g->hot_cols, &g->hot_rowcnt, &g->hotT,
-                      &g->tupA, &g->tupB, &g->misc, &g->meta, &g->surv, &g->pairset})
+                      &g->tupA, &g->tupB, &g->misc, &g->meta, &g->surv, &g->pairset, &g->newpairs,
+                      &g->newpairs_count})
       b->release();
     for (auto& r : g->prof) {
       cudaEventDestroy(r.a);
@@ -552,12 +557,33 @@ sspd_status sspd_scan(sspd_grid* g, const uint32_t* pairs, uint64_t n, int pairs
   // while the copies run (nothing left to fold after the last chunk); device
   // pairs use the deferred bitmap while it is L2-resident, else the pair set.
   int mode = g->scan_mode;
+  if (g->export_pairs) mode = 2;  // only the pair set knows which pairs are new
   if (mode < 0) mode = !pairs_on_device ? (g->n_words * 4 > (48ull << 20) ? 2 : 1)
                                         : (g->n_words * 4 > (48ull << 20) ? 2 : 0);
   const bool direct = mode == 1;
   const bool dedup = mode == 2;
   const bool hist = (direct || dedup) && g->K && g->hist_valid;
   const bool bits = (direct || dedup) && g->record_touched;
+  if (g->export_pairs) {
+    // new pairs <= pairs scanned this slot: grow the list, keeping its prefix
+    const uint64_t need = (g->scanned_in_slot + n) * 8;
+    if (g->newpairs.bytes < need) {
+      DevBuf bigger;
+      if (bigger.ensure(std::max<uint64_t>(need, g->newpairs.bytes * 2)) != cudaSuccess)
+        return fail(SSPD_CUDA_ERROR, "CUDA error: out of memory (pair list)");
+      if (g->newpairs.p) CU(cudaMemcpyAsync(bigger.p, g->newpairs.p, g->newpairs.bytes, cudaMemcpyDeviceToDevice,
+                                            g->stream));
+      CU(cudaStreamSynchronize(g->stream));
+      g->newpairs.release();
+      g->newpairs = bigger;
+      bigger.p = nullptr;
+    }
+    if (!g->newpairs_count.p) {
+      if (g->newpairs_count.ensure(8) != cudaSuccess) return fail(SSPD_CUDA_ERROR, "CUDA error: out of memory");
+      CU(cudaMemsetAsync(g->newpairs_count.p, 0, 8, g->stream));
+    }
+  }
+  g->scanned_in_slot += n;
   if (dedup && !g->pairset.p) {
     // 8 B per key, power of two, at most 64 MiB: stays L2-resident (126 MB L2)
     const uint64_t entries = 8ull << 20;
@@ -575,17 +601,25 @@ sspd_status sspd_scan(sspd_grid* g, const uint32_t* pairs, uint64_t n, int pairs
                                                                     g->now, g->hist, g->K, g->touched)
     if (dedup) {
       auto* tb = g->pairset.as<unsigned long long>();
-#define SSPD_DEDUP(H1, HI, BI)                                                                          \
-  scan_dedup_kernel<H1, HI, BI><<<blocks, 256, 0, g->stream>>>(dp, cnt, g->d_tabs, g->geo, tb, g->pairset_mask, \
-                                                               g->stamps, g->now, g->hist, g->K, g->touched)
-      if (pow2 && hist && bits) SSPD_DEDUP(0, 1, 1);
-      else if (pow2 && hist) SSPD_DEDUP(0, 1, 0);
-      else if (pow2 && bits) SSPD_DEDUP(0, 0, 1);
-      else if (pow2) SSPD_DEDUP(0, 0, 0);
-      else if (hist && bits) SSPD_DEDUP(1, 1, 1);
-      else if (hist) SSPD_DEDUP(1, 1, 0);
-      else if (bits) SSPD_DEDUP(1, 0, 1);
-      else SSPD_DEDUP(1, 0, 0);
+      auto* np = g->newpairs.as<uint2>();
+      auto* nc = g->newpairs_count.as<unsigned long long>();
+#define SSPD_DEDUP(H1, HI, BI, EX)                                                                  \
+  scan_dedup_kernel<H1, HI, BI, EX><<<blocks, 256, 0, g->stream>>>(dp, cnt, g->d_tabs, g->geo, tb,          \
+                                                                   g->pairset_mask, g->stamps, g->now,      \
+                                                                   g->hist, g->K, g->touched, np, nc)
+      const bool ex = g->export_pairs;
+      if (pow2 && ex && hist) SSPD_DEDUP(0, 1, 0, 1);
+      else if (pow2 && ex) SSPD_DEDUP(0, 0, 0, 1);
+      else if (ex && hist) SSPD_DEDUP(1, 1, 0, 1);
+      else if (ex) SSPD_DEDUP(1, 0, 0, 1);
+      else if (pow2 && hist && bits) SSPD_DEDUP(0, 1, 1, 0);
+      else if (pow2 && hist) SSPD_DEDUP(0, 1, 0, 0);
+      else if (pow2 && bits) SSPD_DEDUP(0, 0, 1, 0);
+      else if (pow2) SSPD_DEDUP(0, 0, 0, 0);
+      else if (hist && bits) SSPD_DEDUP(1, 1, 1, 0);
+      else if (hist) SSPD_DEDUP(1, 1, 0, 0);
+      else if (bits) SSPD_DEDUP(1, 0, 1, 0);
+      else SSPD_DEDUP(1, 0, 0, 0);
 #undef SSPD_DEDUP
       g->pairset_dirty = true;
     } else if (!direct) {
@@ -612,7 +646,7 @@ sspd_status sspd_scan(sspd_grid* g, const uint32_t* pairs, uint64_t n, int pairs
   };
   // Direct scans stamp in place; only recorded bits (multi-router) or a
   // stale window ring leave work for the commit.
-  if (!(direct || dedup) || bits) g->pending = true;
+  if (!(direct || dedup) || (bits && !g->export_pairs)) g->pending = true;
   if (pairs_on_device) {
     launch(pairs, n);
     return check_launch();
@@ -661,6 +695,8 @@ sspd_status sspd_advance(sspd_grid* g, uint32_t slots) {
   if (s) return s;
   s = pairset_reset_locked(g);  // the pair set only deduplicates within a slot
   if (s) return s;
+  if (g->newpairs_count.p) CU(cudaMemsetAsync(g->newpairs_count.p, 0, 8, g->stream));
+  g->scanned_in_slot = 0;
   for (uint32_t i = 0; i < slots; ++i) {
     if (g->now >= 0x7fffffffu) return fail(SSPD_OUT_OF_RANGE, "advance_slot: slice counter exhausted");
     ++g->now;
@@ -1043,9 +1079,24 @@ sspd_status sspd_grid_stamps(sspd_grid* g, uint32_t** dev_stamps, uint64_t* word
   return SSPD_OK;
 }
 
-sspd_status sspd_set_exchange(sspd_grid* g, int on) {
+sspd_status sspd_set_exchange(sspd_grid* g, int mode) {
   std::lock_guard<std::mutex> lk(g->mu);
-  g->record_touched = on != 0;
+  g->record_touched = mode == 1;
+  g->export_pairs = mode == 2;
+  return SSPD_OK;
+}
+
+sspd_status sspd_grid_new_pairs(sspd_grid* g, uint32_t** dev_pairs, uint64_t* count) {
+  std::lock_guard<std::mutex> lk(g->mu);
+  DeviceGuard dg(g->device);
+  uint64_t c = 0;
+  if (g->newpairs_count.p) {
+    CU(cudaMemcpyAsync(g->pinned_small, g->newpairs_count.p, 8, cudaMemcpyDeviceToHost, g->stream));
+    CU(cudaStreamSynchronize(g->stream));
+    c = *static_cast<uint64_t*>(g->pinned_small);
+  }
+  *dev_pairs = g->newpairs.as<uint32_t>();
+  *count = c;
   return SSPD_OK;
 }
 

@@ -62,9 +62,159 @@ def device_view(ptr: int, n_words: int, device: int) -> torch.Tensor:
         return torch.as_tensor(_CudaArray(ptr, n_words), device=f"cuda:{device}")
 
 
-def prepare(grid):
-    """Make the grid record each slot's touched bitmap (needed in direct mode)."""
-    grid.set_exchange(True)
+BITMAP = 1
+PAIRS = 2
+
+
+def prepare(grid, exchange: int = PAIRS):
+    """Choose what routers exchange each slot: the slot's distinct (cip, oip)
+    pairs (PAIRS, default: ~5% of a Zipf slot's packets, 8 B each) or the
+    touched bitmap (BITMAP: 1 bit per recorder, fixed size)."""
+    grid.set_exchange(exchange)
+    grid._exchange = exchange
+
+
+def merge(grid, group=None):
+    if getattr(grid, "_exchange", BITMAP) == PAIRS:
+        merge_pairs(grid, group)
+    else:
+        merge_touched(grid, group)
+
+
+def exchange_pairs(local: torch.Tensor, group=None) -> list[torch.Tensor]:
+    """All-gather variable-length (n, 2) int32 pair lists; returns the other
+    ranks' lists (views into one receive buffer), in rank order."""
+    world = dist.get_world_size(group)
+    rank = dist.get_rank(group)
+    n = local.shape[0]
+    counts = torch.tensor([n], dtype=torch.int64, device=local.device)
+    all_counts = torch.empty(world, dtype=torch.int64, device=local.device)
+    dist.all_gather_into_tensor(all_counts, counts, group=group)
+    sizes = [int(c) for c in all_counts.tolist()]
+    width = max(sizes) if sizes else 0
+    if width == 0:
+        return []
+    mine = torch.zeros((width, 2), dtype=torch.int32, device=local.device)
+    if n:
+        mine[:n].copy_(local)
+    everyone = torch.empty((world * width, 2), dtype=torch.int32, device=local.device)
+    dist.all_gather_into_tensor(everyone, mine, group=group)
+    return [everyone[r * width: r * width + sizes[r]] for r in range(world) if r != rank and sizes[r]]
+
+
+def merge_pairs(grid, group=None):
+    """Union-min merge by pair lists: all-gather every router's distinct
+    pairs of the slot and scan the other routers' lists locally.  The union
+    of the touches equals the union-min merge of the node grids; the grid's
+    pair set skips pairs this router already saw."""
+    if dist.get_world_size(group) == 1:
+        return
+    ptr, n = grid.new_pairs_ptr()
+    dev = torch.device(f"cuda:{grid.device}")
+    local = (device_view(ptr, 2 * n, grid.device).view(n, 2) if n
+             else torch.zeros((0, 2), dtype=torch.int32, device=dev))
+    remote = exchange_pairs(local, group)
+    torch.cuda.synchronize(grid.device)
+    grid.set_exchange(0)  # remote pairs are not re-exported
+    try:
+        for part in remote:
+            grid.scan_device(part.data_ptr(), int(part.shape[0]))
+    finally:
+        grid.set_exchange(PAIRS)
+
+
+def or_allreduce_(t: torch.Tensor, group=None) -> torch.Tensor:
+    """In-place bitwise-OR all-reduce of an int32 tensor (NCCL has no OR op).
+
+    Reduce-scatter by all_to_all + a local OR of the received chunks, then
+    all-gather: the 2(N-1)/N per-rank volume of a ring all-reduce.  The same
+    code runs on NCCL (GPU) and gloo (the CPU tests).
+    """
+    world = dist.get_world_size(group)
+    if world == 1:
+        return t
+    flat = t.view(-1)
+    n = flat.numel()
+    per = (n + world - 1) // world
+    padded = flat
+    if per * world != n:
+        padded = torch.zeros(per * world, dtype=flat.dtype, device=flat.device)
+        padded[:n].copy_(flat)
+    recv = torch.empty_like(padded)
+    dist.all_to_all_single(recv, padded, group=group)
+    chunks = recv.view(world, per)
+    mine = chunks[0].clone()
+    for i in range(1, world):
+        mine.bitwise_or_(chunks[i])
+    out = torch.empty_like(padded)
+    dist.all_gather_into_tensor(out, mine, group=group)
+    flat.copy_(out[:n])
+    return t
+
+
+class _CudaArray:
+    """__cuda_array_interface__ view of raw device memory owned by the grid."""
+
+    def __init__(self, ptr: int, n: int, typestr: str = "<i4"):
+        self.__cuda_array_interface__ = {"shape": (n,), "typestr": typestr,
+                                         "data": (ptr, False), "version": 3, "strides": None}
+
+
+def device_view(ptr: int, n_words: int, device: int) -> torch.Tensor:
+    with torch.cuda.device(device):
+        return torch.as_tensor(_CudaArray(ptr, n_words), device=f"cuda:{device}")
+
+
+BITMAP = 1
+PAIRS = 2
+
+
+def prepare(grid, exchange: int = PAIRS):
+    """Choose what routers exchange each slot: the slot's distinct (cip, oip)
+    pairs (PAIRS, default: ~5% of a Zipf slot's packets, 8 B each) or the
+    touched bitmap (BITMAP: 1 bit per recorder, fixed size)."""
+    grid.set_exchange(exchange)
+    grid._exchange = exchange
+
+
+def merge(grid, group=None):
+    if getattr(grid, "_exchange", BITMAP) == PAIRS:
+        merge_pairs(grid, group)
+    else:
+        merge_touched(grid, group)
+
+
+def merge_pairs(grid, group=None):
+    """Union-min merge by pair lists: all-gather every router's distinct
+    pairs of the slot and scan the other routers' lists locally.  The union
+    of the touches equals the union-min merge of the node grids; the grid's
+    pair set skips pairs this router already saw."""
+    world = dist.get_world_size(group)
+    if world == 1:
+        return
+    rank = dist.get_rank(group)
+    ptr, n = grid.new_pairs_ptr()
+    dev = torch.device(f"cuda:{grid.device}")
+    counts = torch.tensor([n], dtype=torch.int64, device=dev)
+    all_counts = torch.empty(world, dtype=torch.int64, device=dev)
+    dist.all_gather_into_tensor(all_counts, counts, group=group)
+    all_counts = all_counts.tolist()
+    width = max(all_counts)
+    if width == 0:
+        return
+    mine = torch.zeros(width * 2, dtype=torch.int32, device=dev)
+    if n:
+        mine[: 2 * n].copy_(device_view(ptr, 2 * n, grid.device))
+    everyone = torch.empty(world * width * 2, dtype=torch.int32, device=dev)
+    dist.all_gather_into_tensor(everyone, mine, group=group)
+    torch.cuda.synchronize(grid.device)
+    grid.set_exchange(0)  # remote pairs are not re-exported
+    try:
+        for r in range(world):
+            if r != rank and all_counts[r]:
+                grid.scan_device(everyone[r * width * 2:].data_ptr(), int(all_counts[r]))
+    finally:
+        grid.set_exchange(PAIRS)
 
 
 def merge_touched(grid, group=None):

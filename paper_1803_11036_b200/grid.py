@@ -232,8 +232,15 @@ class Grid:
         check(self._L.sspd_grid_touched(self._h, C.byref(p), C.byref(n)))
         return p.value, n.value
 
-    def set_exchange(self, on: bool = True):
-        check(self._L.sspd_set_exchange(self._h, int(on)))
+    def set_exchange(self, mode: int = 1):
+        """0 off, 1 touched bitmap, 2 distinct-pair list (see dist.py)."""
+        check(self._L.sspd_set_exchange(self._h, int(mode)))
+
+    def new_pairs_ptr(self) -> tuple[int, int]:
+        p = C.c_void_p()
+        n = C.c_uint64()
+        check(self._L.sspd_grid_new_pairs(self._h, C.byref(p), C.byref(n)))
+        return p.value or 0, n.value
 
     def scan_mode(self, mode: int = -1, filter: int = -1):
         """mode 0 = deferred bitmap, 1 = direct, -1 = auto; filter 0/1 (-1 keeps)."""

@@ -116,3 +116,42 @@ def test_or_allreduce(world):
     out = mgr.dict()
     mp.spawn(_or_worker, args=(world, free_port(), out), nprocs=world, join=True)
     assert all(out[r] for r in range(world))
+
+
+def _pairs_worker(rank, world, port, slots, out):
+    """The pair-list exchange: each router contributes its slot's distinct
+    pairs; folding everyone's pairs gives the union-min merged grid."""
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from paper_1803_11036_b200.dist import exchange_pairs
+
+    rng = O.Mt64(4242)
+    mine = O.OracleGrid(**GEO)   # this router's merged view
+    nodes = [O.OracleGrid(**GEO) for _ in range(world)]
+    ok = True
+    for s in range(slots):
+        p = rng.pairs(2000)
+        p = p[rng.draw(6000) % 2000]          # repeats, like Zipf traffic
+        owner = rng.draw(len(p)) % world
+        for i in range(world):
+            nodes[i].scan(p[owner == i])
+        local = np.unique(p[owner == rank], axis=0)   # the slot's distinct pairs
+        mine.scan(local)
+        for part in exchange_pairs(torch.from_numpy(local.view(np.int32).copy())):
+            mine.scan(part.numpy().view(np.uint32))
+        ok &= bool(np.array_equal(mine.cells(), O.OracleGrid.merge(nodes, 0).cells()))
+        mine.advance()
+        for n in nodes:
+            n.advance()
+    out[rank] = ok
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_pair_list_exchange(world):
+    mgr = mp.Manager()
+    out = mgr.dict()
+    mp.spawn(_pairs_worker, args=(world, free_port(), 4, out), nprocs=world, join=True)
+    assert all(out[r] for r in range(world))
