@@ -378,6 +378,16 @@ def main():
                     "peak_source": "MEASURED_PEAKS.json hbm_gbs" if "hbm_gbs" in peaks else "fallback"}
     kernels_share = {k2: round(v["ms"] / ms, 4) for k2, v in prof.items()}
 
+    # Detection accuracy of the last timed slot against the generator's
+    # truth: the injected super points are the only hosts at or above theta
+    # (background hosts draw from 16-entry pools; C1's uniform pairs spread
+    # 5e6 pairs over 2^32 hosts).  evaluate() semantics (workload.cpp:360-385).
+    truth = {int(L.sspd_synth_super_cip(C.byref(sp), i)) for i in range(cfg["n_super"])}
+    got = {d.cip for d in reps} if reps is not None else set()
+    accuracy = {"true_supers": len(truth), "reported": len(got),
+                "fpr": round(len(got - truth) / max(len(truth), 1), 6),
+                "fnr": round(len(truth - got) / max(len(truth), 1), 6)}
+
     # --- CPU baseline: the compiled reference on this host ---------------------
     cpu = None
     if world == 1 and not args.no_cpu_baseline:
@@ -406,6 +416,7 @@ def main():
         "gbps_800B": round(value * 1e6 * PKT_BYTES * 8 / 1e9, 1),
         "reconstruct_ms": round(statistics.mean(recon), 3),
         "reports_last_step": len(reps) if reps is not None else None,
+        "accuracy": accuracy,
         "kernels_share": kernels_share,
         "roofline": roof,
         "cpu_baseline": cpu,

@@ -255,26 +255,65 @@ __global__ void __launch_bounds__(256) scan_direct_kernel(const uint32_t* __rest
 constexpr uint64_t kEmptyKey = ~0ull;
 constexpr int kProbeLimit = 8;
 
-__device__ __forceinline__ bool pair_is_new(unsigned long long* __restrict__ table, uint64_t mask,
-                                            uint64_t key) {
-  if (key == kEmptyKey) return true;
+__device__ __forceinline__ uint64_t pair_slot_hash(uint64_t key) {
   uint64_t h = key * 0x9e3779b97f4a7c15ull;
-  h ^= h >> 29;
-  for (int i = 0; i < kProbeLimit; ++i) {
+  return h ^ (h >> 29);
+}
+
+// Resolve a probe that started with value `v` at probe distance 0.
+__device__ __forceinline__ bool pair_resolve(unsigned long long* __restrict__ table, uint64_t mask, uint64_t key,
+                                             uint64_t h, unsigned long long v) {
+  if (key == kEmptyKey) return true;
+  for (int i = 0;; ) {
     const uint64_t slot = (h + i) & mask;
-    const unsigned long long v = __ldca(table + slot);
     if (v == key) return false;
     if (v == kEmptyKey) {
       const unsigned long long old = atomicCAS(table + slot, kEmptyKey, key);
       if (old == kEmptyKey) return true;
       if (old == key) return false;
     }
+    if (++i >= kProbeLimit) return true;
+    v = __ldca(table + ((h + i) & mask));
   }
-  return true;
+}
+
+// Stamp the r recorders of a new pair (direct, with the window ring).
+template <int H1MODE, int HIST, int BITS>
+__device__ __forceinline__ void stamp_pair(const ScanTables& t, const Geo& geo, uint32_t cip, uint32_t oip,
+                                           uint32_t* __restrict__ stamps, uint32_t now, uint32_t now_slot,
+                                           uint32_t* __restrict__ hist, uint32_t K, uint32_t* __restrict__ touched) {
+  uint32_t bucket, col0;
+  hash_pair<H1MODE>(t, geo, cip, oip, bucket, col0);
+  for (uint32_t r0 = 0; r0 < geo.r; r0 += 4) {
+    uint32_t cell[4], old[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {  // the atomics of a group are independent: issue them together
+      const uint32_t row = r0 + u;
+      cell[u] = row << geo.q | row_col(geo, row, cip, col0);
+      old[u] = now;
+      if (row < geo.r) {
+        uint32_t* p = stamps + (uint64_t)cell[u] * geo.eta + bucket;
+        if (HIST) old[u] = atomicMax(p, now);
+        else asm volatile("red.relaxed.gpu.global.max.u32 [%0], %1;" ::"l"(p), "r"(now) : "memory");
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      if (r0 + u >= geo.r) break;
+      const uint64_t idx = (uint64_t)cell[u] * geo.eta + bucket;
+      if (HIST && old[u] < now) {
+        atomicAdd(hist + (uint64_t)now_slot * geo.ncells + cell[u], 1u);
+        if (old[u] + K > now) atomicSub(hist + (uint64_t)(old[u] % K) * geo.ncells + cell[u], 1u);
+      }
+      if (BITS) red_or(touched + (idx >> 5), 1u << (idx & 31));
+    }
+  }
 }
 
 // EXPORT: append each new pair to `out_pairs` (the slot's distinct pairs,
 // exchanged between routers instead of a bitmap; paper_1803_11036_b200/dist.py).
+// Each thread takes 4 pairs per iteration and issues their 4 first probes
+// together before resolving any (the probes are the latency chain).
 template <int H1MODE, int HIST, int BITS, int EXPORT>
 __global__ void __launch_bounds__(256) scan_dedup_kernel(const uint32_t* __restrict__ pairs, uint64_t n,
                                                          const HashTabs* __restrict__ tabs, Geo geo,
@@ -288,38 +327,59 @@ __global__ void __launch_bounds__(256) scan_dedup_kernel(const uint32_t* __restr
   load_scan_tables(t, tabs);
   const uint32_t now_slot = HIST ? now % K : 0;
   const uint32_t lane = threadIdx.x & 31;
-  for_each_pair(pairs, n, [&](uint32_t cip, uint32_t oip) {
-    const bool fresh = pair_is_new(table, table_mask, (uint64_t)cip << 32 | oip);
+  const uint64_t tid = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const uint64_t nthreads = (uint64_t)gridDim.x * blockDim.x;
+  const bool vec = (reinterpret_cast<uintptr_t>(pairs) & 15u) == 0;
+  // group g covers pairs [4g, 4g+4): two 16-byte loads
+  const uint64_t ngroups = (n + 3) / 4;
+  for (uint64_t g = tid; g < ngroups; g += nthreads) {
+    uint32_t c[4], o[4];
+    bool valid[4];
+    const uint64_t p0 = g * 4;
+    if (vec && p0 + 4 <= n) {
+      const uint4 a = ld_stream_u4(pairs + 2 * p0);
+      const uint4 b = ld_stream_u4(pairs + 2 * p0 + 4);
+      c[0] = a.x; o[0] = a.y; c[1] = a.z; o[1] = a.w;
+      c[2] = b.x; o[2] = b.y; c[3] = b.z; o[3] = b.w;
+#pragma unroll
+      for (int u = 0; u < 4; ++u) valid[u] = true;
+    } else {
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        valid[u] = p0 + u < n;
+        c[u] = valid[u] ? pairs[2 * (p0 + u)] : 0u;
+        o[u] = valid[u] ? pairs[2 * (p0 + u) + 1] : 0u;
+      }
+    }
+    uint64_t key[4], h[4];
+    unsigned long long v[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      key[u] = (uint64_t)c[u] << 32 | o[u];
+      h[u] = pair_slot_hash(key[u]);
+      v[u] = valid[u] ? __ldca(table + (h[u] & table_mask)) : 0ull;
+    }
+    bool fresh[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) fresh[u] = valid[u] && pair_resolve(table, table_mask, key[u], h[u], v[u]);
     if (EXPORT) {
-      // warp-aggregated append over the lanes present here
-      const unsigned m = __activemask();
-      const unsigned b = __ballot_sync(m, fresh);
-      if (b) {
-        const int leader = __ffs(b) - 1;
-        unsigned long long base = 0;
-        if ((int)lane == leader) base = atomicAdd(out_count, (unsigned long long)__popc(b));
-        base = __shfl_sync(m, base, leader);
-        if (fresh) out_pairs[base + __popc(b & ((1u << lane) - 1u))] = make_uint2(cip, oip);
-      }
-    }
-    if (!fresh) return;
-    uint32_t bucket, col0;
-    hash_pair<H1MODE>(t, geo, cip, oip, bucket, col0);
-    for (uint32_t row = 0; row < geo.r; ++row) {
-      const uint32_t cell = row << geo.q | row_col(geo, row, cip, col0);
-      const uint64_t idx = (uint64_t)cell * geo.eta + bucket;
-      if (HIST) {
-        const uint32_t old = atomicMax(stamps + idx, now);
-        if (old < now) {
-          atomicAdd(hist + (uint64_t)now_slot * geo.ncells + cell, 1u);
-          if (old + K > now) atomicSub(hist + (uint64_t)(old % K) * geo.ncells + cell, 1u);
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const unsigned m = __activemask();
+        const unsigned b = __ballot_sync(m, fresh[u]);
+        if (b) {
+          const int leader = __ffs(b) - 1;
+          unsigned long long base = 0;
+          if ((int)lane == leader) base = atomicAdd(out_count, (unsigned long long)__popc(b));
+          base = __shfl_sync(m, base, leader);
+          if (fresh[u]) out_pairs[base + __popc(b & ((1u << lane) - 1u))] = make_uint2(c[u], o[u]);
         }
-      } else {
-        asm volatile("red.relaxed.gpu.global.max.u32 [%0], %1;" ::"l"(stamps + idx), "r"(now) : "memory");
       }
-      if (BITS) red_or(touched + (idx >> 5), 1u << (idx & 31));
     }
-  });
+#pragma unroll
+    for (int u = 0; u < 4; ++u)
+      if (fresh[u]) stamp_pair<H1MODE, HIST, BITS>(t, geo, c[u], o[u], stamps, now, now_slot, hist, K, touched);
+  }
 }
 
 // ---------------------------------------------------------------------------

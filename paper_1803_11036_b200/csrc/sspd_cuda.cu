@@ -585,12 +585,31 @@ sspd_status sspd_scan(sspd_grid* g, const uint32_t* pairs, uint64_t n, int pairs
   }
   g->scanned_in_slot += n;
   if (dedup && !g->pairset.p) {
-    // 8 B per key, power of two, at most 64 MiB: stays L2-resident (126 MB L2)
-    const uint64_t entries = 8ull << 20;
+    // 8 B per exact key, a power of two of entries (SSPD_PAIRSET_LOG2,
+    // default 2^25 = 256 MiB: ~10M distinct pairs per C2 slot at load 0.3;
+    // measured 2^22..2^25 = 4.23..3.90 ms/slot, profiles/r01_ab_pairset.txt).
+    // Pinning it in L2 (SSPD_L2_PERSIST=<MiB>) measured slower.
+    uint32_t lg = 25;
+    if (const char* e = std::getenv("SSPD_PAIRSET_LOG2")) lg = std::min(30, std::max(16, std::atoi(e)));
+    const uint64_t entries = 1ull << lg;
     if (g->pairset.ensure(entries * 8) != cudaSuccess)
       return fail(SSPD_CUDA_ERROR, "CUDA error: out of memory (pair set)");
     g->pairset_mask = entries - 1;
     CU(cudaMemsetAsync(g->pairset.p, 0xff, entries * 8, g->stream));
+    if (const char* e = std::getenv("SSPD_L2_PERSIST"); e && std::atoi(e) > 0) {
+      cudaDeviceProp prop;
+      CU(cudaGetDeviceProperties(&prop, g->device));
+      const size_t want = std::min<size_t>((size_t)std::atoi(e) << 20, prop.persistingL2CacheMaxSize);
+      CU(cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, want));
+      cudaStreamAttrValue attr{};
+      attr.accessPolicyWindow.base_ptr = g->pairset.p;
+      attr.accessPolicyWindow.num_bytes = std::min<size_t>(entries * 8, prop.accessPolicyMaxWindowSize);
+      attr.accessPolicyWindow.hitRatio =
+          std::min(1.0f, (float)want / (float)attr.accessPolicyWindow.num_bytes);
+      attr.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
+      attr.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
+      CU(cudaStreamSetAttribute(g->stream, cudaStreamAttributeAccessPolicyWindow, &attr));
+    }
   }
   auto launch = [&](const uint32_t* dp, uint64_t cnt) {
     const unsigned blocks = grid_blocks(g, (cnt + 3) / 4, 256, 8);
