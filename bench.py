@@ -185,12 +185,15 @@ def main():
     ap.add_argument("--config", default="c2", choices=sorted(CONFIGS))
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--window", type=int, default=0, help="override the window k (C4 sweeps)")
     ap.add_argument("--scan-mode", default="auto", choices=["auto", "bitmap", "direct", "dedup"])
     ap.add_argument("--filter", type=int, default=-1, help="L1 duplicate probe 0/1 (-1 = default)")
     ap.add_argument("--ref-pairs", type=int, default=100_000_000,
                     help="pairs per reference step (bounded sample of the slot)")
     args = ap.parse_args()
-    cfg = CONFIGS[args.config]
+    cfg = dict(CONFIGS[args.config])
+    if args.window:
+        cfg["k"] = args.window
     rank = env_int("RANK", 0)
     world = env_int("WORLD_SIZE", 1)
     local = env_int("LOCAL_RANK", 0)

@@ -165,8 +165,9 @@ sspd_status sspd_set_exchange(sspd_grid* g, int mode);
 /* This slot's distinct pairs (exchange mode 2): device pointer to `count`
  * interleaved (cip, oip) pairs, valid until the next advance. */
 sspd_status sspd_grid_new_pairs(sspd_grid* g, uint32_t** dev_pairs, uint64_t* count);
-/* Scan strategy: mode 0 = deferred bitmap, 1 = direct stamping, -1 = auto
- * (direct for host pairs, which are PCIe-bound, bitmap for device pairs);
+/* Scan strategy: mode 0 = deferred bitmap, 1 = direct stamping, 2 = direct
+ * behind a per-slot set of seen pairs, -1 = auto (2 when the touched bitmap
+ * would exceed 48 MiB, else 1);
  * filter 0/1 = L1 duplicate probe, -1 = keep.  Results are identical in
  * every mode, and modes may be mixed within a slot. */
 sspd_status sspd_scan_mode(sspd_grid* g, int mode, int filter);

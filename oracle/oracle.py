@@ -397,6 +397,7 @@ def ref():
         L.ref_scan_alpha.argtypes = [C.c_void_p, C.c_void_p, C.c_size_t, C.c_uint, C.c_size_t]
         L.ref_get_cells.argtypes = [C.c_void_p, u16p]
         L.ref_set_cells.argtypes = [C.c_void_p, u16p]
+        L.ref_get_cells_range.argtypes = [C.c_void_p, C.c_size_t, C.c_size_t, u16p]
         L.ref_hot_sets.restype = C.c_size_t
         L.ref_hot_sets.argtypes = [C.c_void_p, C.c_uint32, C.c_double, u32p, u32p]
         L.ref_finalize.argtypes = [C.c_void_p, u32p, C.c_uint32, C.c_double, u32p, f64p]
@@ -456,6 +457,11 @@ class RefGrid:
     def cells(self) -> np.ndarray:
         out = np.empty(ref().ref_grid_size(self._h), dtype=np.uint16)
         ref().ref_get_cells(self._h, _ptr(out, u16p))
+        return out
+
+    def cells_range(self, offset: int, count: int) -> np.ndarray:
+        out = np.empty(count, dtype=np.uint16)
+        ref().ref_get_cells_range(self._h, offset, count, _ptr(out, u16p))
         return out
 
     def set_cells(self, a: np.ndarray):

@@ -109,6 +109,10 @@ void ref_get_cells(void* g, uint16_t* out) {
   auto c = static_cast<Rsea*>(g)->cells();
   std::memcpy(out, c.data(), c.size() * 2);
 }
+void ref_get_cells_range(void* g, size_t offset, size_t count, uint16_t* out) {
+  auto c = static_cast<Rsea*>(g)->cells();
+  std::memcpy(out, c.data() + offset, count * 2);
+}
 void ref_set_cells(void* g, const uint16_t* in) {
   auto c = static_cast<Rsea*>(g)->cells();
   std::memcpy(c.data(), in, c.size() * 2);

@@ -553,13 +553,14 @@ sspd_status sspd_scan(sspd_grid* g, const uint32_t* pairs, uint64_t n, int pairs
   // auto: pairs streamed from the host are PCIe-bound, so stamp them in place
   // while the copies run (nothing left to fold after the last chunk);
   // device-resident pairs use the deferred bitmap, which is faster in HBM.
-  // auto: pairs streamed from the host are PCIe-bound, so stamp them in place
-  // while the copies run (nothing left to fold after the last chunk); device
-  // pairs use the deferred bitmap while it is L2-resident, else the pair set.
+  // auto: never leave deferred work after the last (PCIe) chunk of a host
+  // scan; use the pair set once the grid is far beyond L2.
   int mode = g->scan_mode;
   if (g->export_pairs) mode = 2;  // only the pair set knows which pairs are new
-  if (mode < 0) mode = !pairs_on_device ? (g->n_words * 4 > (48ull << 20) ? 2 : 1)
-                                        : (g->n_words * 4 > (48ull << 20) ? 2 : 0);
+  // Measured (profiles/r01_ab_*.txt): with the touched bitmap L2-sized (C1)
+  // direct stamping is fastest for host and device pairs alike (0.42 vs 0.46
+  // ms/slot bitmap+commit); beyond L2 (C2) the pair set wins (3.9 vs 11.9).
+  if (mode < 0) mode = g->n_words * 4 > (48ull << 20) ? 2 : 1;
   const bool direct = mode == 1;
   const bool dedup = mode == 2;
   const bool hist = (direct || dedup) && g->K && g->hist_valid;
