@@ -133,22 +133,26 @@ def run_reference(cfg, steps, warmup, pairs_cap, time_budget_s):
     trace through scan_batch (alpha=32768 batches, pipeline.cpp:58-63),
     reconstruct_leveled and advance_slot, workers = all host cores."""
     from oracle import oracle as O
-    import paper_1803_11036_b200 as P
 
-    L = P.load()
+    # the workload comes from the host-only generator (no CUDA runtime in
+    # this process): the same traces the device generator makes
+    S = C.CDLL(os.path.join(ROOT, "paper_1803_11036_b200", "lib", "libsspd_synth.so"))
     workers = os.cpu_count() or 1
     t0 = time.time()
     g = O.RefGrid(cfg["q"], cfg["r"], cfg["delta"], cfg["seed"], cfg["eta"])
     t_init = time.time() - t0
-    cdf = zipf_cdf(L, cfg)
+    cdf = np.empty(cfg["hosts"], dtype=np.uint64)
+    assert S.sspd_synth_zipf_cdf_host(C.c_uint32(cfg["hosts"]), C.c_double(cfg["zipf"]),
+                                      C.c_void_p(cdf.ctypes.data)) == 0
     sp = synth_params(cfg, 0, 1)
     n = min(cfg["pairs_per_slot"], pairs_cap)
     buf = np.empty((n, 2), dtype=np.uint32)
     times, scan_t, rec_t, adv_t, n_rep = [], [], [], [], []
     budget_hit = False
     for i in range(warmup + steps):
-        assert L.sspd_synth_host(C.byref(sp), cdf.ctypes.data, i % cfg["trace_slots"], 0, n,
-                                 buf.ctypes.data) == 0
+        assert S.sspd_synth_pairs_host(C.byref(sp), C.c_void_p(cdf.ctypes.data),
+                                       C.c_uint64(i % cfg["trace_slots"]), C.c_uint64(0),
+                                       C.c_uint64(n), C.c_void_p(buf.ctypes.data)) == 0
         a = time.perf_counter()
         g.scan_alpha(buf, workers)
         b = time.perf_counter()

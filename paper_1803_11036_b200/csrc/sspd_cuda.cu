@@ -170,9 +170,13 @@ struct DeviceGuard {
 };
 
 int sm_count(int dev) {
+  static int cached[64] = {0};
+  if (dev >= 0 && dev < 64 && cached[dev]) return cached[dev];
   int n = 0;
   cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
-  return n > 0 ? n : 148;
+  n = n > 0 ? n : 148;
+  if (dev >= 0 && dev < 64) cached[dev] = n;
+  return n;
 }
 
 // Persistent-style grid size: a multiple of the SM count.
