@@ -378,8 +378,18 @@ def main():
                           "merge": 4 * 2}.get(dom)
         if bytes_per_unit is not None:
             achieved = bytes_per_unit * units_per_launch / (per_launch_ms / 1e3) / 1e9
+            # DRAM bytes per launch of the same kernel at the same config, from
+            # the committed ncu --set full capture (bench cannot run ncu itself)
+            traffic = None
+            try:
+                with open(os.path.join(ROOT, "profiles", "r01_traffic.json")) as f:
+                    t = json.load(f).get(args.config, {}).get(dom)
+                if t and t["units_per_launch"] == units_per_launch:
+                    traffic = t["dram_bytes_per_launch"]
+            except Exception:
+                traffic = None
             roof = {"kernel": dom, "bound": "hbm", "achieved": round(achieved, 1), "peak": hbm,
-                    "unit": "GB/s", "frac": round(achieved / hbm, 4), "traffic": None,
+                    "unit": "GB/s", "frac": round(achieved / hbm, 4), "traffic": traffic,
                     "bytes_per_unit": bytes_per_unit, "units_per_launch": units_per_launch,
                     "launch_ms": round(per_launch_ms, 4),
                     "peak_source": "MEASURED_PEAKS.json hbm_gbs" if "hbm_gbs" in peaks else "fallback"}
