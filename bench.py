@@ -190,6 +190,9 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--window", type=int, default=0, help="override the window k (C4 sweeps)")
+    ap.add_argument("--merge", default="pairs", choices=["pairs", "bitmap", "stamps"],
+                    help="router exchange at N>1: distinct-pair lists (default), OR of touched "
+                         "bitmaps, or the literal all-reduce(max) of the full stamp grid")
     ap.add_argument("--scan-mode", default="auto", choices=["auto", "bitmap", "direct", "dedup"])
     ap.add_argument("--filter", type=int, default=-1, help="L1 duplicate probe 0/1 (-1 = default)")
     ap.add_argument("--ref-pairs", type=int, default=100_000_000,
@@ -251,8 +254,8 @@ def main():
     g.set_stream(stream.cuda_stream)
     g.scan_mode({"auto": -1, "bitmap": 0, "direct": 1, "dedup": 2}[args.scan_mode], args.filter)
     g.track_window(cfg["k"])
-    if world > 1:
-        PD.prepare(g)
+    if world > 1 and args.merge != "stamps":
+        PD.prepare(g, PD.PAIRS if args.merge == "pairs" else PD.BITMAP)
     cdf = torch.from_numpy(zipf_cdf(L, cfg).view(np.int64)).to(f"cuda:{dev}")
     sp = synth_params(cfg, rank, world)
     n_local = cfg["pairs_per_slot"]
@@ -283,7 +286,10 @@ def main():
         else:
             g.scan_device(trace[s].data_ptr(), n_local)
         if world > 1:
-            PD.merge(g)
+            if args.merge == "stamps":
+                PD.merge_stamps_max(g)
+            else:
+                PD.merge(g)
         e1.record(stream)
         rep = g.reconstruct_leveled(k, theta)
         e2.record(stream)
@@ -427,7 +433,9 @@ def main():
         "data": "synthetic",
         "config": {"workload": cfg["workload"], "pairs_per_step_per_gpu": n_local,
                    "window_k": k, "theta": theta,
-                   "merge": "union-min: all-gather of each router's distinct pairs per slot",
+                   "merge": {"pairs": "union-min: all-gather of each router's distinct pairs per slot",
+                             "bitmap": "union-min: OR all-reduce of the slot's touched bitmaps",
+                             "stamps": "union-min: NCCL all-reduce(max) of the full stamp grid"}[args.merge],
                    "parallelism": f"{world} routers, one per GPU",
                    "l2": "inputs larger than L2 (800 MB per slot)"},
         "gbps_800B": round(value * 1e6 * PKT_BYTES * 8 / 1e9, 1),

@@ -314,6 +314,13 @@ __device__ __forceinline__ void stamp_pair(const ScanTables& t, const Geo& geo, 
 // exchanged between routers instead of a bitmap; paper_1803_11036_b200/dist.py).
 // Each thread takes 4 pairs per iteration and issues their 4 first probes
 // together before resolving any (the probes are the latency chain).
+// Per-CTA shared-memory front of the pair set: a direct-mapped cache of keys
+// this CTA has already resolved (found or inserted in the global set).  A hit
+// skips the global probe; entries only ever hold keys that are recorded in
+// this slot, so a lost entry (racing overwrite) costs a global probe, never a
+// touch.
+constexpr int kSmemCache = 2048;
+
 template <int H1MODE, int HIST, int BITS, int EXPORT>
 __global__ void __launch_bounds__(256) scan_dedup_kernel(const uint32_t* __restrict__ pairs, uint64_t n,
                                                          const HashTabs* __restrict__ tabs, Geo geo,
@@ -324,7 +331,9 @@ __global__ void __launch_bounds__(256) scan_dedup_kernel(const uint32_t* __restr
                                                          uint2* __restrict__ out_pairs,
                                                          unsigned long long* __restrict__ out_count) {
   __shared__ ScanTables t;
-  load_scan_tables(t, tabs);
+  __shared__ unsigned long long s_seen[kSmemCache];
+  for (int i = threadIdx.x; i < kSmemCache; i += blockDim.x) s_seen[i] = kEmptyKey;
+  load_scan_tables(t, tabs);  // ends with __syncthreads()
   const uint32_t now_slot = HIST ? now % K : 0;
   const uint32_t lane = threadIdx.x & 31;
   const uint64_t tid = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -353,15 +362,20 @@ __global__ void __launch_bounds__(256) scan_dedup_kernel(const uint32_t* __restr
     }
     uint64_t key[4], h[4];
     unsigned long long v[4];
+    bool probe[4];
 #pragma unroll
     for (int u = 0; u < 4; ++u) {
       key[u] = (uint64_t)c[u] << 32 | o[u];
       h[u] = pair_slot_hash(key[u]);
-      v[u] = valid[u] ? __ldca(table + (h[u] & table_mask)) : 0ull;
+      probe[u] = valid[u] && s_seen[(h[u] >> 40) & (kSmemCache - 1)] != key[u];
+      v[u] = probe[u] ? __ldca(table + (h[u] & table_mask)) : 0ull;
     }
     bool fresh[4];
 #pragma unroll
-    for (int u = 0; u < 4; ++u) fresh[u] = valid[u] && pair_resolve(table, table_mask, key[u], h[u], v[u]);
+    for (int u = 0; u < 4; ++u) {
+      fresh[u] = probe[u] && pair_resolve(table, table_mask, key[u], h[u], v[u]);
+      if (probe[u] && key[u] != kEmptyKey) s_seen[(h[u] >> 40) & (kSmemCache - 1)] = key[u];
+    }
     if (EXPORT) {
 #pragma unroll
       for (int u = 0; u < 4; ++u) {
