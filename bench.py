@@ -193,7 +193,7 @@ def main():
     ap.add_argument("--merge", default="pairs", choices=["pairs", "bitmap", "stamps"],
                     help="router exchange at N>1: distinct-pair lists (default), OR of touched "
                          "bitmaps, or the literal all-reduce(max) of the full stamp grid")
-    ap.add_argument("--scan-mode", default="auto", choices=["auto", "bitmap", "direct", "dedup"])
+    ap.add_argument("--scan-mode", default="auto", choices=["auto", "bitmap", "direct", "dedup", "binned"])
     ap.add_argument("--filter", type=int, default=-1, help="L1 duplicate probe 0/1 (-1 = default)")
     ap.add_argument("--ref-pairs", type=int, default=100_000_000,
                     help="pairs per reference step (bounded sample of the slot)")
@@ -252,7 +252,7 @@ def main():
     # --- setup (untimed): grid, trace resident in HBM, pinned host copy ------
     g = P.Grid(cfg["q"], cfg["r"], cfg["delta"], cfg["seed"], cfg["eta"], device=dev)
     g.set_stream(stream.cuda_stream)
-    g.scan_mode({"auto": -1, "bitmap": 0, "direct": 1, "dedup": 2}[args.scan_mode], args.filter)
+    g.scan_mode({"auto": -1, "bitmap": 0, "direct": 1, "dedup": 2, "binned": 3}[args.scan_mode], args.filter)
     g.track_window(cfg["k"])
     if world > 1 and args.merge != "stamps":
         PD.prepare(g, PD.PAIRS if args.merge == "pairs" else PD.BITMAP)
@@ -333,8 +333,8 @@ def main():
     launches = P.launch_count() - launches0
     slot += args.steps
     prof = {}
-    for name in ("scan", "commit", "hist_counts", "count", "hot_compact", "level2", "level_ext",
-                 "finalize", "merge"):
+    for name in ("bin", "scan", "commit", "hist_counts", "count", "hot_compact", "level2",
+                 "level_ext", "finalize", "merge"):
         t, n, u = g.profile_read(name)
         if n:
             prof[name] = {"ms": t, "launches": n, "units": u}

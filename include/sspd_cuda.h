@@ -166,7 +166,8 @@ sspd_status sspd_set_exchange(sspd_grid* g, int mode);
  * interleaved (cip, oip) pairs, valid until the next advance. */
 sspd_status sspd_grid_new_pairs(sspd_grid* g, uint32_t** dev_pairs, uint64_t* count);
 /* Scan strategy: mode 0 = deferred bitmap, 1 = direct stamping, 2 = direct
- * behind a per-slot set of seen pairs, -1 = auto (2 when the touched bitmap
+ * behind a per-slot set of seen pairs, 3 = as 2 after partitioning large
+ * device batches by pair-set region, -1 = auto (2 when the touched bitmap
  * would exceed 48 MiB, else 1);
  * filter 0/1 = L1 duplicate probe, -1 = keep.  Results are identical in
  * every mode, and modes may be mixed within a slot. */

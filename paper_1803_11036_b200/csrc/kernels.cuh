@@ -28,7 +28,6 @@ struct Geo {
   uint32_t q, r, delta, eta;
   uint32_t col_mask;     // 2^q - 1
   uint32_t low_mask;     // 2^(q-delta) - 1: overlap of adjacent blocks
-  uint32_t eta_shift;    // log2(eta) when eta is a power of two, else 0xFF
   uint32_t ncells;       // r * 2^q
   uint64_t n_rec;        // ncells * eta
 };
@@ -79,16 +78,9 @@ __device__ __forceinline__ uint4 ld_stream_u4(const void* p) {
   return v;
 }
 
-__device__ __forceinline__ uint2 ld_stream_u2(const void* p) {
-  uint2 v;
-  asm volatile("ld.global.nc.L1::no_allocate.v2.u32 {%0,%1}, [%2];"
-               : "=r"(v.x), "=r"(v.y)
-               : "l"(p));
-  return v;
-}
-
 // ---------------------------------------------------------------------------
-// SCAN: Rsea::update over a batch (rsea.cpp:29-53).  Two modes:
+// SCAN: Rsea::update over a batch (rsea.cpp:29-53).  Three modes, identical
+// in result (tests/test_gpu_parity.py runs them all):
 //
 //  * bitmap (deferred): each touch sets its recorder's bit in the per-slot
 //    touched bitmap with red.or; commit_kernel folds the bitmap into the
@@ -97,8 +89,11 @@ __device__ __forceinline__ uint2 ld_stream_u2(const void* p) {
 //    L2-resident atomic and the stamp grid is written once, in address order.
 //  * direct: each touch stamps its recorder in place (atomicMax(now) when the
 //    window ring is tracked -- the old stamp says which ring entry to move the
-//    bucket from -- else red.max).  Used when the bitmap itself would not fit
-//    in L2, where streaming it in the commit would cost more than it saves.
+//    bucket from -- else red.max).
+//  * dedup (scan_dedup_kernel below): direct stamping behind a per-slot set
+//    of the (cip, oip) pairs already seen, so a pair repeated within the slot
+//    costs one probe instead of r random read-modify-writes.  The default
+//    once the grid is far beyond L2 (Zipf traffic repeats pairs heavily).
 //
 // FILTER: probe the target word through L1 first and skip the atomic when the
 // touch is already recorded (bit set / stamp == now).  Both only move one way
@@ -255,9 +250,25 @@ __global__ void __launch_bounds__(256) scan_direct_kernel(const uint32_t* __rest
 constexpr uint64_t kEmptyKey = ~0ull;
 constexpr int kProbeLimit = 8;
 
+// The pair set is split into kPairBins regions; a key's region is the top
+// bits of its hash and its slot within the region the low bits, with linear
+// probing inside the region.  Binned scans (bin_count/bin_scatter below)
+// process the pairs region by region, so the active part of the set stays
+// in L2.
+constexpr int kPairBinBits = 6;
+constexpr int kPairBins = 1 << kPairBinBits;
+
 __device__ __forceinline__ uint64_t pair_slot_hash(uint64_t key) {
   uint64_t h = key * 0x9e3779b97f4a7c15ull;
   return h ^ (h >> 29);
+}
+
+__device__ __forceinline__ uint32_t pair_bin(uint64_t h) { return (uint32_t)(h >> (64 - kPairBinBits)); }
+
+// slot of probe i: region base | ((h + i) & region mask); mask = entries - 1
+__device__ __forceinline__ uint64_t pair_slot(uint64_t h, int i, uint64_t mask) {
+  const uint64_t region_mask = mask >> kPairBinBits;
+  return ((uint64_t)pair_bin(h) * (region_mask + 1)) | ((h + i) & region_mask);
 }
 
 // Resolve a probe that started with value `v` at probe distance 0.
@@ -265,7 +276,7 @@ __device__ __forceinline__ bool pair_resolve(unsigned long long* __restrict__ ta
                                              uint64_t h, unsigned long long v) {
   if (key == kEmptyKey) return true;
   for (int i = 0;; ) {
-    const uint64_t slot = (h + i) & mask;
+    const uint64_t slot = pair_slot(h, i, mask);
     if (v == key) return false;
     if (v == kEmptyKey) {
       const unsigned long long old = atomicCAS(table + slot, kEmptyKey, key);
@@ -273,7 +284,7 @@ __device__ __forceinline__ bool pair_resolve(unsigned long long* __restrict__ ta
       if (old == key) return false;
     }
     if (++i >= kProbeLimit) return true;
-    v = __ldca(table + ((h + i) & mask));
+    v = __ldca(table + pair_slot(h, i, mask));
   }
 }
 
@@ -368,7 +379,7 @@ __global__ void __launch_bounds__(256) scan_dedup_kernel(const uint32_t* __restr
       key[u] = (uint64_t)c[u] << 32 | o[u];
       h[u] = pair_slot_hash(key[u]);
       probe[u] = valid[u] && s_seen[(h[u] >> 40) & (kSmemCache - 1)] != key[u];
-      v[u] = probe[u] ? __ldca(table + (h[u] & table_mask)) : 0ull;
+      v[u] = probe[u] ? __ldca(table + pair_slot(h[u], 0, table_mask)) : 0ull;
     }
     bool fresh[4];
 #pragma unroll
@@ -393,6 +404,78 @@ __global__ void __launch_bounds__(256) scan_dedup_kernel(const uint32_t* __restr
 #pragma unroll
     for (int u = 0; u < 4; ++u)
       if (fresh[u]) stamp_pair<H1MODE, HIST, BITS>(t, geo, c[u], o[u], stamps, now, now_slot, hist, K, touched);
+  }
+}
+
+// BINNING (partition pairs by pair-set region before a dedup scan).  Two
+// passes over the input with identical chunking: a per-CTA histogram of
+// regions, then a scatter into region-major order at offsets from an
+// exclusive scan; the dedup kernel then walks the binned pairs in order.
+__global__ void __launch_bounds__(256) bin_count_kernel(const uint32_t* __restrict__ pairs, uint64_t n,
+                                                        uint64_t chunk, uint32_t* __restrict__ counts) {
+  __shared__ uint32_t s_hist[kPairBins];
+  for (int i = threadIdx.x; i < kPairBins; i += blockDim.x) s_hist[i] = 0;
+  __syncthreads();
+  const uint64_t lo = (uint64_t)blockIdx.x * chunk;
+  const uint64_t hi = min(n, lo + chunk);
+  for (uint64_t i = lo + threadIdx.x; i < hi; i += blockDim.x) {
+    const uint2 p = *reinterpret_cast<const uint2*>(pairs + 2 * i);
+    atomicAdd(&s_hist[pair_bin(pair_slot_hash((uint64_t)p.x << 32 | p.y))], 1u);
+  }
+  __syncthreads();
+  for (int b = threadIdx.x; b < kPairBins; b += blockDim.x) counts[(uint64_t)b * gridDim.x + blockIdx.x] = s_hist[b];
+}
+
+// Exclusive scan of counts laid out [bin][cta] (one CTA, in place).
+__global__ void __launch_bounds__(1024) bin_offsets_kernel(uint32_t* __restrict__ counts, uint32_t n_items) {
+  __shared__ uint32_t s_warp[32];
+  __shared__ uint32_t s_carry;
+  if (threadIdx.x == 0) s_carry = 0;
+  __syncthreads();
+  const uint32_t lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  for (uint32_t base = 0; base < n_items; base += blockDim.x) {
+    const uint32_t i = base + threadIdx.x;
+    const uint32_t v = i < n_items ? counts[i] : 0u;
+    uint32_t incl = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t t = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += t;
+    }
+    if (lane == 31) s_warp[wid] = incl;
+    __syncthreads();
+    if (wid == 0) {
+      const uint32_t w = lane < (blockDim.x >> 5) ? s_warp[lane] : 0u;
+      uint32_t wi = w;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t t = __shfl_up_sync(0xffffffffu, wi, o);
+        if (lane >= o) wi += t;
+      }
+      s_warp[lane] = wi - w;
+    }
+    __syncthreads();
+    const uint32_t excl = s_carry + s_warp[wid] + incl - v;
+    if (i < n_items) counts[i] = excl;
+    __syncthreads();
+    if (threadIdx.x == blockDim.x - 1) s_carry = excl + v;
+    __syncthreads();
+  }
+}
+
+__global__ void __launch_bounds__(256) bin_scatter_kernel(const uint32_t* __restrict__ pairs, uint64_t n,
+                                                          uint64_t chunk, const uint32_t* __restrict__ offsets,
+                                                          uint2* __restrict__ out) {
+  __shared__ uint32_t s_pos[kPairBins];
+  for (int b = threadIdx.x; b < kPairBins; b += blockDim.x)
+    s_pos[b] = offsets[(uint64_t)b * gridDim.x + blockIdx.x];
+  __syncthreads();
+  const uint64_t lo = (uint64_t)blockIdx.x * chunk;
+  const uint64_t hi = min(n, lo + chunk);
+  for (uint64_t i = lo + threadIdx.x; i < hi; i += blockDim.x) {
+    const uint2 p = *reinterpret_cast<const uint2*>(pairs + 2 * i);
+    const uint32_t pos = atomicAdd(&s_pos[pair_bin(pair_slot_hash((uint64_t)p.x << 32 | p.y))], 1u);
+    out[pos] = p;
   }
 }
 

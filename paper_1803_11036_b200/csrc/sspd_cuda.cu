@@ -138,7 +138,8 @@ struct sspd_grid {
   ReconMeta* meta_host = nullptr;  // pinned mirror of meta
   uint64_t cap_alloc = 0;       // tuples per candidate buffer
   int scan_filter = 1;          // L1 duplicate filter in the scan (SSPD_SCAN_FILTER=0 disables)
-  int scan_mode = -1;           // 0 bitmap, 1 direct, 2 dedup, -1 auto
+  int scan_mode = -1;           // 0 bitmap, 1 direct, 2 dedup, 3 binned dedup, -1 auto
+  DevBuf bin_counts, binned;    // binned dedup: per-(region, CTA) counts, partitioned pairs
   DevBuf pairset;               // dedup mode: per-slot set of seen (cip, oip) pairs
   uint64_t pairset_mask = 0;
   bool pairset_dirty = false;   // holds keys from the current slot
@@ -410,7 +411,6 @@ sspd_status sspd_grid_create(int device, uint32_t q, uint32_t r, uint32_t delta,
   g->geo.eta = eta;
   g->geo.col_mask = (1u << q) - 1u;
   g->geo.low_mask = (1u << (q - delta)) - 1u;
-  g->geo.eta_shift = (eta & (eta - 1)) == 0 ? (uint32_t)__builtin_ctz(eta) : 0xFFu;
   g->geo.ncells = r << q;
   g->geo.n_rec = (uint64_t)g->geo.ncells * eta;
   g->by_eta = Div40::make(eta);
@@ -421,6 +421,7 @@ sspd_status sspd_grid_create(int device, uint32_t q, uint32_t r, uint32_t delta,
     if (!std::strcmp(m, "bitmap")) g->scan_mode = 0;
     if (!std::strcmp(m, "direct")) g->scan_mode = 1;
     if (!std::strcmp(m, "dedup")) g->scan_mode = 2;
+    if (!std::strcmp(m, "binned")) g->scan_mode = 3;
   }
   g->n_words = (g->geo.n_rec + 31) / 32;
   auto cleanup = [&](const std::string& why) {
@@ -474,7 +475,7 @@ sspd_status sspd_grid_destroy(sspd_grid* g) {
     if (g->meta_host) cudaFreeHost(g->meta_host);
     for (DevBuf* b : {&g->stage[0], &g->stage[1], &g->counts, &g->hot_cols, &g->hot_rowcnt, &g->hotT,
                       &g->tupA, &g->tupB, &g->misc, &g->meta, &g->surv, &g->pairset, &g->newpairs,
-                      &g->newpairs_count})
+                      &g->newpairs_count, &g->bin_counts, &g->binned})
       b->release();
     for (auto& r : g->prof) {
       cudaEventDestroy(r.a);
@@ -560,11 +561,17 @@ sspd_status sspd_scan(sspd_grid* g, const uint32_t* pairs, uint64_t n, int pairs
   // auto: never leave deferred work after the last (PCIe) chunk of a host
   // scan; use the pair set once the grid is far beyond L2.
   int mode = g->scan_mode;
-  if (g->export_pairs) mode = 2;  // only the pair set knows which pairs are new
   // Measured (profiles/r01_ab_*.txt): with the touched bitmap L2-sized (C1)
   // direct stamping is fastest for host and device pairs alike (0.42 vs 0.46
   // ms/slot bitmap+commit); beyond L2 (C2) the pair set wins (3.9 vs 11.9).
+  // Binning by pair-set region first (mode 3) makes the probes L2 hits but
+  // measured slower overall (2.2 + 3.6 ms): the random stamp atomics dominate.
   if (mode < 0) mode = g->n_words * 4 > (48ull << 20) ? 2 : 1;
+  if (g->export_pairs && mode < 2) mode = 2;  // only the pair set knows which pairs are new
+  // binning pays for itself on large device batches (8-byte aligned pairs)
+  const bool use_bins = mode == 3 && pairs_on_device && n >= (4ull << 20) && n < (1ull << 31) &&
+                      (reinterpret_cast<uintptr_t>(pairs) & 7u) == 0;
+  if (mode == 3) mode = 2;
   const bool direct = mode == 1;
   const bool dedup = mode == 2;
   const bool hist = (direct || dedup) && g->K && g->hist_valid;
@@ -671,6 +678,23 @@ sspd_status sspd_scan(sspd_grid* g, const uint32_t* pairs, uint64_t n, int pairs
   // Direct scans stamp in place; only recorded bits (multi-router) or a
   // stale window ring leave work for the commit.
   if (!(direct || dedup) || (bits && !g->export_pairs)) g->pending = true;
+  if (pairs_on_device && use_bins) {
+    // partition by pair-set region, then one dedup pass in region order
+    const unsigned G = (unsigned)sm_count(g->device) * 8;
+    const uint64_t chunk = (n + G - 1) / G;
+    if (g->bin_counts.ensure((size_t)kPairBins * G * 4) != cudaSuccess || g->binned.ensure(n * 8) != cudaSuccess)
+      return fail(SSPD_CUDA_ERROR, "CUDA error: out of memory (binning)");
+    uint32_t* counts = g->bin_counts.as<uint32_t>();
+    {
+      Prof p(g, "bin", n);
+      bin_count_kernel<<<G, 256, 0, g->stream>>>(pairs, n, chunk, counts);
+      bin_offsets_kernel<<<1, 1024, 0, g->stream>>>(counts, kPairBins * G);
+      bin_scatter_kernel<<<G, 256, 0, g->stream>>>(pairs, n, chunk, counts, g->binned.as<uint2>());
+    }
+    g_launches.fetch_add(2, std::memory_order_relaxed);
+    launch(g->binned.as<uint32_t>(), n);
+    return check_launch();
+  }
   if (pairs_on_device) {
     launch(pairs, n);
     return check_launch();
@@ -1129,7 +1153,7 @@ sspd_status sspd_scan_mode(sspd_grid* g, int mode, int filter) {
   DeviceGuard dg(g->device);
   sspd_status s = commit_locked(g);
   if (s) return s;
-  if (mode >= -1 && mode <= 2) g->scan_mode = mode;
+  if (mode >= -1 && mode <= 3) g->scan_mode = mode;
   if (filter >= 0) g->scan_filter = filter != 0;
   return SSPD_OK;
 }

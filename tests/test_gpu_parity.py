@@ -30,8 +30,8 @@ def dets_equal(a, b):
     return [(d.cip, d.estimate) for d in a] == [(d.cip, d.estimate) for d in b]
 
 
-MODES = [(0, 1), (0, 0), (1, 1), (1, 0), (2, -1), (-1, -1)]  # (scan mode, L1 filter)
-MODE_IDS = ["bitmap+filter", "bitmap", "direct+filter", "direct", "dedup", "auto"]
+MODES = [(0, 1), (0, 0), (1, 1), (1, 0), (2, -1), (3, -1), (-1, -1)]  # (scan mode, L1 filter)
+MODE_IDS = ["bitmap+filter", "bitmap", "direct+filter", "direct", "dedup", "binned", "auto"]
 
 
 @pytest.mark.parametrize("mode", MODES, ids=MODE_IDS)
@@ -334,6 +334,70 @@ def test_repeated_pairs_and_imports_within_a_slot(gpu, mode):
         # ... and re-scan the same pairs in the same slot: they must re-touch
         g.scan_batch(rep[:5000])
         o.scan(rep[:5000])
+        assert np.array_equal(g.cells(), o.cells()), s
+        assert np.array_equal(g.active_counts(3), o.active_counts(3)), s
+        g.advance_slot()
+        o.advance()
+
+
+def _hot_grid(gpu, hot_rows, geo=DESK, seed=0x31):
+    """A grid whose hot columns are exactly hot_rows[row] (every bucket of
+    those estimators touched this slot), built through the cells() view."""
+    o = O.OracleGrid(seed=seed, **geo)
+    c = o.cells_view()
+    eta, ncol = geo["eta"], 1 << geo["q"]
+    for row, cols in enumerate(hot_rows):
+        for col in cols:
+            off = (row * ncol + col) * eta
+            c[off:off + eta] = 0
+    g = gpu.Grid(seed=seed, **geo)
+    g.set_cells(o.cells())
+    return g, o
+
+
+def test_candidate_buffers_grow_past_initial_allocation(gpu):
+    """Level counts above the initial 2^20-tuple buffers (but under the cap)
+    force the device-side re-run; results must still equal the oracle's, and
+    a smaller cap must overflow at the same level with the same count."""
+    rows = [range(256), range(256), range(256), range(8), range(1)]
+    g, o = _hot_grid(gpu, rows)
+    ref = o.reconstruct(30, 128.0)
+    assert [(d.cip, d.estimate) for d in g.reconstruct_leveled(30, 128.0)] == \
+        [(d.cip, d.estimate) for d in ref]
+    with pytest.raises(O.CandidateOverflow) as want:
+        o.reconstruct(30, 128.0, cap=5_000_000)
+    g.candidate_cap = 5_000_000
+    with pytest.raises(gpu.CandidateOverflow) as got:
+        g.reconstruct_leveled(30, 128.0)
+    assert (got.value.level, got.value.count) == (want.value.level, want.value.count)
+
+
+def test_empty_hot_row_returns_nothing_even_past_cap(gpu):
+    """rsea.cpp:173-174: any row without hot columns ends reconstruction
+    before the level-2 cap check, however many triples rows 0-2 would give."""
+    rows = [range(1024), range(1024), range(1024), range(4), []]
+    g, o = _hot_grid(gpu, rows)
+    g.candidate_cap = 10
+    assert g.reconstruct_leveled(30, 128.0) == []
+    assert o.reconstruct(30, 128.0, cap=10) == []
+
+
+@pytest.mark.parametrize("mode", [(2, -1), (3, -1)], ids=["dedup", "binned"])
+def test_large_device_batches(gpu, mode):
+    """Device-resident batches big enough to be binned by pair-set region
+    (>= 4M pairs), heavy repetition, window ring on: same grid and counts as
+    the oracle."""
+    import torch
+
+    g, o = make_pair(gpu, DESK, 0x99)
+    g.scan_mode(*mode)
+    g.track_window(3)
+    rng = O.Mt64(99)
+    base = rng.pairs(200_000)
+    for s in range(3):
+        p = base[rng.draw(5_000_000) % 200_000]
+        g.scan_batch(torch.from_numpy(p.view(np.int32)).cuda())
+        o.scan(p)
         assert np.array_equal(g.cells(), o.cells()), s
         assert np.array_equal(g.active_counts(3), o.active_counts(3)), s
         g.advance_slot()
