@@ -429,8 +429,11 @@ def main():
     line = {
         "metric": metric, "value": round(value, 3), "unit": unit, "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms / args.steps, 3),
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u32",
-        "data": "synthetic",
+        "higher_is_better": True, "scaling": "weak",
+        # BASELINE.md's only published packets/s is the paper's GSSD 109 Mpkt/s on a
+        # GTX 950 at the paper parameters -- the C1 geometry
+        "vs_baseline": round(value / 109.0, 2) if args.config == "c1" else None,
+        "dtype": "u32", "data": "synthetic",
         "config": {"workload": cfg["workload"], "pairs_per_step_per_gpu": n_local,
                    "window_k": k, "theta": theta,
                    "merge": {"pairs": "union-min: all-gather of each router's distinct pairs per slot",

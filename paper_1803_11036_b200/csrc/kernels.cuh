@@ -599,54 +599,91 @@ __global__ void __launch_bounds__(256) hist_rebuild_kernel(const uint32_t* __res
 }
 
 // ---------------------------------------------------------------------------
-// HOT SETS: ordered compaction of hot columns per row (rsea.cpp:65-84) and a
-// transposed hot bitmap for the reconstruction joins: for key = col & low_mask
-// and j = col >> (q - delta), bit j of the 2^delta-bit row segment of key.
-// One CTA per row, 1024 threads.
-__global__ void __launch_bounds__(1024) hot_compact_kernel(const uint32_t* __restrict__ counts, Geo geo,
-                                                           uint64_t cutoff, uint32_t* __restrict__ cols_out,
-                                                           uint32_t* __restrict__ row_counts,
-                                                           uint32_t* __restrict__ hotT,
-                                                           uint32_t words_per_key) {
-  const uint32_t row = blockIdx.x;
+// HOT SETS, parallel form (two launches over all r*2^q cells).
+// hot_mark: one thread per cell decides hot (R_k >= cutoff, with R_k from
+// the per-cell counts or straight from the window ring), publishes the hot
+// bitmap word of its warp, the CTA's hot count, and the transposed bits.
+// hot_write: each CTA adds up the counts of the row's earlier chunks and
+// writes its hot columns in ascending order (rsea.cpp:65-84).
+constexpr int kHotChunk = 1024;
+
+__global__ void __launch_bounds__(kHotChunk) hot_mark_kernel(const uint32_t* __restrict__ counts,
+                                                            const uint32_t* __restrict__ hist, uint32_t K,
+                                                            uint32_t now, uint32_t k, Geo geo, uint64_t cutoff,
+                                                            uint32_t* __restrict__ hot_words,
+                                                            uint32_t* __restrict__ chunk_counts,
+                                                            uint32_t* __restrict__ hotT, uint32_t words_per_key) {
   const uint32_t ncol = 1u << geo.q;
-  const uint32_t kbits = geo.q - geo.delta;
-  uint32_t* myT = hotT + (uint64_t)row * ((uint64_t)words_per_key << kbits);
-  uint32_t* myCols = cols_out + (uint64_t)row * ncol;
-  __shared__ uint32_t s_warp[32];
-  __shared__ uint32_t s_base;
-  if (threadIdx.x == 0) s_base = 0;
-  __syncthreads();
-  const uint32_t lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  for (uint32_t c0 = 0; c0 < ncol; c0 += blockDim.x) {
-    const uint32_t col = c0 + threadIdx.x;
-    const bool hot = col < ncol && counts[(uint64_t)row * ncol + col] >= cutoff;
-    const uint32_t b = __ballot_sync(0xffffffffu, hot);
-    if (lane == 0) s_warp[wid] = __popc(b);
-    __syncthreads();
-    if (wid == 0) {
-      uint32_t v = lane < (blockDim.x >> 5) ? s_warp[lane] : 0;
-      uint32_t incl = v;
-#pragma unroll
-      for (int o = 1; o < 32; o <<= 1) {
-        uint32_t t = __shfl_up_sync(0xffffffffu, incl, o);
-        if (lane >= o) incl += t;
-      }
-      s_warp[lane] = incl - v;  // exclusive
+  const uint32_t chunks = (ncol + kHotChunk - 1) / kHotChunk;
+  const uint32_t row = blockIdx.x / chunks, chunk = blockIdx.x % chunks;
+  const uint32_t col = chunk * kHotChunk + threadIdx.x;
+  const uint32_t cell = (row << geo.q) | col;
+  bool hot = false;
+  if (col < ncol) {
+    uint32_t rk;
+    if (hist) {
+      rk = 0;
+      for (uint32_t j = 0; j < k; ++j) rk += hist[(uint64_t)((now - j) % K) * geo.ncells + cell];
+    } else {
+      rk = counts[cell];
     }
-    __syncthreads();
-    const uint32_t pos = s_base + s_warp[wid] + __popc(b & ((1u << lane) - 1u));
-    if (hot) {
-      myCols[pos] = col;
-      const uint32_t key = col & geo.low_mask;
-      const uint32_t j = col >> kbits;
-      atomicOr(myT + (uint64_t)key * words_per_key + (j >> 5), 1u << (j & 31));
-    }
-    __syncthreads();
-    if (threadIdx.x == blockDim.x - 1) s_base = pos + (hot ? 1u : 0u);
-    __syncthreads();
+    hot = rk >= cutoff;
   }
-  if (threadIdx.x == 0) row_counts[row] = s_base;
+  const uint32_t b = __ballot_sync(0xffffffffu, hot);
+  __shared__ uint32_t s_sum;
+  if (threadIdx.x == 0) s_sum = 0;
+  __syncthreads();
+  const uint32_t wpr = (ncol + 31) / 32;  // words per row: rows never share a word
+  if ((threadIdx.x & 31) == 0) {
+    if (col < ncol) hot_words[row * wpr + (col >> 5)] = b;
+    if (b) atomicAdd(&s_sum, (uint32_t)__popc(b));
+  }
+  if (hot) {
+    const uint32_t kbits = geo.q - geo.delta;
+    uint32_t* myT = hotT + (uint64_t)row * ((uint64_t)words_per_key << kbits);
+    const uint32_t key = col & geo.low_mask, j = col >> kbits;
+    atomicOr(myT + (uint64_t)key * words_per_key + (j >> 5), 1u << (j & 31));
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) chunk_counts[blockIdx.x] = s_sum;
+}
+
+__global__ void __launch_bounds__(kHotChunk) hot_write_kernel(const uint32_t* __restrict__ hot_words, Geo geo,
+                                                             const uint32_t* __restrict__ chunk_counts,
+                                                             uint32_t* __restrict__ cols_out,
+                                                             uint32_t* __restrict__ row_counts) {
+  const uint32_t ncol = 1u << geo.q;
+  const uint32_t chunks = (ncol + kHotChunk - 1) / kHotChunk;
+  const uint32_t row = blockIdx.x / chunks, chunk = blockIdx.x % chunks;
+  const uint32_t lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  __shared__ uint32_t s_base, s_warp[kHotChunk / 32];
+  if (wid == 0) {
+    uint32_t v = 0;
+    for (uint32_t c = lane; c < chunk; c += 32) v += chunk_counts[row * chunks + c];
+#pragma unroll
+    for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    if (lane == 0) s_base = v;
+  }
+  const uint32_t col = chunk * kHotChunk + threadIdx.x;
+  const uint32_t wpr = (ncol + 31) / 32;
+  const uint32_t w = col < ncol ? hot_words[row * wpr + (col >> 5)] : 0u;
+  if (lane == 0) s_warp[wid] = __popc(w);
+  __syncthreads();
+  if (wid == 0) {
+    const uint32_t v = lane < kHotChunk / 32 ? s_warp[lane] : 0u;
+    uint32_t incl = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t t = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += t;
+    }
+    s_warp[lane] = incl - v;
+  }
+  __syncthreads();
+  if ((w >> lane) & 1u)
+    cols_out[(uint64_t)row * ncol + s_base + s_warp[wid] + __popc(w & ((1u << lane) - 1u))] = col;
+  if (chunk == chunks - 1 && threadIdx.x == 0)
+    row_counts[row] = s_base + chunk_counts[row * chunks + chunk];
 }
 
 // ---------------------------------------------------------------------------

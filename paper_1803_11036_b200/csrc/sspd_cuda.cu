@@ -134,6 +134,7 @@ struct sspd_grid {
   cudaEvent_t ev_copy[2] = {nullptr, nullptr}, ev_used[2] = {nullptr, nullptr};
   DevBuf stage[2];       // host pair staging
   DevBuf counts, hot_cols, hot_rowcnt, hotT, tupA, tupB, misc;
+  DevBuf hot_words, hot_chunks;  // parallel hot compaction scratch
   DevBuf meta, surv;            // reconstruction bookkeeping, survivors
   ReconMeta* meta_host = nullptr;  // pinned mirror of meta
   uint64_t cap_alloc = 0;       // tuples per candidate buffer
@@ -285,22 +286,38 @@ uint32_t words_per_key(const sspd_grid* g) {
 // copied to host_rowcnt (synchronises).
 sspd_status hot_locked(sspd_grid* g, uint32_t k, uint64_t cutoff, std::vector<uint32_t>* host_rowcnt,
                        uint32_t* d_rowcnt) {
-  sspd_status s = counts_locked(g, k);
+  sspd_status s = commit_locked(g);
   if (s) return s;
+  // R_k straight from the window ring inside hot_mark when it covers k;
+  // otherwise per-cell counts first (full pass over the stamps).
+  const bool ring = k >= 1 && k <= 0xFFFFu && g->K && k <= g->K;
+  if (ring) {
+    s = hist_rebuild_locked(g);
+    if (s) return s;
+  } else {
+    s = counts_locked(g, k);
+    if (s) return s;
+  }
   const uint32_t ncol = 1u << g->q;
+  const uint32_t chunks = (ncol + kHotChunk - 1) / kHotChunk;
   const uint32_t wpk = words_per_key(g);
   const size_t t_words = (size_t)g->r * ((size_t)wpk << (g->q - g->delta));
   if (g->hot_cols.ensure((size_t)g->r * ncol * 4) != cudaSuccess ||
-      g->hot_rowcnt.ensure((size_t)g->r * 4) != cudaSuccess || g->hotT.ensure(t_words * 4) != cudaSuccess)
+      g->hot_rowcnt.ensure((size_t)g->r * 4) != cudaSuccess || g->hotT.ensure(t_words * 4) != cudaSuccess ||
+      g->hot_words.ensure((size_t)g->r * ((ncol + 31) / 32) * 4) != cudaSuccess ||
+      g->hot_chunks.ensure((size_t)g->r * chunks * 4) != cudaSuccess)
     return fail(SSPD_CUDA_ERROR, "CUDA error: out of memory (hot sets)");
   if (!d_rowcnt) d_rowcnt = g->hot_rowcnt.as<uint32_t>();
   CU(cudaMemsetAsync(g->hotT.p, 0, t_words * 4, g->stream));
   {
     Prof p(g, "hot_compact", g->geo.ncells);
-    hot_compact_kernel<<<g->r, 1024, 0, g->stream>>>(g->counts.as<uint32_t>(), g->geo, cutoff,
-                                                     g->hot_cols.as<uint32_t>(), d_rowcnt,
-                                                     g->hotT.as<uint32_t>(), wpk);
+    hot_mark_kernel<<<g->r * chunks, kHotChunk, 0, g->stream>>>(
+        g->counts.as<uint32_t>(), ring ? g->hist : nullptr, g->K, g->now, k, g->geo, cutoff,
+        g->hot_words.as<uint32_t>(), g->hot_chunks.as<uint32_t>(), g->hotT.as<uint32_t>(), wpk);
+    hot_write_kernel<<<g->r * chunks, kHotChunk, 0, g->stream>>>(
+        g->hot_words.as<uint32_t>(), g->geo, g->hot_chunks.as<uint32_t>(), g->hot_cols.as<uint32_t>(), d_rowcnt);
   }
+  g_launches.fetch_add(1, std::memory_order_relaxed);
   s = check_launch();
   if (s) return s;
   if (host_rowcnt) {
@@ -475,7 +492,7 @@ sspd_status sspd_grid_destroy(sspd_grid* g) {
     if (g->meta_host) cudaFreeHost(g->meta_host);
     for (DevBuf* b : {&g->stage[0], &g->stage[1], &g->counts, &g->hot_cols, &g->hot_rowcnt, &g->hotT,
                       &g->tupA, &g->tupB, &g->misc, &g->meta, &g->surv, &g->pairset, &g->newpairs,
-                      &g->newpairs_count, &g->bin_counts, &g->binned})
+                      &g->newpairs_count, &g->bin_counts, &g->binned, &g->hot_words, &g->hot_chunks})
       b->release();
     for (auto& r : g->prof) {
       cudaEventDestroy(r.a);

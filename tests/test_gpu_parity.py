@@ -18,6 +18,7 @@ DESK = dict(q=10, r=5, delta=8, eta=256)       # desk_preset (pipeline.cpp:7-14)
 PAPER = dict(q=14, r=5, delta=6, eta=2048)     # RunConfig defaults (pipeline.hpp:16-26)
 ODD = dict(q=12, r=7, delta=4, eta=1000)       # non-power-of-two eta: u64 % eta path
 WIDE = dict(q=16, r=8, delta=6, eta=64)        # (r-2)*delta >= 32: masked shifts
+TINY = dict(q=4, r=12, delta=3, eta=40)         # 16 columns per row, non-power-of-two eta
 
 
 def make_pair(gpu, geo, seed):
@@ -35,7 +36,8 @@ MODE_IDS = ["bitmap+filter", "bitmap", "direct+filter", "direct", "dedup", "binn
 
 
 @pytest.mark.parametrize("mode", MODES, ids=MODE_IDS)
-@pytest.mark.parametrize("geo", [DESK, PAPER, ODD, WIDE], ids=["desk", "paper", "odd_eta", "wide_r"])
+@pytest.mark.parametrize("geo", [DESK, PAPER, ODD, WIDE, TINY],
+                         ids=["desk", "paper", "odd_eta", "wide_r", "tiny_q"])
 def test_scan_advance_bit_exact(gpu, geo, mode):
     g, o = make_pair(gpu, geo, 0x5eed)
     g.scan_mode(*mode)
@@ -402,3 +404,24 @@ def test_large_device_batches(gpu, mode):
         assert np.array_equal(g.active_counts(3), o.active_counts(3)), s
         g.advance_slot()
         o.advance()
+
+
+@pytest.mark.parametrize("geo", [TINY, ODD, WIDE], ids=["tiny_q", "odd_eta", "wide_r"])
+def test_reconstruct_unusual_geometries(gpu, geo):
+    """Hot sets and reports on geometries with few columns per row (rows
+    sharing a 32-bit word of the hot bitmap), non-power-of-two eta and r=8."""
+    g, o, _ = planted_state(gpu, geo, 0x5151, 4, 3 * geo["eta"], 4 * geo["eta"], 3000, 61)
+    for k in (1, 5):
+        theta = geo["eta"] / 2.0
+        gh, oh = g.hot_sets(k, theta), o.hot_sets(k, theta)
+        assert [h.tolist() for h in gh] == [h.tolist() for h in oh]
+        try:
+            ref = o.reconstruct(k, theta, cap=1 << 20)
+        except O.CandidateOverflow as e:
+            g.candidate_cap = 1 << 20
+            with pytest.raises(gpu.CandidateOverflow) as got:
+                g.reconstruct_leveled(k, theta)
+            assert (got.value.level, got.value.count) == (e.level, e.count)
+            continue
+        g.candidate_cap = 1 << 20
+        assert dets_equal(g.reconstruct_leveled(k, theta), ref)
