@@ -355,7 +355,7 @@ sspd_status queue_finalize(sspd_grid* g, const uint32_t* tuples, uint64_t in_cap
   ReconMeta* meta = g->meta.as<ReconMeta>();
   {
     Prof p(g, "finalize_check", in_cap);
-    finalize_check_kernel<<<grid_blocks(g, in_cap, 256, 8), 256, 0, g->stream>>>(tuples, in_cap, g->d_tabs,
+    finalize_check_kernel<<<grid_blocks(g, in_cap, 256, 2), 256, 0, g->stream>>>(tuples, in_cap, g->d_tabs,
                                                                                    g->geo, meta, s_idx, s_cip);
   }
   sspd_status s = check_launch();
@@ -924,7 +924,9 @@ sspd_status sspd_reconstruct(sspd_grid* g, uint32_t k, uint64_t cutoff, uint64_t
     if (s) return s;
     const uint32_t* cols = g->hot_cols.as<uint32_t>();
     const uint32_t* T = g->hotT.as<uint32_t>();
-    const unsigned blocks = (unsigned)sm_count(g->device) * 8;
+    // level sizes live on the device; a modest persistent grid keeps the
+    // (usually tiny) joins cheap to launch and still strides large levels
+    const unsigned blocks = (unsigned)sm_count(g->device) * 2;
     {
       Prof p(g, "level2", 0);
       level2_kernel<<<blocks, 256, 0, g->stream>>>(cols, ncol, T + 2 * t_stride, wpk, g->geo, g->tupA.as<uint32_t>(),

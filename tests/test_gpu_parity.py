@@ -425,3 +425,32 @@ def test_reconstruct_unusual_geometries(gpu, geo):
             continue
         g.candidate_cap = 1 << 20
         assert dets_equal(g.reconstruct_leveled(k, theta), ref)
+
+
+def test_cabi_argument_errors(gpu):
+    """Entry points reject bad arguments with the reference's exception
+    classes instead of touching memory."""
+    import ctypes as C
+
+    L = gpu.load()
+    g = gpu.Grid(**DESK)
+    n = g.recorder_count()
+    buf = np.zeros(16, dtype=np.uint16)
+    ptr = buf.ctypes.data_as(C.POINTER(C.c_uint16))
+    assert L.sspd_get_distances(g._h, ptr, n - 8, 16) == gpu._cabi.SSPD_OUT_OF_RANGE
+    assert L.sspd_put_distances(g._h, ptr, n + 1, 1) == gpu._cabi.SSPD_OUT_OF_RANGE
+    assert L.sspd_scan(g._h, None, 10, 0) == gpu._cabi.SSPD_INVALID_ARGUMENT
+    assert L.sspd_scan(g._h, None, 0, 0) == gpu._cabi.SSPD_OK  # empty batch is a no-op
+    with pytest.raises(gpu.InvalidArgument):
+        gpu.merge_rseas([g], out=gpu.Grid(q=10, r=5, delta=8, eta=128))
+    with pytest.raises(gpu.InvalidArgument):
+        gpu.Grid(q=14, r=5, delta=6, eta=2048, device=99)
+    # a grid on a stream of the caller's choosing still answers correctly
+    import torch
+
+    s = torch.cuda.Stream()
+    g.set_stream(s.cuda_stream)
+    g.update(1, 2)
+    assert int((g.cells() == 0).sum()) >= 1
+    g.set_stream(None)
+    assert g.now == gpu.BASE_NOW
