@@ -190,9 +190,10 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--window", type=int, default=0, help="override the window k (C4 sweeps)")
-    ap.add_argument("--merge", default="pairs", choices=["pairs", "bitmap", "stamps"],
-                    help="router exchange at N>1: distinct-pair lists (default), OR of touched "
-                         "bitmaps, or the literal all-reduce(max) of the full stamp grid")
+    ap.add_argument("--merge", default="pairs", choices=["pairs", "push", "bitmap", "stamps"],
+                    help="router exchange at N>1: distinct-pair lists all-gathered after the scan "
+                         "(default), the same lists pushed over NVLink during the scan, OR of "
+                         "touched bitmaps, or the literal all-reduce(max) of the full stamp grid")
     ap.add_argument("--scan-mode", default="auto", choices=["auto", "bitmap", "direct", "dedup", "binned"])
     ap.add_argument("--filter", type=int, default=-1, help="L1 duplicate probe 0/1 (-1 = default)")
     ap.add_argument("--ref-pairs", type=int, default=100_000_000,
@@ -255,7 +256,8 @@ def main():
     g.scan_mode({"auto": -1, "bitmap": 0, "direct": 1, "dedup": 2, "binned": 3}[args.scan_mode], args.filter)
     g.track_window(cfg["k"])
     if world > 1 and args.merge != "stamps":
-        PD.prepare(g, PD.PAIRS if args.merge == "pairs" else PD.BITMAP)
+        PD.prepare(g, {"pairs": PD.PAIRS, "push": PD.PUSH, "bitmap": PD.BITMAP}[args.merge],
+                   region_cap=min(cfg["pairs_per_slot"], 32 << 20))
     cdf = torch.from_numpy(zipf_cdf(L, cfg).view(np.int64)).to(f"cuda:{dev}")
     sp = synth_params(cfg, rank, world)
     n_local = cfg["pairs_per_slot"]
@@ -437,6 +439,7 @@ def main():
         "config": {"workload": cfg["workload"], "pairs_per_step_per_gpu": n_local,
                    "window_k": k, "theta": theta,
                    "merge": {"pairs": "union-min: all-gather of each router's distinct pairs per slot",
+                             "push": "union-min: distinct pairs pushed to peers over NVLink during the scan",
                              "bitmap": "union-min: OR all-reduce of the slot's touched bitmaps",
                              "stamps": "union-min: NCCL all-reduce(max) of the full stamp grid"}[args.merge],
                    "parallelism": f"{world} routers, one per GPU",

@@ -162,6 +162,16 @@ sspd_status sspd_commit(sspd_grid* g);
  * (cip, oip) pairs (scans then always use the pair set); routers all-gather
  * the lists and scan each other's.  0: off. */
 sspd_status sspd_set_exchange(sspd_grid* g, int mode);
+/* Fused exchange (with mode 2): while scanning, also store each new pair into
+ * every peer router's inbox over NVLink.  dev_peer_ptrs: device array of
+ * `world` pointers (peer-mapped symmetric memory, e.g. torch
+ * _SymmetricMemory.buffer_ptrs_dev), each the base of `world` regions of
+ * `region_cap` (cip, oip) pairs; router `rank` writes region `rank` of every
+ * other router's inbox at the position its pair has in the local list.
+ * Positions >= region_cap are not pushed (the caller falls back to the list).
+ * world <= 1 disables. */
+sspd_status sspd_set_push(sspd_grid* g, void* dev_peer_ptrs, uint32_t world, uint32_t rank,
+                          uint64_t region_cap);
 /* This slot's distinct pairs (exchange mode 2): device pointer to `count`
  * interleaved (cip, oip) pairs, valid until the next advance. */
 sspd_status sspd_grid_new_pairs(sspd_grid* g, uint32_t** dev_pairs, uint64_t* count);

@@ -323,6 +323,12 @@ __device__ __forceinline__ void stamp_pair(const ScanTables& t, const Geo& geo, 
 
 // EXPORT: append each new pair to `out_pairs` (the slot's distinct pairs,
 // exchanged between routers instead of a bitmap; paper_1803_11036_b200/dist.py).
+// PUSH (with EXPORT): also store each new pair, at the same position, into
+// every peer router's inbox region for this router -- P2P stores over NVLink
+// into symmetric memory, so the exchange overlaps the scan instead of
+// following it.  `peers[p]` is router p's inbox (base of world regions of
+// `region_cap` pairs); positions past region_cap are dropped and the host
+// falls back to an all-gather for that slot.
 // Each thread takes 4 pairs per iteration and issues their 4 first probes
 // together before resolving any (the probes are the latency chain).
 // Per-CTA shared-memory front of the pair set: a direct-mapped cache of keys
@@ -332,7 +338,13 @@ __device__ __forceinline__ void stamp_pair(const ScanTables& t, const Geo& geo, 
 // touch.
 constexpr int kSmemCache = 2048;
 
-template <int H1MODE, int HIST, int BITS, int EXPORT>
+struct PushArgs {
+  uint2* const* peers;  // device array of `world` inbox pointers (peer-mapped)
+  uint32_t world, rank;
+  uint64_t region_cap;
+};
+
+template <int H1MODE, int HIST, int BITS, int EXPORT, int PUSH = 0>
 __global__ void __launch_bounds__(256) scan_dedup_kernel(const uint32_t* __restrict__ pairs, uint64_t n,
                                                          const HashTabs* __restrict__ tabs, Geo geo,
                                                          unsigned long long* __restrict__ table,
@@ -340,7 +352,8 @@ __global__ void __launch_bounds__(256) scan_dedup_kernel(const uint32_t* __restr
                                                          uint32_t now, uint32_t* __restrict__ hist, uint32_t K,
                                                          uint32_t* __restrict__ touched,
                                                          uint2* __restrict__ out_pairs,
-                                                         unsigned long long* __restrict__ out_count) {
+                                                         unsigned long long* __restrict__ out_count,
+                                                         PushArgs push = PushArgs{}) {
   __shared__ ScanTables t;
   __shared__ unsigned long long s_seen[kSmemCache];
   for (int i = threadIdx.x; i < kSmemCache; i += blockDim.x) s_seen[i] = kEmptyKey;
@@ -397,7 +410,14 @@ __global__ void __launch_bounds__(256) scan_dedup_kernel(const uint32_t* __restr
           unsigned long long base = 0;
           if ((int)lane == leader) base = atomicAdd(out_count, (unsigned long long)__popc(b));
           base = __shfl_sync(m, base, leader);
-          if (fresh[u]) out_pairs[base + __popc(b & ((1u << lane) - 1u))] = make_uint2(c[u], o[u]);
+          if (fresh[u]) {
+            const uint64_t pos = base + __popc(b & ((1u << lane) - 1u));
+            const uint2 pr = make_uint2(c[u], o[u]);
+            out_pairs[pos] = pr;
+            if (PUSH && pos < push.region_cap)
+              for (uint32_t p = 0; p < push.world; ++p)
+                if (p != push.rank) push.peers[p][(uint64_t)push.rank * push.region_cap + pos] = pr;
+          }
         }
       }
     }
@@ -405,6 +425,7 @@ __global__ void __launch_bounds__(256) scan_dedup_kernel(const uint32_t* __restr
     for (int u = 0; u < 4; ++u)
       if (fresh[u]) stamp_pair<H1MODE, HIST, BITS>(t, geo, c[u], o[u], stamps, now, now_slot, hist, K, touched);
   }
+  if (PUSH) __threadfence_system();  // peer stores visible before the exchange's barrier
 }
 
 // BINNING (partition pairs by pair-set region before a dedup scan).  Two

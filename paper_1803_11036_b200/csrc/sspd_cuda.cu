@@ -149,6 +149,7 @@ struct sspd_grid {
   DevBuf newpairs;              // this slot's distinct pairs (export_pairs)
   DevBuf newpairs_count;        // u64 on device
   uint64_t scanned_in_slot = 0; // pairs scanned since the last advance (list capacity bound)
+  PushArgs push{};              // fused exchange: peer inboxes (export mode 3)
   void* pinned_small = nullptr;  // 4 KB pinned scratch for counters
   bool profiling = false;
   std::vector<ProfRec> prof;
@@ -656,7 +657,24 @@ sspd_status sspd_scan(sspd_grid* g, const uint32_t* pairs, uint64_t n, int pairs
                                                                    g->pairset_mask, g->stamps, g->now,      \
                                                                    g->hist, g->K, g->touched, np, nc)
       const bool ex = g->export_pairs;
-      if (pow2 && ex && hist) SSPD_DEDUP(0, 1, 0, 1);
+      if (ex && g->push.world > 1) {
+        if (pow2 && hist)
+          scan_dedup_kernel<0, 1, 0, 1, 1><<<blocks, 256, 0, g->stream>>>(dp, cnt, g->d_tabs, g->geo, tb,
+                                                                          g->pairset_mask, g->stamps, g->now,
+                                                                          g->hist, g->K, g->touched, np, nc, g->push);
+        else if (pow2)
+          scan_dedup_kernel<0, 0, 0, 1, 1><<<blocks, 256, 0, g->stream>>>(dp, cnt, g->d_tabs, g->geo, tb,
+                                                                          g->pairset_mask, g->stamps, g->now,
+                                                                          g->hist, g->K, g->touched, np, nc, g->push);
+        else if (hist)
+          scan_dedup_kernel<1, 1, 0, 1, 1><<<blocks, 256, 0, g->stream>>>(dp, cnt, g->d_tabs, g->geo, tb,
+                                                                          g->pairset_mask, g->stamps, g->now,
+                                                                          g->hist, g->K, g->touched, np, nc, g->push);
+        else
+          scan_dedup_kernel<1, 0, 0, 1, 1><<<blocks, 256, 0, g->stream>>>(dp, cnt, g->d_tabs, g->geo, tb,
+                                                                          g->pairset_mask, g->stamps, g->now,
+                                                                          g->hist, g->K, g->touched, np, nc, g->push);
+      } else if (pow2 && ex && hist) SSPD_DEDUP(0, 1, 0, 1);
       else if (pow2 && ex) SSPD_DEDUP(0, 0, 0, 1);
       else if (ex && hist) SSPD_DEDUP(1, 1, 0, 1);
       else if (ex) SSPD_DEDUP(1, 0, 0, 1);
@@ -1150,6 +1168,14 @@ sspd_status sspd_set_exchange(sspd_grid* g, int mode) {
   std::lock_guard<std::mutex> lk(g->mu);
   g->record_touched = mode == 1;
   g->export_pairs = mode == 2;
+  return SSPD_OK;
+}
+
+sspd_status sspd_set_push(sspd_grid* g, void* dev_peer_ptrs, uint32_t world, uint32_t rank, uint64_t region_cap) {
+  std::lock_guard<std::mutex> lk(g->mu);
+  if (world > 1 && (!dev_peer_ptrs || rank >= world || region_cap == 0))
+    return fail(SSPD_INVALID_ARGUMENT, "set_push: bad peer table");
+  g->push = PushArgs{static_cast<uint2* const*>(dev_peer_ptrs), world, rank, region_cap};
   return SSPD_OK;
 }
 

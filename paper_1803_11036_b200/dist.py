@@ -64,21 +64,96 @@ def device_view(ptr: int, n_words: int, device: int) -> torch.Tensor:
 
 BITMAP = 1
 PAIRS = 2
+PUSH = 3
 
 
-def prepare(grid, exchange: int = PAIRS):
+def prepare(grid, exchange: int = PAIRS, region_cap: int = 0, group=None):
     """Choose what routers exchange each slot: the slot's distinct (cip, oip)
-    pairs (PAIRS, default: ~5% of a Zipf slot's packets, 8 B each) or the
-    touched bitmap (BITMAP: 1 bit per recorder, fixed size)."""
+    pairs (PAIRS, default: ~10% of a Zipf slot's packets, 8 B each), the
+    same pairs pushed over NVLink during the scan (PUSH, needs region_cap =
+    the most pairs a router scans per slot) or the touched bitmap (BITMAP:
+    1 bit per recorder, fixed size)."""
+    if exchange == PUSH:
+        PushExchange(grid, region_cap, group)
+        return
     grid.set_exchange(exchange)
     grid._exchange = exchange
 
 
 def merge(grid, group=None):
-    if getattr(grid, "_exchange", BITMAP) == PAIRS:
+    ex = getattr(grid, "_exchange", BITMAP)
+    if ex == PUSH:
+        grid._push.merge(grid)
+    elif ex == PAIRS:
         merge_pairs(grid, group)
     else:
         merge_touched(grid, group)
+
+
+class PushExchange:
+    """Fused scan + exchange over NVLink (exchange PUSH).
+
+    Every router owns two inboxes in torch symmetric memory (one per slot
+    parity), each `world` regions of `region_cap` pairs.  While scanning, the
+    dedup kernel stores each pair new to this router into region `rank` of
+    every peer's current inbox (P2P stores, include/sspd_cuda.h
+    sspd_set_push), so the exchange overlaps the scan.  After the scan an
+    all-gather of the per-router counts is the barrier; each router then scans
+    the other regions of its own inbox.  Parity double-buffering is safe: a
+    router pushes slot s+2 into an inbox only after the all-gather of slot s+1,
+    which the receiver joins only after it finished applying slot s.  A
+    router whose slot overflows region_cap makes every router fall back to
+    the all-gathered lists for that slot (the counts say so consistently).
+    """
+
+    def __init__(self, grid, region_cap: int, group=None):
+        import torch.distributed._symmetric_memory as symm_mem
+
+        self.world = dist.get_world_size(group)
+        self.rank = dist.get_rank(group)
+        self.cap = int(region_cap)
+        self.group = group
+        dev = torch.device(f"cuda:{grid.device}")
+        name = group.group_name if group is not None else dist.group.WORLD.group_name
+        self.inbox, self.handles = [], []
+        for _ in range(2):
+            buf = symm_mem.empty(self.world * self.cap * 2, dtype=torch.int32, device=dev)
+            self.inbox.append(buf)
+            self.handles.append(symm_mem.rendezvous(buf, name))
+        self.parity = 0
+        grid.set_exchange(PAIRS)
+        grid._exchange = PUSH
+        grid._push = self
+        self._arm(grid)
+
+    def _arm(self, grid):
+        grid.set_push(self.handles[self.parity].buffer_ptrs_dev, self.world, self.rank, self.cap)
+
+    def merge(self, grid):
+        ptr, n = grid.new_pairs_ptr()
+        dev = torch.device(f"cuda:{grid.device}")
+        counts = torch.tensor([n], dtype=torch.int64, device=dev)
+        allc = torch.empty(self.world, dtype=torch.int64, device=dev)
+        dist.all_gather_into_tensor(allc, counts, group=self.group)   # also the barrier
+        sizes = [int(c) for c in allc.tolist()]
+        torch.cuda.synchronize(grid.device)
+        box = self.inbox[self.parity].view(self.world, self.cap, 2)
+        grid.set_exchange(0)
+        try:
+            if max(sizes) > self.cap:
+                # someone overflowed its region: everyone uses the lists
+                local = (device_view(ptr, 2 * n, grid.device).view(n, 2) if n
+                         else torch.zeros((0, 2), dtype=torch.int32, device=dev))
+                for part in exchange_pairs(local, self.group):
+                    grid.scan_device(part.data_ptr(), int(part.shape[0]))
+            else:
+                for src in range(self.world):
+                    if src != self.rank and sizes[src]:
+                        grid.scan_device(box[src].data_ptr(), sizes[src])
+        finally:
+            grid.set_exchange(PAIRS)
+        self.parity ^= 1
+        self._arm(grid)
 
 
 def exchange_pairs(local: torch.Tensor, group=None) -> list[torch.Tensor]:
@@ -167,21 +242,96 @@ def device_view(ptr: int, n_words: int, device: int) -> torch.Tensor:
 
 BITMAP = 1
 PAIRS = 2
+PUSH = 3
 
 
-def prepare(grid, exchange: int = PAIRS):
+def prepare(grid, exchange: int = PAIRS, region_cap: int = 0, group=None):
     """Choose what routers exchange each slot: the slot's distinct (cip, oip)
-    pairs (PAIRS, default: ~5% of a Zipf slot's packets, 8 B each) or the
-    touched bitmap (BITMAP: 1 bit per recorder, fixed size)."""
+    pairs (PAIRS, default: ~10% of a Zipf slot's packets, 8 B each), the
+    same pairs pushed over NVLink during the scan (PUSH, needs region_cap =
+    the most pairs a router scans per slot) or the touched bitmap (BITMAP:
+    1 bit per recorder, fixed size)."""
+    if exchange == PUSH:
+        PushExchange(grid, region_cap, group)
+        return
     grid.set_exchange(exchange)
     grid._exchange = exchange
 
 
 def merge(grid, group=None):
-    if getattr(grid, "_exchange", BITMAP) == PAIRS:
+    ex = getattr(grid, "_exchange", BITMAP)
+    if ex == PUSH:
+        grid._push.merge(grid)
+    elif ex == PAIRS:
         merge_pairs(grid, group)
     else:
         merge_touched(grid, group)
+
+
+class PushExchange:
+    """Fused scan + exchange over NVLink (exchange PUSH).
+
+    Every router owns two inboxes in torch symmetric memory (one per slot
+    parity), each `world` regions of `region_cap` pairs.  While scanning, the
+    dedup kernel stores each pair new to this router into region `rank` of
+    every peer's current inbox (P2P stores, include/sspd_cuda.h
+    sspd_set_push), so the exchange overlaps the scan.  After the scan an
+    all-gather of the per-router counts is the barrier; each router then scans
+    the other regions of its own inbox.  Parity double-buffering is safe: a
+    router pushes slot s+2 into an inbox only after the all-gather of slot s+1,
+    which the receiver joins only after it finished applying slot s.  A
+    router whose slot overflows region_cap makes every router fall back to
+    the all-gathered lists for that slot (the counts say so consistently).
+    """
+
+    def __init__(self, grid, region_cap: int, group=None):
+        import torch.distributed._symmetric_memory as symm_mem
+
+        self.world = dist.get_world_size(group)
+        self.rank = dist.get_rank(group)
+        self.cap = int(region_cap)
+        self.group = group
+        dev = torch.device(f"cuda:{grid.device}")
+        name = group.group_name if group is not None else dist.group.WORLD.group_name
+        self.inbox, self.handles = [], []
+        for _ in range(2):
+            buf = symm_mem.empty(self.world * self.cap * 2, dtype=torch.int32, device=dev)
+            self.inbox.append(buf)
+            self.handles.append(symm_mem.rendezvous(buf, name))
+        self.parity = 0
+        grid.set_exchange(PAIRS)
+        grid._exchange = PUSH
+        grid._push = self
+        self._arm(grid)
+
+    def _arm(self, grid):
+        grid.set_push(self.handles[self.parity].buffer_ptrs_dev, self.world, self.rank, self.cap)
+
+    def merge(self, grid):
+        ptr, n = grid.new_pairs_ptr()
+        dev = torch.device(f"cuda:{grid.device}")
+        counts = torch.tensor([n], dtype=torch.int64, device=dev)
+        allc = torch.empty(self.world, dtype=torch.int64, device=dev)
+        dist.all_gather_into_tensor(allc, counts, group=self.group)   # also the barrier
+        sizes = [int(c) for c in allc.tolist()]
+        torch.cuda.synchronize(grid.device)
+        box = self.inbox[self.parity].view(self.world, self.cap, 2)
+        grid.set_exchange(0)
+        try:
+            if max(sizes) > self.cap:
+                # someone overflowed its region: everyone uses the lists
+                local = (device_view(ptr, 2 * n, grid.device).view(n, 2) if n
+                         else torch.zeros((0, 2), dtype=torch.int32, device=dev))
+                for part in exchange_pairs(local, self.group):
+                    grid.scan_device(part.data_ptr(), int(part.shape[0]))
+            else:
+                for src in range(self.world):
+                    if src != self.rank and sizes[src]:
+                        grid.scan_device(box[src].data_ptr(), sizes[src])
+        finally:
+            grid.set_exchange(PAIRS)
+        self.parity ^= 1
+        self._arm(grid)
 
 
 def merge_pairs(grid, group=None):

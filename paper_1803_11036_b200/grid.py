@@ -236,6 +236,10 @@ class Grid:
         """0 off, 1 touched bitmap, 2 distinct-pair list (see dist.py)."""
         check(self._L.sspd_set_exchange(self._h, int(mode)))
 
+    def set_push(self, dev_peer_ptrs: int, world: int, rank: int, region_cap: int):
+        """Fused exchange: push new pairs into peers' inboxes during the scan."""
+        check(self._L.sspd_set_push(self._h, C.c_void_p(dev_peer_ptrs), world, rank, region_cap))
+
     def new_pairs_ptr(self) -> tuple[int, int]:
         p = C.c_void_p()
         n = C.c_uint64()

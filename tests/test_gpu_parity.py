@@ -454,3 +454,35 @@ def test_cabi_argument_errors(gpu):
     assert int((g.cells() == 0).sum()) >= 1
     g.set_stream(None)
     assert g.now == gpu.BASE_NOW
+
+
+def test_fused_push_to_peer_inboxes(gpu):
+    """The scan's PUSH path on one device: 'peer' inboxes are ordinary device
+    buffers here (on an 8-GPU box they are NVLink-mapped symmetric memory).
+    Router 1 of 3 must write exactly its new pairs, in list order, into region
+    1 of the other two inboxes, nothing into its own, and leave the grid as
+    the oracle's."""
+    import torch
+
+    g, o = make_pair(gpu, DESK, 0x321)
+    cap = 50_000
+    boxes = [torch.full((3 * cap, 2), -7, dtype=torch.int32, device="cuda") for _ in range(3)]
+    table = torch.tensor([b.data_ptr() for b in boxes], dtype=torch.int64, device="cuda")
+    g.set_exchange(2)
+    g.set_push(table.data_ptr(), 3, 1, cap)
+    rng = O.Mt64(321)
+    base = rng.pairs(20_000)
+    p = base[rng.draw(100_000) % 20_000]
+    g.scan_batch(torch.from_numpy(p.view(np.int32)).cuda())
+    o.scan(p)
+    ptr, n = g.new_pairs_ptr()
+    assert n == len(np.unique(p, axis=0))
+    from paper_1803_11036_b200.dist import device_view
+    mine = device_view(ptr, 2 * n, g.device).view(n, 2).cpu()
+    for r in (0, 2):
+        got = boxes[r][cap: cap + n].cpu()
+        assert torch.equal(got, mine)
+        assert bool((boxes[r][:cap] == -7).all()) and bool((boxes[r][cap + n: 2 * cap] == -7).all())
+    assert bool((boxes[1] == -7).all())
+    assert np.array_equal(g.cells(), o.cells())
+    g.set_push(0, 1, 0, 0)
