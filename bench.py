@@ -190,10 +190,11 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--window", type=int, default=0, help="override the window k (C4 sweeps)")
-    ap.add_argument("--merge", default="pairs", choices=["pairs", "push", "bitmap", "stamps"],
-                    help="router exchange at N>1: distinct-pair lists all-gathered after the scan "
-                         "(default), the same lists pushed over NVLink during the scan, OR of "
-                         "touched bitmaps, or the literal all-reduce(max) of the full stamp grid")
+    ap.add_argument("--merge", default="auto", choices=["auto", "pairs", "push", "bitmap", "stamps"],
+                    help="router exchange at N>1: distinct pairs pushed over NVLink during the scan "
+                         "(push; auto = push, else pairs if symmetric memory is unavailable), the "
+                         "same lists all-gathered after the scan (pairs), OR of touched bitmaps, or "
+                         "the literal all-reduce(max) of the full stamp grid")
     ap.add_argument("--scan-mode", default="auto", choices=["auto", "bitmap", "direct", "dedup", "binned"])
     ap.add_argument("--filter", type=int, default=-1, help="L1 duplicate probe 0/1 (-1 = default)")
     ap.add_argument("--ref-pairs", type=int, default=100_000_000,
@@ -255,9 +256,21 @@ def main():
     g.set_stream(stream.cuda_stream)
     g.scan_mode({"auto": -1, "bitmap": 0, "direct": 1, "dedup": 2, "binned": 3}[args.scan_mode], args.filter)
     g.track_window(cfg["k"])
+    merge_used = args.merge
     if world > 1 and args.merge != "stamps":
-        PD.prepare(g, {"pairs": PD.PAIRS, "push": PD.PUSH, "bitmap": PD.BITMAP}[args.merge],
-                   region_cap=min(cfg["pairs_per_slot"], 32 << 20))
+        cap = min(cfg["pairs_per_slot"], 32 << 20)
+        if args.merge == "auto":
+            try:
+                PD.prepare(g, PD.PUSH, region_cap=cap)
+                merge_used = "push"
+            except Exception as e:  # symmetric memory unavailable: lists after the scan
+                print(f"[bench] push exchange unavailable ({type(e).__name__}: {e}); using pairs",
+                      file=sys.stderr)
+                PD.prepare(g, PD.PAIRS)
+                merge_used = "pairs"
+        else:
+            PD.prepare(g, {"pairs": PD.PAIRS, "push": PD.PUSH, "bitmap": PD.BITMAP}[args.merge],
+                       region_cap=cap)
     cdf = torch.from_numpy(zipf_cdf(L, cfg).view(np.int64)).to(f"cuda:{dev}")
     sp = synth_params(cfg, rank, world)
     n_local = cfg["pairs_per_slot"]
@@ -441,7 +454,8 @@ def main():
                    "merge": {"pairs": "union-min: all-gather of each router's distinct pairs per slot",
                              "push": "union-min: distinct pairs pushed to peers over NVLink during the scan",
                              "bitmap": "union-min: OR all-reduce of the slot's touched bitmaps",
-                             "stamps": "union-min: NCCL all-reduce(max) of the full stamp grid"}[args.merge],
+                             "stamps": "union-min: NCCL all-reduce(max) of the full stamp grid",
+                             "auto": "none (single router)"}[merge_used],
                    "parallelism": f"{world} routers, one per GPU",
                    "l2": "inputs larger than L2 (800 MB per slot)"},
         "gbps_800B": round(value * 1e6 * PKT_BYTES * 8 / 1e9, 1),
