@@ -10,7 +10,7 @@ import ctypes as C
 import os
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "lib", "libsspd_cuda.so")
+LIB_PATH = os.environ.get("SSPD_LIB") or os.path.join(HERE, "lib", "libsspd_cuda.so")
 
 SSPD_OK = 0
 SSPD_INVALID_ARGUMENT = 1

@@ -344,8 +344,15 @@ struct PushArgs {
   uint64_t region_cap;
 };
 
+#ifndef SSPD_DEDUP_PPT
+#define SSPD_DEDUP_PPT 4  // pairs per thread per iteration (probes in flight)
+#endif
+#ifndef SSPD_DEDUP_MINB
+#define SSPD_DEDUP_MINB 1
+#endif
+
 template <int H1MODE, int HIST, int BITS, int EXPORT, int PUSH = 0>
-__global__ void __launch_bounds__(256) scan_dedup_kernel(const uint32_t* __restrict__ pairs, uint64_t n,
+__global__ void __launch_bounds__(256, SSPD_DEDUP_MINB) scan_dedup_kernel(const uint32_t* __restrict__ pairs, uint64_t n,
                                                          const HashTabs* __restrict__ tabs, Geo geo,
                                                          unsigned long long* __restrict__ table,
                                                          uint64_t table_mask, uint32_t* __restrict__ stamps,
@@ -363,46 +370,47 @@ __global__ void __launch_bounds__(256) scan_dedup_kernel(const uint32_t* __restr
   const uint64_t tid = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
   const uint64_t nthreads = (uint64_t)gridDim.x * blockDim.x;
   const bool vec = (reinterpret_cast<uintptr_t>(pairs) & 15u) == 0;
-  // group g covers pairs [4g, 4g+4): two 16-byte loads
-  const uint64_t ngroups = (n + 3) / 4;
+  // group g covers pairs [P g, P g + P): P/2 16-byte loads
+  constexpr int P = SSPD_DEDUP_PPT;
+  const uint64_t ngroups = (n + P - 1) / P;
   for (uint64_t g = tid; g < ngroups; g += nthreads) {
-    uint32_t c[4], o[4];
-    bool valid[4];
-    const uint64_t p0 = g * 4;
-    if (vec && p0 + 4 <= n) {
-      const uint4 a = ld_stream_u4(pairs + 2 * p0);
-      const uint4 b = ld_stream_u4(pairs + 2 * p0 + 4);
-      c[0] = a.x; o[0] = a.y; c[1] = a.z; o[1] = a.w;
-      c[2] = b.x; o[2] = b.y; c[3] = b.z; o[3] = b.w;
+    uint32_t c[P], o[P];
+    bool valid[P];
+    const uint64_t p0 = g * P;
+    if (vec && p0 + P <= n) {
 #pragma unroll
-      for (int u = 0; u < 4; ++u) valid[u] = true;
+      for (int u = 0; u < P; u += 2) {
+        const uint4 a = ld_stream_u4(pairs + 2 * (p0 + u));
+        c[u] = a.x; o[u] = a.y; c[u + 1] = a.z; o[u + 1] = a.w;
+        valid[u] = valid[u + 1] = true;
+      }
     } else {
 #pragma unroll
-      for (int u = 0; u < 4; ++u) {
+      for (int u = 0; u < P; ++u) {
         valid[u] = p0 + u < n;
         c[u] = valid[u] ? pairs[2 * (p0 + u)] : 0u;
         o[u] = valid[u] ? pairs[2 * (p0 + u) + 1] : 0u;
       }
     }
-    uint64_t key[4], h[4];
-    unsigned long long v[4];
-    bool probe[4];
+    uint64_t key[P], h[P];
+    unsigned long long v[P];
+    bool probe[P];
 #pragma unroll
-    for (int u = 0; u < 4; ++u) {
+    for (int u = 0; u < P; ++u) {
       key[u] = (uint64_t)c[u] << 32 | o[u];
       h[u] = pair_slot_hash(key[u]);
       probe[u] = valid[u] && s_seen[(h[u] >> 40) & (kSmemCache - 1)] != key[u];
       v[u] = probe[u] ? __ldca(table + pair_slot(h[u], 0, table_mask)) : 0ull;
     }
-    bool fresh[4];
+    bool fresh[P];
 #pragma unroll
-    for (int u = 0; u < 4; ++u) {
+    for (int u = 0; u < P; ++u) {
       fresh[u] = probe[u] && pair_resolve(table, table_mask, key[u], h[u], v[u]);
       if (probe[u] && key[u] != kEmptyKey) s_seen[(h[u] >> 40) & (kSmemCache - 1)] = key[u];
     }
     if (EXPORT) {
 #pragma unroll
-      for (int u = 0; u < 4; ++u) {
+      for (int u = 0; u < P; ++u) {
         const unsigned m = __activemask();
         const unsigned b = __ballot_sync(m, fresh[u]);
         if (b) {
@@ -422,7 +430,7 @@ __global__ void __launch_bounds__(256) scan_dedup_kernel(const uint32_t* __restr
       }
     }
 #pragma unroll
-    for (int u = 0; u < 4; ++u)
+    for (int u = 0; u < P; ++u)
       if (fresh[u]) stamp_pair<H1MODE, HIST, BITS>(t, geo, c[u], o[u], stamps, now, now_slot, hist, K, touched);
   }
   if (PUSH) __threadfence_system();  // peer stores visible before the exchange's barrier

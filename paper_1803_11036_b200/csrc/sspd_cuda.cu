@@ -20,6 +20,10 @@
 #include "kernels.cuh"
 #include "synth.h"
 
+#ifndef SSPD_SCAN_BLOCKS_PER_SM
+#define SSPD_SCAN_BLOCKS_PER_SM 8
+#endif
+
 #include <omp.h>
 
 using namespace sspd_dev;
@@ -642,7 +646,7 @@ sspd_status sspd_scan(sspd_grid* g, const uint32_t* pairs, uint64_t n, int pairs
     }
   }
   auto launch = [&](const uint32_t* dp, uint64_t cnt) {
-    const unsigned blocks = grid_blocks(g, (cnt + 3) / 4, 256, 8);
+    const unsigned blocks = grid_blocks(g, (cnt + 3) / 4, 256, SSPD_SCAN_BLOCKS_PER_SM);
     Prof p(g, "scan", cnt);
     const int F = g->scan_filter;
 #define SSPD_DIRECT(H1, FI, HI, BI)                                                                 \

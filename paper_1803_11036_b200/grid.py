@@ -296,5 +296,54 @@ def merge_rseas(grids: list[Grid], policy: int = _cabi.UNION_MIN, out: Grid | No
     return out
 
 
+SNAPSHOT_MAGIC = b"RSEA"
+SNAPSHOT_VERSION = 1
+SNAPSHOT_HEADER = 56
+
+
+def export_snapshot(grid: Grid, f, k: int = 0, theta: int = 0, slot: int = 0, node_id: int = 0,
+                    chunk: int = 1 << 22):
+    """export_snapshot (snapshot.hpp:30-41; snapshot.cpp:36-68): 56-byte
+    little-endian header, then every recorder as a u16 distance in (row,
+    column, bucket) order, streamed from the device in chunks."""
+    import struct
+
+    f.write(SNAPSHOT_MAGIC + struct.pack("<IQIIIIIIQI4x", SNAPSHOT_VERSION, grid.seed, grid.q,
+                                         grid.r, grid.delta, grid.eta, k, theta, slot, node_id))
+    n = grid.recorder_count()
+    buf = np.empty(min(chunk, n), dtype=np.uint16)
+    for pos in range(0, n, chunk):
+        cnt = min(chunk, n - pos)
+        check(load().sspd_get_distances(grid._h, buf.ctypes.data_as(_cabi.u16p), pos, cnt))
+        f.write(buf[:cnt].astype("<u2").tobytes())
+
+
+def import_snapshot(f, device: int = 0, chunk: int = 1 << 22):
+    """import_snapshot (snapshot.cpp:70-115): returns (grid, meta dict) with
+    the reference's validation messages."""
+    import struct
+
+    h = f.read(SNAPSHOT_HEADER)
+    if len(h) != SNAPSHOT_HEADER:
+        raise RuntimeError("import_snapshot: truncated header")
+    if h[:4] != SNAPSHOT_MAGIC:
+        raise RuntimeError("import_snapshot: bad magic")
+    (version, seed, q, r, delta, eta, k, theta, slot, node_id) = struct.unpack("<IQIIIIIIQI4x", h[4:])
+    if version != SNAPSHOT_VERSION:
+        raise RuntimeError(f"import_snapshot: unsupported version {version}")
+    g = Grid(q, r, delta, seed, eta, device=device)
+    n = g.recorder_count()
+    for pos in range(0, n, chunk):
+        cnt = min(chunk, n - pos)
+        raw = f.read(2 * cnt)
+        if len(raw) != 2 * cnt:
+            raise RuntimeError(f"import_snapshot: truncated payload, expected {2 * n} bytes, "
+                               f"got {2 * pos + len(raw)}")
+        g.set_cells(np.frombuffer(raw, dtype="<u2"), pos)
+    meta = dict(seed=seed, q=q, r=r, delta=delta, eta=eta, k=k, theta=theta, slot=slot,
+                node_id=node_id)
+    return g, meta
+
+
 def launch_count() -> int:
     return int(load().sspd_launch_count())

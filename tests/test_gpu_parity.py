@@ -7,6 +7,8 @@ finalisation and reported super point lists; the estimates are compared with
 The cases mirror the reference's own tests (tests/test_rsea.cpp,
 test_snapshot.cpp, acceptance.cpp in /root/reference/proj).
 """
+import os
+
 import numpy as np
 import pytest
 
@@ -486,3 +488,36 @@ def test_fused_push_to_peer_inboxes(gpu):
     assert bool((boxes[1] == -7).all())
     assert np.array_equal(g.cells(), o.cells())
     g.set_push(0, 1, 0, 0)
+
+
+def test_python_snapshot_roundtrip_matches_cli_format(gpu, tmp_path):
+    """export/import in Python produce the reference file format: the same
+    bytes the C++ API writes (sspd snapshot export), and a bit-exact grid."""
+    import io
+    import subprocess
+
+    g, o = make_pair(gpu, DESK, 0x5eed)
+    rng = O.Mt64(3)
+    p = rng.pairs(30_000)
+    g.scan_batch(p)
+    o.scan(p)
+    buf = io.BytesIO()
+    gpu.export_snapshot(g, buf, k=5, theta=128, slot=0, node_id=3)
+    data = buf.getvalue()
+    assert len(data) == 56 + 2 * g.recorder_count()
+    assert np.array_equal(np.frombuffer(data[56:], dtype="<u2"), o.cells())
+    h, meta = gpu.import_snapshot(io.BytesIO(data))
+    assert h == g and meta["node_id"] == 3 and meta["k"] == 5
+    # the CLI (C++ API) writes the same bytes for the same scans
+    trace = np.concatenate([np.zeros((len(p), 1), np.uint32), p], axis=1)
+    tb = tmp_path / "t.bin"
+    with open(tb, "wb") as f:
+        f.write(b"SSPT" + (1).to_bytes(4, "little") + trace.astype("<u4").tobytes())
+    sspd = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))),
+                        "paper_1803_11036_b200", "bin", "sspd")
+    out = tmp_path / "s.snap"
+    subprocess.run([sspd, "snapshot", "export", str(tb), "--desk", "--k", "5", "--seed", "5eed",
+                    "--node-id", "3", "-o", str(out)], check=True)
+    assert out.read_bytes() == data
+    with pytest.raises(RuntimeError, match="truncated payload"):
+        gpu.import_snapshot(io.BytesIO(data[:-2]))
