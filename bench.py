@@ -411,6 +411,10 @@ def main():
                 traffic = None
             roof = {"kernel": dom, "bound": "hbm", "achieved": round(achieved, 1), "peak": hbm,
                     "unit": "GB/s", "frac": round(achieved / hbm, 4), "traffic": traffic,
+                    # what DRAM actually moved per launch at this launch time (the dedup scan
+                    # skips the repeated pairs' work, so traffic < algorithmic bytes)
+                    "traffic_gbs": (round(traffic / (per_launch_ms / 1e3) / 1e9, 1)
+                                    if traffic else None),
                     "bytes_per_unit": bytes_per_unit, "units_per_launch": units_per_launch,
                     "launch_ms": round(per_launch_ms, 4),
                     "peak_source": "MEASURED_PEAKS.json hbm_gbs" if "hbm_gbs" in peaks else "fallback"}
