@@ -9,6 +9,7 @@
 #include <random>
 #include <set>
 #include <sstream>
+#include <thread>
 
 #include "check.hpp"
 #include "sspd/pipeline.hpp"
@@ -352,6 +353,50 @@ TEST_CASE("pipeline: split super point detected only globally") {
   CHECK(cips_of(global[0]).count(cip) == 1);
   rc.policy = MergePolicy::kPaperMax;  // the intersection loses it
   CHECK(cips_of(run_detection(shards, rc)[0]).count(cip) == 0);
+}
+
+TEST_CASE("concurrent SCAN-phase callers (rsea.hpp:49-51) give the serial grid") {
+  std::mt19937_64 rng(90);
+  std::vector<IpPair> pairs(200000);
+  for (auto& p : pairs) p = {static_cast<uint32_t>(rng()), static_cast<uint32_t>(rng())};
+  Rsea serial(kCfg, kEta);
+  serial.scan_batch(pairs, 1);
+  Rsea shared(kCfg, kEta);
+  std::vector<std::thread> th;
+  for (int t = 0; t < 8; ++t)
+    th.emplace_back([&, t] {
+      const std::size_t lo = pairs.size() * t / 8, hi = pairs.size() * (t + 1) / 8;
+      if (t % 2)  // half the threads batch, half update one by one
+        shared.scan_batch(std::span<const IpPair>(pairs.data() + lo, hi - lo), 2);
+      else
+        for (std::size_t i = lo; i < hi; ++i) shared.update(pairs[i].cip, pairs[i].oip);
+    });
+  for (auto& x : th) x.join();
+  CHECK(shared == serial);
+}
+
+TEST_CASE("Rsea value semantics: copies are independent, moves keep the state") {
+  std::mt19937_64 rng(91);
+  Rsea a(kCfg, kEta);
+  plant(a, 0x0A0B0C0D, 300, rng);
+  Rsea b = a;            // copy
+  b.advance_slot(1);
+  CHECK_FALSE(a == b);
+  Rsea c = std::move(b); // move keeps b's state
+  Rsea d(kCfg, kEta);
+  d = a;                 // copy-assign
+  d.advance_slot(1);
+  CHECK(c == d);
+  d = std::move(c);      // move-assign
+  CHECK(d.reconstruct_leveled(kK, kTheta, 1).hosts.size() == a.reconstruct_leveled(kK, kTheta, 1).hosts.size());
+  // writes through a mutable span are seen by the device, later updates too
+  auto cells = a.cells();
+  std::fill(cells.begin(), cells.end(), kNeverSeen);
+  a.update(1, 2);
+  std::size_t zeros = 0;
+  for (Recorder v : std::as_const(a).cells()) zeros += v == 0;
+  CHECK(zeros >= 1);
+  CHECK(zeros <= kCfg.r);
 }
 
 #ifdef HAVE_REF
