@@ -209,6 +209,17 @@ sspd_status sspd_synth_device(int device, const sspd_synth_params_t* p, const ui
  * the injected set). */
 uint32_t sspd_synth_super_cip(const sspd_synth_params_t* p, uint32_t i);
 
+/* Exact ground truth on the device: the number of distinct
+ * oips of every cip over the union of n_segments device arrays of (cip, oip)
+ * pairs (one sliding window's slots) -- what exact_counts reports for that
+ * window (workload.cpp:180-213) -- for cips with count >= min_count, sorted
+ * by cip.  distinct_hint sizes the tables (0 = total pairs); a full table
+ * fails with SSPD_OUT_OF_RANGE rather than dropping anything. */
+sspd_status sspd_exact_counts(int device, const uint32_t* const* dev_segments, const uint64_t* seg_pairs,
+                              uint32_t n_segments, uint64_t distinct_hint, uint32_t min_count,
+                              uint32_t* cips, uint32_t* counts, uint64_t out_cap, uint64_t* n_out,
+                              void* cuda_stream);
+
 /* Per-kernel timing of the last call on this grid (CUDA events on the grid's
  * stream), for bench.py's roofline: name -> milliseconds, launches. */
 sspd_status sspd_profile_enable(sspd_grid* g, int on);

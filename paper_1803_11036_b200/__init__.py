@@ -8,12 +8,13 @@ multi-router runs.
 """
 from ._cabi import (CandidateOverflow, CudaError, InvalidArgument, NoDevice, OutOfRange,
                     PAPER_MAX, UNION_MIN, SspdError, load)
-from .grid import (BASE_NOW, Detection, Grid, device_count, estimate_cardinality, export_snapshot,
+from .grid import (BASE_NOW, Detection, Grid, device_count, estimate_cardinality, exact_counts,
+                   export_snapshot,
                    hot_cutoff, import_snapshot, launch_count, merge_rseas)
 
 __all__ = [
     "BASE_NOW", "CandidateOverflow", "CudaError", "Detection", "Grid", "InvalidArgument",
     "NoDevice", "OutOfRange", "PAPER_MAX", "SspdError", "UNION_MIN", "device_count",
-    "estimate_cardinality", "export_snapshot", "hot_cutoff", "import_snapshot", "launch_count",
+    "estimate_cardinality", "exact_counts", "export_snapshot", "hot_cutoff", "import_snapshot", "launch_count",
     "load", "merge_rseas",
 ]

@@ -77,6 +77,8 @@ SIGNATURES = {
     "sspd_synth_device": (C.c_int, [C.c_int, C.c_void_p, C.c_void_p, C.c_uint64, C.c_uint64,
                                     C.c_uint64, C.c_void_p, C.c_void_p]),
     "sspd_synth_super_cip": (C.c_uint32, [C.c_void_p, C.c_uint32]),
+    "sspd_exact_counts": (C.c_int, [C.c_int, C.POINTER(C.c_void_p), u64p, C.c_uint32, C.c_uint64,
+                                    C.c_uint32, u32p, u32p, C.c_uint64, u64p, C.c_void_p]),
 }
 
 _lib = None

@@ -350,6 +350,9 @@ struct PushArgs {
 #ifndef SSPD_DEDUP_MINB
 #define SSPD_DEDUP_MINB 1
 #endif
+#ifndef SSPD_DEDUP_BATCH_ATOMICS
+#define SSPD_DEDUP_BATCH_ATOMICS 0
+#endif
 
 template <int H1MODE, int HIST, int BITS, int EXPORT, int PUSH = 0>
 __global__ void __launch_bounds__(256, SSPD_DEDUP_MINB) scan_dedup_kernel(const uint32_t* __restrict__ pairs, uint64_t n,
@@ -429,6 +432,36 @@ __global__ void __launch_bounds__(256, SSPD_DEDUP_MINB) scan_dedup_kernel(const 
         }
       }
     }
+#if SSPD_DEDUP_BATCH_ATOMICS
+    // Issue the stamp atomics of every fresh pair of the group before
+    // consuming any old value (one exposed round trip per group, not per pair).
+    if (HIST && !BITS && geo.r <= 8) {
+      uint32_t bucket[P], col0[P], old[P][8];
+#pragma unroll
+      for (int u = 0; u < P; ++u) {
+        if (!fresh[u]) continue;
+        hash_pair<H1MODE>(t, geo, c[u], o[u], bucket[u], col0[u]);
+#pragma unroll
+        for (uint32_t row = 0; row < 8; ++row)
+          if (row < geo.r)
+            old[u][row] = atomicMax(stamps + (uint64_t)(row << geo.q | row_col(geo, row, c[u], col0[u])) * geo.eta +
+                                        bucket[u],
+                                    now);
+      }
+#pragma unroll
+      for (int u = 0; u < P; ++u) {
+        if (!fresh[u]) continue;
+#pragma unroll
+        for (uint32_t row = 0; row < 8; ++row) {
+          if (row >= geo.r || old[u][row] >= now) continue;
+          const uint32_t cell = row << geo.q | row_col(geo, row, c[u], col0[u]);
+          atomicAdd(hist + (uint64_t)now_slot * geo.ncells + cell, 1u);
+          if (old[u][row] + K > now) atomicSub(hist + (uint64_t)(old[u][row] % K) * geo.ncells + cell, 1u);
+        }
+      }
+      continue;
+    }
+#endif
 #pragma unroll
     for (int u = 0; u < P; ++u)
       if (fresh[u]) stamp_pair<H1MODE, HIST, BITS>(t, geo, c[u], o[u], stamps, now, now_slot, hist, K, touched);
@@ -945,6 +978,74 @@ __global__ void __launch_bounds__(256) finalize_count_kernel(const uint32_t* __r
       uint32_t t = 0;
       for (uint32_t w = 0; w < blockDim.x / 32; ++w) t += s_red[w];
       if (t) atomicAdd(surv_rk + sidx, t);
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// EXACT GROUND TRUTH on the device: distinct opposite hosts
+// per cip over one window of pairs -- what exact_counts computes with hash
+// sets per slot and a trailing union (workload.cpp:180-213) -- by an exact
+// set of (cip, oip) keys and a cip -> count map.  Probing is bounded by the
+// table size; a full table raises `overflow` instead of looping.
+__device__ __forceinline__ bool exact_pair_new(unsigned long long* __restrict__ pset, uint64_t pmask, uint64_t key,
+                                               unsigned int* __restrict__ flags) {
+  if (key == kEmptyKey) return atomicExch(&flags[1], 1u) == 0u;  // the one key equal to the marker
+  const uint64_t h = pair_slot_hash(key);
+  for (uint64_t i = 0; i <= pmask; ++i) {
+    const uint64_t slot = (h + i) & pmask;
+    const unsigned long long v = pset[slot];
+    if (v == key) return false;
+    if (v == kEmptyKey) {
+      const unsigned long long old = atomicCAS(pset + slot, kEmptyKey, key);
+      if (old == kEmptyKey) return true;
+      if (old == key) return false;
+    }
+  }
+  atomicExch(&flags[0], 1u);
+  return false;
+}
+
+__global__ void __launch_bounds__(256) exact_insert_kernel(const uint32_t* __restrict__ pairs, uint64_t n,
+                                                           unsigned long long* __restrict__ pset, uint64_t pmask,
+                                                           unsigned long long* __restrict__ ckeys,
+                                                           uint32_t* __restrict__ ccounts, uint64_t cmask,
+                                                           unsigned int* __restrict__ flags) {
+  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
+    const uint32_t cip = pairs[2 * i], oip = pairs[2 * i + 1];
+    if (!exact_pair_new(pset, pmask, (uint64_t)cip << 32 | oip, flags)) continue;
+    const unsigned long long ck = (unsigned long long)cip + 1;  // 0 marks an empty slot
+    uint64_t h = ck * 0x9e3779b97f4a7c15ull;
+    h ^= h >> 31;
+    bool placed = false;
+    for (uint64_t j = 0; j <= cmask && !placed; ++j) {
+      const uint64_t slot = (h + j) & cmask;
+      unsigned long long v = ckeys[slot];
+      if (v == 0ull) {
+        const unsigned long long old = atomicCAS(ckeys + slot, 0ull, ck);
+        v = old == 0ull ? ck : old;
+      }
+      if (v == ck) {
+        atomicAdd(ccounts + slot, 1u);
+        placed = true;
+      }
+    }
+    if (!placed) atomicExch(&flags[0], 1u);
+  }
+}
+
+__global__ void exact_emit_kernel(const unsigned long long* __restrict__ ckeys, const uint32_t* __restrict__ ccounts,
+                                  uint64_t centries, uint32_t min_count, uint32_t* __restrict__ out_cip,
+                                  uint32_t* __restrict__ out_count, uint64_t out_cap,
+                                  unsigned long long* __restrict__ counter) {
+  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < centries;
+       i += (uint64_t)gridDim.x * blockDim.x) {
+    const unsigned long long k = ckeys[i];
+    if (k == 0ull || ccounts[i] < min_count) continue;
+    const unsigned long long pos = atomicAdd(counter, 1ull);
+    if (pos < out_cap) {
+      out_cip[pos] = (uint32_t)(k - 1);
+      out_count[pos] = ccounts[i];
     }
   }
 }

@@ -1263,6 +1263,70 @@ sspd_status sspd_profile_read(sspd_grid* g, const char* kernel, double* total_ms
   return SSPD_OK;
 }
 
+sspd_status sspd_exact_counts(int device, const uint32_t* const* dev_segments, const uint64_t* seg_pairs,
+                              uint32_t n_segments, uint64_t distinct_hint, uint32_t min_count, uint32_t* cips,
+                              uint32_t* counts, uint64_t out_cap, uint64_t* n_out, void* cuda_stream) {
+  *n_out = 0;
+  uint64_t total = 0;
+  for (uint32_t i = 0; i < n_segments; ++i) total += seg_pairs[i];
+  const uint64_t want = std::max<uint64_t>(distinct_hint ? distinct_hint : total, 1024);
+  uint64_t pe = 1;
+  while (pe < 2 * want) pe <<= 1;
+  uint64_t ce = 1;
+  while (ce < 2 * std::min<uint64_t>(want, 1ull << 32)) ce <<= 1;
+  DeviceGuard dg(device);
+  cudaStream_t st = static_cast<cudaStream_t>(cuda_stream);
+  DevBuf pset, ckeys, ccounts, flags, out;
+  if (pset.ensure(pe * 8) != cudaSuccess || ckeys.ensure(ce * 8) != cudaSuccess ||
+      ccounts.ensure(ce * 4) != cudaSuccess || flags.ensure(64) != cudaSuccess ||
+      out.ensure(std::max<uint64_t>(out_cap, 1) * 8 + 64) != cudaSuccess) {
+    cudaGetLastError();
+    return fail(SSPD_CUDA_ERROR, "CUDA error: out of memory (exact counts)");
+  }
+  CU(cudaMemsetAsync(pset.p, 0xff, pe * 8, st));
+  CU(cudaMemsetAsync(ckeys.p, 0, ce * 8, st));
+  CU(cudaMemsetAsync(ccounts.p, 0, ce * 4, st));
+  CU(cudaMemsetAsync(flags.p, 0, 64, st));
+  const unsigned blocks = (unsigned)sm_count(device) * 8;
+  for (uint32_t i = 0; i < n_segments; ++i) {
+    if (!seg_pairs[i]) continue;
+    g_launches.fetch_add(1, std::memory_order_relaxed);
+    exact_insert_kernel<<<blocks, 256, 0, st>>>(dev_segments[i], seg_pairs[i], pset.as<unsigned long long>(),
+                                                pe - 1, ckeys.as<unsigned long long>(), ccounts.as<uint32_t>(),
+                                                ce - 1, flags.as<unsigned int>());
+  }
+  auto* counter = reinterpret_cast<unsigned long long*>(static_cast<char*>(flags.p) + 32);
+  uint32_t* o_cip = out.as<uint32_t>();
+  uint32_t* o_cnt = o_cip + std::max<uint64_t>(out_cap, 1);
+  g_launches.fetch_add(1, std::memory_order_relaxed);
+  exact_emit_kernel<<<blocks, 256, 0, st>>>(ckeys.as<unsigned long long>(), ccounts.as<uint32_t>(), ce, min_count,
+                                            o_cip, o_cnt, out_cap, counter);
+  sspd_status s = check_launch();
+  if (s) return s;
+  uint32_t host_flags[16] = {0};
+  CU(cudaMemcpyAsync(host_flags, flags.p, 64, cudaMemcpyDeviceToHost, st));
+  CU(cudaStreamSynchronize(st));
+  if (host_flags[0]) return fail(SSPD_OUT_OF_RANGE, "exact_counts: table full (raise distinct_hint)");
+  uint64_t cnt = 0;
+  std::memcpy(&cnt, reinterpret_cast<char*>(host_flags) + 32, 8);
+  *n_out = cnt;
+  const uint64_t m = std::min(cnt, out_cap);
+  if (m) {
+    std::vector<uint32_t> a(m), b(m);
+    CU(cudaMemcpyAsync(a.data(), o_cip, m * 4, cudaMemcpyDeviceToHost, st));
+    CU(cudaMemcpyAsync(b.data(), o_cnt, m * 4, cudaMemcpyDeviceToHost, st));
+    CU(cudaStreamSynchronize(st));
+    std::vector<uint64_t> order(m);
+    for (uint64_t i = 0; i < m; ++i) order[i] = (uint64_t)a[i] << 32 | b[i];
+    std::sort(order.begin(), order.end());  // ascending cip, like the reference's sorted tables
+    for (uint64_t i = 0; i < m; ++i) {
+      cips[i] = (uint32_t)(order[i] >> 32);
+      counts[i] = (uint32_t)order[i];
+    }
+  }
+  return SSPD_OK;
+}
+
 static_assert(sizeof(sspd_synth_params_t) == sizeof(sspd_synth_params), "synth params layout");
 
 __global__ void synth_kernel(sspd_synth_params p, const uint64_t* __restrict__ cdf, uint64_t slot,

@@ -345,5 +345,26 @@ def import_snapshot(f, device: int = 0, chunk: int = 1 << 22):
     return g, meta
 
 
+def exact_counts(segments, min_count: int = 1, distinct_hint: int = 0, device: int = 0,
+                 stream_ptr: int | None = None) -> dict:
+    """Exact distinct-oip counts per cip over the union of device segments of
+    (cip, oip) pairs (torch CUDA tensors shaped (n, 2)), like exact_counts
+    for one window (workload.cpp:180-213).  Returns {cip: count >= min_count}."""
+    segs = [s for s in segments if s.numel()]
+    ptrs = (C.c_void_p * max(len(segs), 1))(*[s.data_ptr() for s in segs])
+    sizes = (C.c_uint64 * max(len(segs), 1))(*[s.numel() // 2 for s in segs])
+    cap = 1 << 16
+    while True:
+        cips = np.empty(cap, dtype=np.uint32)
+        counts = np.empty(cap, dtype=np.uint32)
+        n = C.c_uint64()
+        check(load().sspd_exact_counts(device, ptrs, sizes, len(segs), distinct_hint, min_count,
+                                       _u32(cips), _u32(counts), cap, C.byref(n),
+                                       C.c_void_p(stream_ptr or 0)))
+        if n.value <= cap:
+            return {int(c): int(k) for c, k in zip(cips[:n.value], counts[:n.value])}
+        cap = int(n.value)
+
+
 def launch_count() -> int:
     return int(load().sspd_launch_count())

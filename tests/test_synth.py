@@ -73,3 +73,28 @@ def test_device_generator_matches_host(gpu):
                                           C.c_void_p(out.data_ptr()), None))
         torch.cuda.synchronize()
         assert np.array_equal(out.cpu().numpy().view(np.uint32), want)
+
+
+@pytest.mark.gpu
+def test_exact_counts_on_device_match_host(gpu):
+    """sspd_exact_counts == the union-of-sets definition (workload.cpp:180-213)
+    over several overlapping segments, including cip 0xFFFFFFFF and the pair
+    equal to the empty-key marker."""
+    import torch
+
+    rng = np.random.default_rng(17)
+    segs = []
+    for n in (50_000, 80_000, 3):
+        cip = rng.integers(0, 3000, n).astype(np.uint32)
+        oip = rng.integers(0, 400, n).astype(np.uint32)
+        segs.append(np.stack([cip, oip], 1))
+    segs[2][:] = [[0xFFFFFFFF, 0xFFFFFFFF], [0xFFFFFFFF, 7], [5, 0xFFFFFFFF]]
+    allp = np.concatenate(segs)
+    uniq = np.unique(allp, axis=0)
+    cips, cnt = np.unique(uniq[:, 0], return_counts=True)
+    want = {int(c): int(k) for c, k in zip(cips, cnt)}
+    dev = [torch.from_numpy(s.view(np.int32)).cuda() for s in segs]
+    assert gpu.exact_counts(dev) == want
+    assert gpu.exact_counts(dev, min_count=200) == {c: k for c, k in want.items() if k >= 200}
+    with pytest.raises(gpu.OutOfRange):
+        gpu.exact_counts(dev, distinct_hint=16)   # table too small: an error, never a wrong count
