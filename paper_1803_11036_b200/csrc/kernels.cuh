@@ -344,14 +344,18 @@ struct PushArgs {
   uint64_t region_cap;
 };
 
+// Tuned on B200 at C2 (profiles/r01_ab_dedup_tuning*.txt): 2 pairs per
+// thread with every fresh pair's stamp atomics issued before any old value
+// is consumed beat 4 pairs with per-pair round trips (3.64 vs 3.76 ms/slot);
+// 8 pairs or tighter register caps were slower.
 #ifndef SSPD_DEDUP_PPT
-#define SSPD_DEDUP_PPT 4  // pairs per thread per iteration (probes in flight)
+#define SSPD_DEDUP_PPT 2  // pairs per thread per iteration (probes in flight)
 #endif
 #ifndef SSPD_DEDUP_MINB
 #define SSPD_DEDUP_MINB 1
 #endif
 #ifndef SSPD_DEDUP_BATCH_ATOMICS
-#define SSPD_DEDUP_BATCH_ATOMICS 0
+#define SSPD_DEDUP_BATCH_ATOMICS 1
 #endif
 
 template <int H1MODE, int HIST, int BITS, int EXPORT, int PUSH = 0>
