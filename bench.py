@@ -428,7 +428,23 @@ def main():
     got = {d.cip for d in reps} if reps is not None else set()
     accuracy = {"true_supers": len(truth), "reported": len(got),
                 "fpr": round(len(got - truth) / max(len(truth), 1), 6),
-                "fnr": round(len(truth - got) / max(len(truth), 1), 6)}
+                "fnr": round(len(truth - got) / max(len(truth), 1), 6),
+                "truth": "generator"}
+    if world == 1:
+        # and against exact distinct counts of the same window, on the device
+        # (sspd_exact_counts): the union of the last k slots' pairs
+        last = args.warmup + args.steps - 1
+        segs = [trace[(last - j) % S] for j in range(min(k, last + 1))]
+        try:
+            exact = P.exact_counts(segs, min_count=int(np.ceil(theta)), distinct_hint=32 << 20,
+                                   device=dev, stream_ptr=stream.cuda_stream)
+            ex = set(exact)
+            accuracy.update({"exact_true_supers": len(ex),
+                             "exact_fpr": round(len(got - ex) / max(len(ex), 1), 6),
+                             "exact_fnr": round(len(ex - got) / max(len(ex), 1), 6),
+                             "truth": "generator + exact device counts of the window"})
+        except Exception as e:
+            accuracy["exact"] = f"unavailable: {type(e).__name__}: {e}"
 
     # --- CPU baseline: the compiled reference on this host ---------------------
     cpu = None

@@ -1,0 +1,2 @@
+python -m pytest tests -q -m gpu > gpurun_out/pytest_gpu.log 2>&1
+python bench.py > gpurun_out/bench_c2.json 2> gpurun_out/bench_c2.err
