@@ -12,7 +12,10 @@ from .grid import (BASE_NOW, Detection, Grid, device_count, estimate_cardinality
                    export_snapshot,
                    hot_cutoff, import_snapshot, launch_count, merge_rseas)
 
+from .pipeline import run_detection, validate_config
+
 __all__ = [
+    "run_detection", "validate_config",
     "BASE_NOW", "CandidateOverflow", "CudaError", "Detection", "Grid", "InvalidArgument",
     "NoDevice", "OutOfRange", "PAPER_MAX", "SspdError", "UNION_MIN", "device_count",
     "estimate_cardinality", "exact_counts", "export_snapshot", "hot_cutoff", "import_snapshot", "launch_count",

@@ -521,3 +521,24 @@ def test_python_snapshot_roundtrip_matches_cli_format(gpu, tmp_path):
     assert out.read_bytes() == data
     with pytest.raises(RuntimeError, match="truncated payload"):
         gpu.import_snapshot(io.BytesIO(data[:-2]))
+
+
+@pytest.mark.parametrize("label,shards,policy", [("single", 1, 0), ("sharded_union", 4, 0),
+                                                 ("sharded_paper", 4, 1)])
+def test_run_detection_matches_reference_fixture(gpu, label, shards, policy):
+    """run_detection on the device against the compiled reference's reports
+    on its own synth trace (tests/golden/, made by make_golden.py): same
+    slots, cips and estimates, bit for bit."""
+    import json
+
+    here = os.path.dirname(os.path.abspath(__file__))
+    gold = json.load(open(os.path.join(here, "golden", "golden.json")))["pipeline"]
+    z = np.load(os.path.join(here, "golden", gold["trace"]))
+    trace, owner = z["trace"], z["owner"]
+    parts = [trace] if shards == 1 else [trace[owner == i] for i in range(shards)]
+    reps = gpu.run_detection(parts, q=10, r=5, delta=8, seed=0x5eed, eta=256, k=5, theta=128.0,
+                             policy=policy)
+    want = gold["runs"][label]
+    assert len(reps) == want["n_reports"]
+    got = [[s, d.cip, d.estimate.hex()] for s, dets in reps for d in dets]
+    assert got == want["rows"]
