@@ -542,3 +542,53 @@ def test_run_detection_matches_reference_fixture(gpu, label, shards, policy):
     assert len(reps) == want["n_reports"]
     got = [[s, d.cip, d.estimate.hex()] for s, dets in reps for d in dets]
     assert got == want["rows"]
+
+
+def test_three_routers_push_exchange_on_one_device(gpu):
+    """The fused exchange end to end with the real kernels: three router grids
+    on one device push their new pairs into each other's inboxes while
+    scanning (parity double-buffered, as dist.PushExchange does across
+    GPUs), then fold the received pairs.  Every router's grid and report must
+    equal the oracle's union-min merge of the three node grids, every slot.
+    (Routers run one after another: no kernel waits on another.)"""
+    import torch
+
+    world, cap = 3, 40_000
+    geo = dict(DESK)
+    grids = [gpu.Grid(seed=0x707, **geo) for _ in range(world)]
+    nodes = [O.OracleGrid(seed=0x707, **geo) for _ in range(world)]
+    inbox = [[torch.zeros((world * cap, 2), dtype=torch.int32, device="cuda") for _ in range(world)]
+             for _ in range(2)]
+    tables = [torch.tensor([b.data_ptr() for b in inbox[p]], dtype=torch.int64, device="cuda")
+              for p in range(2)]
+    for g in grids:
+        g.track_window(5)
+        g.set_exchange(2)
+    rng = O.Mt64(707)
+    base = rng.pairs(6000)
+    for slot in range(4):
+        par = slot & 1
+        p = base[rng.draw(30_000) % 6000]
+        owner = rng.draw(len(p)) % world
+        counts = []
+        for r, g in enumerate(grids):
+            g.set_push(tables[par].data_ptr(), world, r, cap)
+            mine = p[owner == r]
+            g.scan_batch(torch.from_numpy(mine.view(np.int32)).cuda())
+            nodes[r].scan(mine)
+            counts.append(g.new_pairs_ptr()[1])
+        torch.cuda.synchronize()
+        for r, g in enumerate(grids):
+            g.set_exchange(0)
+            for src in range(world):
+                if src != r and counts[src]:
+                    g.scan_batch(inbox[par][r][src * cap: src * cap + counts[src]])
+            g.set_exchange(2)
+        want = O.OracleGrid.merge(nodes, 0)
+        ref = [(d.cip, d.estimate) for d in want.reconstruct(5, 128.0)]
+        for g in grids:
+            assert np.array_equal(g.cells(), want.cells()), slot
+            assert [(d.cip, d.estimate) for d in g.reconstruct_leveled(5, 128.0)] == ref
+        for g, nd in zip(grids, nodes):
+            g.advance_slot()
+            nd.advance()
