@@ -115,6 +115,14 @@ struct DevBuf {
   }
 };
 
+// DevBuf owned by one call: released on every exit path.
+struct ScopedBuf : DevBuf {
+  ScopedBuf() = default;
+  ScopedBuf(const ScopedBuf&) = delete;
+  ScopedBuf& operator=(const ScopedBuf&) = delete;
+  ~ScopedBuf() { release(); }
+};
+
 }  // namespace
 
 struct sspd_grid {
@@ -1076,7 +1084,7 @@ sspd_status sspd_merge(const sspd_grid* const* grids_c, uint64_t n, int policy, 
     srcs[i] = MergeSrc{grids[i]->stamps, now_common - grids[i]->now};
   }
   const size_t sbytes = n * sizeof(MergeSrc);
-  DevBuf tmp;
+  ScopedBuf tmp;
   if (tmp.ensure(sbytes) != cudaSuccess) return fail(SSPD_CUDA_ERROR, "CUDA error: out of memory (merge)");
   CU(cudaMemcpyAsync(tmp.p, srcs.data(), sbytes, cudaMemcpyHostToDevice, out->stream));
   out->h2d_bytes += (sbytes);
@@ -1088,7 +1096,6 @@ sspd_status sspd_merge(const sspd_grid* const* grids_c, uint64_t n, int policy, 
   }
   sspd_status s = check_launch();
   CU(cudaStreamSynchronize(out->stream));
-  tmp.release();
   if (s) return s;
   out->now = now_common;
   out->hist_valid = false;
@@ -1276,7 +1283,7 @@ sspd_status sspd_exact_counts(int device, const uint32_t* const* dev_segments, c
   while (ce < 2 * std::min<uint64_t>(want, 1ull << 32)) ce <<= 1;
   DeviceGuard dg(device);
   cudaStream_t st = static_cast<cudaStream_t>(cuda_stream);
-  DevBuf pset, ckeys, ccounts, flags, out;
+  ScopedBuf pset, ckeys, ccounts, flags, out;
   if (pset.ensure(pe * 8) != cudaSuccess || ckeys.ensure(ce * 8) != cudaSuccess ||
       ccounts.ensure(ce * 4) != cudaSuccess || flags.ensure(64) != cudaSuccess ||
       out.ensure(std::max<uint64_t>(out_cap, 1) * 8 + 64) != cudaSuccess) {
