@@ -890,6 +890,7 @@ sspd_status sspd_hot_sets(sspd_grid* g, uint32_t k, uint64_t cutoff, uint32_t* c
 
 sspd_status sspd_finalize(sspd_grid* g, const uint32_t* tuples, uint64_t n, uint32_t k, uint64_t cutoff,
                           uint8_t* accepted, uint32_t* cips, uint32_t* r_ks) {
+  if (g->r > 64) return fail(SSPD_INVALID_ARGUMENT, "finalize_candidate: r > 64 unsupported");
   std::lock_guard<std::mutex> lk(g->mu);
   DeviceGuard dg(g->device);
   sspd_status s = commit_locked(g);
