@@ -126,7 +126,7 @@ sspd_status sspd_finalize(sspd_grid* g, const uint32_t* tuples, uint64_t n, uint
  * as CandidateOverflow(level, count, cap) would be.  Writes at most out_cap
  * detections; *n_out is the full count.  The same cip set as
  * reconstruct_recursive (rsea.cpp:126-166), which has no cap (pass
- * cap = UINT64_MAX). */
+ * cap = UINT64_MAX).  Supports r <= 64 (as does sspd_finalize). */
 sspd_status sspd_reconstruct(sspd_grid* g, uint32_t k, uint64_t cutoff, uint64_t cap,
                              sspd_detection* out, uint64_t out_cap, uint64_t* n_out,
                              uint32_t* ovf_level, uint64_t* ovf_count);
