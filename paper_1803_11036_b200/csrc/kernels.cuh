@@ -331,13 +331,6 @@ __device__ __forceinline__ void stamp_pair(const ScanTables& t, const Geo& geo, 
 // falls back to an all-gather for that slot.
 // Each thread takes 4 pairs per iteration and issues their 4 first probes
 // together before resolving any (the probes are the latency chain).
-// Per-CTA shared-memory front of the pair set: a direct-mapped cache of keys
-// this CTA has already resolved (found or inserted in the global set).  A hit
-// skips the global probe; entries only ever hold keys that are recorded in
-// this slot, so a lost entry (racing overwrite) costs a global probe, never a
-// touch.
-constexpr int kSmemCache = 2048;
-
 struct PushArgs {
   uint2* const* peers;  // device array of `world` inbox pointers (peer-mapped)
   uint32_t world, rank;
@@ -369,9 +362,7 @@ __global__ void __launch_bounds__(256, SSPD_DEDUP_MINB) scan_dedup_kernel(const 
                                                          unsigned long long* __restrict__ out_count,
                                                          PushArgs push = PushArgs{}) {
   __shared__ ScanTables t;
-  __shared__ unsigned long long s_seen[kSmemCache];
-  for (int i = threadIdx.x; i < kSmemCache; i += blockDim.x) s_seen[i] = kEmptyKey;
-  load_scan_tables(t, tabs);  // ends with __syncthreads()
+  load_scan_tables(t, tabs);
   const uint32_t now_slot = HIST ? now % K : 0;
   const uint32_t lane = threadIdx.x & 31;
   const uint64_t tid = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -406,14 +397,13 @@ __global__ void __launch_bounds__(256, SSPD_DEDUP_MINB) scan_dedup_kernel(const 
     for (int u = 0; u < P; ++u) {
       key[u] = (uint64_t)c[u] << 32 | o[u];
       h[u] = pair_slot_hash(key[u]);
-      probe[u] = valid[u] && s_seen[(h[u] >> 40) & (kSmemCache - 1)] != key[u];
+      probe[u] = valid[u];
       v[u] = probe[u] ? __ldca(table + pair_slot(h[u], 0, table_mask)) : 0ull;
     }
     bool fresh[P];
 #pragma unroll
     for (int u = 0; u < P; ++u) {
       fresh[u] = probe[u] && pair_resolve(table, table_mask, key[u], h[u], v[u]);
-      if (probe[u] && key[u] != kEmptyKey) s_seen[(h[u] >> 40) & (kSmemCache - 1)] = key[u];
     }
     if (EXPORT) {
 #pragma unroll
