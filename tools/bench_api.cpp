@@ -1,0 +1,99 @@
+// bench_api -- per-entry-point timings of the drop-in C++ API against the
+// compiled reference, call for call: the cases of the reference's own
+// benchmark (proj/bench/bench_kernels.cpp:35-78 -- scan_batch, advance_slot,
+// reconstruct_recursive, reconstruct_leveled at the desk geometry) plus the
+// paper geometry.  Wall-clock per call (the API is synchronous), median of
+// repetitions; the reference runs with every host core as workers.
+//
+//   make -C tools bench_api && tools/bin/bench_api
+#include <algorithm>
+#include <chrono>
+#include <cstdio>
+#include <functional>
+#include <random>
+#include <thread>
+#include <vector>
+
+#include "../tests/cpp/ref_abi.hpp"
+#include "sspd/rsea.hpp"
+
+extern "C" {
+void* ref_grid_create(uint32_t q, uint32_t r, uint32_t delta, uint64_t seed, uint32_t eta);
+}
+
+namespace {
+
+double median_ms(int reps, const std::function<void()>& f) {
+  std::vector<double> t;
+  for (int i = 0; i < reps; ++i) {
+    const auto a = std::chrono::steady_clock::now();
+    f();
+    t.push_back(std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - a).count());
+  }
+  std::sort(t.begin(), t.end());
+  return t[t.size() / 2];
+}
+
+void planted(std::vector<sspd::IpPair>& out, uint32_t hosts, uint32_t fanout, std::mt19937_64& rng) {
+  for (uint32_t h = 0; h < hosts; ++h) {
+    const uint32_t cip = static_cast<uint32_t>(rng());
+    for (uint32_t j = 0; j < fanout; ++j) out.push_back({cip, static_cast<uint32_t>(rng())});
+  }
+}
+
+void run(const char* name, sspd::RhfgConfig cfg, uint32_t eta, uint32_t k, double theta, std::size_t batch) {
+  const unsigned workers = std::max(1u, std::thread::hardware_concurrency());
+  std::mt19937_64 rng(42);
+  std::vector<sspd::IpPair> pairs(batch);
+  for (auto& p : pairs) p = {static_cast<uint32_t>(rng()), static_cast<uint32_t>(rng())};
+  std::vector<sspd::IpPair> supers;
+  planted(supers, 20, static_cast<uint32_t>(2 * theta), rng);
+
+  sspd::Rsea ours(cfg, eta);
+  void* ref = ref_grid_create(cfg.q, cfg.r, cfg.delta, cfg.seed, eta);
+  ours.scan_batch(supers, 1);
+  ref_scan(ref, reinterpret_cast<const uint32_t*>(supers.data()), supers.size(), workers);
+
+  const int reps = 7;
+  const double scan_o = median_ms(reps, [&] { ours.scan_batch(pairs, 1); (void)ours.hot_sets(k, theta); });
+  const double scan_r = median_ms(reps, [&] {
+    ref_scan(ref, reinterpret_cast<const uint32_t*>(pairs.data()), pairs.size(), workers);
+  });
+  const double adv_o = median_ms(reps, [&] { ours.advance_slot(1); (void)ours.hot_sets(k, theta); });
+  const double adv_r = median_ms(3, [&] { ref_advance(ref, workers); });
+  ours.scan_batch(supers, 1);
+  ref_scan(ref, reinterpret_cast<const uint32_t*>(supers.data()), supers.size(), workers);
+  std::vector<uint32_t> cips(1 << 16);
+  std::vector<double> ests(1 << 16);
+  size_t n = 0, cnt = 0;
+  uint32_t lvl = 0;
+  const double lev_o = median_ms(reps, [&] { (void)ours.reconstruct_leveled(k, theta, 1); });
+  const double lev_r = median_ms(3, [&] {
+    ref_reconstruct(ref, 1, k, theta, workers, std::size_t{1} << 24, cips.data(), ests.data(), cips.size(), &n, &lvl,
+                    &cnt);
+  });
+  const double rec_o = median_ms(reps, [&] { (void)ours.reconstruct_recursive(k, theta); });
+  const double rec_r = median_ms(3, [&] {
+    ref_reconstruct(ref, 0, k, theta, workers, std::size_t{1} << 24, cips.data(), ests.data(), cips.size(), &n, &lvl,
+                    &cnt);
+  });
+  std::printf("| %s | scan_batch(%zu pairs) | %.3f | %.3f | %.0fx |\n", name, batch, scan_o, scan_r, scan_r / scan_o);
+  std::printf("| %s | advance_slot | %.3f | %.3f | %.0fx |\n", name, adv_o, adv_r, adv_r / adv_o);
+  std::printf("| %s | reconstruct_leveled (%zu hosts) | %.3f | %.3f | %.0fx |\n", name, n, lev_o, lev_r,
+              lev_r / lev_o);
+  std::printf("| %s | reconstruct_recursive | %.3f | %.3f | %.0fx |\n", name, rec_o, rec_r, rec_r / rec_o);
+  ref_grid_destroy(ref);
+}
+
+}  // namespace
+
+int main() {
+  std::printf("host cores: %u\n\n", std::thread::hardware_concurrency());
+  std::printf("| geometry | call | B200 ms | reference ms | speed-up |\n|---|---|---|---|---|\n");
+  // ours: the scan and advance rows include a hot_sets call, which forces
+  // the device work to finish (the C++ API defers it until observed)
+  run("desk (q10 r5 d8 eta256)", sspd::RhfgConfig{10, 5, 8, 0x5eed}, 256, 30, 128, 32768);
+  run("paper (q14 r5 d6 eta2048)", sspd::RhfgConfig{14, 5, 6, 0x5eed}, 2048, 5, 1024, 32768);
+  run("paper, 1M-pair batches", sspd::RhfgConfig{14, 5, 6, 0x5eed}, 2048, 5, 1024, 1 << 20);
+  return 0;
+}
