@@ -770,9 +770,13 @@ sspd_status sspd_scan(sspd_grid* g, const uint32_t* pairs, uint64_t n, int pairs
     done += cnt;
     buf ^= 1;
   }
-  // Pageable sources are consumed by the time cudaMemcpyAsync returns; for
-  // pinned ones the caller may reuse its buffer only after the copies land.
-  CU(cudaStreamSynchronize(g->copy_stream));
+  // Pageable sources are consumed by the time cudaMemcpyAsync returns (the
+  // driver stages them), so the call can return at once; pinned ones are
+  // read by DMA later, and the caller may reuse its buffer on return
+  // (scan_batch semantics), so wait for those copies.
+  cudaPointerAttributes attr{};
+  if (cudaPointerGetAttributes(&attr, pairs) != cudaSuccess) cudaGetLastError();
+  if (attr.type == cudaMemoryTypeHost) CU(cudaStreamSynchronize(g->copy_stream));
   return check_launch();
 }
 
