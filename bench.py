@@ -85,7 +85,8 @@ class ClockSampler:
         self.device = device
         self.proc = None
         self.nvml = None
-        self.samples = []  # (sm_mhz, reasons bitmask)
+        self.samples = []  # (sm_mhz, reasons bitmask) taken while `active`
+        self.active = False   # set by the timed loops between their synchronizes
         self.path = os.path.join(ROOT, "gpurun_out", f"clocks_dev{device}.csv")
 
     def _nvml_index(self):
@@ -111,8 +112,11 @@ class ClockSampler:
 
             def run():
                 while not self.stop.is_set():
-                    self.samples.append((N.nvmlDeviceGetClockInfo(h, N.NVML_CLOCK_SM),
-                                         N.nvmlDeviceGetCurrentClocksEventReasons(h)))
+                    if self.active:
+                        sample = (N.nvmlDeviceGetClockInfo(h, N.NVML_CLOCK_SM),
+                                  N.nvmlDeviceGetCurrentClocksEventReasons(h))
+                        if self.active:
+                            self.samples.append(sample)
                     time.sleep(0.002)
 
             self.nvml = N
@@ -153,7 +157,8 @@ class ClockSampler:
             sm = [c for c, _ in self.samples]
             reasons = sorted({nm for _, m in self.samples for nm, b in self.bits.items() if m & b})
             return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": self.max_mhz,
-                    "reasons": reasons, "samples": len(sm), "source": "nvml, 2 ms period"}
+                    "reasons": reasons, "samples": len(sm),
+                    "source": "nvml every 2 ms inside the timed regions (device + e2e loops)"}
         if not self.proc:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
         sm, mx, reasons = [], None, set()
@@ -374,11 +379,13 @@ def main():
         g.advance_slot()
         return rep, (e1, e2)
 
-    def timed_loop(n_steps, start, from_host):
+    def timed_loop(n_steps, start, from_host, clk=None):
         marks = []
         if world > 1:
             dist.barrier()
         torch.cuda.synchronize()
+        if clk is not None:
+            clk.active = True
         ev_a = torch.cuda.Event(enable_timing=True)
         ev_b = torch.cuda.Event(enable_timing=True)
         ev_a.record(stream)
@@ -388,6 +395,8 @@ def main():
             marks.append(m)
         ev_b.record(stream)
         torch.cuda.synchronize()
+        if clk is not None:
+            clk.active = False
         if world > 1:
             dist.barrier()
         ms = ev_a.elapsed_time(ev_b)
@@ -406,8 +415,8 @@ def main():
     g.profile(True)
     g.profile_reset()
     launches0 = P.launch_count()
-    with ClockSampler(dev) as clk:
-        ms, recon, reps = timed_loop(args.steps, slot, False)
+    clk = ClockSampler(dev).__enter__()
+    ms, recon, reps = timed_loop(args.steps, slot, False, clk)
     launches = P.launch_count() - launches0
     slot += args.steps
     prof = {}
@@ -428,12 +437,14 @@ def main():
             step(slot + i, True)
         slot += 2
         g.io_bytes(reset=True)
-        ms_e, _, _ = timed_loop(args.steps, slot, True)
+        ms_e, _, _ = timed_loop(args.steps, slot, True, clk)
         h2d, d2h = g.io_bytes(reset=True)
         slot += args.steps
         e2e = {"value": round(total_pairs / (ms_e / 1e3) / 1e6, 3), "unit": unit,
                "h2d_bytes_per_step": h2d // args.steps, "d2h_bytes_per_step": d2h // args.steps,
                "ms_per_step": round(ms_e / args.steps, 3)}
+
+    clk.__exit__(None, None, None)
 
     if rank != 0:
         if world > 1:

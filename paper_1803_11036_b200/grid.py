@@ -66,6 +66,7 @@ class Grid:
             _handle = h
         self._h = _handle
         self.candidate_cap = 1 << 24
+        self._report_buf = None
 
     def close(self):
         if getattr(self, "_h", None):
@@ -192,9 +193,13 @@ class Grid:
         return self.finalize_candidates(np.asarray(cols).reshape(1, -1), k, theta)[0]
 
     def _reconstruct(self, k: int, theta: float, cap: int) -> list[Detection]:
-        out_cap = 1 << 16
+        # the report buffer is kept across calls (reports are usually a few
+        # hundred hosts at most) and regrown when a slot reports more
         while True:
-            buf = (_cabi.Detection_t * out_cap)()
+            buf = self._report_buf
+            if buf is None:
+                buf = self._report_buf = (_cabi.Detection_t * 4096)()
+            out_cap = len(buf)
             n = C.c_uint64()
             lvl = C.c_uint32()
             cnt = C.c_uint64()
@@ -204,8 +209,8 @@ class Grid:
                 raise CandidateOverflow(self._L.sspd_last_error().decode(), lvl.value, cnt.value)
             check(st)
             if n.value <= out_cap:
-                return [Detection(buf[i].cip, buf[i].estimate, buf[i].r_k) for i in range(n.value)]
-            out_cap = n.value
+                return [Detection(d.cip, d.estimate, d.r_k) for d in buf[:n.value]]
+            self._report_buf = (_cabi.Detection_t * n.value)()
 
     def reconstruct_leveled(self, k: int, theta: float, workers: int = 1) -> list[Detection]:
         """Rsea::reconstruct_leveled (rsea.cpp:168-255)."""
