@@ -249,6 +249,9 @@ def main():
                          "(push; auto = push, else pairs if symmetric memory is unavailable), the "
                          "same lists all-gathered after the scan (pairs), OR of touched bitmaps, or "
                          "the literal all-reduce(max) of the full stamp grid")
+    ap.add_argument("--stamp-width", type=int, default=32, choices=[8, 16, 32],
+                    help="bits per recorder stamp (C4): 8/16 keep R_k (k <= window) and the reports "
+                         "exact, 32 also the full distances")
     ap.add_argument("--scan-mode", default="auto", choices=["auto", "bitmap", "direct", "dedup", "binned"])
     ap.add_argument("--filter", type=int, default=-1, help="L1 duplicate probe 0/1 (-1 = default)")
     ap.add_argument("--ref-pairs", type=int, default=100_000_000,
@@ -306,10 +309,10 @@ def main():
     torch.cuda.set_stream(stream)
 
     # --- setup (untimed): grid, trace resident in HBM, pinned host copy ------
-    g = P.Grid(cfg["q"], cfg["r"], cfg["delta"], cfg["seed"], cfg["eta"], device=dev)
+    g = P.Grid(cfg["q"], cfg["r"], cfg["delta"], cfg["seed"], cfg["eta"], device=dev,
+               width=args.stamp_width, k_max=cfg["k"])
     g.set_stream(stream.cuda_stream)
     g.scan_mode({"auto": -1, "bitmap": 0, "direct": 1, "dedup": 2, "binned": 3}[args.scan_mode], args.filter)
-    g.track_window(cfg["k"])
     merge_used = args.merge
     if world > 1 and args.merge != "stamps":
         cap = min(cfg["pairs_per_slot"], 32 << 20)
@@ -421,7 +424,7 @@ def main():
     slot += args.steps
     prof = {}
     for name in ("bin", "scan", "commit", "hist_counts", "count", "hot_compact", "level2",
-                 "level_ext", "finalize", "merge"):
+                 "level_ext", "finalize", "merge", "rebase"):
         t, n, u = g.profile_read(name)
         if n:
             prof[name] = {"ms": t, "launches": n, "units": u}
@@ -542,9 +545,9 @@ def main():
         # BASELINE.md's only published packets/s is the paper's GSSD 109 Mpkt/s on a
         # GTX 950 at the paper parameters -- the C1 geometry
         "vs_baseline": round(value / 109.0, 2) if args.config == "c1" else None,
-        "dtype": "u32", "data": "synthetic",
+        "dtype": {8: "u8 stamps", 16: "u16 stamps", 32: "u32"}[args.stamp_width], "data": "synthetic",
         "config": {"workload": cfg["workload"], "pairs_per_step_per_gpu": n_local,
-                   "window_k": k, "theta": theta,
+                   "window_k": k, "theta": theta, "stamp_bits": args.stamp_width,
                    "merge": {"pairs": "union-min: all-gather of each router's distinct pairs per slot",
                              "push": "union-min: distinct pairs pushed to peers over NVLink during the scan",
                              "bitmap": "union-min: OR all-reduce of the slot's touched bitmaps",

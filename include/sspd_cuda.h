@@ -71,6 +71,19 @@ sspd_status sspd_device_count(int* n);
  * fails with "Rsea: <first diagnostic>".  All recorders start never-seen. */
 sspd_status sspd_grid_create(int device, uint32_t q, uint32_t r, uint32_t delta,
                              uint64_t seed, uint32_t eta, sspd_grid** out);
+/* B200 extension (BASELINE config C4's stamp-width axis): a grid whose
+ * recorders hold `width`-bit stamps (8 or 16; 32 = sspd_grid_create plus
+ * sspd_track_window(k_max)).  Narrow grids are exact for in-window counts
+ * with k <= k_max and everything derived from them -- active_counts,
+ * hot_sets, finalize, reconstruct -- and keep the window ring on; k_max must
+ * be below 2^width - 1.  Entry points that need full distances or stamps
+ * (get/put_distances, clone, merge, equal, commit, the exchange hooks) fail
+ * with SSPD_INVALID_ARGUMENT on them. */
+sspd_status sspd_grid_create_narrow(int device, uint32_t q, uint32_t r, uint32_t delta,
+                                    uint64_t seed, uint32_t eta, uint32_t width,
+                                    uint32_t k_max, sspd_grid** out);
+/* Stamp width (8, 16, 32) and tracked window (0 = none). */
+sspd_status sspd_grid_stamp_width(const sspd_grid* g, uint32_t* width, uint32_t* k_max);
 /* Copy constructor (Rsea is copyable: snapshot.cpp:127, pipeline.cpp:39):
  * device-to-device copy onto `device` (-1 = the source's device). */
 sspd_status sspd_grid_clone(const sspd_grid* src, int device, sspd_grid** out);

@@ -44,6 +44,9 @@ SIGNATURES = {
     "sspd_grid_clone": (C.c_int, [grid_p, C.c_int, C.POINTER(grid_p)]),
     "sspd_grid_destroy": (C.c_int, [grid_p]),
     "sspd_grid_info": (C.c_int, [grid_p, u64p, C.POINTER(C.c_int), u32p]),
+    "sspd_grid_create_narrow": (C.c_int, [C.c_int, C.c_uint32, C.c_uint32, C.c_uint32, C.c_uint64,
+                                          C.c_uint32, C.c_uint32, C.c_uint32, C.POINTER(grid_p)]),
+    "sspd_grid_stamp_width": (C.c_int, [grid_p, u32p, u32p]),
     "sspd_grid_set_stream": (C.c_int, [grid_p, C.c_void_p]),
     "sspd_grid_synchronize": (C.c_int, [grid_p]),
     "sspd_scan": (C.c_int, [grid_p, C.c_void_p, C.c_uint64, C.c_int]),

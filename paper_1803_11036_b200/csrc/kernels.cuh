@@ -1117,4 +1117,244 @@ __global__ void equal_kernel(const uint32_t* __restrict__ a, uint32_t now_a, con
   }
 }
 
+// ---------------------------------------------------------------------------
+// NARROW STAMPS (w = 8 or 16 bits per recorder; BASELINE config C4's
+// stamp-width axis).  Exactness domain: in-window counts R_k for k <= K (the
+// grid's window, fixed at creation) and everything derived from them (hot
+// sets, finalize, reconstruction reports); full distances are not kept.
+//
+// Codes rise with time inside an epoch: 0 = not seen in the window, and slot
+// `s` writes code(s) = lo + (s - epoch0), so a recorder's age is
+// code(now) - c.  Before code(now) would pass `hi`, a rebase pass
+// (narrow_rebase_kernel) clears codes older than K and shifts the rest so
+// that code(now) = lo + K - 1: an epoch lasts hi - lo - K + 2 slots.
+//   w = 16: lo = 0x0080, hi = 0x7F7F -- the positive normal bf16 bit
+//           patterns, which order like the integers, so a touch is ONE
+//           returning packed-bf16 max atomic (ATOMG.E.MAX.BF16x2) whose other
+//           lane is +0.0 (a no-op), exactly like the 32-bit atomicMax.
+//   w = 8:  lo = 1, hi = 255; no 8-bit atomic exists, so a touch is a load
+//           of the 32-bit word and a CAS on it (retried if a neighbour moved).
+// The old code drives the window ring exactly as in the 32-bit scan.
+struct NarrowCodes {
+  uint32_t now;     // code(now)
+  uint32_t lo;      // smallest live code
+};
+
+__device__ __forceinline__ uint32_t narrow_max(uint16_t* p, uint32_t code) {
+  uint32_t* w = reinterpret_cast<uint32_t*>(reinterpret_cast<uintptr_t>(p) & ~uintptr_t(3));
+  const bool upper = (reinterpret_cast<uintptr_t>(p) & 2u) != 0;
+  const unsigned short a = upper ? 0 : (unsigned short)code, b = upper ? (unsigned short)code : 0;
+  unsigned short oa, ob;
+  asm volatile("atom.global.max.noftz.v2.bf16 {%0, %1}, [%2], {%3, %4};"
+               : "=h"(oa), "=h"(ob)
+               : "l"(w), "h"(a), "h"(b)
+               : "memory");
+  return upper ? ob : oa;
+}
+
+// u8: CAS on the containing word, starting from the value `cur` read earlier.
+__device__ __forceinline__ uint32_t narrow_max_from(uint8_t* p, uint32_t code, uint32_t cur) {
+  uint32_t* w = reinterpret_cast<uint32_t*>(reinterpret_cast<uintptr_t>(p) & ~uintptr_t(3));
+  const uint32_t sh = (uint32_t)(reinterpret_cast<uintptr_t>(p) & 3u) * 8u;
+  for (;;) {
+    const uint32_t old = (cur >> sh) & 0xffu;
+    if (old >= code) return old;
+    const uint32_t prev = atomicCAS(w, cur, (cur & ~(0xffu << sh)) | (code << sh));
+    if (prev == cur) return old;
+    cur = prev;
+  }
+}
+
+__device__ __forceinline__ uint32_t word_of(const uint8_t* p) {
+  return __ldcg(reinterpret_cast<const uint32_t*>(reinterpret_cast<uintptr_t>(p) & ~uintptr_t(3)));
+}
+
+// Ring bookkeeping of one touch whose previous code was `old`.
+__device__ __forceinline__ void narrow_ring(uint32_t old, uint32_t cell, const NarrowCodes& nc, uint32_t now,
+                                           uint32_t now_slot, const Geo& geo, uint32_t* __restrict__ hist,
+                                           uint32_t K) {
+  if (old >= nc.now) return;  // already stamped this slot
+  atomicAdd(hist + (uint64_t)now_slot * geo.ncells + cell, 1u);
+  if (old >= nc.lo) {
+    const uint32_t age = nc.now - old;
+    if (age < K) atomicSub(hist + (uint64_t)((now - age) % K) * geo.ncells + cell, 1u);
+  }
+}
+
+// Scan into a narrow grid: direct stamping, optionally behind the per-slot
+// pair set (DEDUP) of scan_dedup_kernel; 2 pairs per thread, every touch's
+// atomic issued before any old code is consumed.  The window ring is always
+// kept.
+template <class T, int H1MODE, int DEDUP>
+__global__ void __launch_bounds__(256) scan_narrow_kernel(const uint32_t* __restrict__ pairs, uint64_t n,
+                                                          const HashTabs* __restrict__ tabs, Geo geo,
+                                                          unsigned long long* __restrict__ table, uint64_t table_mask,
+                                                          T* __restrict__ codes, uint32_t now, NarrowCodes nc,
+                                                          uint32_t* __restrict__ hist, uint32_t K) {
+  __shared__ ScanTables t;
+  load_scan_tables(t, tabs);
+  const uint32_t now_slot = now % K;
+  constexpr int P = 2;
+  const uint64_t tid = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const uint64_t nthreads = (uint64_t)gridDim.x * blockDim.x;
+  const bool vec = (reinterpret_cast<uintptr_t>(pairs) & 15u) == 0;
+  const uint64_t ngroups = (n + P - 1) / P;
+  for (uint64_t g = tid; g < ngroups; g += nthreads) {
+    uint32_t c[P], o[P];
+    bool fresh[P];
+    const uint64_t p0 = g * P;
+    if (vec && p0 + P <= n) {
+      const uint4 a = ld_stream_u4(pairs + 2 * p0);
+      c[0] = a.x; o[0] = a.y; c[1] = a.z; o[1] = a.w;
+      fresh[0] = fresh[1] = true;
+    } else {
+#pragma unroll
+      for (int u = 0; u < P; ++u) {
+        fresh[u] = p0 + u < n;
+        c[u] = fresh[u] ? pairs[2 * (p0 + u)] : 0u;
+        o[u] = fresh[u] ? pairs[2 * (p0 + u) + 1] : 0u;
+      }
+    }
+    if (DEDUP) {
+      uint64_t key[P], h[P];
+      unsigned long long v[P];
+#pragma unroll
+      for (int u = 0; u < P; ++u) {
+        key[u] = (uint64_t)c[u] << 32 | o[u];
+        h[u] = pair_slot_hash(key[u]);
+        v[u] = fresh[u] ? __ldca(table + pair_slot(h[u], 0, table_mask)) : 0ull;
+      }
+#pragma unroll
+      for (int u = 0; u < P; ++u) fresh[u] = fresh[u] && pair_resolve(table, table_mask, key[u], h[u], v[u]);
+    }
+    if (geo.r <= 8) {
+      uint32_t bucket[P], col0[P], old[P][8];
+#pragma unroll
+      for (int u = 0; u < P; ++u) {
+        if (!fresh[u]) continue;
+        hash_pair<H1MODE>(t, geo, c[u], o[u], bucket[u], col0[u]);
+#pragma unroll
+        for (uint32_t row = 0; row < 8; ++row) {
+          if (row >= geo.r) break;
+          T* p = codes + (uint64_t)(row << geo.q | row_col(geo, row, c[u], col0[u])) * geo.eta + bucket[u];
+          if constexpr (sizeof(T) == 2) old[u][row] = narrow_max(p, nc.now);
+          else old[u][row] = word_of(p);
+        }
+      }
+      if constexpr (sizeof(T) == 1) {
+#pragma unroll
+        for (int u = 0; u < P; ++u) {
+          if (!fresh[u]) continue;
+#pragma unroll
+          for (uint32_t row = 0; row < 8; ++row) {
+            if (row >= geo.r) break;
+            T* p = codes + (uint64_t)(row << geo.q | row_col(geo, row, c[u], col0[u])) * geo.eta + bucket[u];
+            old[u][row] = narrow_max_from(p, nc.now, old[u][row]);
+          }
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < P; ++u) {
+        if (!fresh[u]) continue;
+#pragma unroll
+        for (uint32_t row = 0; row < 8; ++row) {
+          if (row >= geo.r) break;
+          narrow_ring(old[u][row], row << geo.q | row_col(geo, row, c[u], col0[u]), nc, now, now_slot, geo, hist,
+                      K);
+        }
+      }
+    } else {
+#pragma unroll
+      for (int u = 0; u < P; ++u) {
+        if (!fresh[u]) continue;
+        uint32_t bucket, col0;
+        hash_pair<H1MODE>(t, geo, c[u], o[u], bucket, col0);
+        for (uint32_t row = 0; row < geo.r; ++row) {
+          const uint32_t cell = row << geo.q | row_col(geo, row, c[u], col0);
+          T* p = codes + (uint64_t)cell * geo.eta + bucket;
+          uint32_t old;
+          if constexpr (sizeof(T) == 2) old = narrow_max(p, nc.now);
+          else old = narrow_max_from(p, nc.now, word_of(p));
+          narrow_ring(old, cell, nc, now, now_slot, geo, hist, K);
+        }
+      }
+    }
+  }
+}
+
+// Epoch rebase: codes older than K become 0, the rest move down by `shift`
+// (streaming pass, 16-byte words).
+template <class T>
+__global__ void __launch_bounds__(256) narrow_rebase_kernel(T* __restrict__ codes, uint64_t n, uint32_t code_now,
+                                                            uint32_t lo, uint32_t K, uint32_t shift) {
+  constexpr uint32_t per = 16 / sizeof(T);
+  const uint64_t nvec = n / per;
+  uint4* v = reinterpret_cast<uint4*>(codes);
+  auto fix = [&](uint32_t c) -> uint32_t {
+    if (c < lo || code_now - c >= K) return 0u;
+    return c - shift;
+  };
+  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < nvec;
+       i += (uint64_t)gridDim.x * blockDim.x) {
+    uint4 x = v[i];
+    T* e = reinterpret_cast<T*>(&x);
+    bool dirty = false;
+#pragma unroll
+    for (uint32_t j = 0; j < per; ++j) {
+      const uint32_t f = fix(e[j]);
+      dirty |= f != e[j];
+      e[j] = (T)f;
+    }
+    if (dirty) v[i] = x;
+  }
+  for (uint64_t i = nvec * per + (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (uint64_t)gridDim.x * blockDim.x)
+    codes[i] = (T)fix(codes[i]);
+}
+
+// finalize_count_kernel over narrow codes: a bucket counts when all r rows
+// hold a live code younger than k (max distance < k), i.e. min code > thr
+// with thr = code(now) - k clamped below lo.
+template <class T>
+__global__ void __launch_bounds__(256) finalize_count_narrow_kernel(const uint32_t* __restrict__ tuples,
+                                                                    const T* __restrict__ codes, Geo geo,
+                                                                    uint32_t thr, int kmode,
+                                                                    const ReconMeta* __restrict__ meta,
+                                                                    const uint32_t* __restrict__ surv_idx,
+                                                                    uint32_t* __restrict__ surv_rk) {
+  constexpr uint32_t kChunk = 1024;
+  const uint64_t n_surv = meta->surv;
+  const uint32_t chunks = (geo.eta + kChunk - 1) / kChunk;
+  __shared__ uint32_t s_cols[64];
+  __shared__ uint32_t s_red[8];
+  for (uint64_t item = blockIdx.x; item < n_surv * chunks; item += gridDim.x) {
+    const uint64_t sidx = item / chunks;
+    const uint32_t c0 = (uint32_t)(item % chunks) * kChunk;
+    const uint32_t c1 = min(c0 + kChunk, geo.eta);
+    __syncthreads();
+    if (threadIdx.x < geo.r) s_cols[threadIdx.x] = tuples[(uint64_t)surv_idx[sidx] * geo.r + threadIdx.x];
+    __syncthreads();
+    uint32_t cnt = 0;
+    if (kmode == 0) {
+      for (uint32_t b = c0 + threadIdx.x; b < c1; b += blockDim.x) {
+        uint32_t m = 0xffffffffu;
+        for (uint32_t row = 0; row < geo.r; ++row)
+          m = min(m, (uint32_t)codes[((uint64_t)row << geo.q | s_cols[row]) * geo.eta + b]);
+        cnt += m > thr;
+      }
+    } else if (kmode == 2) {
+      for (uint32_t b = c0 + threadIdx.x; b < c1; b += blockDim.x) ++cnt;
+    }
+#pragma unroll
+    for (int o = 16; o; o >>= 1) cnt += __shfl_xor_sync(0xffffffffu, cnt, o);
+    if ((threadIdx.x & 31) == 0) s_red[threadIdx.x >> 5] = cnt;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      uint32_t tt = 0;
+      for (uint32_t w = 0; w < blockDim.x / 32; ++w) tt += s_red[w];
+      if (tt) atomicAdd(surv_rk + sidx, tt);
+    }
+  }
+}
+
 }  // namespace sspd_dev

@@ -166,6 +166,14 @@ struct sspd_grid {
   bool profiling = false;
   std::vector<ProfRec> prof;
   uint64_t h2d_bytes = 0, d2h_bytes = 0;  // host<->device traffic, for e2e accounting
+  // narrow stamps (width 8 or 16, kernels.cuh "NARROW STAMPS"): `codes`
+  // replaces `stamps`, the window ring (K = k_max) is always on, and codes
+  // are rebased before code(now) passes code_hi
+  uint32_t width = 32;
+  void* codes = nullptr;
+  uint32_t code_lo = 0, code_hi = 0;
+  uint32_t epoch0 = 0;  // code(now) = code_lo + (now - epoch0)
+  uint32_t code_now() const { return code_lo + (now - epoch0); }
   std::mutex mu;
 };
 
@@ -219,6 +227,15 @@ struct Prof {
     g->prof.push_back(rec);
   }
 };
+
+// Entry points that need the full 32-bit stamps (distances, merges,
+// exchanges) refuse narrow grids instead of returning inexact data.
+sspd_status wide_only(const sspd_grid* g, const char* what) {
+  if (g->width == 32) return SSPD_OK;
+  return fail(SSPD_INVALID_ARGUMENT, std::string(what) + ": not available on a grid with " +
+                                         std::to_string(g->width) + "-bit stamps (exact for in-window counts "
+                                         "with k <= " + std::to_string(g->K) + " only)");
+}
 
 sspd_status check_launch() {
   cudaError_t e = cudaGetLastError();
@@ -274,6 +291,10 @@ sspd_status counts_locked(sspd_grid* g, uint32_t k) {
     Prof p(g, "fill", g->geo.ncells);
     fill_u32_kernel<<<blocks, 256, 0, g->stream>>>(g->counts.as<uint32_t>(), g->geo.ncells,
                                                    k == 0 ? 0u : g->eta);
+  } else if (g->width != 32 && k > g->K) {
+    return fail(SSPD_INVALID_ARGUMENT, "active_count: k = " + std::to_string(k) + " exceeds the window K = " +
+                                           std::to_string(g->K) + " of a " + std::to_string(g->width) +
+                                           "-bit grid");
   } else if (g->K && k <= g->K) {
     s = hist_rebuild_locked(g);
     if (s) return s;
@@ -376,9 +397,21 @@ sspd_status queue_finalize(sspd_grid* g, const uint32_t* tuples, uint64_t in_cap
   CU(cudaMemsetAsync(s_rk, 0, (size_t)std::max<uint64_t>(in_cap, 1) * 4, g->stream));
   {
     const uint32_t chunks = (g->eta + 1023) / 1024;
+    const unsigned blocks = (unsigned)sm_count(g->device) * 8;
     Prof p(g, "finalize", in_cap * chunks);
-    finalize_count_kernel<<<(unsigned)sm_count(g->device) * 8, 256, 0, g->stream>>>(
-        tuples, g->stamps, g->geo, g->now - (k <= 0xFFFFu ? k : 0u), kmode_of(k), meta, s_idx, s_rk);
+    // live codes younger than k: code > code(now) - k, and never 0
+    const uint32_t thr = (uint32_t)std::max<int64_t>((int64_t)g->code_now() - (k <= 0xFFFFu ? k : 0u),
+                                                     (int64_t)g->code_lo - 1);
+    if (g->width == 8)
+      finalize_count_narrow_kernel<uint8_t><<<blocks, 256, 0, g->stream>>>(
+          tuples, static_cast<const uint8_t*>(g->codes), g->geo, thr, kmode_of(k), meta, s_idx, s_rk);
+    else if (g->width == 16)
+      finalize_count_narrow_kernel<uint16_t><<<blocks, 256, 0, g->stream>>>(
+          tuples, static_cast<const uint16_t*>(g->codes), g->geo, thr, kmode_of(k), meta, s_idx, s_rk);
+    else
+      finalize_count_kernel<<<blocks, 256, 0, g->stream>>>(tuples, g->stamps, g->geo,
+                                                            g->now - (k <= 0xFFFFu ? k : 0u), kmode_of(k), meta,
+                                                            s_idx, s_rk);
   }
   return check_launch();
 }
@@ -416,8 +449,10 @@ sspd_status sspd_device_count(int* n) {
   return SSPD_OK;
 }
 
-sspd_status sspd_grid_create(int device, uint32_t q, uint32_t r, uint32_t delta, uint64_t seed, uint32_t eta,
-                             sspd_grid** out) {
+namespace {
+
+sspd_status create_impl(int device, uint32_t q, uint32_t r, uint32_t delta, uint64_t seed, uint32_t eta,
+                        uint32_t width, uint32_t k_max, sspd_grid** out) {
   *out = nullptr;
   const std::string prob = first_problem(q, r, delta, eta);
   if (!prob.empty()) return fail(SSPD_INVALID_ARGUMENT, "Rsea: " + prob);
@@ -444,6 +479,7 @@ sspd_status sspd_grid_create(int device, uint32_t q, uint32_t r, uint32_t delta,
   g->geo.ncells = r << q;
   g->geo.n_rec = (uint64_t)g->geo.ncells * eta;
   g->by_eta = Div40::make(eta);
+  g->width = width;
   if (const char* f = std::getenv("SSPD_SCAN_FILTER")) g->scan_filter = std::atoi(f) != 0;
   // Device-resident pairs: deferred bitmap, measured faster than direct
   // stamping at both geometries (profiles/r01_ab_scan_modes.txt).
@@ -465,12 +501,33 @@ sspd_status sspd_grid_create(int device, uint32_t q, uint32_t r, uint32_t delta,
     cudaEventCreateWithFlags(&g->ev_copy[i], cudaEventDisableTiming);
     cudaEventCreateWithFlags(&g->ev_used[i], cudaEventDisableTiming);
   }
-  if (cudaMalloc(&g->stamps, g->geo.n_rec * 4) != cudaSuccess) {
+  if (width != 32) {
+    // narrow codes (all 0: nothing seen) and the always-on window ring
+    const uint64_t bytes = g->geo.n_rec * (width / 8);
+    if (cudaMalloc(&g->codes, bytes) != cudaSuccess) {
+      cudaGetLastError();
+      return cleanup("CUDA error: out of memory allocating " + std::to_string(bytes) + " bytes of stamps");
+    }
+    // u16 codes are positive normal bf16 bit patterns (the packed-bf16 max
+    // atomic orders them like integers); u8 codes are plain bytes
+    g->code_lo = width == 16 ? 0x0080u : 1u;
+    g->code_hi = width == 16 ? 0x7F7Fu : 255u;
+    g->epoch0 = g->now;
+    g->K = k_max;
+    if (cudaMalloc(&g->hist, (size_t)g->K * g->geo.ncells * 4) != cudaSuccess) {
+      cudaGetLastError();
+      return cleanup("CUDA error: out of memory (window ring)");
+    }
+    if (cudaMemsetAsync(g->codes, 0, bytes, g->stream) != cudaSuccess ||
+        cudaMemsetAsync(g->hist, 0, (size_t)g->K * g->geo.ncells * 4, g->stream) != cudaSuccess)
+      return cleanup("CUDA error: grid init");
+    g->hist_valid = true;
+  } else if (cudaMalloc(&g->stamps, g->geo.n_rec * 4) != cudaSuccess) {
     cudaGetLastError();
     return cleanup("CUDA error: out of memory allocating " + std::to_string(g->geo.n_rec * 4) +
                    " bytes of stamps");
   }
-  if (cudaMalloc(&g->touched, g->n_words * 4) != cudaSuccess) {
+  if (width == 32 && cudaMalloc(&g->touched, g->n_words * 4) != cudaSuccess) {
     cudaGetLastError();
     return cleanup("CUDA error: out of memory allocating the touched bitmap");
   }
@@ -483,11 +540,48 @@ sspd_status sspd_grid_create(int device, uint32_t q, uint32_t r, uint32_t delta,
   if (cudaMemcpyAsync(g->d_tabs, &h, sizeof h, cudaMemcpyHostToDevice, g->stream) != cudaSuccess)
     return cleanup("CUDA error: table upload");
   // All recorders never seen: stamp 0.
-  if (cudaMemsetAsync(g->stamps, 0, g->geo.n_rec * 4, g->stream) != cudaSuccess ||
-      cudaMemsetAsync(g->touched, 0, g->n_words * 4, g->stream) != cudaSuccess)
+  if (width == 32 && (cudaMemsetAsync(g->stamps, 0, g->geo.n_rec * 4, g->stream) != cudaSuccess ||
+                      cudaMemsetAsync(g->touched, 0, g->n_words * 4, g->stream) != cudaSuccess))
     return cleanup("CUDA error: grid init");
   if (cudaStreamSynchronize(g->stream) != cudaSuccess) return cleanup("CUDA error: grid init sync");
   *out = g;
+  return SSPD_OK;
+}
+
+}  // namespace
+
+sspd_status sspd_grid_create(int device, uint32_t q, uint32_t r, uint32_t delta, uint64_t seed, uint32_t eta,
+                             sspd_grid** out) {
+  return create_impl(device, q, r, delta, seed, eta, 32, 0, out);
+}
+
+sspd_status sspd_grid_create_narrow(int device, uint32_t q, uint32_t r, uint32_t delta, uint64_t seed, uint32_t eta,
+                                    uint32_t width, uint32_t k_max, sspd_grid** out) {
+  *out = nullptr;
+  if (width != 8 && width != 16 && width != 32)
+    return fail(SSPD_INVALID_ARGUMENT, "stamp width must be 8, 16 or 32, got " + std::to_string(width));
+  if (k_max < 1 || k_max > 65534)
+    return fail(SSPD_INVALID_ARGUMENT, "k must be in [1, 65534], got " + std::to_string(k_max));
+  // an epoch of codes holds hi - lo - K + 2 slots; keep it >= 2
+  if ((width == 8 && k_max > 254) || (width == 16 && k_max > 32511))
+    return fail(SSPD_INVALID_ARGUMENT, "window k = " + std::to_string(k_max) + " needs more than " +
+                                           std::to_string(width) + "-bit stamps");
+  if (width == 32) {
+    sspd_status s = create_impl(device, q, r, delta, seed, eta, 32, 0, out);
+    if (s) return s;
+    s = sspd_track_window(*out, k_max);
+    if (s) {
+      sspd_grid_destroy(*out);
+      *out = nullptr;
+    }
+    return s;
+  }
+  return create_impl(device, q, r, delta, seed, eta, width, k_max, out);
+}
+
+sspd_status sspd_grid_stamp_width(const sspd_grid* g, uint32_t* width, uint32_t* k_max) {
+  if (width) *width = g->width;
+  if (k_max) *k_max = g->K;
   return SSPD_OK;
 }
 
@@ -498,6 +592,7 @@ sspd_status sspd_grid_destroy(sspd_grid* g) {
     if (g->stream) cudaStreamSynchronize(g->stream);
     if (g->copy_stream) cudaStreamSynchronize(g->copy_stream);
     cudaFree(g->stamps);
+    cudaFree(g->codes);
     cudaFree(g->touched);
     cudaFree(g->hist);
     cudaFree(g->d_tabs);
@@ -524,6 +619,7 @@ sspd_status sspd_grid_destroy(sspd_grid* g) {
 
 sspd_status sspd_grid_clone(const sspd_grid* src_c, int device, sspd_grid** out) {
   auto* src = const_cast<sspd_grid*>(src_c);
+  if (sspd_status w = wide_only(src, "Rsea copy")) return w;
   std::lock_guard<std::mutex> lk(src->mu);
   DeviceGuard dg(src->device);
   sspd_status s = commit_locked(src);
@@ -597,6 +693,7 @@ sspd_status sspd_scan(sspd_grid* g, const uint32_t* pairs, uint64_t n, int pairs
   // Binning by pair-set region first (mode 3) makes the probes L2 hits but
   // measured slower overall (2.2 + 3.6 ms): the random stamp atomics dominate.
   if (mode < 0) mode = g->n_words * 4 > (48ull << 20) ? 2 : 1;
+  if (g->width != 32) mode = mode == 0 ? 1 : (mode == 3 ? 2 : mode);  // narrow: direct or dedup
   if (g->export_pairs && mode < 2) mode = 2;  // only the pair set knows which pairs are new
   // binning pays for itself on large device batches (8-byte aligned pairs)
   const bool use_bins = mode == 3 && pairs_on_device && n >= (4ull << 20) && n < (1ull << 31) &&
@@ -656,6 +753,28 @@ sspd_status sspd_scan(sspd_grid* g, const uint32_t* pairs, uint64_t n, int pairs
   auto launch = [&](const uint32_t* dp, uint64_t cnt) {
     const unsigned blocks = grid_blocks(g, (cnt + 3) / 4, 256, SSPD_SCAN_BLOCKS_PER_SM);
     Prof p(g, "scan", cnt);
+    if (g->width != 32) {
+      auto* tb = g->pairset.as<unsigned long long>();
+      const NarrowCodes nc{g->code_now(), g->code_lo};
+#define SSPD_NARROW(T, H1, DD)                                                                       \
+  scan_narrow_kernel<T, H1, DD><<<blocks, 256, 0, g->stream>>>(dp, cnt, g->d_tabs, g->geo, tb, g->pairset_mask, \
+                                                               static_cast<T*>(g->codes), g->now, nc,            \
+                                                               g->hist, g->K)
+      if (g->width == 8) {
+        if (pow2 && dedup) SSPD_NARROW(uint8_t, 0, 1);
+        else if (pow2) SSPD_NARROW(uint8_t, 0, 0);
+        else if (dedup) SSPD_NARROW(uint8_t, 1, 1);
+        else SSPD_NARROW(uint8_t, 1, 0);
+      } else {
+        if (pow2 && dedup) SSPD_NARROW(uint16_t, 0, 1);
+        else if (pow2) SSPD_NARROW(uint16_t, 0, 0);
+        else if (dedup) SSPD_NARROW(uint16_t, 1, 1);
+        else SSPD_NARROW(uint16_t, 1, 0);
+      }
+#undef SSPD_NARROW
+      if (dedup) g->pairset_dirty = true;
+      return;
+    }
     const int F = g->scan_filter;
 #define SSPD_DIRECT(H1, FI, HI, BI)                                                                 \
   scan_direct_kernel<H1, FI, HI, BI><<<blocks, 256, 0, g->stream>>>(dp, cnt, g->d_tabs, g->geo, g->stamps, \
@@ -781,6 +900,7 @@ sspd_status sspd_scan(sspd_grid* g, const uint32_t* pairs, uint64_t n, int pairs
 }
 
 sspd_status sspd_commit(sspd_grid* g) {
+  if (sspd_status w = wide_only(g, "commit")) return w;
   std::lock_guard<std::mutex> lk(g->mu);
   DeviceGuard dg(g->device);
   g->pending = true;  // the caller may have OR-merged remote touches in
@@ -804,11 +924,28 @@ sspd_status sspd_advance(sspd_grid* g, uint32_t slots) {
       CU(cudaMemsetAsync(g->hist + (uint64_t)(g->now % g->K) * g->geo.ncells, 0, (size_t)g->geo.ncells * 4,
                          g->stream));
     }
+    if (g->width != 32 && g->code_now() > g->code_hi) {
+      // epoch end: drop codes older than the window, move the rest down so
+      // that code(now) = lo + K - 1 (ages unchanged)
+      const uint32_t cn = g->code_now(), shift = cn - (g->code_lo + g->K - 1);
+      const unsigned blocks = grid_blocks(g, g->geo.n_rec / 16 + 1, 256, 8);
+      Prof p(g, "rebase", g->geo.n_rec);
+      if (g->width == 8)
+        narrow_rebase_kernel<uint8_t><<<blocks, 256, 0, g->stream>>>(static_cast<uint8_t*>(g->codes),
+                                                                     g->geo.n_rec, cn, g->code_lo, g->K, shift);
+      else
+        narrow_rebase_kernel<uint16_t><<<blocks, 256, 0, g->stream>>>(static_cast<uint16_t*>(g->codes),
+                                                                      g->geo.n_rec, cn, g->code_lo, g->K, shift);
+      g->epoch0 = g->now - (g->K - 1);
+      s = check_launch();
+      if (s) return s;
+    }
   }
   return SSPD_OK;
 }
 
 sspd_status sspd_get_distances(sspd_grid* g, uint16_t* host_out, uint64_t offset, uint64_t count) {
+  if (sspd_status w = wide_only(g, "cells")) return w;
   if (offset > g->geo.n_rec || count > g->geo.n_rec - offset)
     return fail(SSPD_OUT_OF_RANGE, "cells: range out of bounds");
   std::lock_guard<std::mutex> lk(g->mu);
@@ -834,6 +971,7 @@ sspd_status sspd_get_distances(sspd_grid* g, uint16_t* host_out, uint64_t offset
 }
 
 sspd_status sspd_put_distances(sspd_grid* g, const uint16_t* host_in, uint64_t offset, uint64_t count) {
+  if (sspd_status w = wide_only(g, "cells")) return w;
   if (offset > g->geo.n_rec || count > g->geo.n_rec - offset)
     return fail(SSPD_OUT_OF_RANGE, "cells: range out of bounds");
   std::lock_guard<std::mutex> lk(g->mu);
@@ -1050,6 +1188,9 @@ sspd_status sspd_merge(const sspd_grid* const* grids_c, uint64_t n, int policy, 
   if (n == 0) return fail(SSPD_INVALID_ARGUMENT, "merge_rseas: empty set");
   auto** grids = const_cast<sspd_grid**>(grids_c);
   for (uint64_t i = 0; i < n; ++i)
+    if (sspd_status w = wide_only(grids[i], "merge_rseas")) return w;
+  if (sspd_status w = wide_only(out, "merge_rseas")) return w;
+  for (uint64_t i = 0; i < n; ++i)
     if (!compatible(grids[i], grids[0]))
       return fail(SSPD_INVALID_ARGUMENT, "merge_rseas: incompatible snapshots (seed/q/r/delta/eta differ)");
   if (!compatible(out, grids[0]))
@@ -1109,6 +1250,8 @@ sspd_status sspd_merge(const sspd_grid* const* grids_c, uint64_t n, int policy, 
 
 sspd_status sspd_equal(sspd_grid* a, sspd_grid* b, int* equal) {
   *equal = 0;
+  if (sspd_status w = wide_only(a, "operator==")) return w;
+  if (sspd_status w = wide_only(b, "operator==")) return w;
   if (a->geo.n_rec != b->geo.n_rec) return SSPD_OK;
   for (sspd_grid* g : {a, b}) {
     std::lock_guard<std::mutex> lk(g->mu);
@@ -1142,6 +1285,8 @@ sspd_status sspd_equal(sspd_grid* a, sspd_grid* b, int* equal) {
 
 sspd_status sspd_track_window(sspd_grid* g, uint32_t k_max) {
   if (k_max > 65534) return fail(SSPD_OUT_OF_RANGE, "track_window: k must be in [0, 65534]");
+  if (g->width != 32 && k_max == g->K) return SSPD_OK;  // fixed at creation
+  if (sspd_status w = wide_only(g, "track_window")) return w;
   std::lock_guard<std::mutex> lk(g->mu);
   DeviceGuard dg(g->device);
   sspd_status s = commit_locked(g);
@@ -1165,6 +1310,7 @@ sspd_status sspd_track_window(sspd_grid* g, uint32_t k_max) {
 }
 
 sspd_status sspd_grid_stamps(sspd_grid* g, uint32_t** dev_stamps, uint64_t* words) {
+  if (sspd_status w = wide_only(g, "grid_stamps")) return w;
   std::lock_guard<std::mutex> lk(g->mu);
   DeviceGuard dg(g->device);
   sspd_status s = commit_locked(g);
@@ -1181,6 +1327,8 @@ sspd_status sspd_grid_stamps(sspd_grid* g, uint32_t** dev_stamps, uint64_t* word
 }
 
 sspd_status sspd_set_exchange(sspd_grid* g, int mode) {
+  if (mode != 0)
+    if (sspd_status w = wide_only(g, "set_exchange")) return w;
   std::lock_guard<std::mutex> lk(g->mu);
   g->record_touched = mode == 1;
   g->export_pairs = mode == 2;
@@ -1188,6 +1336,8 @@ sspd_status sspd_set_exchange(sspd_grid* g, int mode) {
 }
 
 sspd_status sspd_set_push(sspd_grid* g, void* dev_peer_ptrs, uint32_t world, uint32_t rank, uint64_t region_cap) {
+  if (world > 1)
+    if (sspd_status w = wide_only(g, "set_push")) return w;
   std::lock_guard<std::mutex> lk(g->mu);
   if (world > 1 && (!dev_peer_ptrs || rank >= world || region_cap == 0))
     return fail(SSPD_INVALID_ARGUMENT, "set_push: bad peer table");
@@ -1220,6 +1370,7 @@ sspd_status sspd_scan_mode(sspd_grid* g, int mode, int filter) {
 }
 
 sspd_status sspd_grid_touched(sspd_grid* g, uint32_t** dev_bits, uint64_t* words) {
+  if (sspd_status w = wide_only(g, "grid_touched")) return w;
   std::lock_guard<std::mutex> lk(g->mu);
   DeviceGuard dg(g->device);
   CU(cudaStreamSynchronize(g->stream));

@@ -57,12 +57,18 @@ class Grid:
     """An RSEA grid resident on one B200 (Rsea, rsea.hpp:52-114)."""
 
     def __init__(self, q: int = 14, r: int = 5, delta: int = 6, seed: int = 0,
-                 eta: int = 2048, device: int = 0, _handle=None):
+                 eta: int = 2048, device: int = 0, _handle=None, width: int = 32, k_max: int = 0):
+        """width 8/16 (with the window k_max): a narrow-stamp grid, exact for
+        R_k with k <= k_max and the reports (sspd_grid_create_narrow)."""
         self._L = load()
         self.q, self.r, self.delta, self.seed, self.eta = q, r, delta, seed, eta
         if _handle is None:
             h = C.c_void_p()
-            check(self._L.sspd_grid_create(device, q, r, delta, seed, eta, C.byref(h)))
+            if width == 32 and not k_max:
+                check(self._L.sspd_grid_create(device, q, r, delta, seed, eta, C.byref(h)))
+            else:
+                check(self._L.sspd_grid_create_narrow(device, q, r, delta, seed, eta, width, k_max,
+                                                      C.byref(h)))
             _handle = h
         self._h = _handle
         self.candidate_cap = 1 << 24
@@ -88,6 +94,13 @@ class Grid:
         n = C.c_uint64()
         check(self._L.sspd_grid_info(self._h, C.byref(n), None, None))
         return n.value
+
+    @property
+    def stamp_width(self) -> tuple[int, int]:
+        """(bits per stamp, tracked window k_max)."""
+        w, k = C.c_uint32(), C.c_uint32()
+        check(self._L.sspd_grid_stamp_width(self._h, C.byref(w), C.byref(k)))
+        return w.value, k.value
 
     @property
     def now(self) -> int:
