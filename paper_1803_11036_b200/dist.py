@@ -2,17 +2,23 @@
 the plumbing (reference run_detection's merge branch,
 pipeline.cpp:76-85, and merge_rseas, snapshot.cpp:117-142).
 
-Union-min (the reference default, SPEC.md:437) is idempotent and commutes with
+Union-min (the reference default) is idempotent and commutes with
 advance_slot, so every router can keep the *merged* grid: in lockstep the
 merged grid changes per slot exactly by "stamp = now on every recorder any
-router touched".  The exchange is therefore the slot's touched bitmap (1 bit
-per recorder, 1/32 of the stamp grid), OR-reduced across routers, then folded
-into each router's stamps by the same commit kernel a single router uses.  The
-result equals merge_rseas(node grids, kUnionMin) of the reference bit for bit
-(tests/test_dist_gloo.py on CPU, tests/test_gpu_parity.py on the device).
+router touched".  So routers exchange only what they touched in the slot and
+fold the peers' touches into their own grid with the same kernels a single
+router uses.  Three exchange formats give the same grid:
 
-paper-max keeps per-node grids and needs the full stamps: element-wise MIN
-into a scratch copy (out of place, or it would corrupt later slots).
+  PUSH    the slot's distinct (cip, oip) pairs, stored into the peers'
+          symmetric-memory inboxes by the scan kernel itself (P2P over NVLink),
+          so the exchange overlaps the scan;
+  PAIRS   the same lists, all-gathered after the scan;
+  BITMAP  the slot's touched bitmap (1 bit per recorder), OR-all-reduced.
+
+merge_stamps_max is the literal all-reduce(max) of the full stamp grid, kept as
+the baseline.  Every variant equals merge_rseas(node grids, kUnionMin) of the
+reference bit for bit (tests/test_dist_gloo.py on CPU, tests/test_gpu_parity.py
+on the device).
 """
 from __future__ import annotations
 
@@ -194,175 +200,6 @@ def merge_pairs(grid, group=None):
     try:
         for part in remote:
             grid.scan_device(part.data_ptr(), int(part.shape[0]))
-    finally:
-        grid.set_exchange(PAIRS)
-
-
-def or_allreduce_(t: torch.Tensor, group=None) -> torch.Tensor:
-    """In-place bitwise-OR all-reduce of an int32 tensor (NCCL has no OR op).
-
-    Reduce-scatter by all_to_all + a local OR of the received chunks, then
-    all-gather: the 2(N-1)/N per-rank volume of a ring all-reduce.  The same
-    code runs on NCCL (GPU) and gloo (the CPU tests).
-    """
-    world = dist.get_world_size(group)
-    if world == 1:
-        return t
-    flat = t.view(-1)
-    n = flat.numel()
-    per = (n + world - 1) // world
-    padded = flat
-    if per * world != n:
-        padded = torch.zeros(per * world, dtype=flat.dtype, device=flat.device)
-        padded[:n].copy_(flat)
-    recv = torch.empty_like(padded)
-    dist.all_to_all_single(recv, padded, group=group)
-    chunks = recv.view(world, per)
-    mine = chunks[0].clone()
-    for i in range(1, world):
-        mine.bitwise_or_(chunks[i])
-    out = torch.empty_like(padded)
-    dist.all_gather_into_tensor(out, mine, group=group)
-    flat.copy_(out[:n])
-    return t
-
-
-class _CudaArray:
-    """__cuda_array_interface__ view of raw device memory owned by the grid."""
-
-    def __init__(self, ptr: int, n: int, typestr: str = "<i4"):
-        self.__cuda_array_interface__ = {"shape": (n,), "typestr": typestr,
-                                         "data": (ptr, False), "version": 3, "strides": None}
-
-
-def device_view(ptr: int, n_words: int, device: int) -> torch.Tensor:
-    with torch.cuda.device(device):
-        return torch.as_tensor(_CudaArray(ptr, n_words), device=f"cuda:{device}")
-
-
-BITMAP = 1
-PAIRS = 2
-PUSH = 3
-
-
-def prepare(grid, exchange: int = PAIRS, region_cap: int = 0, group=None):
-    """Choose what routers exchange each slot: the slot's distinct (cip, oip)
-    pairs (PAIRS, default: ~10% of a Zipf slot's packets, 8 B each), the
-    same pairs pushed over NVLink during the scan (PUSH, needs region_cap =
-    the most pairs a router scans per slot) or the touched bitmap (BITMAP:
-    1 bit per recorder, fixed size)."""
-    if exchange == PUSH:
-        PushExchange(grid, region_cap, group)
-        return
-    grid.set_exchange(exchange)
-    grid._exchange = exchange
-
-
-def merge(grid, group=None):
-    ex = getattr(grid, "_exchange", BITMAP)
-    if ex == PUSH:
-        grid._push.merge(grid)
-    elif ex == PAIRS:
-        merge_pairs(grid, group)
-    else:
-        merge_touched(grid, group)
-
-
-class PushExchange:
-    """Fused scan + exchange over NVLink (exchange PUSH).
-
-    Every router owns two inboxes in torch symmetric memory (one per slot
-    parity), each `world` regions of `region_cap` pairs.  While scanning, the
-    dedup kernel stores each pair new to this router into region `rank` of
-    every peer's current inbox (P2P stores, include/sspd_cuda.h
-    sspd_set_push), so the exchange overlaps the scan.  After the scan an
-    all-gather of the per-router counts is the barrier; each router then scans
-    the other regions of its own inbox.  Parity double-buffering is safe: a
-    router pushes slot s+2 into an inbox only after the all-gather of slot s+1,
-    which the receiver joins only after it finished applying slot s.  A
-    router whose slot overflows region_cap makes every router fall back to
-    the all-gathered lists for that slot (the counts say so consistently).
-    """
-
-    def __init__(self, grid, region_cap: int, group=None):
-        import torch.distributed._symmetric_memory as symm_mem
-
-        self.world = dist.get_world_size(group)
-        self.rank = dist.get_rank(group)
-        self.cap = int(region_cap)
-        self.group = group
-        dev = torch.device(f"cuda:{grid.device}")
-        name = group.group_name if group is not None else dist.group.WORLD.group_name
-        self.inbox, self.handles = [], []
-        for _ in range(2):
-            buf = symm_mem.empty(self.world * self.cap * 2, dtype=torch.int32, device=dev)
-            self.inbox.append(buf)
-            self.handles.append(symm_mem.rendezvous(buf, name))
-        self.parity = 0
-        grid.set_exchange(PAIRS)
-        grid._exchange = PUSH
-        grid._push = self
-        self._arm(grid)
-
-    def _arm(self, grid):
-        grid.set_push(self.handles[self.parity].buffer_ptrs_dev, self.world, self.rank, self.cap)
-
-    def merge(self, grid):
-        ptr, n = grid.new_pairs_ptr()
-        dev = torch.device(f"cuda:{grid.device}")
-        counts = torch.tensor([n], dtype=torch.int64, device=dev)
-        allc = torch.empty(self.world, dtype=torch.int64, device=dev)
-        dist.all_gather_into_tensor(allc, counts, group=self.group)   # also the barrier
-        sizes = [int(c) for c in allc.tolist()]
-        torch.cuda.synchronize(grid.device)
-        box = self.inbox[self.parity].view(self.world, self.cap, 2)
-        grid.set_exchange(0)
-        try:
-            if max(sizes) > self.cap:
-                # someone overflowed its region: everyone uses the lists
-                local = (device_view(ptr, 2 * n, grid.device).view(n, 2) if n
-                         else torch.zeros((0, 2), dtype=torch.int32, device=dev))
-                for part in exchange_pairs(local, self.group):
-                    grid.scan_device(part.data_ptr(), int(part.shape[0]))
-            else:
-                for src in range(self.world):
-                    if src != self.rank and sizes[src]:
-                        grid.scan_device(box[src].data_ptr(), sizes[src])
-        finally:
-            grid.set_exchange(PAIRS)
-        self.parity ^= 1
-        self._arm(grid)
-
-
-def merge_pairs(grid, group=None):
-    """Union-min merge by pair lists: all-gather every router's distinct
-    pairs of the slot and scan the other routers' lists locally.  The union
-    of the touches equals the union-min merge of the node grids; the grid's
-    pair set skips pairs this router already saw."""
-    world = dist.get_world_size(group)
-    if world == 1:
-        return
-    rank = dist.get_rank(group)
-    ptr, n = grid.new_pairs_ptr()
-    dev = torch.device(f"cuda:{grid.device}")
-    counts = torch.tensor([n], dtype=torch.int64, device=dev)
-    all_counts = torch.empty(world, dtype=torch.int64, device=dev)
-    dist.all_gather_into_tensor(all_counts, counts, group=group)
-    all_counts = all_counts.tolist()
-    width = max(all_counts)
-    if width == 0:
-        return
-    mine = torch.zeros(width * 2, dtype=torch.int32, device=dev)
-    if n:
-        mine[: 2 * n].copy_(device_view(ptr, 2 * n, grid.device))
-    everyone = torch.empty(world * width * 2, dtype=torch.int32, device=dev)
-    dist.all_gather_into_tensor(everyone, mine, group=group)
-    torch.cuda.synchronize(grid.device)
-    grid.set_exchange(0)  # remote pairs are not re-exported
-    try:
-        for r in range(world):
-            if r != rank and all_counts[r]:
-                grid.scan_device(everyone[r * width * 2:].data_ptr(), int(all_counts[r]))
     finally:
         grid.set_exchange(PAIRS)
 
