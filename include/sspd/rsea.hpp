@@ -52,9 +52,20 @@ class CandidateOverflow : public std::runtime_error {
   std::size_t count;
 };
 
+// B200 extension: bits per recorder stamp.  32 keeps the full distances;
+// 8 and 16 keep in-window counts exact for k <= window only (and hence hot
+// sets, finalize and reconstruction), at 1/4 and 1/2 of the memory.  Narrow
+// grids throw std::invalid_argument from cells()/estimator(), copies,
+// merge_rseas and operator== (include/sspd_cuda.h sspd_grid_create_narrow).
+struct StampWidth {
+  uint32_t bits = 32;
+  uint32_t window = 0;  // k_max; required for bits < 32
+};
+
 class Rsea {
  public:
   Rsea(const RhfgConfig& cfg, uint32_t eta);
+  Rsea(const RhfgConfig& cfg, uint32_t eta, StampWidth width);  // B200 extension
   Rsea(const Rsea& other);
   Rsea(Rsea&& other) noexcept;
   Rsea& operator=(const Rsea& other);
@@ -93,6 +104,7 @@ class Rsea {
   void track_window(uint32_t k);
   // The underlying C-ABI handle (include/sspd_cuda.h).
   sspd_grid* handle() const;
+  StampWidth stamp_width() const;
 
  private:
   struct Uninitialised {};

@@ -62,6 +62,23 @@ Rsea::Rsea(const RhfgConfig& cfg, uint32_t eta) : Rsea(Uninitialised{}, cfg, eta
   check(sspd_grid_create(current_device(), cfg.q, cfg.r, cfg.delta, cfg.seed, eta, &h_));
 }
 
+Rsea::Rsea(const RhfgConfig& cfg, uint32_t eta, StampWidth width) : Rsea(Uninitialised{}, cfg, eta) {
+  const auto problems = validate_config(cfg, eta, 1, 1.0);
+  if (!problems.empty()) throw std::invalid_argument("Rsea: " + problems.front());
+  n_ = std::size_t{cfg.r} * cfg.columns() * eta;
+  if (width.bits == 32 && width.window == 0)
+    check(sspd_grid_create(current_device(), cfg.q, cfg.r, cfg.delta, cfg.seed, eta, &h_));
+  else
+    check(sspd_grid_create_narrow(current_device(), cfg.q, cfg.r, cfg.delta, cfg.seed, eta, width.bits,
+                                  width.window, &h_));
+}
+
+StampWidth Rsea::stamp_width() const {
+  StampWidth w;
+  check(sspd_grid_stamp_width(h_, &w.bits, &w.window));
+  return w;
+}
+
 Rsea::Rsea(const Rsea& other) : Rsea(Uninitialised{}, other.cfg_, other.eta_) {
   other.sync();
   n_ = other.n_;

@@ -319,6 +319,37 @@ TEST_CASE("pipeline: strategies and worker counts agree") {
   }
 }
 
+TEST_CASE("narrow stamps (B200 extension): same reports, distances refused") {
+  RunConfig rc = test_config();
+  const auto w = workload(3, 256, 12, rc, 79);
+  const auto wide = run_detection({w.trace}, rc);
+  for (uint32_t bits : {8u, 16u}) {
+    rc.stamp_bits = bits;
+    const auto narrow = run_detection(split(w.trace, 3, 82), rc);
+    REQUIRE(narrow.size() == wide.size());
+    for (std::size_t s = 0; s < wide.size(); ++s) {
+      REQUIRE(narrow[s].hosts.size() == wide[s].hosts.size());
+      for (std::size_t h = 0; h < wide[s].hosts.size(); ++h) {
+        CHECK(narrow[s].hosts[h].cip == wide[s].hosts[h].cip);
+        CHECK(narrow[s].hosts[h].estimate == wide[s].hosts[h].estimate);
+      }
+    }
+    rc.policy = MergePolicy::kPaperMax;  // needs full stamps for merge_rseas
+    CHECK_THROWS_AS(run_detection(split(w.trace, 2, 83), rc), std::invalid_argument);
+    rc.policy = MergePolicy::kUnionMin;
+  }
+  Rsea g(kCfg, kEta, StampWidth{8, kK});
+  CHECK(g.stamp_width().bits == 8);
+  CHECK(g.stamp_width().window == kK);
+  std::mt19937_64 rng(5);
+  plant(g, 0x0A0B0C0D, 300, rng);
+  CHECK(cips_of(g.reconstruct_leveled(kK, kTheta, 1)).count(0x0A0B0C0D) == 1);
+  CHECK_THROWS_AS(g.cells(), std::invalid_argument);
+  CHECK_THROWS_AS(Rsea{g}, std::invalid_argument);
+  CHECK_THROWS_AS((Rsea(kCfg, kEta, StampWidth{8, 0})), std::invalid_argument);
+  CHECK_THROWS_AS((Rsea(kCfg, kEta, StampWidth{12, 5})), std::invalid_argument);
+}
+
 TEST_CASE("pipeline: 4-way union-min sharding equals the single-node run") {
   const RunConfig rc = test_config();
   const auto w = workload(3, 256, 6, rc, 80);

@@ -84,6 +84,13 @@ def test_detect_and_snapshots(gpu, work):
         "recursive", "-o", work / "rr.csv")
     assert (work / "r8.csv").read_bytes() == (work / "r.csv").read_bytes()
     assert (work / "rr.csv").read_bytes() == (work / "r.csv").read_bytes()
+    for bits in (8, 16):  # narrow-stamp grids (B200 extension): byte-identical reports
+        run("detect", work / "trace.bin", "--desk", "--k", 5, "--seed", "5eed", "--stamp-width", bits,
+            "-o", work / f"rw{bits}.csv")
+        assert (work / f"rw{bits}.csv").read_bytes() == (work / "r.csv").read_bytes()
+    p = run("detect", work / "trace.bin", "--desk", "--k", 5, "--stamp-width", 12, "-o", os.devnull,
+            check=False)
+    assert p.returncode == 2 and "stamp width" in p.stderr
 
     run("snapshot", "export", work / "trace.bin", "--desk", "--k", 5, "--seed", "5eed",
         "-o", work / "s1")
