@@ -165,6 +165,7 @@ struct sspd_grid {
   void* pinned_small = nullptr;  // 4 KB pinned scratch for counters
   bool profiling = false;
   std::vector<ProfRec> prof;
+  std::vector<cudaEvent_t> event_pool;  // recycled profiling events (creation is the costly part)
   uint64_t h2d_bytes = 0, d2h_bytes = 0;  // host<->device traffic, for e2e accounting
   // narrow stamps (width 8 or 16, kernels.cuh "NARROW STAMPS"): `codes`
   // replaces `stamps`, the window ring (K = k_max) is always on, and codes
@@ -209,6 +210,17 @@ unsigned grid_blocks(const sspd_grid* g, uint64_t work_items, unsigned threads, 
   return (unsigned)std::max<uint64_t>(1, std::min(need, cap));
 }
 
+cudaEvent_t take_event(sspd_grid* g) {
+  cudaEvent_t e = nullptr;
+  if (!g->event_pool.empty()) {
+    e = g->event_pool.back();
+    g->event_pool.pop_back();
+  } else {
+    cudaEventCreate(&e);
+  }
+  return e;
+}
+
 struct Prof {
   sspd_grid* g;
   ProfRec rec{};
@@ -217,8 +229,8 @@ struct Prof {
     if (!g->profiling) return;
     rec.name = name;
     rec.units = units;
-    cudaEventCreate(&rec.a);
-    cudaEventCreate(&rec.b);
+    rec.a = take_event(g);
+    rec.b = take_event(g);
     cudaEventRecord(rec.a, g->stream);
   }
   ~Prof() {
@@ -606,6 +618,7 @@ sspd_status sspd_grid_destroy(sspd_grid* g) {
       cudaEventDestroy(r.a);
       cudaEventDestroy(r.b);
     }
+    for (cudaEvent_t e : g->event_pool) cudaEventDestroy(e);
     for (int i = 0; i < 2; ++i) {
       if (g->ev_copy[i]) cudaEventDestroy(g->ev_copy[i]);
       if (g->ev_used[i]) cudaEventDestroy(g->ev_used[i]);
@@ -1389,7 +1402,15 @@ sspd_status sspd_grid_io_bytes(sspd_grid* g, uint64_t* h2d, uint64_t* d2h, int r
 
 sspd_status sspd_profile_enable(sspd_grid* g, int on) {
   std::lock_guard<std::mutex> lk(g->mu);
+  DeviceGuard dg(g->device);
   g->profiling = on != 0;
+  // events for a few hundred launches up front, so profiling adds only
+  // cudaEventRecord calls to the timed work
+  while (g->profiling && g->event_pool.size() < 512) {
+    cudaEvent_t e;
+    CU(cudaEventCreate(&e));
+    g->event_pool.push_back(e);
+  }
   return SSPD_OK;
 }
 
@@ -1398,8 +1419,8 @@ sspd_status sspd_profile_reset(sspd_grid* g) {
   DeviceGuard dg(g->device);
   cudaStreamSynchronize(g->stream);
   for (auto& r : g->prof) {
-    cudaEventDestroy(r.a);
-    cudaEventDestroy(r.b);
+    g->event_pool.push_back(r.a);
+    g->event_pool.push_back(r.b);
   }
   g->prof.clear();
   return SSPD_OK;
