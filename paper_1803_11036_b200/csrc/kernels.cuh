@@ -1185,7 +1185,7 @@ __device__ __forceinline__ void narrow_ring(uint32_t old, uint32_t cell, const N
 // pair set (DEDUP) of scan_dedup_kernel; 2 pairs per thread, every touch's
 // atomic issued before any old code is consumed.  The window ring is always
 // kept.
-template <class T, int H1MODE, int DEDUP>
+template <class T, int H1MODE, int DEDUP, int PRELOAD = 0>
 __global__ void __launch_bounds__(256) scan_narrow_kernel(const uint32_t* __restrict__ pairs, uint64_t n,
                                                           const HashTabs* __restrict__ tabs, Geo geo,
                                                           unsigned long long* __restrict__ table, uint64_t table_mask,
@@ -1237,8 +1237,23 @@ __global__ void __launch_bounds__(256) scan_narrow_kernel(const uint32_t* __rest
         for (uint32_t row = 0; row < 8; ++row) {
           if (row >= geo.r) break;
           T* p = codes + (uint64_t)(row << geo.q | row_col(geo, row, c[u], col0[u])) * geo.eta + bucket[u];
-          if constexpr (sizeof(T) == 2) old[u][row] = narrow_max(p, nc.now);
+          if constexpr (sizeof(T) == 2 && !PRELOAD) old[u][row] = narrow_max(p, nc.now);
+          else if constexpr (sizeof(T) == 2) old[u][row] = __ldcg(reinterpret_cast<const unsigned short*>(p));
           else old[u][row] = word_of(p);
+        }
+      }
+      if constexpr (sizeof(T) == 2 && PRELOAD) {
+        // the load pulled the line into L2: the atomic now hits there
+#pragma unroll
+        for (int u = 0; u < P; ++u) {
+          if (!fresh[u]) continue;
+#pragma unroll
+          for (uint32_t row = 0; row < 8; ++row) {
+            if (row >= geo.r) break;
+            if (old[u][row] >= nc.now) continue;
+            T* p = codes + (uint64_t)(row << geo.q | row_col(geo, row, c[u], col0[u])) * geo.eta + bucket[u];
+            old[u][row] = narrow_max(p, nc.now);
+          }
         }
       }
       if constexpr (sizeof(T) == 1) {

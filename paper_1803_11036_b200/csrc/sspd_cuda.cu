@@ -174,6 +174,10 @@ struct sspd_grid {
   void* codes = nullptr;
   uint32_t code_lo = 0, code_hi = 0;
   uint32_t epoch0 = 0;  // code(now) = code_lo + (now - epoch0)
+  // 16-bit scan: load the recorders before the atomics, so the atomics hit
+  // L2 (C2 at 40 GiB: 4.19 vs 4.76 ms/slot, profiles/r01_ab_narrow_preload.md);
+  // SSPD_NARROW_PRELOAD=0 turns it off
+  bool narrow_preload = true;
   uint32_t code_now() const { return code_lo + (now - epoch0); }
   std::mutex mu;
 };
@@ -493,6 +497,7 @@ sspd_status create_impl(int device, uint32_t q, uint32_t r, uint32_t delta, uint
   g->by_eta = Div40::make(eta);
   g->width = width;
   if (const char* f = std::getenv("SSPD_SCAN_FILTER")) g->scan_filter = std::atoi(f) != 0;
+  if (const char* f = std::getenv("SSPD_NARROW_PRELOAD")) g->narrow_preload = std::atoi(f) != 0;
   // Device-resident pairs: deferred bitmap, measured faster than direct
   // stamping at both geometries (profiles/r01_ab_scan_modes.txt).
   if (const char* m = std::getenv("SSPD_SCAN_MODE")) {
@@ -769,6 +774,9 @@ sspd_status sspd_scan(sspd_grid* g, const uint32_t* pairs, uint64_t n, int pairs
     if (g->width != 32) {
       auto* tb = g->pairset.as<unsigned long long>();
       const NarrowCodes nc{g->code_now(), g->code_lo};
+#define SSPD_NARROW_PL(T, H1, DD)                                                                    \
+  scan_narrow_kernel<T, H1, DD, 1><<<blocks, 256, 0, g->stream>>>(dp, cnt, g->d_tabs, g->geo, tb, g->pairset_mask, \
+                                                                  static_cast<T*>(g->codes), g->now, nc, g->hist, g->K)
 #define SSPD_NARROW(T, H1, DD)                                                                       \
   scan_narrow_kernel<T, H1, DD><<<blocks, 256, 0, g->stream>>>(dp, cnt, g->d_tabs, g->geo, tb, g->pairset_mask, \
                                                                static_cast<T*>(g->codes), g->now, nc,            \
@@ -778,12 +786,18 @@ sspd_status sspd_scan(sspd_grid* g, const uint32_t* pairs, uint64_t n, int pairs
         else if (pow2) SSPD_NARROW(uint8_t, 0, 0);
         else if (dedup) SSPD_NARROW(uint8_t, 1, 1);
         else SSPD_NARROW(uint8_t, 1, 0);
+      } else if (g->narrow_preload) {
+        if (pow2 && dedup) SSPD_NARROW_PL(uint16_t, 0, 1);
+        else if (pow2) SSPD_NARROW_PL(uint16_t, 0, 0);
+        else if (dedup) SSPD_NARROW_PL(uint16_t, 1, 1);
+        else SSPD_NARROW_PL(uint16_t, 1, 0);
       } else {
         if (pow2 && dedup) SSPD_NARROW(uint16_t, 0, 1);
         else if (pow2) SSPD_NARROW(uint16_t, 0, 0);
         else if (dedup) SSPD_NARROW(uint16_t, 1, 1);
         else SSPD_NARROW(uint16_t, 1, 0);
       }
+#undef SSPD_NARROW_PL
 #undef SSPD_NARROW
       if (dedup) g->pairset_dirty = true;
       return;

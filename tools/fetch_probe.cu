@@ -70,6 +70,16 @@ __global__ void __launch_bounds__(256) access5(size_t n, uint32_t* grid, uint64_
       for (int j = 0; j < 5; ++j) asm volatile("prefetch.global.L2 [%0];" ::"l"(p[j]));
 #pragma unroll
       for (int j = 0; j < 5; ++j) acc += atomicMax(p[j], val);
+    } else if (MODE == 8) {  // packed-bf16 max atomic, returning (the 16-bit narrow scan)
+#pragma unroll
+      for (int j = 0; j < 5; ++j) {
+        unsigned short a, b;
+        asm volatile("atom.global.max.noftz.v2.bf16 {%0, %1}, [%2], {%3, %4};"
+                     : "=h"(a), "=h"(b)
+                     : "l"(p[j]), "h"((unsigned short)(val & 0x7f7f)), "h"((unsigned short)0)
+                     : "memory");
+        acc += a + b;
+      }
     } else {  // loads only (the read half alone)
 #pragma unroll
       for (int j = 0; j < 5; ++j) acc += __ldcg(p[j]);
@@ -104,7 +114,7 @@ int main() {
   const size_t n = 20u << 20;  // packets per launch
   uint32_t* sink;
   CK(cudaMalloc(&sink, 4));
-  for (uint64_t mb : {640ull, 10240ull, 81920ull}) {
+  for (uint64_t mb : {640ull, 10240ull, 40960ull, 81920ull}) {
     const uint64_t words = mb << 18;
     uint32_t* grid;
     if (cudaMalloc(&grid, words * 4) != cudaSuccess) {
@@ -122,7 +132,8 @@ int main() {
       printf(" | ld.cg+red %.2f", n / run<4>(n, grid, words, sink, blocks) / 1e6);
       printf(" | ld.cg+atom %.2f", n / run<5>(n, grid, words, sink, blocks) / 1e6);
       printf(" | pf+atom %.2f", n / run<6>(n, grid, words, sink, blocks) / 1e6);
-      printf(" | ld only %.2f Gpkt/s\n", n / run<7>(n, grid, words, sink, blocks) / 1e6);
+      printf(" | ld only %.2f", n / run<7>(n, grid, words, sink, blocks) / 1e6);
+      printf(" | bf16x2 atom %.2f Gpkt/s\n", n / run<8>(n, grid, words, sink, blocks) / 1e6);
     }
     CK(cudaDeviceSetLimit(cudaLimitMaxL2FetchGranularity, dflt));
     CK(cudaFree(grid));
