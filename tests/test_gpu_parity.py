@@ -429,6 +429,44 @@ def test_reconstruct_unusual_geometries(gpu, geo):
         assert dets_equal(g.reconstruct_leveled(k, theta), ref)
 
 
+EXTREMES = [dict(q=2, r=32, delta=1, eta=2),     # fewest columns, r=32, eta at its minimum
+            dict(q=3, r=64, delta=1, eta=5),     # r at the reconstruct limit (64)
+            dict(q=16, r=4, delta=15, eta=3),    # widest rows, delta = q - 1
+            dict(q=16, r=5, delta=7, eta=1)]     # eta = 1 is invalid: checked below
+
+
+@pytest.mark.parametrize("geo", EXTREMES[:3], ids=["q2_r32_eta2", "q3_r64", "q16_delta15"])
+def test_extreme_geometries(gpu, geo):
+    """validate_config's corners (hashing.cpp:63-87): grids, counts, hot sets
+    and reports against the oracle, every slot."""
+    g, o = make_pair(gpu, geo, 0xE7)
+    rng = O.Mt64(0xE7)
+    theta = max(1.0, geo["eta"] / 2.0)
+    for s in range(5):
+        p = rng.pairs(2000)
+        cip = int(rng.next()) & 0xffffffff
+        p = np.concatenate([p, np.stack([np.full(64, cip, np.uint32), rng.draw(64).astype(np.uint32)], 1)])
+        g.scan_batch(p)
+        o.scan(p)
+        assert np.array_equal(g.cells(), o.cells()), s
+        for k in (1, 3):
+            assert np.array_equal(g.active_counts(k), o.active_counts(k)), (s, k)
+            assert [h.tolist() for h in g.hot_sets(k, theta)] == [h.tolist() for h in o.hot_sets(k, theta)]
+            g.candidate_cap = 1 << 16
+            try:
+                ref = o.reconstruct(k, theta, cap=1 << 16)
+            except O.CandidateOverflow as e:
+                with pytest.raises(gpu.CandidateOverflow) as got:
+                    g.reconstruct_leveled(k, theta)
+                assert (got.value.level, got.value.count) == (e.level, e.count)
+            else:
+                assert dets_equal(g.reconstruct_leveled(k, theta), ref), (s, k)
+        g.advance_slot()
+        o.advance()
+    with pytest.raises(gpu.InvalidArgument, match="eta must be >= 2"):
+        gpu.Grid(**EXTREMES[3])
+
+
 def test_cabi_argument_errors(gpu):
     """Entry points reject bad arguments with the reference's exception
     classes instead of touching memory."""
