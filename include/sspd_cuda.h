@@ -193,7 +193,8 @@ sspd_status sspd_grid_new_pairs(sspd_grid* g, uint32_t** dev_pairs, uint64_t* co
  * device batches by pair-set region, -1 = auto (2 when the touched bitmap
  * would exceed 48 MiB, else 1);
  * filter 0/1 = L1 duplicate probe, -1 = keep.  Results are identical in
- * every mode, and modes may be mixed within a slot. */
+ * every mode, and modes may be mixed within a slot.  Narrow-stamp grids run
+ * mode 0 as 1 and mode 3 as 2. */
 sspd_status sspd_scan_mode(sspd_grid* g, int mode, int filter);
 
 /* ---- synthetic traces (shape of synth_trace,

@@ -265,7 +265,10 @@ class Grid:
         return p.value or 0, n.value
 
     def scan_mode(self, mode: int = -1, filter: int = -1):
-        """mode 0 = deferred bitmap, 1 = direct, -1 = auto; filter 0/1 (-1 keeps)."""
+        """Scan strategy (include/sspd_cuda.h sspd_scan_mode): 0 = deferred bitmap,
+        1 = direct stamping, 2 = direct behind the per-slot pair set, 3 = 2 after
+        binning large device batches, -1 = auto; filter 0/1 = L1 duplicate probe
+        (-1 keeps).  Narrow-stamp grids run 0 as 1 and 3 as 2."""
         check(self._L.sspd_scan_mode(self._h, mode, filter))
 
     def commit(self):
