@@ -630,3 +630,35 @@ def test_three_routers_push_exchange_on_one_device(gpu):
         for g, nd in zip(grids, nodes):
             g.advance_slot()
             nd.advance()
+
+
+@pytest.mark.parametrize("mode", [(1, -1), (2, -1), (-1, -1)], ids=["direct", "dedup", "auto"])
+def test_scan_input_forms(gpu, mode):
+    """Ragged and misaligned device slices (the 16-byte vector path and the
+    scalar tail), pageable temporaries, and pinned host buffers the caller
+    overwrites as soon as scan_batch returns (rsea.hpp:71-75 semantics)."""
+    import torch
+
+    g, o = make_pair(gpu, DESK, 0xA1)
+    g.scan_mode(*mode)
+    rng = O.Mt64(0xA1)
+    dev = torch.from_numpy(rng.pairs(40_000).view(np.int32)).cuda()
+    host = dev.cpu().numpy().view(np.uint32)
+    for off, n in [(1, 1), (3, 2), (5, 3), (1, 7), (2, 1001), (7, 12_345), (0, 0)]:
+        g.scan_batch(dev[off:off + n])
+        o.scan(host[off:off + n])
+    assert np.array_equal(g.cells(), o.cells())
+    p = rng.pairs(30_000)
+    g.scan_batch(p[::-1][::2])           # non-contiguous: a temporary copy, freed on return
+    o.scan(np.ascontiguousarray(p[::-1][::2]))
+    pinned = torch.empty((50_000, 2), dtype=torch.int32).pin_memory()
+    for s in range(3):
+        q = rng.pairs(50_000)
+        pinned.numpy().view(np.uint32)[:] = q
+        g.scan_host_ptr(pinned.data_ptr(), 50_000)
+        pinned.fill_(0)                   # reused at once: the scan must already own the data
+        o.scan(q)
+    assert np.array_equal(g.cells(), o.cells())
+    g.advance_slot()
+    o.advance()
+    assert np.array_equal(g.active_counts(2), o.active_counts(2))
