@@ -11,7 +11,7 @@ from __future__ import annotations
 
 import ctypes as C
 import math
-from dataclasses import dataclass
+from typing import NamedTuple
 
 import numpy as np
 
@@ -21,11 +21,17 @@ from ._cabi import CandidateOverflow, check, load
 BASE_NOW = 65535
 
 
-@dataclass(frozen=True)
-class Detection:
+class Detection(NamedTuple):
+    """Detection (rsea.hpp:25-28) plus the integer in-window count behind the
+    estimate.  A NamedTuple: immutable and cheap to build per report."""
     cip: int
     estimate: float
     r_k: int
+
+
+# sspd_detection (include/sspd_cuda.h) as a numpy record, to read report
+# buffers without one ctypes object per entry
+_DET_DTYPE = np.dtype([("cip", "<u4"), ("r_k", "<u4"), ("estimate", "<f8")])
 
 
 def hot_cutoff(eta: int, theta: float) -> int:
@@ -222,7 +228,8 @@ class Grid:
                 raise CandidateOverflow(self._L.sspd_last_error().decode(), lvl.value, cnt.value)
             check(st)
             if n.value <= out_cap:
-                return [Detection(d.cip, d.estimate, d.r_k) for d in buf[:n.value]]
+                rows = np.frombuffer(buf, dtype=_DET_DTYPE, count=n.value).tolist()
+                return [Detection(c, e, r) for c, r, e in rows]
             self._report_buf = (_cabi.Detection_t * n.value)()
 
     def reconstruct_leveled(self, k: int, theta: float, workers: int = 1) -> list[Detection]:
