@@ -1131,7 +1131,8 @@ __global__ void equal_kernel(const uint32_t* __restrict__ a, uint32_t now_a, con
 //   w = 16: lo = 0x0080, hi = 0x7F7F -- the positive normal bf16 bit
 //           patterns, which order like the integers, so a touch is ONE
 //           returning packed-bf16 max atomic (ATOMG.E.MAX.BF16x2) whose other
-//           lane is +0.0 (a no-op), exactly like the 32-bit atomicMax.
+//           lane is +0.0 (a no-op), like the 32-bit atomicMax; by default an
+//           ld.cg of the code goes first (PRELOAD), so the atomic hits L2.
 //   w = 8:  lo = 1, hi = 255; no 8-bit atomic exists, so a touch is a load
 //           of the 32-bit word and a CAS on it (retried if a neighbour moved).
 // The old code drives the window ring exactly as in the 32-bit scan.
