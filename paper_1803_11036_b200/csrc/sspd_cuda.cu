@@ -139,6 +139,7 @@ struct sspd_grid {
   uint32_t K = 0;        // tracked window (0 = off)
   uint32_t* hist = nullptr;
   bool hist_valid = false;
+  bool pristine = true;  // every stamp still 0 (nothing scanned, imported or merged in)
   HashTabs* d_tabs = nullptr;
   cudaStream_t stream = nullptr;
   bool own_stream = true;
@@ -651,6 +652,7 @@ sspd_status sspd_grid_clone(const sspd_grid* src_c, int device, sspd_grid** out)
     DeviceGuard dg2(dev);
     CU(cudaMemcpyPeerAsync(g->stamps, dev, src->stamps, src->device, src->geo.n_rec * 4, g->stream));
     g->now = src->now;
+    g->pristine = src->pristine;
     if (src->K) {
       g->K = src->K;
       CU(cudaMalloc(&g->hist, (size_t)g->K * g->geo.ncells * 4));
@@ -698,6 +700,7 @@ sspd_status sspd_scan(sspd_grid* g, const uint32_t* pairs, uint64_t n, int pairs
   if (!pairs) return fail(SSPD_INVALID_ARGUMENT, "scan_batch: null pairs");
   std::lock_guard<std::mutex> lk(g->mu);
   DeviceGuard dg(g->device);
+  g->pristine = false;
   const bool pow2 = (g->eta & (g->eta - 1)) == 0 && g->eta <= (1u << 31);
   // auto: pairs streamed from the host are PCIe-bound, so stamp them in place
   // while the copies run (nothing left to fold after the last chunk);
@@ -930,6 +933,7 @@ sspd_status sspd_commit(sspd_grid* g) {
   if (sspd_status w = wide_only(g, "commit")) return w;
   std::lock_guard<std::mutex> lk(g->mu);
   DeviceGuard dg(g->device);
+  g->pristine = false;
   g->pending = true;  // the caller may have OR-merged remote touches in
   return commit_locked(g);
 }
@@ -1023,6 +1027,7 @@ sspd_status sspd_put_distances(sspd_grid* g, const uint16_t* host_in, uint64_t o
     done += cnt;
   }
   g->hist_valid = false;
+  g->pristine = false;
   return check_launch();
 }
 
@@ -1272,6 +1277,7 @@ sspd_status sspd_merge(const sspd_grid* const* grids_c, uint64_t n, int policy, 
   if (s) return s;
   out->now = now_common;
   out->hist_valid = false;
+  out->pristine = false;
   return SSPD_OK;
 }
 
@@ -1331,6 +1337,11 @@ sspd_status sspd_track_window(sspd_grid* g, uint32_t k_max) {
       g->K = 0;
       return fail(SSPD_CUDA_ERROR, "CUDA error: out of memory (window ring)");
     }
+    if (g->pristine) {  // nothing seen yet: the ring is all zero, no pass over the stamps
+      CU(cudaMemsetAsync(g->hist, 0, (size_t)k_max * g->geo.ncells * 4, g->stream));
+      g->hist_valid = true;
+      return SSPD_OK;
+    }
     return hist_rebuild_locked(g);
   }
   return SSPD_OK;
@@ -1350,6 +1361,7 @@ sspd_status sspd_grid_stamps(sspd_grid* g, uint32_t** dev_stamps, uint64_t* word
   // the caller may rewrite stamps (e.g. an in-place NCCL max); the ring is
   // rebuilt from them on next use
   g->hist_valid = false;
+  g->pristine = false;
   return SSPD_OK;
 }
 

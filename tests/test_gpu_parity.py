@@ -662,3 +662,30 @@ def test_scan_input_forms(gpu, mode):
     g.advance_slot()
     o.advance()
     assert np.array_equal(g.active_counts(2), o.active_counts(2))
+
+
+def test_window_ring_on_fresh_imported_and_merged_grids(gpu):
+    """track_window skips the stamp pass only while every stamp is 0: after
+    an import, a merge or a raw stamp view it rebuilds from the stamps."""
+    g, o = make_pair(gpu, DESK, 0xB2)
+    rng = O.Mt64(0xB2)
+    p = rng.pairs(30_000)
+    o.scan(p)
+    o.advance()
+    o.scan(rng.pairs(10_000))
+    fresh = gpu.Grid(seed=0xB2, **DESK)
+    fresh.track_window(4)                      # pristine: ring zeroed, no pass
+    assert int(fresh.active_counts(4).sum()) == 0
+    g.set_cells(o.cells())                     # import, then track
+    g.track_window(4)
+    assert np.array_equal(g.active_counts(3), o.active_counts(3))
+    m = gpu.merge_rseas([g, fresh])            # merge output, then track
+    m.track_window(4)
+    assert np.array_equal(m.active_counts(4), o.active_counts(4))
+    c = gpu.Grid(seed=0xB2, **DESK)
+    c.scan_batch(p)
+    c.stamps_ptr()                             # raw view: the caller may rewrite stamps
+    c.track_window(2)
+    o2 = O.OracleGrid(seed=0xB2, **DESK)
+    o2.scan(p)
+    assert np.array_equal(c.active_counts(2), o2.active_counts(2))
