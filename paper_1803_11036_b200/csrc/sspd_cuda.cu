@@ -897,8 +897,11 @@ sspd_status sspd_scan(sspd_grid* g, const uint32_t* pairs, uint64_t n, int pairs
   }
   // Host pairs: double-buffered chunks; the copy stream fills one staging
   // buffer while the scan consumes the other.
-  const uint64_t chunk = 4ull << 20;  // pairs per chunk (32 MiB): small first-copy latency
-  const uint64_t chunk_pairs = std::min<uint64_t>(chunk, n);
+  // Pairs per chunk: at most 4M (32 MiB: small first-copy latency), and at
+  // least 4 chunks down to 256K pairs, so the copy of a chunk overlaps the
+  // scan of the one before even for a C1-sized (1M-pair) batch.
+  const uint64_t chunk_pairs = std::min<uint64_t>(
+      n, std::min<uint64_t>(4ull << 20, std::max<uint64_t>(256ull << 10, (n + 3) / 4)));
   for (int i = 0; i < 2; ++i)
     if (g->stage[i].ensure(chunk_pairs * 8) != cudaSuccess)
       return fail(SSPD_CUDA_ERROR, "CUDA error: out of memory (scan staging)");
