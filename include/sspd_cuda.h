@@ -93,6 +93,8 @@ sspd_status sspd_grid_info(const sspd_grid* g, uint64_t* recorders, int* device,
                            uint32_t* now);
 /* Queue the grid's work on an external cudaStream_t (NULL = the grid's own). */
 sspd_status sspd_grid_set_stream(sspd_grid* g, void* cuda_stream);
+/* The cudaStream_t the grid's work is queued on (its own or the one set). */
+sspd_status sspd_grid_stream(const sspd_grid* g, void** cuda_stream);
 sspd_status sspd_grid_synchronize(sspd_grid* g);
 
 /* ---- SCAN phase ---- */
@@ -160,6 +162,38 @@ sspd_status sspd_equal(sspd_grid* a, sspd_grid* b, int* equal);
  * slots, so hot_sets / reconstruct at k <= k_max skip the full-grid count
  * pass.  0 disables.  Results are identical either way. */
 sspd_status sspd_track_window(sspd_grid* g, uint32_t k_max);
+
+/* ---- sharded routers (B200 extension; paper_1803_11036_b200/dist.py SHARD) ----
+ * Router `rank` of `world` owns the cells c with c * world / (r * 2^q) == rank
+ * (a contiguous slice) and keeps exact stamps only there.  Its own scans stamp
+ * owned recorders and push each pair new to the router to the owners of the
+ * pair's other cells: P2P stores into dev_inbox_ptrs[owner] (a device array of
+ * `world` peer-mapped inbox bases, each world * region_cap (cip, oip) pairs;
+ * region `rank` of an inbox is this router's).  Per slot, after the scans:
+ *   sspd_shard_sent      device u64[world]: pairs pushed to each owner (the
+ *                        caller all-gathers them; a count past region_cap is
+ *                        an error the caller must raise);
+ *   sspd_shard_receive   scan the pairs peers pushed here (owned cells only);
+ *   sspd_shard_hot       this router's hot bits (device u32 words): OR them
+ *                        across routers in place;
+ *   sspd_shard_select    joins and address checks on the merged hot sets, then
+ *                        per-survivor bucket masks (device u32): AND them
+ *                        across routers in place;
+ *   sspd_shard_finish    R_k = popcount of the merged masks; reports as
+ *                        sspd_reconstruct.
+ * The reports equal sspd_reconstruct on the union-min merge of the routers'
+ * grids.  world = 0 turns sharding off. */
+sspd_status sspd_set_shard(sspd_grid* g, void* dev_inbox_ptrs, uint32_t world, uint32_t rank,
+                           uint64_t region_cap);
+sspd_status sspd_shard_sent(sspd_grid* g, uint64_t** dev_counts);
+sspd_status sspd_shard_receive(sspd_grid* g, const uint32_t* dev_pairs, uint64_t n);
+sspd_status sspd_shard_hot(sspd_grid* g, uint32_t k, uint64_t cutoff, uint32_t** dev_hot_words,
+                           uint64_t* n_words);
+sspd_status sspd_shard_select(sspd_grid* g, uint32_t k, uint64_t cutoff, uint64_t cap, uint64_t* n_surv,
+                              uint32_t** dev_masks, uint64_t* mask_words, uint32_t* ovf_level,
+                              uint64_t* ovf_count);
+sspd_status sspd_shard_finish(sspd_grid* g, uint64_t cutoff, sspd_detection* out, uint64_t out_cap,
+                              uint64_t* n_out);
 
 /* ---- raw device views, for torch.distributed / NCCL plumbing ---- */
 /* Device pointer to the u32 stamp array (recorders words) after folding any

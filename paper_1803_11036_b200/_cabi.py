@@ -47,7 +47,15 @@ SIGNATURES = {
     "sspd_grid_create_narrow": (C.c_int, [C.c_int, C.c_uint32, C.c_uint32, C.c_uint32, C.c_uint64,
                                           C.c_uint32, C.c_uint32, C.c_uint32, C.POINTER(grid_p)]),
     "sspd_grid_stamp_width": (C.c_int, [grid_p, u32p, u32p]),
+    "sspd_set_shard": (C.c_int, [grid_p, C.c_void_p, C.c_uint32, C.c_uint32, C.c_uint64]),
+    "sspd_shard_sent": (C.c_int, [grid_p, C.POINTER(C.c_void_p)]),
+    "sspd_shard_receive": (C.c_int, [grid_p, C.c_void_p, C.c_uint64]),
+    "sspd_shard_hot": (C.c_int, [grid_p, C.c_uint32, C.c_uint64, C.POINTER(C.c_void_p), u64p]),
+    "sspd_shard_select": (C.c_int, [grid_p, C.c_uint32, C.c_uint64, C.c_uint64, u64p, C.POINTER(C.c_void_p), u64p,
+                                    u32p, u64p]),
+    "sspd_shard_finish": (C.c_int, [grid_p, C.c_uint64, C.POINTER(Detection_t), C.c_uint64, u64p]),
     "sspd_grid_set_stream": (C.c_int, [grid_p, C.c_void_p]),
+    "sspd_grid_stream": (C.c_int, [grid_p, C.POINTER(C.c_void_p)]),
     "sspd_grid_synchronize": (C.c_int, [grid_p]),
     "sspd_scan": (C.c_int, [grid_p, C.c_void_p, C.c_uint64, C.c_int]),
     "sspd_advance": (C.c_int, [grid_p, C.c_uint32]),

@@ -668,14 +668,19 @@ __global__ void __launch_bounds__(kHotChunk) hot_mark_kernel(const uint32_t* __r
                                                             uint32_t now, uint32_t k, Geo geo, uint64_t cutoff,
                                                             uint32_t* __restrict__ hot_words,
                                                             uint32_t* __restrict__ chunk_counts,
-                                                            uint32_t* __restrict__ hotT, uint32_t words_per_key) {
+                                                            uint32_t* __restrict__ hotT, uint32_t words_per_key,
+                                                            int from_words = 0) {
   const uint32_t ncol = 1u << geo.q;
   const uint32_t chunks = (ncol + kHotChunk - 1) / kHotChunk;
   const uint32_t row = blockIdx.x / chunks, chunk = blockIdx.x % chunks;
   const uint32_t col = chunk * kHotChunk + threadIdx.x;
   const uint32_t cell = (row << geo.q) | col;
+  const uint32_t wpr0 = (ncol + 31) / 32;
   bool hot = false;
-  if (col < ncol) {
+  if (col < ncol && from_words) {
+    // sharded routers: the hot bits were computed per owner and OR-merged
+    hot = (hot_words[row * wpr0 + (col >> 5)] >> (col & 31)) & 1u;
+  } else if (col < ncol) {
     uint32_t rk;
     if (hist) {
       rk = 0;
@@ -691,7 +696,7 @@ __global__ void __launch_bounds__(kHotChunk) hot_mark_kernel(const uint32_t* __r
   __syncthreads();
   const uint32_t wpr = (ncol + 31) / 32;  // words per row: rows never share a word
   if ((threadIdx.x & 31) == 0) {
-    if (col < ncol) hot_words[row * wpr + (col >> 5)] = b;
+    if (col < ncol && !from_words) hot_words[row * wpr + (col >> 5)] = b;
     if (b) atomicAdd(&s_sum, (uint32_t)__popc(b));
   }
   if (hot) {
@@ -1114,6 +1119,176 @@ __global__ void equal_kernel(const uint32_t* __restrict__ a, uint32_t now_a, con
       *differ = 1;
       return;
     }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// SHARDED ROUTERS (union-min across N routers, each owning a contiguous 1/N
+// slice of the cells; dist.py ShardExchange).  A router stamps only the
+// recorders of cells it owns and pushes each pair new to it to the owners of
+// its other cells (P2P stores into their inboxes), so per-router stamping
+// scales with 1/N of the union of the routers' pairs instead of all of it.
+// Hot sets are OR-merged across owners; a survivor's in-window count is the
+// popcount of the AND, across owners, of per-owner bucket masks.
+struct ShardArgs {
+  uint2* const* inbox;            // device array of `world` inbox bases (peer-mapped)
+  unsigned long long* sent;       // `world` counters: pairs pushed to each owner this slot
+  uint32_t world, rank;
+  uint64_t region_cap;            // pairs per (destination, source) region
+};
+
+__device__ __forceinline__ uint32_t shard_owner(uint32_t cell, uint32_t ncells, uint32_t world) {
+  return (uint32_t)(((uint64_t)cell * world) / ncells);
+}
+
+// PUSH = 1: the router's own pairs (stamp owned cells, push to other owners);
+// PUSH = 0: pairs received from peers (stamp owned cells only).  Pairs the
+// router already saw this slot are skipped by the pair set, as in dedup mode.
+template <int H1MODE, int HIST, int PUSH>
+__global__ void __launch_bounds__(256) scan_shard_kernel(const uint32_t* __restrict__ pairs, uint64_t n,
+                                                         const HashTabs* __restrict__ tabs, Geo geo,
+                                                         unsigned long long* __restrict__ table, uint64_t table_mask,
+                                                         uint32_t* __restrict__ stamps, uint32_t now,
+                                                         uint32_t* __restrict__ hist, uint32_t K, ShardArgs sh) {
+  __shared__ ScanTables t;
+  load_scan_tables(t, tabs);
+  const uint32_t now_slot = HIST ? now % K : 0;
+  const uint32_t lane = threadIdx.x & 31;
+  constexpr int P = 2;
+  const uint64_t tid = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const uint64_t nthreads = (uint64_t)gridDim.x * blockDim.x;
+  const bool vec = (reinterpret_cast<uintptr_t>(pairs) & 15u) == 0;
+  const uint64_t ngroups = (n + P - 1) / P;
+  for (uint64_t g = tid; g < ngroups; g += nthreads) {
+    uint32_t c[P], o[P];
+    bool fresh[P];
+    const uint64_t p0 = g * P;
+    if (vec && p0 + P <= n) {
+      const uint4 a = ld_stream_u4(pairs + 2 * p0);
+      c[0] = a.x; o[0] = a.y; c[1] = a.z; o[1] = a.w;
+      fresh[0] = fresh[1] = true;
+    } else {
+#pragma unroll
+      for (int u = 0; u < P; ++u) {
+        fresh[u] = p0 + u < n;
+        c[u] = fresh[u] ? pairs[2 * (p0 + u)] : 0u;
+        o[u] = fresh[u] ? pairs[2 * (p0 + u) + 1] : 0u;
+      }
+    }
+    {
+      uint64_t key[P], h[P];
+      unsigned long long v[P];
+#pragma unroll
+      for (int u = 0; u < P; ++u) {
+        key[u] = (uint64_t)c[u] << 32 | o[u];
+        h[u] = pair_slot_hash(key[u]);
+        v[u] = fresh[u] ? __ldca(table + pair_slot(h[u], 0, table_mask)) : 0ull;
+      }
+#pragma unroll
+      for (int u = 0; u < P; ++u) fresh[u] = fresh[u] && pair_resolve(table, table_mask, key[u], h[u], v[u]);
+    }
+    uint32_t dmask[P] = {0u, 0u};
+#pragma unroll
+    for (int u = 0; u < P; ++u) {
+      if (!fresh[u]) continue;
+      uint32_t bucket, col0;
+      hash_pair<H1MODE>(t, geo, c[u], o[u], bucket, col0);
+      for (uint32_t r0 = 0; r0 < geo.r; r0 += 8) {
+        uint32_t cell[8], old[8];
+#pragma unroll
+        for (uint32_t j = 0; j < 8; ++j) {  // owned touches: atomics issued together
+          const uint32_t row = r0 + j;
+          old[j] = now;
+          if (row >= geo.r) continue;
+          cell[j] = row << geo.q | row_col(geo, row, c[u], col0);
+          const uint32_t owner = shard_owner(cell[j], geo.ncells, sh.world);
+          if (owner != sh.rank) {
+            dmask[u] |= 1u << owner;
+            continue;
+          }
+          uint32_t* p = stamps + (uint64_t)cell[j] * geo.eta + bucket;
+          if (HIST) old[j] = atomicMax(p, now);
+          else asm volatile("red.relaxed.gpu.global.max.u32 [%0], %1;" ::"l"(p), "r"(now) : "memory");
+        }
+        if (HIST) {
+#pragma unroll
+          for (uint32_t j = 0; j < 8; ++j) {
+            if (old[j] >= now) continue;
+            atomicAdd(hist + (uint64_t)now_slot * geo.ncells + cell[j], 1u);
+            if (old[j] + K > now) atomicSub(hist + (uint64_t)(old[j] % K) * geo.ncells + cell[j], 1u);
+          }
+        }
+      }
+    }
+    if (PUSH) {
+      // one warp-aggregated reservation per destination
+#pragma unroll
+      for (int u = 0; u < P; ++u) {
+        for (uint32_t d = 0; d < sh.world; ++d) {
+          const unsigned m = __activemask();
+          const bool mine = (dmask[u] >> d) & 1u;
+          const unsigned b = __ballot_sync(m, mine);
+          if (!b) continue;
+          const int leader = __ffs(b) - 1;
+          unsigned long long base = 0;
+          if ((int)lane == leader) base = atomicAdd(sh.sent + d, (unsigned long long)__popc(b));
+          base = __shfl_sync(m, base, leader);
+          if (mine) {
+            const uint64_t pos = base + __popc(b & ((1u << lane) - 1u));
+            if (pos < sh.region_cap) sh.inbox[d][(uint64_t)sh.rank * sh.region_cap + pos] = make_uint2(c[u], o[u]);
+          }
+        }
+      }
+    }
+  }
+  if (PUSH) __threadfence_system();  // peer stores visible before the exchange's barrier
+}
+
+// Per survivor and 32-bucket word: the AND over the survivor's owned rows of
+// "in window" (stamp > thr); rows owned elsewhere contribute all ones, so the
+// AND across routers of these masks is the intersected estimator's bitmap.
+// kmode as finalize_count_kernel.  Bits past eta are 0.
+__global__ void __launch_bounds__(256) shard_mask_kernel(const uint32_t* __restrict__ tuples,
+                                                         const uint32_t* __restrict__ stamps, Geo geo, uint32_t thr,
+                                                         int kmode, const ReconMeta* __restrict__ meta,
+                                                         const uint32_t* __restrict__ surv_idx, uint32_t world,
+                                                         uint32_t rank, uint32_t* __restrict__ masks) {
+  const uint32_t W = (geo.eta + 31) / 32;
+  const uint64_t n = meta->surv * W;
+  for (uint64_t item = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; item < n;
+       item += (uint64_t)gridDim.x * blockDim.x) {
+    const uint64_t sidx = item / W;
+    const uint32_t w = (uint32_t)(item % W);
+    const uint32_t nb = min(32u, geo.eta - w * 32);
+    const uint32_t valid = nb == 32 ? 0xffffffffu : ((1u << nb) - 1u);
+    uint32_t m = kmode == 1 ? 0u : valid;
+    if (kmode == 0) {
+      const uint32_t* cols = tuples + (uint64_t)surv_idx[sidx] * geo.r;
+      for (uint32_t row = 0; row < geo.r && m; ++row) {
+        const uint32_t cell = row << geo.q | cols[row];
+        if (shard_owner(cell, geo.ncells, world) != rank) continue;
+        const uint32_t* e = stamps + (uint64_t)cell * geo.eta + w * 32;
+        uint32_t bits = 0;
+        for (uint32_t j = 0; j < nb; ++j) bits |= (uint32_t)(e[j] > thr) << j;
+        m &= bits;
+      }
+    }
+    masks[item] = m;
+  }
+}
+
+// R_k of each survivor = popcount of its merged mask (one warp per survivor).
+__global__ void shard_popcount_kernel(const uint32_t* __restrict__ masks, const ReconMeta* __restrict__ meta,
+                                      uint32_t W, uint32_t* __restrict__ surv_rk) {
+  const uint64_t n = meta->surv;
+  const uint32_t lane = threadIdx.x & 31;
+  for (uint64_t s = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; s < n;
+       s += ((uint64_t)gridDim.x * blockDim.x) >> 5) {
+    uint32_t c = 0;
+    for (uint32_t w = lane; w < W; w += 32) c += __popc(masks[s * W + w]);
+#pragma unroll
+    for (int o = 16; o; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
+    if (lane == 0) surv_rk[s] = c;
   }
 }
 

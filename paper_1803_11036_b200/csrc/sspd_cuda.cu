@@ -155,6 +155,12 @@ struct sspd_grid {
   int scan_mode = -1;           // 0 bitmap, 1 direct, 2 dedup, 3 binned dedup, -1 auto
   DevBuf bin_counts, binned;    // binned dedup: per-(region, CTA) counts, partitioned pairs
   DevBuf pairset;               // dedup mode: per-slot set of seen (cip, oip) pairs
+  bool shard = false;           // sharded routers (sspd_set_shard): own a 1/world slice of the cells
+  ShardArgs shard_args{};
+  DevBuf shard_sent;            // world u64: pairs pushed to each owner this slot
+  DevBuf masks;                 // sharded reconstruction: per-survivor bucket masks
+  DevBuf* last_tuples = nullptr;  // buffer holding the last reconstruction's r-tuples
+  uint64_t surv_cap = 0;          // tuple capacity the survivor arrays were laid out for
   uint64_t pairset_mask = 0;
   bool pairset_dirty = false;   // holds keys from the current slot
   bool record_touched = false;  // direct/dedup: also record the slot's bitmap (multi-router merge)
@@ -335,18 +341,19 @@ uint32_t words_per_key(const sspd_grid* g) {
 
 // Hot compaction into g->hot_cols / hot_rowcnt / hotT (device); row counts
 // copied to host_rowcnt (synchronises).
+// from_words: the hot bits are already in g->hot_words (OR-merged across
+// sharded routers); only the transposed bits, chunk counts and compaction
+// are rebuilt from them.
 sspd_status hot_locked(sspd_grid* g, uint32_t k, uint64_t cutoff, std::vector<uint32_t>* host_rowcnt,
-                       uint32_t* d_rowcnt) {
-  sspd_status s = commit_locked(g);
-  if (s) return s;
+                       uint32_t* d_rowcnt, bool from_words = false) {
+  sspd_status s = SSPD_OK;
   // R_k straight from the window ring inside hot_mark when it covers k;
   // otherwise per-cell counts first (full pass over the stamps).
-  const bool ring = k >= 1 && k <= 0xFFFFu && g->K && k <= g->K;
-  if (ring) {
-    s = hist_rebuild_locked(g);
+  const bool ring = !from_words && k >= 1 && k <= 0xFFFFu && g->K && k <= g->K;
+  if (!from_words) {
+    s = commit_locked(g);
     if (s) return s;
-  } else {
-    s = counts_locked(g, k);
+    s = ring ? hist_rebuild_locked(g) : counts_locked(g, k);
     if (s) return s;
   }
   const uint32_t ncol = 1u << g->q;
@@ -364,7 +371,7 @@ sspd_status hot_locked(sspd_grid* g, uint32_t k, uint64_t cutoff, std::vector<ui
     Prof p(g, "hot_compact", g->geo.ncells);
     hot_mark_kernel<<<g->r * chunks, kHotChunk, 0, g->stream>>>(
         g->counts.as<uint32_t>(), ring ? g->hist : nullptr, g->K, g->now, k, g->geo, cutoff,
-        g->hot_words.as<uint32_t>(), g->hot_chunks.as<uint32_t>(), g->hotT.as<uint32_t>(), wpk);
+        g->hot_words.as<uint32_t>(), g->hot_chunks.as<uint32_t>(), g->hotT.as<uint32_t>(), wpk, from_words ? 1 : 0);
     hot_write_kernel<<<g->r * chunks, kHotChunk, 0, g->stream>>>(
         g->hot_words.as<uint32_t>(), g->geo, g->hot_chunks.as<uint32_t>(), g->hot_cols.as<uint32_t>(), d_rowcnt);
   }
@@ -431,6 +438,37 @@ sspd_status queue_finalize(sspd_grid* g, const uint32_t* tuples, uint64_t in_cap
                                                             s_idx, s_rk);
   }
   return check_launch();
+}
+
+// The per-slot pair set (dedup and shard scans), allocated on first use.
+sspd_status ensure_pairset_locked(sspd_grid* g) {
+  if (g->pairset.p) return SSPD_OK;
+  // 8 B per exact key, a power of two of entries (SSPD_PAIRSET_LOG2,
+  // default 2^25 = 256 MiB: ~10M distinct pairs per C2 slot at load 0.3;
+  // measured 2^22..2^25 = 4.23..3.90 ms/slot, profiles/r01_ab_pairset.txt).
+  // Pinning it in L2 (SSPD_L2_PERSIST=<MiB>) measured slower.
+  uint32_t lg = 25;
+  if (const char* e = std::getenv("SSPD_PAIRSET_LOG2")) lg = std::min(30, std::max(16, std::atoi(e)));
+  const uint64_t entries = 1ull << lg;
+  if (g->pairset.ensure(entries * 8) != cudaSuccess)
+    return fail(SSPD_CUDA_ERROR, "CUDA error: out of memory (pair set)");
+  g->pairset_mask = entries - 1;
+  CU(cudaMemsetAsync(g->pairset.p, 0xff, entries * 8, g->stream));
+  if (const char* e = std::getenv("SSPD_L2_PERSIST"); e && std::atoi(e) > 0) {
+    cudaDeviceProp prop;
+    CU(cudaGetDeviceProperties(&prop, g->device));
+    const size_t want = std::min<size_t>((size_t)std::atoi(e) << 20, prop.persistingL2CacheMaxSize);
+    CU(cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, want));
+    cudaStreamAttrValue attr{};
+    attr.accessPolicyWindow.base_ptr = g->pairset.p;
+    attr.accessPolicyWindow.num_bytes = std::min<size_t>(entries * 8, prop.accessPolicyMaxWindowSize);
+    attr.accessPolicyWindow.hitRatio =
+        std::min(1.0f, (float)want / (float)attr.accessPolicyWindow.num_bytes);
+    attr.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
+    attr.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
+    CU(cudaStreamSetAttribute(g->stream, cudaStreamAttributeAccessPolicyWindow, &attr));
+  }
+  return SSPD_OK;
 }
 
 bool compatible(const sspd_grid* a, const sspd_grid* b) {
@@ -689,6 +727,11 @@ sspd_status sspd_grid_set_stream(sspd_grid* g, void* cuda_stream) {
   return SSPD_OK;
 }
 
+sspd_status sspd_grid_stream(const sspd_grid* g, void** cuda_stream) {
+  *cuda_stream = g->stream;
+  return SSPD_OK;
+}
+
 sspd_status sspd_grid_synchronize(sspd_grid* g) {
   DeviceGuard dg(g->device);
   CU(cudaStreamSynchronize(g->stream));
@@ -715,7 +758,7 @@ sspd_status sspd_scan(sspd_grid* g, const uint32_t* pairs, uint64_t n, int pairs
   // measured slower overall (2.2 + 3.6 ms): the random stamp atomics dominate.
   if (mode < 0) mode = g->n_words * 4 > (48ull << 20) ? 2 : 1;
   if (g->width != 32) mode = mode == 0 ? 1 : (mode == 3 ? 2 : mode);  // narrow: direct or dedup
-  if (g->export_pairs && mode < 2) mode = 2;  // only the pair set knows which pairs are new
+  if ((g->export_pairs || g->shard) && mode < 2) mode = 2;  // only the pair set knows which pairs are new
   // binning pays for itself on large device batches (8-byte aligned pairs)
   const bool use_bins = mode == 3 && pairs_on_device && n >= (4ull << 20) && n < (1ull << 31) &&
                       (reinterpret_cast<uintptr_t>(pairs) & 7u) == 0;
@@ -744,36 +787,27 @@ sspd_status sspd_scan(sspd_grid* g, const uint32_t* pairs, uint64_t n, int pairs
     }
   }
   g->scanned_in_slot += n;
-  if (dedup && !g->pairset.p) {
-    // 8 B per exact key, a power of two of entries (SSPD_PAIRSET_LOG2,
-    // default 2^25 = 256 MiB: ~10M distinct pairs per C2 slot at load 0.3;
-    // measured 2^22..2^25 = 4.23..3.90 ms/slot, profiles/r01_ab_pairset.txt).
-    // Pinning it in L2 (SSPD_L2_PERSIST=<MiB>) measured slower.
-    uint32_t lg = 25;
-    if (const char* e = std::getenv("SSPD_PAIRSET_LOG2")) lg = std::min(30, std::max(16, std::atoi(e)));
-    const uint64_t entries = 1ull << lg;
-    if (g->pairset.ensure(entries * 8) != cudaSuccess)
-      return fail(SSPD_CUDA_ERROR, "CUDA error: out of memory (pair set)");
-    g->pairset_mask = entries - 1;
-    CU(cudaMemsetAsync(g->pairset.p, 0xff, entries * 8, g->stream));
-    if (const char* e = std::getenv("SSPD_L2_PERSIST"); e && std::atoi(e) > 0) {
-      cudaDeviceProp prop;
-      CU(cudaGetDeviceProperties(&prop, g->device));
-      const size_t want = std::min<size_t>((size_t)std::atoi(e) << 20, prop.persistingL2CacheMaxSize);
-      CU(cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, want));
-      cudaStreamAttrValue attr{};
-      attr.accessPolicyWindow.base_ptr = g->pairset.p;
-      attr.accessPolicyWindow.num_bytes = std::min<size_t>(entries * 8, prop.accessPolicyMaxWindowSize);
-      attr.accessPolicyWindow.hitRatio =
-          std::min(1.0f, (float)want / (float)attr.accessPolicyWindow.num_bytes);
-      attr.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
-      attr.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
-      CU(cudaStreamSetAttribute(g->stream, cudaStreamAttributeAccessPolicyWindow, &attr));
-    }
+  if (dedup || g->shard) {
+    sspd_status ps = ensure_pairset_locked(g);
+    if (ps) return ps;
   }
   auto launch = [&](const uint32_t* dp, uint64_t cnt) {
     const unsigned blocks = grid_blocks(g, (cnt + 3) / 4, 256, SSPD_SCAN_BLOCKS_PER_SM);
     Prof p(g, "scan", cnt);
+    if (g->shard) {  // own pairs of a sharded router: stamp owned cells, push to the other owners
+      auto* tb = g->pairset.as<unsigned long long>();
+      const bool hs = g->K && g->hist_valid;
+#define SSPD_SHARD(H1, HI)                                                                                    \
+  scan_shard_kernel<H1, HI, 1><<<blocks, 256, 0, g->stream>>>(dp, cnt, g->d_tabs, g->geo, tb, g->pairset_mask, \
+                                                              g->stamps, g->now, g->hist, g->K, g->shard_args)
+      if (pow2 && hs) SSPD_SHARD(0, 1);
+      else if (pow2) SSPD_SHARD(0, 0);
+      else if (hs) SSPD_SHARD(1, 1);
+      else SSPD_SHARD(1, 0);
+#undef SSPD_SHARD
+      g->pairset_dirty = true;
+      return;
+    }
     if (g->width != 32) {
       auto* tb = g->pairset.as<unsigned long long>();
       const NarrowCodes nc{g->code_now(), g->code_lo};
@@ -949,6 +983,7 @@ sspd_status sspd_advance(sspd_grid* g, uint32_t slots) {
   s = pairset_reset_locked(g);  // the pair set only deduplicates within a slot
   if (s) return s;
   if (g->newpairs_count.p) CU(cudaMemsetAsync(g->newpairs_count.p, 0, 8, g->stream));
+  if (g->shard) CU(cudaMemsetAsync(g->shard_sent.p, 0, 32 * 8, g->stream));
   g->scanned_in_slot = 0;
   for (uint32_t i = 0; i < slots; ++i) {
     if (g->now >= 0x7fffffffu) return fail(SSPD_OUT_OF_RANGE, "advance_slot: slice counter exhausted");
@@ -1107,93 +1142,151 @@ sspd_status sspd_finalize(sspd_grid* g, const uint32_t* tuples, uint64_t n, uint
   return SSPD_OK;
 }
 
-sspd_status sspd_reconstruct(sspd_grid* g, uint32_t k, uint64_t cutoff, uint64_t cap, sspd_detection* out,
-                             uint64_t out_cap, uint64_t* n_out, uint32_t* ovf_level, uint64_t* ovf_count) {
-  std::lock_guard<std::mutex> lk(g->mu);
-  DeviceGuard dg(g->device);
-  *n_out = 0;
-  if (g->r > 64) return fail(SSPD_INVALID_ARGUMENT, "reconstruct: r > 64 unsupported");
+}  // extern "C"
+
+namespace {
+
+enum class RecStep { kSurvivors, kEmptyRow, kRetry };
+
+// One reconstruction attempt up to the survivors of finalize_check: hot
+// compaction (from the stamps, or from OR-merged hot bits when from_words),
+// the joins of levels 2..r-1, finalize_check and -- unless sharded --
+// finalize_count, all queued; then one synchronisation reads the row and
+// level counts (plus a prefix of the survivors).  Overflow is decided level
+// by level, as the reference does (rsea.cpp:206-216); a level whose count
+// exceeds the buffer but not the cap asks for a re-run with larger buffers.
+sspd_status recon_attempt(sspd_grid* g, uint32_t k, uint64_t cutoff, uint64_t cap, bool from_words, bool count_rk,
+                          uint64_t* C_out, RecStep* step, uint32_t* ovf_level, uint64_t* ovf_count) {
   const uint32_t ncol = 1u << g->q;
   const uint32_t wpk = words_per_key(g);
   const uint64_t t_stride = (uint64_t)wpk << (g->q - g->delta);
   ReconMeta* meta = g->meta.as<ReconMeta>();
   ReconMeta* mh = g->meta_host;
   if (g->cap_alloc == 0) g->cap_alloc = std::min<uint64_t>(cap, 1u << 20);
-  // Everything below is queued without host round trips; one synchronisation
-  // at the end reads the row counts, per-level counts and survivors.
-  for (int attempt = 0;; ++attempt) {
-    const uint64_t C = std::max<uint64_t>(g->cap_alloc, 1);
-    if (g->tupA.ensure(C * g->r * 4) != cudaSuccess || g->tupB.ensure(C * g->r * 4) != cudaSuccess)
-      return fail(SSPD_CUDA_ERROR, "CUDA error: out of memory (candidate buffer)");
-    sspd_status s = ensure_surv(g, C);
-    if (s) return s;
-    CU(cudaMemsetAsync(meta, 0, sizeof(ReconMeta), g->stream));
-    s = hot_locked(g, k, cutoff, nullptr, meta->rowcnt);
-    if (s) return s;
-    const uint32_t* cols = g->hot_cols.as<uint32_t>();
-    const uint32_t* T = g->hotT.as<uint32_t>();
-    // level sizes live on the device; a modest persistent grid keeps the
-    // (usually tiny) joins cheap to launch and still strides large levels
-    const unsigned blocks = (unsigned)sm_count(g->device) * 2;
+  const uint64_t C = std::max<uint64_t>(g->cap_alloc, 1);
+  *C_out = C;
+  if (g->tupA.ensure(C * g->r * 4) != cudaSuccess || g->tupB.ensure(C * g->r * 4) != cudaSuccess)
+    return fail(SSPD_CUDA_ERROR, "CUDA error: out of memory (candidate buffer)");
+  sspd_status s = ensure_surv(g, C);
+  if (s) return s;
+  CU(cudaMemsetAsync(meta, 0, sizeof(ReconMeta), g->stream));
+  s = hot_locked(g, k, cutoff, nullptr, meta->rowcnt, from_words);
+  if (s) return s;
+  const uint32_t* cols = g->hot_cols.as<uint32_t>();
+  const uint32_t* T = g->hotT.as<uint32_t>();
+  // level sizes live on the device; a modest persistent grid keeps the
+  // (usually tiny) joins cheap to launch and still strides large levels
+  const unsigned blocks = (unsigned)sm_count(g->device) * 2;
+  {
+    Prof p(g, "level2", 0);
+    level2_kernel<<<blocks, 256, 0, g->stream>>>(cols, ncol, T + 2 * t_stride, wpk, g->geo, g->tupA.as<uint32_t>(), C,
+                                                 meta);
+  }
+  s = check_launch();
+  if (s) return s;
+  DevBuf* rd = &g->tupA;
+  DevBuf* wr = &g->tupB;
+  for (uint32_t row = 3; row < g->r; ++row) {
     {
-      Prof p(g, "level2", 0);
-      level2_kernel<<<blocks, 256, 0, g->stream>>>(cols, ncol, T + 2 * t_stride, wpk, g->geo, g->tupA.as<uint32_t>(),
-                                                   C, meta);
+      Prof p(g, "level_ext", 0);
+      level_ext_kernel<<<blocks, 256, 0, g->stream>>>(rd->as<uint32_t>(), C, row, T + (uint64_t)row * t_stride, wpk,
+                                                      g->geo, wr->as<uint32_t>(), C, meta);
     }
     s = check_launch();
     if (s) return s;
-    DevBuf* rd = &g->tupA;
-    DevBuf* wr = &g->tupB;
-    for (uint32_t row = 3; row < g->r; ++row) {
-      {
-        Prof p(g, "level_ext", 0);
-        level_ext_kernel<<<blocks, 256, 0, g->stream>>>(rd->as<uint32_t>(), C, row, T + (uint64_t)row * t_stride,
-                                                        wpk, g->geo, wr->as<uint32_t>(), C, meta);
-      }
-      s = check_launch();
-      if (s) return s;
-      std::swap(rd, wr);
-    }
+    std::swap(rd, wr);
+  }
+  g->last_tuples = rd;
+  uint32_t* s_idx = g->surv.as<uint32_t>();
+  if (count_rk) {
     s = queue_finalize(g, rd->as<uint32_t>(), C, k);
-    if (s) return s;
-    // Survivors are few (true super points plus hash-consistent impostors):
-    // copy a fixed prefix in the same batch.
-    const uint64_t pre = std::min<uint64_t>(C, 4096);
-    uint32_t* s_idx = g->surv.as<uint32_t>();
-    uint32_t* hbuf = static_cast<uint32_t*>(g->pinned_small);  // 4 KB: 2 x 512 entries
-    const uint64_t pre_small = std::min<uint64_t>(pre, 512);
-    CU(cudaMemcpyAsync(mh, meta, sizeof(ReconMeta), cudaMemcpyDeviceToHost, g->stream));
+  } else {
+    Prof p(g, "finalize_check", C);
+    finalize_check_kernel<<<grid_blocks(g, C, 256, 2), 256, 0, g->stream>>>(rd->as<uint32_t>(), C, g->d_tabs, g->geo,
+                                                                             meta, s_idx, s_idx + C);
+    s = check_launch();
+  }
+  if (s) return s;
+  // Survivors are few (true super points plus hash-consistent impostors):
+  // copy a fixed prefix in the same batch.
+  uint32_t* hbuf = static_cast<uint32_t*>(g->pinned_small);  // 4 KB: 2 x 512 entries
+  const uint64_t pre_small = std::min<uint64_t>(C, 512);
+  CU(cudaMemcpyAsync(mh, meta, sizeof(ReconMeta), cudaMemcpyDeviceToHost, g->stream));
+  if (count_rk) {
     CU(cudaMemcpyAsync(hbuf, s_idx + C, pre_small * 4, cudaMemcpyDeviceToHost, g->stream));
     CU(cudaMemcpyAsync(hbuf + 512, s_idx + 2 * C, pre_small * 4, cudaMemcpyDeviceToHost, g->stream));
-    CU(cudaStreamSynchronize(g->stream));
-    g->d2h_bytes += sizeof(ReconMeta) + pre_small * 8;
-    for (uint32_t row = 0; row < g->r; ++row)
-      if (mh->rowcnt[row] == 0) return SSPD_OK;  // rsea.cpp:173-174
-    // Overflow is decided level by level, as the reference does (rsea.cpp:206-216);
-    // a level whose count exceeds our buffer but not the cap forces a re-run.
-    uint64_t need = 0;
-    bool truncated = false;
-    for (uint32_t lvl = 2; lvl < g->r && !truncated; ++lvl) {
-      const uint64_t cnt = mh->level[lvl];
-      if (cnt > cap) {
-        *ovf_level = lvl;
-        *ovf_count = cnt;
-        return fail(SSPD_CANDIDATE_OVERFLOW, "candidate buffer cap exceeded at level " + std::to_string(lvl) +
-                                                 ": " + std::to_string(cnt) + " tuples, cap " + std::to_string(cap));
-      }
-      if (cnt > C) {
-        need = cnt;
-        truncated = true;
-      }
+    g->d2h_bytes += pre_small * 8;
+  }
+  CU(cudaStreamSynchronize(g->stream));
+  g->d2h_bytes += sizeof(ReconMeta);
+  *step = RecStep::kSurvivors;
+  for (uint32_t row = 0; row < g->r; ++row)
+    if (mh->rowcnt[row] == 0) {  // rsea.cpp:173-174
+      *step = RecStep::kEmptyRow;
+      return SSPD_OK;
     }
-    if (truncated) {
-      g->cap_alloc = need;
+  for (uint32_t lvl = 2; lvl < g->r; ++lvl) {
+    const uint64_t cnt = mh->level[lvl];
+    if (cnt > cap) {
+      *ovf_level = lvl;
+      *ovf_count = cnt;
+      return fail(SSPD_CANDIDATE_OVERFLOW, "candidate buffer cap exceeded at level " + std::to_string(lvl) + ": " +
+                                               std::to_string(cnt) + " tuples, cap " + std::to_string(cap));
+    }
+    if (cnt > C) {
+      g->cap_alloc = cnt;
+      *step = RecStep::kRetry;
+      return SSPD_OK;
+    }
+  }
+  return SSPD_OK;
+}
+
+// dedup_report (rsea.cpp:112-122) of the survivors' (cip, R_k): by cip,
+// larger estimate kept, sorted by cip; estimates in host double.
+void report(const sspd_grid* g, const std::vector<uint32_t>& cip, const std::vector<uint32_t>& rk, uint64_t cutoff,
+            sspd_detection* out, uint64_t out_cap, uint64_t* n_out) {
+  std::map<uint32_t, uint32_t> best;
+  for (size_t i = 0; i < cip.size(); ++i) {
+    if (rk[i] < cutoff) continue;
+    auto it = best.emplace(cip[i], rk[i]);
+    if (!it.second && rk[i] > it.first->second) it.first->second = rk[i];
+  }
+  *n_out = best.size();
+  uint64_t w = 0;
+  for (const auto& [c, r_k] : best) {
+    if (w < out_cap) out[w] = sspd_detection{c, r_k, estimate(g->eta, r_k)};
+    ++w;
+  }
+}
+
+}  // namespace
+
+extern "C" {
+
+sspd_status sspd_reconstruct(sspd_grid* g, uint32_t k, uint64_t cutoff, uint64_t cap, sspd_detection* out,
+                             uint64_t out_cap, uint64_t* n_out, uint32_t* ovf_level, uint64_t* ovf_count) {
+  std::lock_guard<std::mutex> lk(g->mu);
+  DeviceGuard dg(g->device);
+  *n_out = 0;
+  if (g->r > 64) return fail(SSPD_INVALID_ARGUMENT, "reconstruct: r > 64 unsupported");
+  if (g->shard && g->shard_args.world > 1)
+    return fail(SSPD_INVALID_ARGUMENT, "reconstruct: a sharded grid reconstructs through the shard calls");
+  for (int attempt = 0;; ++attempt) {
+    uint64_t C = 0;
+    RecStep step;
+    sspd_status s = recon_attempt(g, k, cutoff, cap, false, true, &C, &step, ovf_level, ovf_count);
+    if (s) return s;
+    if (step == RecStep::kEmptyRow) return SSPD_OK;
+    if (step == RecStep::kRetry) {
       if (attempt > 8) return fail(SSPD_CUDA_ERROR, "reconstruct: candidate buffer did not converge");
       continue;
     }
-    const uint64_t ns = mh->surv;
+    const uint64_t ns = g->meta_host->surv;
+    const uint32_t* hbuf = static_cast<const uint32_t*>(g->pinned_small);
+    uint32_t* s_idx = g->surv.as<uint32_t>();
     std::vector<uint32_t> cip(ns), rk(ns);
-    if (ns <= pre_small) {
+    if (ns <= std::min<uint64_t>(C, 512)) {
       std::memcpy(cip.data(), hbuf, ns * 4);
       std::memcpy(rk.data(), hbuf + 512, ns * 4);
     } else {
@@ -1202,21 +1295,163 @@ sspd_status sspd_reconstruct(sspd_grid* g, uint32_t k, uint64_t cutoff, uint64_t
       CU(cudaStreamSynchronize(g->stream));
       g->d2h_bytes += ns * 8;
     }
-    // dedup_report (rsea.cpp:112-122): by cip, larger estimate kept, sorted by cip.
-    std::map<uint32_t, uint32_t> best;
-    for (uint64_t i = 0; i < ns; ++i) {
-      if (rk[i] < cutoff) continue;
-      auto it = best.emplace(cip[i], rk[i]);
-      if (!it.second && rk[i] > it.first->second) it.first->second = rk[i];
-    }
-    *n_out = best.size();
-    uint64_t w = 0;
-    for (const auto& [c, r_k] : best) {
-      if (w < out_cap) out[w] = sspd_detection{c, r_k, estimate(g->eta, r_k)};
-      ++w;
-    }
+    report(g, cip, rk, cutoff, out, out_cap, n_out);
     return SSPD_OK;
   }
+}
+
+// ---- sharded routers ----
+
+sspd_status sspd_set_shard(sspd_grid* g, void* dev_inbox_ptrs, uint32_t world, uint32_t rank, uint64_t region_cap) {
+  if (sspd_status w = wide_only(g, "set_shard")) return w;
+  std::lock_guard<std::mutex> lk(g->mu);
+  DeviceGuard dg(g->device);
+  if (world == 0) {
+    g->shard = false;
+    return SSPD_OK;
+  }
+  if (world > 32 || rank >= world || (world > 1 && (!dev_inbox_ptrs || region_cap == 0)))
+    return fail(SSPD_INVALID_ARGUMENT, "set_shard: need world <= 32, rank < world, inboxes and region_cap > 0");
+  if (g->export_pairs || g->record_touched)
+    return fail(SSPD_INVALID_ARGUMENT, "set_shard: turn the other exchange hooks off first");
+  sspd_status s = commit_locked(g);
+  if (s) return s;
+  if (g->shard_sent.ensure(32 * 8) != cudaSuccess) return fail(SSPD_CUDA_ERROR, "CUDA error: out of memory");
+  CU(cudaMemsetAsync(g->shard_sent.p, 0, 32 * 8, g->stream));
+  g->shard_args = ShardArgs{static_cast<uint2* const*>(dev_inbox_ptrs), g->shard_sent.as<unsigned long long>(),
+                            world, rank, region_cap};
+  g->shard = true;
+  return SSPD_OK;
+}
+
+sspd_status sspd_shard_sent(sspd_grid* g, uint64_t** dev_counts) {
+  std::lock_guard<std::mutex> lk(g->mu);
+  if (!g->shard) return fail(SSPD_INVALID_ARGUMENT, "shard_sent: not a sharded grid");
+  *dev_counts = reinterpret_cast<uint64_t*>(g->shard_sent.p);
+  return SSPD_OK;
+}
+
+sspd_status sspd_shard_receive(sspd_grid* g, const uint32_t* dev_pairs, uint64_t n) {
+  if (n == 0) return SSPD_OK;
+  std::lock_guard<std::mutex> lk(g->mu);
+  DeviceGuard dg(g->device);
+  if (!g->shard) return fail(SSPD_INVALID_ARGUMENT, "shard_receive: not a sharded grid");
+  sspd_status s = ensure_pairset_locked(g);
+  if (s) return s;
+  g->pristine = false;
+  const bool pow2 = (g->eta & (g->eta - 1)) == 0 && g->eta <= (1u << 31);
+  const bool hist = g->K && g->hist_valid;
+  const unsigned blocks = grid_blocks(g, (n + 3) / 4, 256, SSPD_SCAN_BLOCKS_PER_SM);
+  auto* tb = g->pairset.as<unsigned long long>();
+  Prof p(g, "scan", n);
+#define SSPD_SHARD(H1, HI)                                                                                  \
+  scan_shard_kernel<H1, HI, 0><<<blocks, 256, 0, g->stream>>>(dev_pairs, n, g->d_tabs, g->geo, tb, g->pairset_mask, \
+                                                              g->stamps, g->now, g->hist, g->K, g->shard_args)
+  if (pow2 && hist) SSPD_SHARD(0, 1);
+  else if (pow2) SSPD_SHARD(0, 0);
+  else if (hist) SSPD_SHARD(1, 1);
+  else SSPD_SHARD(1, 0);
+#undef SSPD_SHARD
+  g->pairset_dirty = true;
+  return check_launch();
+}
+
+sspd_status sspd_shard_hot(sspd_grid* g, uint32_t k, uint64_t cutoff, uint32_t** dev_hot_words, uint64_t* n_words) {
+  std::lock_guard<std::mutex> lk(g->mu);
+  DeviceGuard dg(g->device);
+  if (!g->shard) return fail(SSPD_INVALID_ARGUMENT, "shard_hot: not a sharded grid");
+  sspd_status s = hot_locked(g, k, cutoff, nullptr, nullptr, false);
+  if (s) return s;
+  CU(cudaStreamSynchronize(g->stream));
+  *dev_hot_words = g->hot_words.as<uint32_t>();
+  *n_words = (uint64_t)g->r * (((1u << g->q) + 31) / 32);
+  return SSPD_OK;
+}
+
+sspd_status sspd_shard_select(sspd_grid* g, uint32_t k, uint64_t cutoff, uint64_t cap, uint64_t* n_surv,
+                              uint32_t** dev_masks, uint64_t* mask_words, uint32_t* ovf_level, uint64_t* ovf_count) {
+  std::lock_guard<std::mutex> lk(g->mu);
+  DeviceGuard dg(g->device);
+  *n_surv = 0;
+  *mask_words = 0;
+  *dev_masks = nullptr;
+  if (!g->shard) return fail(SSPD_INVALID_ARGUMENT, "shard_select: not a sharded grid");
+  if (g->r > 64) return fail(SSPD_INVALID_ARGUMENT, "reconstruct: r > 64 unsupported");
+  for (int attempt = 0;; ++attempt) {
+    uint64_t C = 0;
+    RecStep step;
+    sspd_status s = recon_attempt(g, k, cutoff, cap, true, false, &C, &step, ovf_level, ovf_count);
+    if (s) return s;
+    if (step == RecStep::kEmptyRow) return SSPD_OK;
+    if (step == RecStep::kRetry) {
+      if (attempt > 8) return fail(SSPD_CUDA_ERROR, "reconstruct: candidate buffer did not converge");
+      continue;
+    }
+    const uint64_t ns = g->meta_host->surv;
+    const uint32_t W = (g->eta + 31) / 32;
+    if (g->masks.ensure(std::max<uint64_t>(ns * W, 1) * 4) != cudaSuccess)
+      return fail(SSPD_CUDA_ERROR, "CUDA error: out of memory (survivor masks)");
+    if (ns) {
+      // The joins append survivors in a timing-dependent order, so each
+      // router's list is put in one canonical order -- by cip, which fixes
+      // the whole tuple (rhfg) -- before the masks are AND-ed index by index.
+      uint32_t* s_idx = g->surv.as<uint32_t>();
+      std::vector<uint32_t> idx(ns), cip(ns), order(ns);
+      CU(cudaMemcpyAsync(idx.data(), s_idx, ns * 4, cudaMemcpyDeviceToHost, g->stream));
+      CU(cudaMemcpyAsync(cip.data(), s_idx + C, ns * 4, cudaMemcpyDeviceToHost, g->stream));
+      CU(cudaStreamSynchronize(g->stream));
+      for (uint64_t i = 0; i < ns; ++i) order[i] = (uint32_t)i;
+      std::sort(order.begin(), order.end(), [&](uint32_t a, uint32_t b) { return cip[a] < cip[b]; });
+      std::vector<uint32_t> idx2(ns), cip2(ns);
+      for (uint64_t i = 0; i < ns; ++i) {
+        idx2[i] = idx[order[i]];
+        cip2[i] = cip[order[i]];
+      }
+      CU(cudaMemcpyAsync(s_idx, idx2.data(), ns * 4, cudaMemcpyHostToDevice, g->stream));
+      CU(cudaMemcpyAsync(s_idx + C, cip2.data(), ns * 4, cudaMemcpyHostToDevice, g->stream));
+      g->d2h_bytes += ns * 8;
+      g->h2d_bytes += ns * 8;
+      Prof p(g, "finalize", ns * W);
+      shard_mask_kernel<<<grid_blocks(g, ns * W, 256, 8), 256, 0, g->stream>>>(
+          g->last_tuples->as<uint32_t>(), g->stamps, g->geo, g->now - (k <= 0xFFFFu ? k : 0u), kmode_of(k),
+          g->meta.as<ReconMeta>(), g->surv.as<uint32_t>(), g->shard_args.world, g->shard_args.rank,
+          g->masks.as<uint32_t>());
+      s = check_launch();
+      if (s) return s;
+    }
+    CU(cudaStreamSynchronize(g->stream));
+    g->surv_cap = C;
+    *n_surv = ns;
+    *dev_masks = g->masks.as<uint32_t>();
+    *mask_words = ns * W;
+    return SSPD_OK;
+  }
+}
+
+sspd_status sspd_shard_finish(sspd_grid* g, uint64_t cutoff, sspd_detection* out, uint64_t out_cap,
+                              uint64_t* n_out) {
+  std::lock_guard<std::mutex> lk(g->mu);
+  DeviceGuard dg(g->device);
+  *n_out = 0;
+  if (!g->shard) return fail(SSPD_INVALID_ARGUMENT, "shard_finish: not a sharded grid");
+  const uint64_t ns = g->meta_host->surv;
+  if (ns == 0) return SSPD_OK;
+  const uint64_t C = g->surv_cap;
+  uint32_t* s_idx = g->surv.as<uint32_t>();
+  {
+    Prof p(g, "finalize", ns);
+    shard_popcount_kernel<<<grid_blocks(g, ns * 32, 256, 4), 256, 0, g->stream>>>(
+        g->masks.as<uint32_t>(), g->meta.as<ReconMeta>(), (g->eta + 31) / 32, s_idx + 2 * C);
+  }
+  sspd_status s = check_launch();
+  if (s) return s;
+  std::vector<uint32_t> cip(ns), rk(ns);
+  CU(cudaMemcpyAsync(cip.data(), s_idx + C, ns * 4, cudaMemcpyDeviceToHost, g->stream));
+  CU(cudaMemcpyAsync(rk.data(), s_idx + 2 * C, ns * 4, cudaMemcpyDeviceToHost, g->stream));
+  CU(cudaStreamSynchronize(g->stream));
+  g->d2h_bytes += ns * 8;
+  report(g, cip, rk, cutoff, out, out_cap, n_out);
+  return SSPD_OK;
 }
 
 sspd_status sspd_merge(const sspd_grid* const* grids_c, uint64_t n, int policy, sspd_grid* out) {

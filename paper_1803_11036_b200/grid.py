@@ -137,8 +137,20 @@ class Grid:
         if workers == 0:
             raise _cabi.InvalidArgument("scan_batch: workers == 0")
         if hasattr(pairs, "data_ptr") and getattr(pairs, "is_cuda", False):
+            # A torch tensor: the scan runs after the work that produced it
+            # on torch's current stream, and torch's later work -- including
+            # the caching allocator handing this memory to a new tensor --
+            # runs after the scan has read it.
+            import torch
+
             n = pairs.numel() // 2
+            cur = torch.cuda.current_stream(pairs.device)
+            s = torch.cuda.ExternalStream(self.stream_handle(), device=pairs.device)
+            if s.cuda_stream != cur.cuda_stream:
+                s.wait_stream(cur)
             check(self._L.sspd_scan(self._h, C.c_void_p(pairs.data_ptr()), n, 1))
+            if s.cuda_stream != cur.cuda_stream:
+                cur.wait_stream(s)
             return
         p = np.ascontiguousarray(pairs, dtype=np.uint32).reshape(-1, 2)
         if p.shape[0] == 0:
@@ -271,6 +283,50 @@ class Grid:
         check(self._L.sspd_grid_new_pairs(self._h, C.byref(p), C.byref(n)))
         return p.value or 0, n.value
 
+    # -- sharded routers (include/sspd_cuda.h "sharded routers"; dist.py SHARD)
+    def set_shard(self, dev_inbox_ptrs: int, world: int, rank: int, region_cap: int):
+        check(self._L.sspd_set_shard(self._h, C.c_void_p(dev_inbox_ptrs), world, rank, region_cap))
+
+    def shard_sent_ptr(self) -> int:
+        """Device u64[world]: pairs this router pushed to each owner this slot."""
+        p = C.c_void_p()
+        check(self._L.sspd_shard_sent(self._h, C.byref(p)))
+        return p.value
+
+    def shard_receive(self, dev_ptr: int, n_pairs: int):
+        check(self._L.sspd_shard_receive(self._h, C.c_void_p(dev_ptr), n_pairs))
+
+    def shard_hot(self, k: int, theta: float) -> tuple[int, int]:
+        """(device pointer, u32 words) of this router's hot bits, to OR-merge."""
+        p, n = C.c_void_p(), C.c_uint64()
+        check(self._L.sspd_shard_hot(self._h, k, hot_cutoff(self.eta, theta), C.byref(p), C.byref(n)))
+        return p.value, n.value
+
+    def shard_select(self, k: int, theta: float, cap: int | None = None) -> tuple[int, int, int]:
+        """(survivors, device pointer, u32 words) of the per-survivor bucket
+        masks, to AND-merge; raises CandidateOverflow like reconstruct."""
+        ns, p, w = C.c_uint64(), C.c_void_p(), C.c_uint64()
+        lvl, cnt = C.c_uint32(), C.c_uint64()
+        cap = self.candidate_cap if cap is None else cap
+        st = self._L.sspd_shard_select(self._h, k, hot_cutoff(self.eta, theta), cap, C.byref(ns), C.byref(p),
+                                       C.byref(w), C.byref(lvl), C.byref(cnt))
+        if st == _cabi.SSPD_CANDIDATE_OVERFLOW:
+            raise CandidateOverflow(self._L.sspd_last_error().decode(), lvl.value, cnt.value)
+        check(st)
+        return ns.value, p.value or 0, w.value
+
+    def shard_finish(self, theta: float) -> list[Detection]:
+        while True:
+            buf = self._report_buf
+            if buf is None:
+                buf = self._report_buf = (_cabi.Detection_t * 4096)()
+            n = C.c_uint64()
+            check(self._L.sspd_shard_finish(self._h, hot_cutoff(self.eta, theta), buf, len(buf), C.byref(n)))
+            if n.value <= len(buf):
+                rows = np.frombuffer(buf, dtype=_DET_DTYPE, count=n.value).tolist()
+                return [Detection(c, e, r) for c, r, e in rows]
+            self._report_buf = (_cabi.Detection_t * n.value)()
+
     def scan_mode(self, mode: int = -1, filter: int = -1):
         """Scan strategy (include/sspd_cuda.h sspd_scan_mode): 0 = deferred bitmap,
         1 = direct stamping, 2 = direct behind the per-slot pair set, 3 = 2 after
@@ -283,6 +339,12 @@ class Grid:
 
     def synchronize(self):
         check(self._L.sspd_grid_synchronize(self._h))
+
+    def stream_handle(self) -> int:
+        """The cudaStream_t (as an int) the grid queues its work on."""
+        p = C.c_void_p()
+        check(self._L.sspd_grid_stream(self._h, C.byref(p)))
+        return p.value or 0
 
     def set_stream(self, stream_ptr: int | None):
         check(self._L.sspd_grid_set_stream(self._h, C.c_void_p(stream_ptr or 0)))

@@ -689,3 +689,89 @@ def test_window_ring_on_fresh_imported_and_merged_grids(gpu):
     o2 = O.OracleGrid(seed=0xB2, **DESK)
     o2.scan(p)
     assert np.array_equal(c.active_counts(2), o2.active_counts(2))
+
+
+def _shard_slot(gpu, grids, inboxes, cap, parts, k, theta):
+    """One slot of the sharded union-min exchange among routers on one
+    device, the collectives done in-process (dist.py ShardExchange does them
+    with NCCL): scans, pushes, received scans, OR of hot bits, AND of masks."""
+    import torch
+
+    from paper_1803_11036_b200 import dist as PD
+
+    world = len(grids)
+    for g, p in zip(grids, parts):
+        g.scan_batch(torch.from_numpy(p.view(np.int32)).cuda())
+    torch.cuda.synchronize()
+    sent = []
+    for g in grids:
+        g.synchronize()
+        sent.append(PD.device_view(g.shard_sent_ptr(), 2 * world, 0).view(torch.int64)[:world].tolist())
+    for dst, g in enumerate(grids):
+        box = inboxes[dst].view(world, cap, 2)
+        for src in range(world):
+            if src != dst and sent[src][dst]:
+                assert sent[src][dst] <= cap
+                g.shard_receive(box[src].data_ptr(), sent[src][dst])
+    hot = []
+    for g in grids:
+        p, n = g.shard_hot(k, theta)
+        hot.append(PD.device_view(p, n, 0))
+    merged = hot[0].clone()
+    for h in hot[1:]:
+        merged |= h
+    for h in hot:
+        h.copy_(merged)
+    torch.cuda.synchronize()
+    sel = [g.shard_select(k, theta) for g in grids]
+    assert len({ns for ns, _, _ in sel}) == 1
+    if sel[0][0]:
+        masks = [PD.device_view(p, w, 0) for _, p, w in sel]
+        anded = masks[0].clone()
+        for m in masks[1:]:
+            anded &= m
+        for m in masks:
+            m.copy_(anded)
+        torch.cuda.synchronize()
+    return [g.shard_finish(theta) for g in grids]
+
+
+@pytest.mark.parametrize("world", [1, 3, 4])
+def test_sharded_routers_on_one_device(gpu, world):
+    """Routers owning 1/world of the cells each: every router reports exactly
+    the oracle's union-min merge, and the cells it owns equal the merged
+    grid's, every slot (include/sspd_cuda.h "sharded routers")."""
+    import torch
+
+    geo = DESK
+    cap = 1 << 16
+    grids = [gpu.Grid(seed=0x5a, **geo) for _ in range(world)]
+    inboxes = [torch.zeros(world * cap * 2, dtype=torch.int32, device="cuda") for _ in range(world)]
+    table = torch.tensor([b.data_ptr() for b in inboxes], dtype=torch.int64, device="cuda")
+    for r, g in enumerate(grids):
+        g.track_window(5)
+        g.set_shard(table.data_ptr(), world, r, cap)
+    o = O.OracleGrid(seed=0x5a, **geo)
+    rng = O.Mt64(0x5a)
+    ncells = geo["r"] << geo["q"]
+    for s in range(5):
+        parts = []
+        for r in range(world):
+            p = rng.pairs(3000)
+            for h in range(2 if r == 0 else 1):
+                cip = 0x0A000000 + h  # super points split across routers
+                p = np.concatenate([p, np.stack([np.full(90, cip, np.uint32), rng.draw(90).astype(np.uint32)], 1)])
+            parts.append(p)
+            o.scan(p)
+        reps = _shard_slot(gpu, grids, inboxes, cap, parts, 5, 128.0)
+        ref = o.reconstruct(5, 128.0)
+        for rep in reps:
+            assert dets_equal(rep, ref), s
+        cells = o.cells()
+        for r, g in enumerate(grids):
+            lo = -(-r * ncells // world) * geo["eta"]
+            hi = -(-(r + 1) * ncells // world) * geo["eta"]
+            assert np.array_equal(g.cells()[lo:hi], cells[lo:hi]), (s, r)
+        for g in grids:
+            g.advance_slot()
+        o.advance()
