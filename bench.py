@@ -244,11 +244,12 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--window", type=int, default=0, help="override the window k (C4 sweeps)")
-    ap.add_argument("--merge", default="auto", choices=["auto", "pairs", "push", "bitmap", "stamps"],
-                    help="router exchange at N>1: distinct pairs pushed over NVLink during the scan "
-                         "(push; auto = push, else pairs if symmetric memory is unavailable), the "
-                         "same lists all-gathered after the scan (pairs), OR of touched bitmaps, or "
-                         "the literal all-reduce(max) of the full stamp grid")
+    ap.add_argument("--merge", default="auto", choices=["auto", "pairs", "push", "bitmap", "stamps", "shard"],
+                    help="router exchange at N>1 (auto = shard, else pairs if symmetric memory is "
+                         "unavailable): distinct pairs pushed over NVLink during the scan (push), the "
+                         "same lists all-gathered after the scan (pairs), OR of touched bitmaps, "
+                         "the literal all-reduce(max) of the full stamp grid, or cells sharded among "
+                         "routers with pairs pushed to their owners (shard)")
     ap.add_argument("--stamp-width", type=int, default=32, choices=[8, 16, 32],
                     help="bits per recorder stamp (C4): 8/16 keep R_k (k <= window) and the reports "
                          "exact, 32 also the full distances")
@@ -317,17 +318,17 @@ def main():
     if world > 1 and args.merge != "stamps":
         cap = min(cfg["pairs_per_slot"], 32 << 20)
         if args.merge == "auto":
-            try:
-                PD.prepare(g, PD.PUSH, region_cap=cap)
-                merge_used = "push"
+            try:  # cells sharded among the routers; pair lists if symmetric memory is missing
+                PD.prepare(g, PD.SHARD, region_cap=cfg["pairs_per_slot"])
+                merge_used = "shard"
             except Exception as e:  # symmetric memory unavailable: lists after the scan
-                print(f"[bench] push exchange unavailable ({type(e).__name__}: {e}); using pairs",
+                print(f"[bench] shard exchange unavailable ({type(e).__name__}: {e}); using pairs",
                       file=sys.stderr)
                 PD.prepare(g, PD.PAIRS)
                 merge_used = "pairs"
         else:
-            PD.prepare(g, {"pairs": PD.PAIRS, "push": PD.PUSH, "bitmap": PD.BITMAP}[args.merge],
-                       region_cap=cap)
+            PD.prepare(g, {"pairs": PD.PAIRS, "push": PD.PUSH, "bitmap": PD.BITMAP, "shard": PD.SHARD}[args.merge],
+                       region_cap=cfg["pairs_per_slot"] if args.merge == "shard" else cap)
     cdf = torch.from_numpy(zipf_cdf(L, cfg).view(np.int64)).to(f"cuda:{dev}")
     sp = synth_params(cfg, rank, world)
     n_local = cfg["pairs_per_slot"]
@@ -377,7 +378,7 @@ def main():
             else:
                 PD.merge(g)
         e1.record(stream)
-        rep = g.reconstruct_leveled(k, theta)
+        rep = PD.reconstruct(g, k, theta) if world > 1 else g.reconstruct_leveled(k, theta)
         e2.record(stream)
         g.advance_slot()
         return rep, (e1, e2)
@@ -552,6 +553,8 @@ def main():
                              "push": "union-min: distinct pairs pushed to peers over NVLink during the scan",
                              "bitmap": "union-min: OR all-reduce of the slot's touched bitmaps",
                              "stamps": "union-min: NCCL all-reduce(max) of the full stamp grid",
+                             "shard": "union-min over cells sharded among routers: new pairs pushed to "
+                                      "their cells' owners, hot bits OR- and survivor masks AND-reduced",
                              "auto": "none (single router)"}[merge_used],
                    "parallelism": f"{world} routers, one per GPU",
                    "l2": l2_note},

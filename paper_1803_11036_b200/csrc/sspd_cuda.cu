@@ -1352,7 +1352,6 @@ sspd_status sspd_shard_receive(sspd_grid* g, const uint32_t* dev_pairs, uint64_t
   else if (hist) SSPD_SHARD(1, 1);
   else SSPD_SHARD(1, 0);
 #undef SSPD_SHARD
-  g->pairset_dirty = true;
   return check_launch();
 }
 

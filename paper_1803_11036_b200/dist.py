@@ -14,6 +14,11 @@ router uses.  Three exchange formats give the same grid:
           so the exchange overlaps the scan;
   PAIRS   the same lists, all-gathered after the scan;
   BITMAP  the slot's touched bitmap (1 bit per recorder), OR-all-reduced.
+  SHARD   each router owns 1/N of the cells and stamps only those: the scan
+          pushes each new pair to the owners of its other cells (P2P over
+          NVLink), hot bits are OR-merged and each survivor's in-window
+          bucket masks AND-merged at reconstruction (ShardExchange); per-router
+          stamping then scales with 1/N of the routers' union of pairs.
 
 merge_stamps_max is the literal all-reduce(max) of the full stamp grid, kept as
 the baseline.  Every variant equals merge_rseas(node grids, kUnionMin) of the
@@ -71,6 +76,7 @@ def device_view(ptr: int, n_words: int, device: int) -> torch.Tensor:
 BITMAP = 1
 PAIRS = 2
 PUSH = 3
+SHARD = 4
 
 
 def prepare(grid, exchange: int = PAIRS, region_cap: int = 0, group=None):
@@ -82,13 +88,18 @@ def prepare(grid, exchange: int = PAIRS, region_cap: int = 0, group=None):
     if exchange == PUSH:
         PushExchange(grid, region_cap, group)
         return
+    if exchange == SHARD:
+        ShardExchange(grid, region_cap, group)
+        return
     grid.set_exchange(exchange)
     grid._exchange = exchange
 
 
 def merge(grid, group=None):
     ex = getattr(grid, "_exchange", BITMAP)
-    if ex == PUSH:
+    if ex == SHARD:
+        grid._shard.merge(grid)
+    elif ex == PUSH:
         grid._push.merge(grid)
     elif ex == PAIRS:
         merge_pairs(grid, group)
@@ -160,6 +171,93 @@ class PushExchange:
             grid.set_exchange(PAIRS)
         self.parity ^= 1
         self._arm(grid)
+
+
+def and_allreduce_(t: torch.Tensor, group=None) -> torch.Tensor:
+    """In-place bitwise-AND all-reduce of an int32 tensor: NOT(OR(NOT x))."""
+    t.bitwise_not_()
+    or_allreduce_(t, group)
+    return t.bitwise_not_()
+
+
+def reconstruct(grid, k: int, theta: float, group=None):
+    """reconstruct_leveled on the merged grid, for every exchange: sharded
+    routers merge their hot bits and survivor masks (ShardExchange); the
+    others hold the merged grid already."""
+    if getattr(grid, "_exchange", None) == SHARD:
+        return grid._shard.reconstruct(grid, k, theta)
+    return grid.reconstruct_leveled(k, theta)
+
+
+class ShardExchange:
+    """Sharded union-min (exchange SHARD; include/sspd_cuda.h "sharded
+    routers").
+
+    Router `rank` owns the cells c with c * world // (r * 2^q) == rank and
+    stamps only those.  Its scan stores each pair new to it into region
+    `rank` of the inbox of every other owner of the pair's cells (P2P stores
+    into symmetric memory, double-buffered by slot parity as in PushExchange).
+    merge(): an all-gather of the per-owner push counts is the barrier; each
+    router then scans what was pushed to it (owned cells only).
+    reconstruct(): OR-all-reduce of the routers' hot bits (r * 2^q bits), the
+    same joins on every router, AND-all-reduce of the per-survivor bucket
+    masks (n_surv * eta bits), popcount -- the reports equal reconstruct on the
+    union-min merged grid.  region_cap must cover the pairs a router scans per
+    slot (a router pushes each new pair at most once per owner); a count past
+    it raises instead of dropping touches.
+    """
+
+    def __init__(self, grid, region_cap: int, group=None):
+        import torch.distributed._symmetric_memory as symm_mem
+
+        self.world = dist.get_world_size(group)
+        self.rank = dist.get_rank(group)
+        self.cap = int(region_cap)
+        self.group = group
+        dev = torch.device(f"cuda:{grid.device}")
+        name = group.group_name if group is not None else dist.group.WORLD.group_name
+        self.inbox, self.handles = [], []
+        for _ in range(2):
+            buf = symm_mem.empty(self.world * self.cap * 2, dtype=torch.int32, device=dev)
+            self.inbox.append(buf)
+            self.handles.append(symm_mem.rendezvous(buf, name))
+        self.parity = 0
+        grid._exchange = SHARD
+        grid._shard = self
+        self._arm(grid)
+
+    def _arm(self, grid):
+        grid.set_shard(self.handles[self.parity].buffer_ptrs_dev, self.world, self.rank, self.cap)
+
+    def merge(self, grid):
+        grid.synchronize()  # this router's pushes are complete (the kernel fences them)
+        dev = torch.device(f"cuda:{grid.device}")
+        mine = device_view(grid.shard_sent_ptr(), 2 * self.world, grid.device).view(torch.int64)
+        mine = mine[: self.world].clone()
+        allsent = torch.empty(self.world * self.world, dtype=torch.int64, device=dev)
+        dist.all_gather_into_tensor(allsent, mine, group=self.group)  # also the barrier
+        sent = allsent.view(self.world, self.world).tolist()
+        torch.cuda.synchronize(grid.device)
+        over = max(max(row) for row in sent)
+        if over > self.cap:
+            raise RuntimeError(f"shard exchange: {over} pairs for one owner exceed region_cap {self.cap}")
+        box = self.inbox[self.parity].view(self.world, self.cap, 2)
+        for src in range(self.world):
+            if src != self.rank and sent[src][self.rank]:
+                grid.shard_receive(box[src].data_ptr(), sent[src][self.rank])
+        grid.synchronize()
+        self.parity ^= 1
+        self._arm(grid)
+
+    def reconstruct(self, grid, k: int, theta: float):
+        ptr, n = grid.shard_hot(k, theta)
+        or_allreduce_(device_view(ptr, n, grid.device), self.group)
+        torch.cuda.synchronize(grid.device)
+        ns, mptr, words = grid.shard_select(k, theta)
+        if ns:
+            and_allreduce_(device_view(mptr, words, grid.device), self.group)
+            torch.cuda.synchronize(grid.device)
+        return grid.shard_finish(theta)
 
 
 def exchange_pairs(local: torch.Tensor, group=None) -> list[torch.Tensor]:

@@ -91,22 +91,24 @@ def _or_worker(rank, world, port, out):
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=world)
-    from paper_1803_11036_b200.dist import or_allreduce_
+    from paper_1803_11036_b200.dist import and_allreduce_, or_allreduce_
 
     g = torch.Generator().manual_seed(rank)
+    ok = True
     for n in (1, 7, 64, 1001):  # padding paths
-        x = torch.randint(-2**31, 2**31 - 1, (n,), dtype=torch.int32, generator=g)
-        parts = [torch.empty_like(x) for _ in range(world)]
-        dist.all_gather(parts, x)
-        want = parts[0].clone()
-        for q in parts[1:]:
-            want |= q
-        or_allreduce_(x)
-        if not torch.equal(x, want):
-            out[rank] = False
-            break
-    else:
-        out[rank] = True
+        for op, fn in (("or", or_allreduce_), ("and", and_allreduce_)):
+            x = torch.randint(-2**31, 2**31 - 1, (n,), dtype=torch.int32, generator=g)
+            parts = [torch.empty_like(x) for _ in range(world)]
+            dist.all_gather(parts, x)
+            want = parts[0].clone()
+            for q in parts[1:]:
+                if op == "or":
+                    want |= q
+                else:
+                    want &= q
+            fn(x)
+            ok = ok and torch.equal(x, want)
+    out[rank] = ok
     dist.destroy_process_group()
 
 
@@ -154,4 +156,101 @@ def test_pair_list_exchange(world):
     mgr = mp.Manager()
     out = mgr.dict()
     mp.spawn(_pairs_worker, args=(world, free_port(), 4, out), nprocs=world, join=True)
+    assert all(out[r] for r in range(world))
+
+
+def _shard_worker(rank, world, port, slots, out):
+    """The sharded union-min algebra (dist.py ShardExchange) on numpy grids:
+    each router owns cells c with c * world // ncells == rank, stamps its own
+    pairs' owned recorders, sends each pair to the owners of its other cells,
+    stamps what it receives; hot bits are OR-merged and a host's bucket masks
+    AND-merged.  Must equal the single merged grid: hot sets and every
+    planted host's R_k."""
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from paper_1803_11036_b200.dist import and_allreduce_, or_allreduce_
+
+    q, r, delta, eta, seed, k = 10, 5, 8, 256, 0x5a, 3
+    ncells = r << q
+    cutoff = O.hot_cutoff(eta, 128.0)
+    stamps = np.zeros((ncells, eta), np.int64)      # this router's view (exact on owned cells)
+    merged = np.zeros((ncells, eta), np.int64)      # the single merged grid, for reference
+    owner = (np.arange(ncells) * world) // ncells
+    cols_cache = {}
+
+    def touches(cip, oip):
+        if cip not in cols_cache:
+            cols_cache[cip] = [(row << q) | c for row, c in enumerate(O.rhfg_cols(q, r, delta, seed, cip))]
+        return cols_cache[cip], O.h1_raw(seed, oip) % eta
+
+    ok = True
+    now = 65535
+    hosts = [0x0A000000 + h for h in range(3)]
+    for slot in range(slots):
+        rng = np.random.default_rng(1000 * slot + 7)
+        everyone = []
+        for src in range(world):  # every router's traffic, from a shared seed
+            p = rng.integers(0, 2**32, size=(300, 2), dtype=np.uint64).astype(np.uint32)
+            for h in hosts[: src + 1]:
+                p = np.concatenate([p, np.stack([np.full(60, h, np.uint32),
+                                                 rng.integers(0, 2**32, 60, dtype=np.uint64).astype(np.uint32)], 1)])
+            everyone.append(p)
+        for cip, oip in np.concatenate(everyone):
+            cells, b = touches(int(cip), int(oip))
+            merged[cells, b] = now
+        own = everyone[rank]
+        outbox = [[] for _ in range(world)]
+        for cip, oip in own:
+            cells, b = touches(int(cip), int(oip))
+            for c in cells:
+                if owner[c] == rank:
+                    stamps[c, b] = now
+                else:
+                    outbox[owner[c]].append((int(cip), int(oip)))
+        # the exchange: every router receives the pairs pushed to it
+        objs = [None] * world
+        dist.all_gather_object(objs, outbox)
+        for src in range(world):
+            if src == rank:
+                continue
+            for cip, oip in set(objs[src][rank]):
+                cells, b = touches(cip, oip)
+                for c in cells:
+                    if owner[c] == rank:
+                        stamps[c, b] = now
+        mine = owner == rank
+        ok = ok and np.array_equal(stamps[mine], merged[mine])
+        # hot sets: per-owner R_k, OR-merged
+        rk = ((stamps > 0) & (stamps > now - k)).sum(1)
+        hot = torch.from_numpy(np.packbits((rk >= cutoff) & mine, bitorder="little").view(np.uint8).copy())
+        hot32 = torch.zeros((hot.numel() + 3) // 4 * 4, dtype=torch.uint8)
+        hot32[: hot.numel()] = hot
+        hot32 = hot32.view(torch.int32)
+        or_allreduce_(hot32)
+        want = ((merged > 0) & (merged > now - k)).sum(1) >= cutoff
+        got = np.unpackbits(hot32.view(torch.uint8).numpy(), bitorder="little")[:ncells].astype(bool)
+        ok = ok and np.array_equal(got, want)
+        # a host's R_k: AND over its r estimators, each router masking its owned rows
+        for h in hosts:
+            cells, _ = touches(h, 0)
+            m = np.ones(eta, bool)
+            for c in cells:
+                if owner[c] == rank:
+                    m &= (stamps[c] > 0) & (stamps[c] > now - k)
+            words = torch.from_numpy(np.packbits(m, bitorder="little").view(np.int32).copy())
+            and_allreduce_(words)
+            got_rk = int(np.unpackbits(words.view(torch.uint8).numpy(), bitorder="little")[:eta].sum())
+            want_rk = int(np.all([(merged[c] > 0) & (merged[c] > now - k) for c in cells], axis=0).sum())
+            ok = ok and got_rk == want_rk
+        now += 1
+    out[rank] = ok
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_sharded_union_min_algebra(world):
+    mgr = mp.Manager()
+    out = mgr.dict()
+    mp.spawn(_shard_worker, args=(world, free_port(), 4, out), nprocs=world, join=True)
     assert all(out[r] for r in range(world))

@@ -37,7 +37,7 @@ def pg():
     dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("exchange", ["pairs", "push", "bitmap", "stamps"])
+@pytest.mark.parametrize("exchange", ["pairs", "push", "bitmap", "stamps", "shard"])
 def test_exchange_paths_single_rank(gpu, pg, exchange):
     import torch
 
@@ -47,7 +47,7 @@ def test_exchange_paths_single_rank(gpu, pg, exchange):
     g.track_window(5)
     o = O.OracleGrid(seed=0x44, **DESK)
     if exchange != "stamps":
-        PD.prepare(g, {"pairs": PD.PAIRS, "push": PD.PUSH, "bitmap": PD.BITMAP}[exchange],
+        PD.prepare(g, {"pairs": PD.PAIRS, "push": PD.PUSH, "bitmap": PD.BITMAP, "shard": PD.SHARD}[exchange],
                    region_cap=1 << 16)
     rng = O.Mt64(44)
     for s in range(3):
@@ -59,7 +59,7 @@ def test_exchange_paths_single_rank(gpu, pg, exchange):
         else:
             PD.merge(g)
         assert np.array_equal(g.cells(), o.cells()), (exchange, s)
-        assert [(d.cip, d.estimate) for d in g.reconstruct_leveled(5, 128.0)] == \
+        assert [(d.cip, d.estimate) for d in PD.reconstruct(g, 5, 128.0)] == \
             [(d.cip, d.estimate) for d in o.reconstruct(5, 128.0)]
         g.advance_slot()
         o.advance()
