@@ -360,6 +360,17 @@ def main():
         l2_note = (f"inputs larger than L2: {slot_bytes / 1e6:g} MB per slot vs "
                    f"{l2_bytes >> 20} MiB L2, no flush")
 
+    # Slots pipeline: slot i's reconstruction is queued (sspd_reconstruct_async)
+    # and its reports collected after slot i+1's scan is queued, so the GPU
+    # never waits for the host between slots.  Sharded routers reconstruct
+    # through collectives and stay synchronous.
+    pipelined = not (world > 1 and merge_used == "shard")
+    queued = [False]
+
+    def collect():
+        queued[0] = False
+        return g.reconstruct_collect()
+
     def step(i, from_host=False):
         s = i % S
         e0 = torch.cuda.Event(enable_timing=True)
@@ -378,7 +389,14 @@ def main():
             else:
                 PD.merge(g)
         e1.record(stream)
-        rep = PD.reconstruct(g, k, theta) if world > 1 else g.reconstruct_leveled(k, theta)
+        rep = None
+        if pipelined:
+            if queued[0]:
+                rep = collect()  # the previous slot's reports
+            g.reconstruct_async(k, theta)
+            queued[0] = True
+        else:
+            rep = PD.reconstruct(g, k, theta)
         e2.record(stream)
         g.advance_slot()
         return rep, (e1, e2)
@@ -397,6 +415,8 @@ def main():
         for i in range(n_steps):
             reps, m = step(start + i, from_host)
             marks.append(m)
+        if queued[0]:
+            reps = collect()  # the last slot's reports, inside the timed region
         ev_b.record(stream)
         torch.cuda.synchronize()
         if clk is not None:

@@ -146,6 +146,20 @@ sspd_status sspd_reconstruct(sspd_grid* g, uint32_t k, uint64_t cutoff, uint64_t
                              sspd_detection* out, uint64_t out_cap, uint64_t* n_out,
                              uint32_t* ovf_level, uint64_t* ovf_count);
 
+/* B200 extension: sspd_reconstruct split in two so a stream of slots
+ * pipelines.  _async queues the whole reconstruction (hot sets, joins,
+ * finalize, the read-back of counts and survivors) on the grid's stream and
+ * returns at once; _collect waits for it and returns what sspd_reconstruct
+ * would have (reports, or SSPD_CANDIDATE_OVERFLOW with level and count).
+ * Scans and advances may be queued in between: the stream orders them after
+ * the reconstruction, which sees the grid as of the _async call.  One
+ * reconstruction may be queued per grid; sspd_reconstruct, sspd_finalize and
+ * the shard calls refuse while it is.  Candidate buffers are sized for `cap`
+ * up front (cap <= 2^26). */
+sspd_status sspd_reconstruct_async(sspd_grid* g, uint32_t k, uint64_t cutoff, uint64_t cap);
+sspd_status sspd_reconstruct_collect(sspd_grid* g, sspd_detection* out, uint64_t out_cap,
+                                     uint64_t* n_out, uint32_t* ovf_level, uint64_t* ovf_count);
+
 /* merge_rseas (snapshot.hpp:54; snapshot.cpp:117-142): element-wise combine
  * of n grids into `out` (which may alias grids[0] for an in-place merge).
  * Grids must share (seed, q, r, delta, eta) -- else SSPD_INVALID_ARGUMENT with

@@ -160,6 +160,12 @@ struct sspd_grid {
   DevBuf shard_sent;            // world u64: pairs pushed to each owner this slot
   DevBuf masks;                 // sharded reconstruction: per-survivor bucket masks
   DevBuf* last_tuples = nullptr;  // buffer holding the last reconstruction's r-tuples
+  // sspd_reconstruct_async: one queued reconstruction awaiting collect
+  bool recon_pending = false;
+  cudaEvent_t ev_recon = nullptr;
+  uint64_t pend_cutoff = 0, pend_cap = 0, pend_C = 0;
+  std::vector<sspd_detection> collected;  // the last collect's reports (re-read with a larger buffer)
+  bool collected_ready = false;
   uint64_t surv_cap = 0;          // tuple capacity the survivor arrays were laid out for
   uint64_t pairset_mask = 0;
   bool pairset_dirty = false;   // holds keys from the current slot
@@ -258,6 +264,11 @@ sspd_status wide_only(const sspd_grid* g, const char* what) {
   return fail(SSPD_INVALID_ARGUMENT, std::string(what) + ": not available on a grid with " +
                                          std::to_string(g->width) + "-bit stamps (exact for in-window counts "
                                          "with k <= " + std::to_string(g->K) + " only)");
+}
+
+sspd_status no_pending(const sspd_grid* g, const char* what) {
+  if (!g->recon_pending) return SSPD_OK;
+  return fail(SSPD_INVALID_ARGUMENT, std::string(what) + ": a queued reconstruction awaits sspd_reconstruct_collect");
 }
 
 sspd_status check_launch() {
@@ -553,6 +564,7 @@ sspd_status create_impl(int device, uint32_t q, uint32_t r, uint32_t delta, uint
   if (cudaStreamCreateWithFlags(&g->stream, cudaStreamNonBlocking) != cudaSuccess ||
       cudaStreamCreateWithFlags(&g->copy_stream, cudaStreamNonBlocking) != cudaSuccess)
     return cleanup("CUDA error: stream creation failed");
+  cudaEventCreateWithFlags(&g->ev_recon, cudaEventDisableTiming);
   for (int i = 0; i < 2; ++i) {
     cudaEventCreateWithFlags(&g->ev_copy[i], cudaEventDisableTiming);
     cudaEventCreateWithFlags(&g->ev_used[i], cudaEventDisableTiming);
@@ -663,6 +675,7 @@ sspd_status sspd_grid_destroy(sspd_grid* g) {
       cudaEventDestroy(r.b);
     }
     for (cudaEvent_t e : g->event_pool) cudaEventDestroy(e);
+    if (g->ev_recon) cudaEventDestroy(g->ev_recon);
     for (int i = 0; i < 2; ++i) {
       if (g->ev_copy[i]) cudaEventDestroy(g->ev_copy[i]);
       if (g->ev_used[i]) cudaEventDestroy(g->ev_used[i]);
@@ -1105,6 +1118,7 @@ sspd_status sspd_finalize(sspd_grid* g, const uint32_t* tuples, uint64_t n, uint
   if (g->r > 64) return fail(SSPD_INVALID_ARGUMENT, "finalize_candidate: r > 64 unsupported");
   std::lock_guard<std::mutex> lk(g->mu);
   DeviceGuard dg(g->device);
+  if (sspd_status s = no_pending(g, "finalize_candidate")) return s;
   sspd_status s = commit_locked(g);
   if (s) return s;
   if (n == 0) return SSPD_OK;
@@ -1155,8 +1169,8 @@ enum class RecStep { kSurvivors, kEmptyRow, kRetry };
 // level counts (plus a prefix of the survivors).  Overflow is decided level
 // by level, as the reference does (rsea.cpp:206-216); a level whose count
 // exceeds the buffer but not the cap asks for a re-run with larger buffers.
-sspd_status recon_attempt(sspd_grid* g, uint32_t k, uint64_t cutoff, uint64_t cap, bool from_words, bool count_rk,
-                          uint64_t* C_out, RecStep* step, uint32_t* ovf_level, uint64_t* ovf_count) {
+sspd_status recon_queue(sspd_grid* g, uint32_t k, uint64_t cutoff, uint64_t cap, bool from_words, bool count_rk,
+                        uint64_t* C_out) {
   const uint32_t ncol = 1u << g->q;
   const uint32_t wpk = words_per_key(g);
   const uint64_t t_stride = (uint64_t)wpk << (g->q - g->delta);
@@ -1217,8 +1231,14 @@ sspd_status recon_attempt(sspd_grid* g, uint32_t k, uint64_t cutoff, uint64_t ca
     CU(cudaMemcpyAsync(hbuf + 512, s_idx + 2 * C, pre_small * 4, cudaMemcpyDeviceToHost, g->stream));
     g->d2h_bytes += pre_small * 8;
   }
-  CU(cudaStreamSynchronize(g->stream));
   g->d2h_bytes += sizeof(ReconMeta);
+  return SSPD_OK;
+}
+
+// After the queued attempt has completed: the row and level counts decide.
+sspd_status recon_decide(sspd_grid* g, uint64_t cap, uint64_t C, RecStep* step, uint32_t* ovf_level,
+                         uint64_t* ovf_count) {
+  const ReconMeta* mh = g->meta_host;
   *step = RecStep::kSurvivors;
   for (uint32_t row = 0; row < g->r; ++row)
     if (mh->rowcnt[row] == 0) {  // rsea.cpp:173-174
@@ -1241,6 +1261,38 @@ sspd_status recon_attempt(sspd_grid* g, uint32_t k, uint64_t cutoff, uint64_t ca
   }
   return SSPD_OK;
 }
+
+sspd_status recon_attempt(sspd_grid* g, uint32_t k, uint64_t cutoff, uint64_t cap, bool from_words, bool count_rk,
+                          uint64_t* C_out, RecStep* step, uint32_t* ovf_level, uint64_t* ovf_count) {
+  sspd_status s = recon_queue(g, k, cutoff, cap, from_words, count_rk, C_out);
+  if (s) return s;
+  CU(cudaStreamSynchronize(g->stream));
+  return recon_decide(g, cap, *C_out, step, ovf_level, ovf_count);
+}
+
+// The survivors' (cip, R_k) of a completed count_rk attempt: the pinned
+// prefix, or a read-back of all of them (on the copy stream, after `after`).
+sspd_status survivors(sspd_grid* g, uint64_t C, cudaEvent_t after, std::vector<uint32_t>* cip,
+                      std::vector<uint32_t>* rk) {
+  const uint64_t ns = g->meta_host->surv;
+  const uint32_t* hbuf = static_cast<const uint32_t*>(g->pinned_small);
+  const uint32_t* s_idx = g->surv.as<uint32_t>();
+  cip->resize(ns);
+  rk->resize(ns);
+  if (ns <= std::min<uint64_t>(C, 512)) {
+    std::memcpy(cip->data(), hbuf, ns * 4);
+    std::memcpy(rk->data(), hbuf + 512, ns * 4);
+    return SSPD_OK;
+  }
+  cudaStream_t st = after ? g->copy_stream : g->stream;
+  if (after) CU(cudaStreamWaitEvent(st, after, 0));
+  CU(cudaMemcpyAsync(cip->data(), s_idx + C, ns * 4, cudaMemcpyDeviceToHost, st));
+  CU(cudaMemcpyAsync(rk->data(), s_idx + 2 * C, ns * 4, cudaMemcpyDeviceToHost, st));
+  CU(cudaStreamSynchronize(st));
+  g->d2h_bytes += ns * 8;
+  return SSPD_OK;
+}
+
 
 // dedup_report (rsea.cpp:112-122) of the survivors' (cip, R_k): by cip,
 // larger estimate kept, sorted by cip; estimates in host double.
@@ -1269,6 +1321,7 @@ sspd_status sspd_reconstruct(sspd_grid* g, uint32_t k, uint64_t cutoff, uint64_t
   std::lock_guard<std::mutex> lk(g->mu);
   DeviceGuard dg(g->device);
   *n_out = 0;
+  if (sspd_status s = no_pending(g, "reconstruct")) return s;
   if (g->r > 64) return fail(SSPD_INVALID_ARGUMENT, "reconstruct: r > 64 unsupported");
   if (g->shard && g->shard_args.world > 1)
     return fail(SSPD_INVALID_ARGUMENT, "reconstruct: a sharded grid reconstructs through the shard calls");
@@ -1282,22 +1335,67 @@ sspd_status sspd_reconstruct(sspd_grid* g, uint32_t k, uint64_t cutoff, uint64_t
       if (attempt > 8) return fail(SSPD_CUDA_ERROR, "reconstruct: candidate buffer did not converge");
       continue;
     }
-    const uint64_t ns = g->meta_host->surv;
-    const uint32_t* hbuf = static_cast<const uint32_t*>(g->pinned_small);
-    uint32_t* s_idx = g->surv.as<uint32_t>();
-    std::vector<uint32_t> cip(ns), rk(ns);
-    if (ns <= std::min<uint64_t>(C, 512)) {
-      std::memcpy(cip.data(), hbuf, ns * 4);
-      std::memcpy(rk.data(), hbuf + 512, ns * 4);
-    } else {
-      CU(cudaMemcpyAsync(cip.data(), s_idx + C, ns * 4, cudaMemcpyDeviceToHost, g->stream));
-      CU(cudaMemcpyAsync(rk.data(), s_idx + 2 * C, ns * 4, cudaMemcpyDeviceToHost, g->stream));
-      CU(cudaStreamSynchronize(g->stream));
-      g->d2h_bytes += ns * 8;
-    }
+    std::vector<uint32_t> cip, rk;
+    s = survivors(g, C, nullptr, &cip, &rk);
+    if (s) return s;
     report(g, cip, rk, cutoff, out, out_cap, n_out);
     return SSPD_OK;
   }
+}
+
+sspd_status sspd_reconstruct_async(sspd_grid* g, uint32_t k, uint64_t cutoff, uint64_t cap) {
+  std::lock_guard<std::mutex> lk(g->mu);
+  DeviceGuard dg(g->device);
+  if (sspd_status s = no_pending(g, "reconstruct_async")) return s;
+  if (g->r > 64) return fail(SSPD_INVALID_ARGUMENT, "reconstruct: r > 64 unsupported");
+  if (g->shard && g->shard_args.world > 1)
+    return fail(SSPD_INVALID_ARGUMENT, "reconstruct: a sharded grid reconstructs through the shard calls");
+  if (cap > (1ull << 26)) return fail(SSPD_INVALID_ARGUMENT, "reconstruct_async: cap above 2^26 tuples");
+  // buffers for `cap` tuples up front: a level either fits or overflows the
+  // cap, so collect never has to re-run anything
+  g->cap_alloc = std::max<uint64_t>(g->cap_alloc, std::max<uint64_t>(cap, 1));
+  uint64_t C = 0;
+  sspd_status s = recon_queue(g, k, cutoff, cap, false, true, &C);
+  if (s) return s;
+  CU(cudaEventRecord(g->ev_recon, g->stream));
+  g->recon_pending = true;
+  g->collected_ready = false;
+  g->pend_cutoff = cutoff;
+  g->pend_cap = cap;
+  g->pend_C = C;
+  return SSPD_OK;
+}
+
+sspd_status sspd_reconstruct_collect(sspd_grid* g, sspd_detection* out, uint64_t out_cap, uint64_t* n_out,
+                                     uint32_t* ovf_level, uint64_t* ovf_count) {
+  std::lock_guard<std::mutex> lk(g->mu);
+  DeviceGuard dg(g->device);
+  *n_out = 0;
+  if (!g->recon_pending && !g->collected_ready)
+    return fail(SSPD_INVALID_ARGUMENT, "reconstruct_collect: nothing queued");
+  if (g->recon_pending) {
+    g->recon_pending = false;
+    g->collected.clear();
+    CU(cudaEventSynchronize(g->ev_recon));
+    RecStep step;
+    sspd_status s = recon_decide(g, g->pend_cap, g->pend_C, &step, ovf_level, ovf_count);
+    if (s) return s;
+    if (step == RecStep::kRetry) return fail(SSPD_CUDA_ERROR, "reconstruct_collect: candidate buffer too small");
+    if (step == RecStep::kSurvivors) {
+      std::vector<uint32_t> cip, rk;
+      s = survivors(g, g->pend_C, g->ev_recon, &cip, &rk);
+      if (s) return s;
+      uint64_t n = 0;
+      report(g, cip, rk, g->pend_cutoff, nullptr, 0, &n);
+      g->collected.resize(n);
+      report(g, cip, rk, g->pend_cutoff, g->collected.data(), n, &n);
+    }
+    g->collected_ready = true;
+  }
+  // the reports stay readable (e.g. again with a larger buffer) until the next queue
+  *n_out = g->collected.size();
+  std::memcpy(out, g->collected.data(), std::min<uint64_t>(out_cap, g->collected.size()) * sizeof(sspd_detection));
+  return SSPD_OK;
 }
 
 // ---- sharded routers ----
@@ -1375,6 +1473,7 @@ sspd_status sspd_shard_select(sspd_grid* g, uint32_t k, uint64_t cutoff, uint64_
   *mask_words = 0;
   *dev_masks = nullptr;
   if (!g->shard) return fail(SSPD_INVALID_ARGUMENT, "shard_select: not a sharded grid");
+  if (sspd_status s = no_pending(g, "shard_select")) return s;
   if (g->r > 64) return fail(SSPD_INVALID_ARGUMENT, "reconstruct: r > 64 unsupported");
   for (int attempt = 0;; ++attempt) {
     uint64_t C = 0;

@@ -250,6 +250,27 @@ class Grid:
             raise _cabi.InvalidArgument("reconstruct_leveled: workers == 0")
         return self._reconstruct(k, theta, self.candidate_cap)
 
+    def reconstruct_async(self, k: int, theta: float):
+        """Queue reconstruct_leveled on the grid's stream and return at once
+        (sspd_reconstruct_async); reconstruct_collect() returns its reports."""
+        check(self._L.sspd_reconstruct_async(self._h, k, hot_cutoff(self.eta, theta), self.candidate_cap))
+
+    def reconstruct_collect(self) -> list[Detection]:
+        while True:
+            buf = self._report_buf
+            if buf is None:
+                buf = self._report_buf = (_cabi.Detection_t * 4096)()
+            n, lvl, cnt = C.c_uint64(), C.c_uint32(), C.c_uint64()
+            st = self._L.sspd_reconstruct_collect(self._h, buf, len(buf), C.byref(n), C.byref(lvl),
+                                                  C.byref(cnt))
+            if st == _cabi.SSPD_CANDIDATE_OVERFLOW:
+                raise CandidateOverflow(self._L.sspd_last_error().decode(), lvl.value, cnt.value)
+            check(st)
+            if n.value <= len(buf):
+                rows = np.frombuffer(buf, dtype=_DET_DTYPE, count=n.value).tolist()
+                return [Detection(c, e, r) for c, r, e in rows]
+            self._report_buf = (_cabi.Detection_t * n.value)()  # the reports stay readable: read again
+
     def reconstruct_recursive(self, k: int, theta: float) -> list[Detection]:
         """Rsea::reconstruct_recursive (rsea.cpp:126-166): no candidate cap."""
         return self._reconstruct(k, theta, (1 << 64) - 1)

@@ -775,3 +775,46 @@ def test_sharded_routers_on_one_device(gpu, world):
         for g in grids:
             g.advance_slot()
         o.advance()
+
+
+def test_reconstruct_async_pipelines_slots(gpu):
+    """sspd_reconstruct_async / _collect: the reports of slot s equal the
+    oracle's for slot s although slot s+1's scan and the advance were queued
+    before they were collected; collect re-reads with a larger buffer; calls
+    that would clobber a queued reconstruction refuse."""
+    import torch
+
+    g, o = make_pair(gpu, DESK, 0xC3)
+    g.track_window(30)
+    rng = O.Mt64(0xC3)
+    want = []
+    got = []
+    for s in range(6):
+        parts = [rng.pairs(3000)]
+        for h in range(1 + s % 3):
+            cip = 0x0B000000 + h
+            parts.append(np.stack([np.full(200, cip, np.uint32), rng.draw(200).astype(np.uint32)], 1))
+        p = np.concatenate(parts)
+        g.scan_batch(torch.from_numpy(p.view(np.int32)).cuda())
+        o.scan(p)
+        if s:
+            got.append(g.reconstruct_collect())
+        g.reconstruct_async(30, 128.0)
+        want.append(o.reconstruct(30, 128.0))
+        if s == 2:
+            with pytest.raises(gpu.InvalidArgument, match="awaits"):
+                g.reconstruct_leveled(30, 128.0)
+            with pytest.raises(gpu.InvalidArgument, match="awaits"):
+                g.finalize_candidates(np.zeros((1, 5), np.uint32), 30, 128.0)
+        g.advance_slot()
+        o.advance()
+    got.append(g.reconstruct_collect())
+    assert len(got) == len(want)
+    for s, (a, b) in enumerate(zip(got, want)):
+        assert dets_equal(a, b), s
+    g._report_buf = (gpu._cabi.Detection_t * 1)()  # too small: collect reads again with a larger one
+    g.reconstruct_async(30, 128.0)
+    assert dets_equal(g.reconstruct_collect(), o.reconstruct(30, 128.0))
+    with pytest.raises(gpu.InvalidArgument, match="nothing queued"):
+        g2 = gpu.Grid(seed=1, **DESK)
+        g2.reconstruct_collect()
