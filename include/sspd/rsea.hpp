@@ -105,6 +105,11 @@ class Rsea {
   // The underlying C-ABI handle (include/sspd_cuda.h).
   sspd_grid* handle() const;
   StampWidth stamp_width() const;
+  // Queue reconstruct_leveled on the device and return at once; the next
+  // collect_reconstruction() returns its report (sspd_reconstruct_async).
+  // Scans and advances may be issued in between.
+  void reconstruct_leveled_async(uint32_t k, double theta) const;
+  DetectionReport collect_reconstruction() const;
 
  private:
   struct Uninitialised {};
@@ -124,6 +129,7 @@ class Rsea {
   mutable bool mirror_dirty_ = false;
   mutable std::vector<IpPair> pending_;
   mutable std::unique_ptr<std::mutex> mu_;
+  mutable std::size_t pending_cap_ = 0;  // candidate cap of the queued reconstruction
 };
 
 }  // namespace sspd

@@ -287,6 +287,31 @@ DetectionReport Rsea::reconstruct(uint32_t k, double theta, uint64_t cap) const 
   }
 }
 
+void Rsea::reconstruct_leveled_async(uint32_t k, double theta) const {
+  sync();
+  pending_cap_ = candidate_cap_;
+  check(sspd_reconstruct_async(h_, k, hot_cutoff(eta_, theta), candidate_cap_));
+}
+
+DetectionReport Rsea::collect_reconstruction() const {
+  std::vector<sspd_detection> buf(1024);
+  for (;;) {
+    uint64_t n = 0, ovf_count = 0;
+    uint32_t ovf_level = 0;
+    const sspd_status st = sspd_reconstruct_collect(h_, buf.data(), buf.size(), &n, &ovf_level, &ovf_count);
+    if (st == SSPD_CANDIDATE_OVERFLOW) throw CandidateOverflow(ovf_level, ovf_count, pending_cap_);
+    check(st);
+    if (n > buf.size()) {  // the reports stay readable: read again
+      buf.resize(n);
+      continue;
+    }
+    DetectionReport rep;
+    rep.hosts.reserve(n);
+    for (uint64_t i = 0; i < n; ++i) rep.hosts.push_back({buf[i].cip, estimate_cardinality(eta_, buf[i].r_k)});
+    return rep;
+  }
+}
+
 DetectionReport Rsea::reconstruct_leveled(uint32_t k, double theta, unsigned workers) const {
   if (workers == 0) throw std::invalid_argument("reconstruct_leveled: workers == 0");
   return reconstruct(k, theta, candidate_cap_);
