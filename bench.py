@@ -444,7 +444,7 @@ def main():
     launches = P.launch_count() - launches0
     slot += args.steps
     prof = {}
-    for name in ("bin", "scan", "commit", "hist_counts", "count", "hot_compact", "level2",
+    for name in ("bin", "scan", "commit", "hist_counts", "count", "reconstruct", "hot_compact", "level2",
                  "level_ext", "finalize", "merge", "rebase"):
         t, n, u = g.profile_read(name)
         if n:

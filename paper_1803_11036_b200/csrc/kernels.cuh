@@ -663,14 +663,24 @@ __global__ void __launch_bounds__(256) hist_rebuild_kernel(const uint32_t* __res
 // writes its hot columns in ascending order (rsea.cpp:65-84).
 constexpr int kHotChunk = 1024;
 
+// Programmatic dependent launch (the reconstruction chain is launched with
+// cudaLaunchAttributeProgrammaticStreamSerialization): a kernel lets its
+// successor start launching at once, and waits for its predecessor's results
+// only where it first reads them.  Without the attribute both are no-ops.
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+
 __global__ void __launch_bounds__(kHotChunk) hot_mark_kernel(const uint32_t* __restrict__ counts,
                                                             const uint32_t* __restrict__ hist, uint32_t K,
                                                             uint32_t now, uint32_t k, Geo geo, uint64_t cutoff,
                                                             uint32_t* __restrict__ hot_words,
-                                                            uint32_t* __restrict__ chunk_counts,
-                                                            uint32_t* __restrict__ hotT, uint32_t words_per_key,
-                                                            int from_words = 0) {
+                                                            uint32_t* __restrict__ chunk_counts, int from_words,
+                                                            unsigned long long* __restrict__ zero,
+                                                            uint32_t zero_words) {
   const uint32_t ncol = 1u << geo.q;
+  // the reconstruction's bookkeeping starts at zero (one memset fewer)
+  if (zero && blockIdx.x == 0)
+    for (uint32_t i = threadIdx.x; i < zero_words; i += blockDim.x) zero[i] = 0ull;
   const uint32_t chunks = (ncol + kHotChunk - 1) / kHotChunk;
   const uint32_t row = blockIdx.x / chunks, chunk = blockIdx.x % chunks;
   const uint32_t col = chunk * kHotChunk + threadIdx.x;
@@ -699,20 +709,19 @@ __global__ void __launch_bounds__(kHotChunk) hot_mark_kernel(const uint32_t* __r
     if (col < ncol && !from_words) hot_words[row * wpr + (col >> 5)] = b;
     if (b) atomicAdd(&s_sum, (uint32_t)__popc(b));
   }
-  if (hot) {
-    const uint32_t kbits = geo.q - geo.delta;
-    uint32_t* myT = hotT + (uint64_t)row * ((uint64_t)words_per_key << kbits);
-    const uint32_t key = col & geo.low_mask, j = col >> kbits;
-    atomicOr(myT + (uint64_t)key * words_per_key + (j >> 5), 1u << (j & 31));
-  }
   __syncthreads();
   if (threadIdx.x == 0) chunk_counts[blockIdx.x] = s_sum;
 }
 
+// Also writes the transposed hot bits the joins index by key:
+// hotT[row][key][j / 32] bit j%32 = hot(row, col = j << (q - delta) | key).
 __global__ void __launch_bounds__(kHotChunk) hot_write_kernel(const uint32_t* __restrict__ hot_words, Geo geo,
                                                              const uint32_t* __restrict__ chunk_counts,
                                                              uint32_t* __restrict__ cols_out,
-                                                             uint32_t* __restrict__ row_counts) {
+                                                             uint32_t* __restrict__ row_counts,
+                                                             uint32_t* __restrict__ hotT, uint32_t words_per_key) {
+  pdl_trigger();
+  pdl_wait();
   const uint32_t ncol = 1u << geo.q;
   const uint32_t chunks = (ncol + kHotChunk - 1) / kHotChunk;
   const uint32_t row = blockIdx.x / chunks, chunk = blockIdx.x % chunks;
@@ -745,6 +754,24 @@ __global__ void __launch_bounds__(kHotChunk) hot_write_kernel(const uint32_t* __
     cols_out[(uint64_t)row * ncol + s_base + s_warp[wid] + __popc(w & ((1u << lane) - 1u))] = col;
   if (chunk == chunks - 1 && threadIdx.x == 0)
     row_counts[row] = s_base + chunk_counts[row * chunks + chunk];
+  // transposed bits, one word per thread (no atomics, so no zeroing first)
+  const uint32_t kbits = geo.q - geo.delta;
+  const uint32_t seg_bits = 1u << geo.delta;
+  const uint64_t t_words = (uint64_t)geo.r * ((uint64_t)words_per_key << kbits);
+  for (uint64_t t = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; t < t_words;
+       t += (uint64_t)gridDim.x * blockDim.x) {
+    const uint32_t trow = (uint32_t)(t / ((uint64_t)words_per_key << kbits));
+    const uint32_t rest = (uint32_t)(t % ((uint64_t)words_per_key << kbits));
+    const uint32_t key = rest / words_per_key, jw = rest % words_per_key;
+    uint32_t bits = 0;
+    for (uint32_t b = 0; b < 32; ++b) {
+      const uint32_t j = jw * 32 + b;
+      if (j >= seg_bits) break;
+      const uint32_t c = (j << kbits) | key;
+      bits |= ((hot_words[trow * wpr + (c >> 5)] >> (c & 31)) & 1u) << b;
+    }
+    hotT[t] = bits;
+  }
 }
 
 // ---------------------------------------------------------------------------
@@ -793,6 +820,8 @@ __global__ void __launch_bounds__(256) level2_kernel(const uint32_t* __restrict_
                                                      const uint32_t* __restrict__ T2, uint32_t wpk, Geo geo,
                                                      uint32_t* __restrict__ out, uint64_t out_cap,
                                                      ReconMeta* __restrict__ meta) {
+  pdl_trigger();
+  pdl_wait();
   const uint32_t n0 = meta->rowcnt[0], n1 = meta->rowcnt[1];
   const uint32_t* H0 = cols;
   const uint32_t* H1 = cols + ncol;
@@ -838,6 +867,8 @@ __global__ void __launch_bounds__(256) level_ext_kernel(const uint32_t* __restri
                                                         uint32_t m, const uint32_t* __restrict__ Tm,
                                                         uint32_t wpk, Geo geo, uint32_t* __restrict__ out,
                                                         uint64_t out_cap, ReconMeta* __restrict__ meta) {
+  pdl_trigger();
+  pdl_wait();
   const uint64_t n_in = meta->level[m - 1];
   if (n_in > in_cap) return;  // input truncated: the host re-runs with larger buffers
   unsigned long long* counter = &meta->level[m];
@@ -884,11 +915,14 @@ __global__ void __launch_bounds__(256) finalize_check_kernel(const uint32_t* __r
                                                              uint64_t in_cap, const HashTabs* __restrict__ tabs,
                                                              Geo geo, ReconMeta* __restrict__ meta,
                                                              uint32_t* __restrict__ surv_idx,
-                                                             uint32_t* __restrict__ surv_cip) {
+                                                             uint32_t* __restrict__ surv_cip,
+                                                             uint32_t* __restrict__ surv_rk) {
+  pdl_trigger();
   __shared__ uint16_t s_row0[4][256];
   for (int i = threadIdx.x; i < 1024; i += blockDim.x)
     s_row0[i >> 8][i & 255] = (uint16_t)tabs->row0[i >> 8][i & 255];
   __syncthreads();
+  pdl_wait();
   const uint64_t n = meta->level[geo.r - 1];
   if (n > in_cap) return;
   const uint32_t lane = threadIdx.x & 31;
@@ -917,6 +951,7 @@ __global__ void __launch_bounds__(256) finalize_check_kernel(const uint32_t* __r
     if (ok) {
       surv_idx[pos] = (uint32_t)t;
       surv_cip[pos] = ip;
+      if (surv_rk) surv_rk[pos] = 0;  // finalize_count adds into it
     }
   }
 }
@@ -931,6 +966,8 @@ __global__ void __launch_bounds__(256) finalize_count_kernel(const uint32_t* __r
                                                              const ReconMeta* __restrict__ meta,
                                                              const uint32_t* __restrict__ surv_idx,
                                                              uint32_t* __restrict__ surv_rk) {
+  pdl_trigger();
+  pdl_wait();
   constexpr uint32_t kChunk = 1024;
   const uint64_t n_surv = meta->surv;
   const uint32_t chunks = (geo.eta + kChunk - 1) / kChunk;
@@ -1516,6 +1553,8 @@ __global__ void __launch_bounds__(256) finalize_count_narrow_kernel(const uint32
                                                                     const ReconMeta* __restrict__ meta,
                                                                     const uint32_t* __restrict__ surv_idx,
                                                                     uint32_t* __restrict__ surv_rk) {
+  pdl_trigger();
+  pdl_wait();
   constexpr uint32_t kChunk = 1024;
   const uint64_t n_surv = meta->surv;
   const uint32_t chunks = (geo.eta + kChunk - 1) / kChunk;

@@ -177,6 +177,7 @@ struct sspd_grid {
   PushArgs push{};              // fused exchange: peer inboxes (export mode 3)
   void* pinned_small = nullptr;  // 4 KB pinned scratch for counters
   bool profiling = false;
+  int prof_suspend = 0;  // inside a PDL launch chain: one event pair around the chain only
   std::vector<ProfRec> prof;
   std::vector<cudaEvent_t> event_pool;  // recycled profiling events (creation is the costly part)
   uint64_t h2d_bytes = 0, d2h_bytes = 0;  // host<->device traffic, for e2e accounting
@@ -241,9 +242,11 @@ cudaEvent_t take_event(sspd_grid* g) {
 struct Prof {
   sspd_grid* g;
   ProfRec rec{};
+  bool on = false;
   Prof(sspd_grid* g_, const char* name, uint64_t units) : g(g_) {
     g_launches.fetch_add(1, std::memory_order_relaxed);
-    if (!g->profiling) return;
+    if (!g->profiling || g->prof_suspend) return;
+    on = true;
     rec.name = name;
     rec.units = units;
     rec.a = take_event(g);
@@ -251,7 +254,7 @@ struct Prof {
     cudaEventRecord(rec.a, g->stream);
   }
   ~Prof() {
-    if (!g->profiling) return;
+    if (!on) return;
     cudaEventRecord(rec.b, g->stream);
     g->prof.push_back(rec);
   }
@@ -273,6 +276,27 @@ sspd_status no_pending(const sspd_grid* g, const char* what) {
 
 sspd_status check_launch() {
   cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return fail(SSPD_CUDA_ERROR, std::string("CUDA launch: ") + cudaGetErrorString(e));
+  return SSPD_OK;
+}
+
+// Launch with programmatic stream serialization: the kernel may begin while
+// its predecessor in the stream finishes, and waits for the predecessor's
+// results at its pdl_wait() (kernels.cuh).  Used along the reconstruction
+// chain, whose kernels are each a few microseconds long.
+template <class... KArgs, class... Args>
+sspd_status launch_pdl(sspd_grid* g, void (*kernel)(KArgs...), unsigned grid, unsigned block, Args... args) {
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(block);
+  cfg.stream = g->stream;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  g_launches.fetch_add(1, std::memory_order_relaxed);
+  const cudaError_t e = cudaLaunchKernelEx(&cfg, kernel, static_cast<KArgs>(args)...);
   if (e != cudaSuccess) return fail(SSPD_CUDA_ERROR, std::string("CUDA launch: ") + cudaGetErrorString(e));
   return SSPD_OK;
 }
@@ -356,7 +380,8 @@ uint32_t words_per_key(const sspd_grid* g) {
 // sharded routers); only the transposed bits, chunk counts and compaction
 // are rebuilt from them.
 sspd_status hot_locked(sspd_grid* g, uint32_t k, uint64_t cutoff, std::vector<uint32_t>* host_rowcnt,
-                       uint32_t* d_rowcnt, bool from_words = false) {
+                       uint32_t* d_rowcnt, bool from_words = false, unsigned long long* zero = nullptr,
+                       uint32_t zero_words = 0) {
   sspd_status s = SSPD_OK;
   // R_k straight from the window ring inside hot_mark when it covers k;
   // otherwise per-cell counts first (full pass over the stamps).
@@ -377,18 +402,17 @@ sspd_status hot_locked(sspd_grid* g, uint32_t k, uint64_t cutoff, std::vector<ui
       g->hot_chunks.ensure((size_t)g->r * chunks * 4) != cudaSuccess)
     return fail(SSPD_CUDA_ERROR, "CUDA error: out of memory (hot sets)");
   if (!d_rowcnt) d_rowcnt = g->hot_rowcnt.as<uint32_t>();
-  CU(cudaMemsetAsync(g->hotT.p, 0, t_words * 4, g->stream));
   {
     Prof p(g, "hot_compact", g->geo.ncells);
     hot_mark_kernel<<<g->r * chunks, kHotChunk, 0, g->stream>>>(
         g->counts.as<uint32_t>(), ring ? g->hist : nullptr, g->K, g->now, k, g->geo, cutoff,
-        g->hot_words.as<uint32_t>(), g->hot_chunks.as<uint32_t>(), g->hotT.as<uint32_t>(), wpk, from_words ? 1 : 0);
-    hot_write_kernel<<<g->r * chunks, kHotChunk, 0, g->stream>>>(
-        g->hot_words.as<uint32_t>(), g->geo, g->hot_chunks.as<uint32_t>(), g->hot_cols.as<uint32_t>(), d_rowcnt);
+        g->hot_words.as<uint32_t>(), g->hot_chunks.as<uint32_t>(), from_words ? 1 : 0, zero, zero_words);
+    s = check_launch();
+    if (s) return s;
+    s = launch_pdl(g, hot_write_kernel, g->r * chunks, kHotChunk, g->hot_words.as<uint32_t>(), g->geo,
+                   g->hot_chunks.as<uint32_t>(), g->hot_cols.as<uint32_t>(), d_rowcnt, g->hotT.as<uint32_t>(), wpk);
+    if (s) return s;
   }
-  g_launches.fetch_add(1, std::memory_order_relaxed);
-  s = check_launch();
-  if (s) return s;
   if (host_rowcnt) {
     host_rowcnt->resize(g->r);
     CU(cudaMemcpyAsync(host_rowcnt->data(), d_rowcnt, g->r * 4, cudaMemcpyDeviceToHost, g->stream));
@@ -422,14 +446,13 @@ sspd_status queue_finalize(sspd_grid* g, const uint32_t* tuples, uint64_t in_cap
   uint32_t* s_cip = s_idx + in_cap;
   uint32_t* s_rk = s_cip + in_cap;
   ReconMeta* meta = g->meta.as<ReconMeta>();
+  sspd_status s;
   {
     Prof p(g, "finalize_check", in_cap);
-    finalize_check_kernel<<<grid_blocks(g, in_cap, 256, 2), 256, 0, g->stream>>>(tuples, in_cap, g->d_tabs,
-                                                                                   g->geo, meta, s_idx, s_cip);
+    s = launch_pdl(g, finalize_check_kernel, grid_blocks(g, in_cap, 256, 2), 256, tuples, in_cap,
+                   (const HashTabs*)g->d_tabs, g->geo, meta, s_idx, s_cip, s_rk);
   }
-  sspd_status s = check_launch();
   if (s) return s;
-  CU(cudaMemsetAsync(s_rk, 0, (size_t)std::max<uint64_t>(in_cap, 1) * 4, g->stream));
   {
     const uint32_t chunks = (g->eta + 1023) / 1024;
     const unsigned blocks = (unsigned)sm_count(g->device) * 8;
@@ -437,18 +460,19 @@ sspd_status queue_finalize(sspd_grid* g, const uint32_t* tuples, uint64_t in_cap
     // live codes younger than k: code > code(now) - k, and never 0
     const uint32_t thr = (uint32_t)std::max<int64_t>((int64_t)g->code_now() - (k <= 0xFFFFu ? k : 0u),
                                                      (int64_t)g->code_lo - 1);
+    const ReconMeta* cmeta = meta;
+    const uint32_t* cidx = s_idx;
     if (g->width == 8)
-      finalize_count_narrow_kernel<uint8_t><<<blocks, 256, 0, g->stream>>>(
-          tuples, static_cast<const uint8_t*>(g->codes), g->geo, thr, kmode_of(k), meta, s_idx, s_rk);
+      s = launch_pdl(g, finalize_count_narrow_kernel<uint8_t>, blocks, 256, tuples,
+                     static_cast<const uint8_t*>(g->codes), g->geo, thr, kmode_of(k), cmeta, cidx, s_rk);
     else if (g->width == 16)
-      finalize_count_narrow_kernel<uint16_t><<<blocks, 256, 0, g->stream>>>(
-          tuples, static_cast<const uint16_t*>(g->codes), g->geo, thr, kmode_of(k), meta, s_idx, s_rk);
+      s = launch_pdl(g, finalize_count_narrow_kernel<uint16_t>, blocks, 256, tuples,
+                     static_cast<const uint16_t*>(g->codes), g->geo, thr, kmode_of(k), cmeta, cidx, s_rk);
     else
-      finalize_count_kernel<<<blocks, 256, 0, g->stream>>>(tuples, g->stamps, g->geo,
-                                                            g->now - (k <= 0xFFFFu ? k : 0u), kmode_of(k), meta,
-                                                            s_idx, s_rk);
+      s = launch_pdl(g, finalize_count_kernel, blocks, 256, tuples, (const uint32_t*)g->stamps, g->geo,
+                     g->now - (k <= 0xFFFFu ? k : 0u), kmode_of(k), cmeta, cidx, s_rk);
   }
-  return check_launch();
+  return s;
 }
 
 // The per-slot pair set (dedup and shard scans), allocated on first use.
@@ -1183,30 +1207,31 @@ sspd_status recon_queue(sspd_grid* g, uint32_t k, uint64_t cutoff, uint64_t cap,
     return fail(SSPD_CUDA_ERROR, "CUDA error: out of memory (candidate buffer)");
   sspd_status s = ensure_surv(g, C);
   if (s) return s;
-  CU(cudaMemsetAsync(meta, 0, sizeof(ReconMeta), g->stream));
-  s = hot_locked(g, k, cutoff, nullptr, meta->rowcnt, from_words);
+  // One event pair around the chain when profiling (events between its
+  // kernels would break the programmatic dependent launches).
+  Prof chain(g, "reconstruct", C);
+  ++g->prof_suspend;
+  struct Resume {
+    sspd_grid* g;
+    ~Resume() { --g->prof_suspend; }
+  } resume{g};
+  // hot_mark zeroes the bookkeeping (meta) before anything reads it
+  s = hot_locked(g, k, cutoff, nullptr, meta->rowcnt, from_words, reinterpret_cast<unsigned long long*>(meta),
+                 sizeof(ReconMeta) / 8);
   if (s) return s;
   const uint32_t* cols = g->hot_cols.as<uint32_t>();
   const uint32_t* T = g->hotT.as<uint32_t>();
   // level sizes live on the device; a modest persistent grid keeps the
   // (usually tiny) joins cheap to launch and still strides large levels
   const unsigned blocks = (unsigned)sm_count(g->device) * 2;
-  {
-    Prof p(g, "level2", 0);
-    level2_kernel<<<blocks, 256, 0, g->stream>>>(cols, ncol, T + 2 * t_stride, wpk, g->geo, g->tupA.as<uint32_t>(), C,
-                                                 meta);
-  }
-  s = check_launch();
+  s = launch_pdl(g, level2_kernel, blocks, 256, cols, ncol, T + 2 * t_stride, wpk, g->geo, g->tupA.as<uint32_t>(), C,
+                 meta);
   if (s) return s;
   DevBuf* rd = &g->tupA;
   DevBuf* wr = &g->tupB;
   for (uint32_t row = 3; row < g->r; ++row) {
-    {
-      Prof p(g, "level_ext", 0);
-      level_ext_kernel<<<blocks, 256, 0, g->stream>>>(rd->as<uint32_t>(), C, row, T + (uint64_t)row * t_stride, wpk,
-                                                      g->geo, wr->as<uint32_t>(), C, meta);
-    }
-    s = check_launch();
+    s = launch_pdl(g, level_ext_kernel, blocks, 256, (const uint32_t*)rd->as<uint32_t>(), C, row,
+                   T + (uint64_t)row * t_stride, wpk, g->geo, wr->as<uint32_t>(), C, meta);
     if (s) return s;
     std::swap(rd, wr);
   }
@@ -1215,10 +1240,8 @@ sspd_status recon_queue(sspd_grid* g, uint32_t k, uint64_t cutoff, uint64_t cap,
   if (count_rk) {
     s = queue_finalize(g, rd->as<uint32_t>(), C, k);
   } else {
-    Prof p(g, "finalize_check", C);
-    finalize_check_kernel<<<grid_blocks(g, C, 256, 2), 256, 0, g->stream>>>(rd->as<uint32_t>(), C, g->d_tabs, g->geo,
-                                                                             meta, s_idx, s_idx + C);
-    s = check_launch();
+    s = launch_pdl(g, finalize_check_kernel, grid_blocks(g, C, 256, 2), 256, (const uint32_t*)rd->as<uint32_t>(), C,
+                   (const HashTabs*)g->d_tabs, g->geo, meta, s_idx, s_idx + C, (uint32_t*)nullptr);
   }
   if (s) return s;
   // Survivors are few (true super points plus hash-consistent impostors):
