@@ -243,8 +243,9 @@ struct Prof {
   sspd_grid* g;
   ProfRec rec{};
   bool on = false;
-  Prof(sspd_grid* g_, const char* name, uint64_t units) : g(g_) {
-    g_launches.fetch_add(1, std::memory_order_relaxed);
+  // counts_launch: false for a span of several launches counted on their own
+  Prof(sspd_grid* g_, const char* name, uint64_t units, bool counts_launch = true) : g(g_) {
+    if (counts_launch) g_launches.fetch_add(1, std::memory_order_relaxed);
     if (!g->profiling || g->prof_suspend) return;
     on = true;
     rec.name = name;
@@ -448,7 +449,7 @@ sspd_status queue_finalize(sspd_grid* g, const uint32_t* tuples, uint64_t in_cap
   ReconMeta* meta = g->meta.as<ReconMeta>();
   sspd_status s;
   {
-    Prof p(g, "finalize_check", in_cap);
+    Prof p(g, "finalize_check", in_cap, false);  // launch_pdl counts the launch
     s = launch_pdl(g, finalize_check_kernel, grid_blocks(g, in_cap, 256, 2), 256, tuples, in_cap,
                    (const HashTabs*)g->d_tabs, g->geo, meta, s_idx, s_cip, s_rk);
   }
@@ -456,7 +457,7 @@ sspd_status queue_finalize(sspd_grid* g, const uint32_t* tuples, uint64_t in_cap
   {
     const uint32_t chunks = (g->eta + 1023) / 1024;
     const unsigned blocks = (unsigned)sm_count(g->device) * 8;
-    Prof p(g, "finalize", in_cap * chunks);
+    Prof p(g, "finalize", in_cap * chunks, false);
     // live codes younger than k: code > code(now) - k, and never 0
     const uint32_t thr = (uint32_t)std::max<int64_t>((int64_t)g->code_now() - (k <= 0xFFFFu ? k : 0u),
                                                      (int64_t)g->code_lo - 1);
@@ -1209,7 +1210,7 @@ sspd_status recon_queue(sspd_grid* g, uint32_t k, uint64_t cutoff, uint64_t cap,
   if (s) return s;
   // One event pair around the chain when profiling (events between its
   // kernels would break the programmatic dependent launches).
-  Prof chain(g, "reconstruct", C);
+  Prof chain(g, "reconstruct", C, false);
   ++g->prof_suspend;
   struct Resume {
     sspd_grid* g;
