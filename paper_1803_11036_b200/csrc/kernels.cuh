@@ -754,23 +754,21 @@ __global__ void __launch_bounds__(kHotChunk) hot_write_kernel(const uint32_t* __
     cols_out[(uint64_t)row * ncol + s_base + s_warp[wid] + __popc(w & ((1u << lane) - 1u))] = col;
   if (chunk == chunks - 1 && threadIdx.x == 0)
     row_counts[row] = s_base + chunk_counts[row * chunks + chunk];
-  // transposed bits, one word per thread (no atomics, so no zeroing first)
+  // transposed bits, one warp per word and one lane per bit (no atomics, so
+  // no zeroing first)
   const uint32_t kbits = geo.q - geo.delta;
   const uint32_t seg_bits = 1u << geo.delta;
-  const uint64_t t_words = (uint64_t)geo.r * ((uint64_t)words_per_key << kbits);
-  for (uint64_t t = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; t < t_words;
-       t += (uint64_t)gridDim.x * blockDim.x) {
-    const uint32_t trow = (uint32_t)(t / ((uint64_t)words_per_key << kbits));
-    const uint32_t rest = (uint32_t)(t % ((uint64_t)words_per_key << kbits));
-    const uint32_t key = rest / words_per_key, jw = rest % words_per_key;
-    uint32_t bits = 0;
-    for (uint32_t b = 0; b < 32; ++b) {
-      const uint32_t j = jw * 32 + b;
-      if (j >= seg_bits) break;
-      const uint32_t c = (j << kbits) | key;
-      bits |= ((hot_words[trow * wpr + (c >> 5)] >> (c & 31)) & 1u) << b;
-    }
-    hotT[t] = bits;
+  const uint64_t per_row = (uint64_t)words_per_key << kbits;
+  const uint64_t t_words = (uint64_t)geo.r * per_row;
+  const uint64_t nwarps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+  for (uint64_t t = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; t < t_words; t += nwarps) {
+    const uint32_t trow = (uint32_t)(t / per_row);
+    const uint32_t rest = (uint32_t)(t % per_row);
+    const uint32_t key = rest / words_per_key, j = (rest % words_per_key) * 32 + lane;
+    const uint32_t c = (j << kbits) | key;
+    const bool bit = j < seg_bits && ((hot_words[trow * wpr + (c >> 5)] >> (c & 31)) & 1u);
+    const uint32_t b = __ballot_sync(0xffffffffu, bit);
+    if (lane == 0) hotT[t] = b;
   }
 }
 
