@@ -1,0 +1,82 @@
+"""Randomised differential tests: the CUDA path against the CPU oracle over
+random valid geometries (validate_config's whole domain, hashing.cpp:63-87),
+scan modes, stamp widths, windows and traffic mixes.  Seeded, so every run
+checks the same cases; each case compares grids (32-bit), in-window counts,
+hot sets and reconstruction reports -- or the CandidateOverflow level and
+count -- slot by slot.
+"""
+import numpy as np
+import pytest
+
+from oracle import oracle as O
+
+pytestmark = pytest.mark.gpu
+
+
+def random_geometry(rng):
+    while True:
+        q = int(rng.integers(2, 17))
+        delta = int(rng.integers(1, q))
+        r_min = max(3, -(-(32 - q) // delta) + 2)
+        if r_min > 14:
+            continue
+        r = int(rng.integers(r_min, min(r_min + 3, 15) + 1))
+        eta = int(rng.choice([2, 3, 7, 16, 40, 64, 100, 256, 1000]))
+        if (r << q) * eta > (1 << 21):  # keep the oracle's per-slot work small
+            continue
+        return dict(q=q, r=r, delta=delta, eta=eta)
+
+
+def recon_both(gpu, g, o, k, theta, cap):
+    try:
+        ref = o.reconstruct(k, theta, cap=cap)
+    except O.CandidateOverflow as e:
+        with pytest.raises(gpu.CandidateOverflow) as got:
+            g.reconstruct_leveled(k, theta)
+        return (got.value.level, got.value.count) == (e.level, e.count)
+    got = g.reconstruct_leveled(k, theta)
+    return [(d.cip, d.estimate) for d in got] == [(d.cip, d.estimate) for d in ref]
+
+
+@pytest.mark.timeout(300)
+@pytest.mark.parametrize("case", range(60))
+def test_random_case(gpu, case):
+    rng = np.random.default_rng(0xF0220 + case)
+    geo = random_geometry(rng)
+    seed = int(rng.integers(0, 2**63))
+    width = int(rng.choice([32, 32, 16, 8]))
+    k = int(rng.integers(1, 9))
+    mode = int(rng.choice([-1, 0, 1, 2, 3]))
+    g = gpu.Grid(seed=seed, width=width, k_max=k if width < 32 or rng.random() < 0.5 else 0, **geo)
+    g.scan_mode(mode, int(rng.choice([-1, 0, 1])))
+    cap = 1 << 18
+    g.candidate_cap = cap
+    o = O.OracleGrid(seed=seed, **geo)
+    mt = O.Mt64(seed & 0xFFFFFFFF)
+    theta = float(max(1.0, geo["eta"] * rng.uniform(0.2, 0.9)))
+    hosts = [int(mt.next()) & 0xFFFFFFFF for _ in range(int(rng.integers(1, 5)))]
+    for s in range(int(rng.integers(3, 7))):
+        parts = [mt.pairs(int(rng.integers(0, 3000)))]
+        for h in hosts:
+            if rng.random() < 0.7:
+                fan = int(rng.integers(1, 3 * geo["eta"] + 2))
+                parts.append(np.stack([np.full(fan, h, np.uint32), mt.draw(fan).astype(np.uint32)], 1))
+        p = np.concatenate(parts)
+        if len(p) and rng.random() < 0.5:
+            p = np.concatenate([p, p[: len(p) // 3]])  # repeats inside the slot
+        g.scan_batch(p)
+        o.scan(p)
+        if width == 32:
+            assert np.array_equal(g.cells(), o.cells()), (case, s)
+        for kk in sorted({1, k}):
+            assert np.array_equal(g.active_counts(kk), o.active_counts(kk)), (case, s, kk)
+        hot = o.hot_sets(k, theta)
+        assert [h.tolist() for h in g.hot_sets(k, theta)] == [h.tolist() for h in hot], (case, s)
+        # the reference enumerates |H0|*|H1|*|H2| triples (rsea.cpp:184-200): only
+        # compare reconstructions the oracle finishes quickly
+        if int(np.prod([len(h) for h in hot[:3]], dtype=np.float64)) <= 20_000_000:
+            assert recon_both(gpu, g, o, k, theta, cap), (case, s, geo, width, mode)
+        adv = int(rng.choice([1, 1, 1, 2, 5]))
+        g.advance_slot(slots=adv)
+        for _ in range(adv):
+            o.advance()
