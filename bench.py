@@ -182,16 +182,18 @@ class ClockSampler:
 # ---------------------------------------------------------------------------
 # Reference arm / cpu baseline: the compiled reference on host cores.
 
-def run_reference(cfg, steps, warmup, pairs_cap, time_budget_s):
+def run_reference(cfg, steps, warmup, pairs_cap, time_budget_s, workers=None):
     """Reference Rsea at the same geometry: per step one slot of the same
     trace through scan_batch (alpha=32768 batches, pipeline.cpp:58-63),
-    reconstruct_leveled and advance_slot, workers = all host cores."""
+    reconstruct_leveled and advance_slot, workers = all host cores (or
+    $SSPD_REF_WORKERS, or `workers`)."""
     from oracle import oracle as O
 
     # the workload comes from the host-only generator (no CUDA runtime in
     # this process): the same traces the device generator makes
     S = C.CDLL(os.path.join(ROOT, "paper_1803_11036_b200", "lib", "libsspd_synth.so"))
-    workers = os.cpu_count() or 1
+    if workers is None:
+        workers = env_int("SSPD_REF_WORKERS", os.cpu_count() or 1)
     t0 = time.time()
     g = O.RefGrid(cfg["q"], cfg["r"], cfg["delta"], cfg["seed"], cfg["eta"])
     t_init = time.time() - t0
@@ -558,6 +560,20 @@ def main():
         except Exception as e:  # report, do not hide
             cpu = {"value": None, "unit": unit, "cores": os.cpu_count(), "kind": "reference",
                    "sample": f"failed: {type(e).__name__}: {e}"}
+        if cpu and cpu["value"] and cfg["pairs_per_slot"] <= 10_000_000:
+            # BASELINE.md section 3 also asks for a 1-core row (cheap at the C1
+            # geometry): the reference arm in a child process with one OpenMP
+            # thread, since hot_sets uses every OpenMP thread whatever `workers` says
+            try:
+                env = dict(os.environ, OMP_NUM_THREADS="1", SSPD_REF_WORKERS="1")
+                out = subprocess.run([sys.executable, os.path.abspath(__file__), "--impl", "reference",
+                                      "--config", args.config, "--steps", "1", "--warmup", "1"],
+                                     env=env, capture_output=True, text=True, timeout=300)
+                r1 = json.loads(out.stdout.strip().splitlines()[-1])
+                cpu["one_core"] = {"value": r1["value"], "step_ms": r1["ms_per_step"],
+                                   "reconstruct_ms": r1["reconstruct_ms"], "cores": r1["cpu_baseline"]["cores"]}
+            except Exception as e:
+                cpu["one_core"] = f"failed: {type(e).__name__}: {e}"
 
     line = {
         "metric": metric, "value": round(value, 3), "unit": unit, "n_gpus": world,
