@@ -1128,16 +1128,32 @@ __device__ __forceinline__ uint32_t rebase(uint32_t s, uint32_t now_common, uint
   return d == 0xffffu ? 0u : now_common - d;
 }
 
+// Streams 16 bytes per source per step (every grid's stamps are 256-byte
+// aligned); a scalar loop covers a tail of n % 4.
 __global__ void __launch_bounds__(256) merge_kernel(const MergeSrc* __restrict__ srcs, uint32_t nsrc,
                                                     uint64_t n, uint32_t now_common, int take_max,
                                                     uint32_t* __restrict__ out) {
-  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
-       i += (uint64_t)gridDim.x * blockDim.x) {
-    uint32_t acc = rebase(srcs[0].p[i], now_common, srcs[0].lag);
+  auto pick = [&](uint32_t a, uint32_t v) { return take_max ? (v > a ? v : a) : (v < a ? v : a); };
+  const uint64_t nv = n / 4;
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < nv; i += stride) {
+    const uint4 a0 = ld_stream_u4(srcs[0].p + 4 * i);
+    const uint32_t l0 = srcs[0].lag;
+    uint4 acc = make_uint4(rebase(a0.x, now_common, l0), rebase(a0.y, now_common, l0), rebase(a0.z, now_common, l0),
+                           rebase(a0.w, now_common, l0));
     for (uint32_t g = 1; g < nsrc; ++g) {
-      const uint32_t v = rebase(srcs[g].p[i], now_common, srcs[g].lag);
-      acc = take_max ? (v > acc ? v : acc) : (v < acc ? v : acc);
+      const uint4 v = ld_stream_u4(srcs[g].p + 4 * i);
+      const uint32_t lg = srcs[g].lag;
+      acc.x = pick(acc.x, rebase(v.x, now_common, lg));
+      acc.y = pick(acc.y, rebase(v.y, now_common, lg));
+      acc.z = pick(acc.z, rebase(v.z, now_common, lg));
+      acc.w = pick(acc.w, rebase(v.w, now_common, lg));
     }
+    reinterpret_cast<uint4*>(out)[i] = acc;
+  }
+  for (uint64_t i = nv * 4 + (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
+    uint32_t acc = rebase(srcs[0].p[i], now_common, srcs[0].lag);
+    for (uint32_t g = 1; g < nsrc; ++g) acc = pick(acc, rebase(srcs[g].p[i], now_common, srcs[g].lag));
     out[i] = acc;
   }
 }

@@ -1628,7 +1628,7 @@ sspd_status sspd_merge(const sspd_grid* const* grids_c, uint64_t n, int policy, 
   out->h2d_bytes += (sbytes);
   {
     Prof p(out, "merge", out->geo.n_rec * n);
-    merge_kernel<<<grid_blocks(out, out->geo.n_rec, 256, 8), 256, 0, out->stream>>>(
+    merge_kernel<<<grid_blocks(out, out->geo.n_rec / 4 + 1, 256, 8), 256, 0, out->stream>>>(
         tmp.as<MergeSrc>(), (uint32_t)n, out->geo.n_rec, now_common, policy == SSPD_UNION_MIN ? 1 : 0,
         out->stamps);
   }
