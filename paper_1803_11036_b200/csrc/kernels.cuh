@@ -657,10 +657,11 @@ __global__ void __launch_bounds__(256) hist_rebuild_kernel(const uint32_t* __res
 // ---------------------------------------------------------------------------
 // HOT SETS, parallel form (two launches over all r*2^q cells).
 // hot_mark: one thread per cell decides hot (R_k >= cutoff, with R_k from
-// the per-cell counts or straight from the window ring), publishes the hot
-// bitmap word of its warp, the CTA's hot count, and the transposed bits.
+// the per-cell counts or straight from the window ring) and publishes the
+// hot bitmap word of its warp and the CTA's hot count.
 // hot_write: each CTA adds up the counts of the row's earlier chunks and
-// writes its hot columns in ascending order (rsea.cpp:65-84).
+// writes its hot columns in ascending order (rsea.cpp:65-84); the kernel
+// also builds the transposed hot bits the joins index by key.
 constexpr int kHotChunk = 1024;
 
 // Programmatic dependent launch (the reconstruction chain is launched with
