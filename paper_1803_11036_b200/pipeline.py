@@ -61,6 +61,10 @@ def run_detection(shards, q=14, r=5, delta=6, seed=0, eta=2048, mu=1.0, k=300, s
         g.candidate_cap = candidate_cap
         g.track_window(k)
     reports = []
+    # union-min + leveled pipelines like the C++ run_detection: a slot's
+    # reconstruction is queued and collected after the next slot's scan
+    pipelined = union and not recursive and candidate_cap <= (1 << 26)
+    pending = None
     for slot in range(n_slots):
         parts = [s[so == slot][:, 1:] for s, so in zip(shards, slot_of)]
         if union:
@@ -74,11 +78,20 @@ def run_detection(shards, q=14, r=5, delta=6, seed=0, eta=2048, mu=1.0, k=300, s
                     g.scan_batch(p)
             target = merge_rseas(nodes, PAPER_MAX)
             target.candidate_cap = candidate_cap
+        if pending is not None:
+            reports.append((pending, target.reconstruct_collect()))
+            pending = None
         if probe is not None:
             probe(slot, target)
-        dets = (target.reconstruct_recursive(k, theta) if recursive
-                else target.reconstruct_leveled(k, theta))
-        reports.append((slot, dets))
+        if pipelined:
+            target.reconstruct_async(k, theta)
+            pending = slot
+        else:
+            dets = (target.reconstruct_recursive(k, theta) if recursive
+                    else target.reconstruct_leveled(k, theta))
+            reports.append((slot, dets))
         for g in nodes:
             g.advance_slot()
+    if pending is not None:
+        reports.append((pending, nodes[0].reconstruct_collect()))
     return reports
