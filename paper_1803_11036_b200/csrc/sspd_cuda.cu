@@ -21,7 +21,7 @@
 #include "synth.h"
 
 #ifndef SSPD_SCAN_BLOCKS_PER_SM
-#define SSPD_SCAN_BLOCKS_PER_SM 8
+#define SSPD_SCAN_BLOCKS_PER_SM 4  // one resident wave (profiles/r01_ab_scan_grid.md)
 #endif
 
 #include <omp.h>
