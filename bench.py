@@ -319,9 +319,12 @@ def main():
     merge_used = args.merge
     if world > 1 and args.merge != "stamps":
         cap = min(cfg["pairs_per_slot"], 32 << 20)
+        # a router pushes each of its new pairs at most once per owner, plus the
+        # padding of its warps' last list blocks (kernels.cuh list_pad) per launch
+        shard_cap = cfg["pairs_per_slot"] + 40 * torch.cuda.get_device_properties(local).multi_processor_count * 4 * 8 * 64
         if args.merge == "auto":
             try:  # cells sharded among the routers; pair lists if symmetric memory is missing
-                PD.prepare(g, PD.SHARD, region_cap=cfg["pairs_per_slot"])
+                PD.prepare(g, PD.SHARD, region_cap=shard_cap)
                 merge_used = "shard"
             except Exception as e:  # symmetric memory unavailable: lists after the scan
                 print(f"[bench] shard exchange unavailable ({type(e).__name__}: {e}); using pairs",
@@ -330,7 +333,7 @@ def main():
                 merge_used = "pairs"
         else:
             PD.prepare(g, {"pairs": PD.PAIRS, "push": PD.PUSH, "bitmap": PD.BITMAP, "shard": PD.SHARD}[args.merge],
-                       region_cap=cfg["pairs_per_slot"] if args.merge == "shard" else cap)
+                       region_cap=shard_cap if args.merge == "shard" else cap)
     cdf = torch.from_numpy(zipf_cdf(L, cfg).view(np.int64)).to(f"cuda:{dev}")
     sp = synth_params(cfg, rank, world)
     n_local = cfg["pairs_per_slot"]

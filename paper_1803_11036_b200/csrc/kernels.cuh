@@ -331,6 +331,69 @@ __device__ __forceinline__ void stamp_pair(const ScanTables& t, const Geo& geo, 
 // falls back to an all-gather for that slot.
 // Each thread takes 4 pairs per iteration and issues their 4 first probes
 // together before resolving any (the probes are the latency chain).
+// Append-only pair lists (the exchange list, peer inboxes) grown in blocks:
+// a warp reserves kListBlock slots with ONE atomic and fills them over
+// several iterations, instead of one atomic per warp per iteration on a
+// counter every warp of the GPU shares (that contention cost 13 vs 3.5 ms
+// per C2 slot, profiles/r01_ab_list_blocks.md).  The warp's last block is
+// padded with copies of its last pair, so a list is dense up to its counter;
+// a repeated pair is harmless to every consumer (stamping is idempotent).
+constexpr uint32_t kListBlock = 64;
+
+struct ListState {
+  unsigned long long base;  // first slot of the warp's current block
+  uint32_t fill;            // slots used in it (kListBlock: no block yet)
+  uint32_t unused;
+  uint2 last;               // the last pair appended (the padding value)
+};
+
+__device__ __forceinline__ void list_init(ListState& st, uint32_t lane) {
+  if (lane == 0) {
+    st.base = 0;
+    st.fill = kListBlock;
+  }
+  __syncwarp();
+}
+
+// The lanes of `m` with `mine` set append `pr`; returns this lane's slot
+// (meaningful only when `mine`).  Call with the same `m` on every lane in it.
+__device__ __forceinline__ uint64_t list_append(ListState& st, unsigned long long* counter, unsigned m, bool mine,
+                                                uint2 pr, uint32_t lane) {
+  const unsigned b = __ballot_sync(m, mine);
+  if (!b) return 0;
+  const uint32_t cnt = __popc(b), rank = __popc(b & ((1u << lane) - 1u));
+  const int leader = __ffs(m) - 1;
+  const uint32_t fill = st.fill;
+  const unsigned long long base = st.base;
+  const uint32_t room = kListBlock - fill;
+  unsigned long long nb = 0;
+  if (cnt > room) {
+    if ((int)lane == leader) nb = atomicAdd(counter, (unsigned long long)kListBlock);
+    nb = __shfl_sync(m, nb, leader);
+  }
+  const uint64_t pos = rank < room ? base + fill + rank : nb + (rank - room);
+  __syncwarp(m);
+  if ((int)lane == leader) {
+    if (cnt > room) {
+      st.base = nb;
+      st.fill = cnt - room;
+    } else {
+      st.fill = fill + cnt;
+    }
+  }
+  if ((int)lane == 31 - __clz(b)) st.last = pr;
+  __syncwarp(m);
+  return pos;
+}
+
+// After the loop (all 32 lanes): the unused tail of the warp's block, padded.
+template <class W>
+__device__ __forceinline__ void list_pad(ListState& st, uint32_t lane, W&& write) {
+  __syncwarp();
+  const uint32_t fill = st.fill;
+  for (uint32_t i = fill + lane; i < kListBlock; i += 32) write(st.base + i, st.last);
+}
+
 struct PushArgs {
   uint2* const* peers;  // device array of `world` inbox pointers (peer-mapped)
   uint32_t world, rank;
@@ -362,9 +425,12 @@ __global__ void __launch_bounds__(256, SSPD_DEDUP_MINB) scan_dedup_kernel(const 
                                                          unsigned long long* __restrict__ out_count,
                                                          PushArgs push = PushArgs{}) {
   __shared__ ScanTables t;
+  __shared__ ListState s_list[8];  // EXPORT: one list state per warp (blockDim 256)
   load_scan_tables(t, tabs);
   const uint32_t now_slot = HIST ? now % K : 0;
   const uint32_t lane = threadIdx.x & 31;
+  ListState& wl = s_list[threadIdx.x >> 5];
+  if (EXPORT) list_init(wl, lane);
   const uint64_t tid = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
   const uint64_t nthreads = (uint64_t)gridDim.x * blockDim.x;
   const bool vec = (reinterpret_cast<uintptr_t>(pairs) & 15u) == 0;
@@ -409,20 +475,13 @@ __global__ void __launch_bounds__(256, SSPD_DEDUP_MINB) scan_dedup_kernel(const 
 #pragma unroll
       for (int u = 0; u < P; ++u) {
         const unsigned m = __activemask();
-        const unsigned b = __ballot_sync(m, fresh[u]);
-        if (b) {
-          const int leader = __ffs(b) - 1;
-          unsigned long long base = 0;
-          if ((int)lane == leader) base = atomicAdd(out_count, (unsigned long long)__popc(b));
-          base = __shfl_sync(m, base, leader);
-          if (fresh[u]) {
-            const uint64_t pos = base + __popc(b & ((1u << lane) - 1u));
-            const uint2 pr = make_uint2(c[u], o[u]);
-            out_pairs[pos] = pr;
-            if (PUSH && pos < push.region_cap)
-              for (uint32_t p = 0; p < push.world; ++p)
-                if (p != push.rank) push.peers[p][(uint64_t)push.rank * push.region_cap + pos] = pr;
-          }
+        const uint2 pr = make_uint2(c[u], o[u]);
+        const uint64_t pos = list_append(wl, out_count, m, fresh[u], pr, lane);
+        if (fresh[u]) {
+          out_pairs[pos] = pr;
+          if (PUSH && pos < push.region_cap)
+            for (uint32_t p = 0; p < push.world; ++p)
+              if (p != push.rank) push.peers[p][(uint64_t)push.rank * push.region_cap + pos] = pr;
         }
       }
     }
@@ -460,6 +519,13 @@ __global__ void __launch_bounds__(256, SSPD_DEDUP_MINB) scan_dedup_kernel(const 
     for (int u = 0; u < P; ++u)
       if (fresh[u]) stamp_pair<H1MODE, HIST, BITS>(t, geo, c[u], o[u], stamps, now, now_slot, hist, K, touched);
   }
+  if (EXPORT)
+    list_pad(wl, lane, [&](uint64_t pos, uint2 pr) {
+      out_pairs[pos] = pr;
+      if (PUSH && pos < push.region_cap)
+        for (uint32_t p = 0; p < push.world; ++p)
+          if (p != push.rank) push.peers[p][(uint64_t)push.rank * push.region_cap + pos] = pr;
+    });
   if (PUSH) __threadfence_system();  // peer stores visible before the exchange's barrier
 }
 
@@ -1206,14 +1272,21 @@ __global__ void __launch_bounds__(256) scan_shard_kernel(const uint32_t* __restr
                                                          uint32_t* __restrict__ stamps, uint32_t now,
                                                          uint32_t* __restrict__ hist, uint32_t K, ShardArgs sh) {
   __shared__ ScanTables t;
+  __shared__ ListState s_lists[8][PUSH ? 32 : 1];  // per warp (blockDim 256), per owner
   load_scan_tables(t, tabs);
   const uint32_t now_slot = HIST ? now % K : 0;
   const uint32_t lane = threadIdx.x & 31;
+  ListState* wl = s_lists[threadIdx.x >> 5];
+  if (PUSH)
+    for (uint32_t d = 0; d < sh.world; ++d) list_init(wl[d], lane);
   constexpr int P = 2;
   const uint64_t tid = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
   const uint64_t nthreads = (uint64_t)gridDim.x * blockDim.x;
   const bool vec = (reinterpret_cast<uintptr_t>(pairs) & 15u) == 0;
   const uint64_t ngroups = (n + P - 1) / P;
+  auto deliver = [&](uint32_t d, uint64_t pos, uint2 pr) {
+    if (pos < sh.region_cap) sh.inbox[d][(uint64_t)sh.rank * sh.region_cap + pos] = pr;
+  };
   for (uint64_t g = tid; g < ngroups; g += nthreads) {
     uint32_t c[P], o[P];
     bool fresh[P];
@@ -1276,27 +1349,23 @@ __global__ void __launch_bounds__(256) scan_shard_kernel(const uint32_t* __restr
       }
     }
     if (PUSH) {
-      // one warp-aggregated reservation per destination
+      // block-reserved list per owner (list_append)
 #pragma unroll
       for (int u = 0; u < P; ++u) {
         for (uint32_t d = 0; d < sh.world; ++d) {
           const unsigned m = __activemask();
           const bool mine = (dmask[u] >> d) & 1u;
-          const unsigned b = __ballot_sync(m, mine);
-          if (!b) continue;
-          const int leader = __ffs(b) - 1;
-          unsigned long long base = 0;
-          if ((int)lane == leader) base = atomicAdd(sh.sent + d, (unsigned long long)__popc(b));
-          base = __shfl_sync(m, base, leader);
-          if (mine) {
-            const uint64_t pos = base + __popc(b & ((1u << lane) - 1u));
-            if (pos < sh.region_cap) sh.inbox[d][(uint64_t)sh.rank * sh.region_cap + pos] = make_uint2(c[u], o[u]);
-          }
+          const uint2 pr = make_uint2(c[u], o[u]);
+          const uint64_t pos = list_append(wl[d], sh.sent + d, m, mine, pr, lane);
+          if (mine) deliver(d, pos, pr);
         }
       }
     }
   }
-  if (PUSH) __threadfence_system();  // peer stores visible before the exchange's barrier
+  if (PUSH) {
+    for (uint32_t d = 0; d < sh.world; ++d) list_pad(wl[d], lane, [&](uint64_t pos, uint2 pr) { deliver(d, pos, pr); });
+    __threadfence_system();  // peer stores visible before the exchange's barrier
+  }
 }
 
 // Per survivor and 32-bucket word: the AND over the survivor's owned rows of

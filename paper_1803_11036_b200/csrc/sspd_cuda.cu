@@ -174,6 +174,7 @@ struct sspd_grid {
   DevBuf newpairs;              // this slot's distinct pairs (export_pairs)
   DevBuf newpairs_count;        // u64 on device
   uint64_t scanned_in_slot = 0; // pairs scanned since the last advance (list capacity bound)
+  uint64_t list_pad_slots = 0;  // bound on the list blocks' padding since the last advance
   PushArgs push{};              // fused exchange: peer inboxes (export mode 3)
   void* pinned_small = nullptr;  // 4 KB pinned scratch for counters
   bool profiling = false;
@@ -806,8 +807,12 @@ sspd_status sspd_scan(sspd_grid* g, const uint32_t* pairs, uint64_t n, int pairs
   const bool hist = (direct || dedup) && g->K && g->hist_valid;
   const bool bits = (direct || dedup) && g->record_touched;
   if (g->export_pairs) {
-    // new pairs <= pairs scanned this slot: grow the list, keeping its prefix
-    const uint64_t need = (g->scanned_in_slot + n) * 8;
+    // new pairs <= pairs scanned this slot, plus each launch's padding of
+    // its warps' last list blocks (kernels.cuh list_pad): grow the list,
+    // keeping its prefix
+    const uint64_t launches = pairs_on_device ? 1 : (n + (4ull << 20) - 1) / (256ull << 10);
+    g->list_pad_slots += launches * (uint64_t)sm_count(g->device) * SSPD_SCAN_BLOCKS_PER_SM * 8 * kListBlock;
+    const uint64_t need = (g->scanned_in_slot + n + g->list_pad_slots) * 8;
     if (g->newpairs.bytes < need) {
       DevBuf bigger;
       if (bigger.ensure(std::max<uint64_t>(need, g->newpairs.bytes * 2)) != cudaSuccess)
@@ -1023,6 +1028,7 @@ sspd_status sspd_advance(sspd_grid* g, uint32_t slots) {
   if (g->newpairs_count.p) CU(cudaMemsetAsync(g->newpairs_count.p, 0, 8, g->stream));
   if (g->shard) CU(cudaMemsetAsync(g->shard_sent.p, 0, 32 * 8, g->stream));
   g->scanned_in_slot = 0;
+  g->list_pad_slots = 0;
   for (uint32_t i = 0; i < slots; ++i) {
     if (g->now >= 0x7fffffffu) return fail(SSPD_OUT_OF_RANGE, "advance_slot: slice counter exhausted");
     ++g->now;
