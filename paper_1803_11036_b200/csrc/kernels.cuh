@@ -1255,16 +1255,18 @@ struct ShardArgs {
   uint64_t region_cap;            // pairs per (destination, source) region
 };
 
+// cell * world < 2^22 * 32: the 32-bit division is exact (and cheap next to
+// a 64-bit one)
 __device__ __forceinline__ uint32_t shard_owner(uint32_t cell, uint32_t ncells, uint32_t world) {
-  return (uint32_t)(((uint64_t)cell * world) / ncells);
+  return (cell * world) / ncells;
 }
 
 // PUSH = 1: the router's own pairs -- those it already saw this slot are
 // skipped by the pair set, as in dedup mode; the rest stamp owned cells and
-// are pushed to the other owners.  PUSH = 0: pairs received from peers stamp
-// owned cells directly: stamping is idempotent (a repeat finds `now` and
-// leaves the ring alone), so the pair set only has to hold the router's own
-// distinct pairs.
+// are pushed to the other owners.  PUSH = 0: pairs received from peers go
+// through the same pair set (a pair several routers saw arrives several
+// times; at N=8 on C2 a router receives ~3 copies per distinct pair), then
+// stamp owned cells only.
 template <int H1MODE, int HIST, int PUSH>
 __global__ void __launch_bounds__(256) scan_shard_kernel(const uint32_t* __restrict__ pairs, uint64_t n,
                                                          const HashTabs* __restrict__ tabs, Geo geo,
@@ -1303,7 +1305,7 @@ __global__ void __launch_bounds__(256) scan_shard_kernel(const uint32_t* __restr
         o[u] = fresh[u] ? pairs[2 * (p0 + u) + 1] : 0u;
       }
     }
-    if (PUSH) {
+    {
       uint64_t key[P], h[P];
       unsigned long long v[P];
 #pragma unroll

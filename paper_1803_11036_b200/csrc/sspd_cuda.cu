@@ -484,7 +484,9 @@ sspd_status ensure_pairset_locked(sspd_grid* g) {
   // default 2^25 = 256 MiB: ~10M distinct pairs per C2 slot at load 0.3;
   // measured 2^22..2^25 = 4.23..3.90 ms/slot, profiles/r01_ab_pairset.txt).
   // Pinning it in L2 (SSPD_L2_PERSIST=<MiB>) measured slower.
-  uint32_t lg = 25;
+  // sharded routers also keep what peers push to them (~2.4x their own new
+  // pairs at N=8 on C2): twice the entries from 4 routers up
+  uint32_t lg = g->shard && g->shard_args.world >= 4 ? 26 : 25;
   if (const char* e = std::getenv("SSPD_PAIRSET_LOG2")) lg = std::min(30, std::max(16, std::atoi(e)));
   const uint64_t entries = 1ull << lg;
   if (g->pairset.ensure(entries * 8) != cudaSuccess)
@@ -1467,6 +1469,7 @@ sspd_status sspd_shard_receive(sspd_grid* g, const uint32_t* dev_pairs, uint64_t
   sspd_status s = ensure_pairset_locked(g);
   if (s) return s;
   g->pristine = false;
+  g->pairset_dirty = true;
   const bool pow2 = (g->eta & (g->eta - 1)) == 0 && g->eta <= (1u << 31);
   const bool hist = g->K && g->hist_valid;
   const unsigned blocks = grid_blocks(g, (n + 3) / 4, 256, SSPD_SCAN_BLOCKS_PER_SM);
