@@ -233,8 +233,11 @@ sspd_status sspd_set_exchange(sspd_grid* g, int mode);
  * world <= 1 disables. */
 sspd_status sspd_set_push(sspd_grid* g, void* dev_peer_ptrs, uint32_t world, uint32_t rank,
                           uint64_t region_cap);
-/* This slot's distinct pairs (exchange mode 2): device pointer to `count`
- * interleaved (cip, oip) pairs, valid until the next advance. */
+/* This slot's new pairs (exchange mode 2): device pointer to `count`
+ * interleaved (cip, oip) pairs, valid until the next advance.  Every pair new
+ * to the grid this slot appears at least once; the list is grown in blocks
+ * reserved per warp, whose unused tails hold copies of listed pairs (a
+ * repeated pair changes nothing where it is applied). */
 sspd_status sspd_grid_new_pairs(sspd_grid* g, uint32_t** dev_pairs, uint64_t* count);
 /* Scan strategy: mode 0 = deferred bitmap, 1 = direct stamping, 2 = direct
  * behind a per-slot set of seen pairs, 3 = as 2 after partitioning large
