@@ -1354,8 +1354,10 @@ __global__ void __launch_bounds__(256) scan_shard_kernel(const uint32_t* __restr
       // block-reserved list per owner (list_append)
 #pragma unroll
       for (int u = 0; u < P; ++u) {
-        for (uint32_t d = 0; d < sh.world; ++d) {
-          const unsigned m = __activemask();
+        const unsigned m = __activemask();
+        // only the owners some lane of the warp sends to
+        for (unsigned todo = __reduce_or_sync(m, dmask[u]); todo; todo &= todo - 1) {
+          const uint32_t d = __ffs(todo) - 1;
           const bool mine = (dmask[u] >> d) & 1u;
           const uint2 pr = make_uint2(c[u], o[u]);
           const uint64_t pos = list_append(wl[d], sh.sent + d, m, mine, pr, lane);
