@@ -265,6 +265,8 @@ def main():
         cfg["k"] = args.window
     rank = env_int("RANK", 0)
     world = env_int("WORLD_SIZE", 1)
+    if world > 1 and args.stamp_width != 32 and args.impl == "ours":
+        ap.error("--stamp-width 8/16 is single-router only: the router exchanges need full stamps")
     local = env_int("LOCAL_RANK", 0)
     unit = "Mpackets/s"
     metric = "scan+reconstruct throughput, Mpackets/s (Gb/s at 800 B/pkt in gbps_800B)"
