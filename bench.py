@@ -246,6 +246,9 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--window", type=int, default=0, help="override the window k (C4 sweeps)")
+    ap.add_argument("--theta", type=float, default=0.0, help="override theta (C5 sweeps)")
+    ap.add_argument("--eta", type=int, default=0, help="override eta, buckets per estimator (C5 sweeps)")
+    ap.add_argument("--q", type=int, default=0, help="override q, log2 columns per row (C5 sweeps)")
     ap.add_argument("--merge", default="auto", choices=["auto", "pairs", "push", "bitmap", "stamps", "shard"],
                     help="router exchange at N>1 (auto = shard, else pairs if symmetric memory is "
                          "unavailable): distinct pairs pushed over NVLink during the scan (push), the "
@@ -263,6 +266,10 @@ def main():
     cfg = dict(CONFIGS[args.config])
     if args.window:
         cfg["k"] = args.window
+    for key in ("theta", "eta", "q"):
+        if getattr(args, key):
+            cfg[key] = getattr(args, key)
+            cfg["workload"] += f"; {key} overridden to {getattr(args, key):g}"
     rank = env_int("RANK", 0)
     world = env_int("WORLD_SIZE", 1)
     if world > 1 and args.stamp_width != 32 and args.impl == "ours":
