@@ -483,7 +483,7 @@ sspd_status ensure_pairset_locked(sspd_grid* g) {
   // 8 B per exact key, a power of two of entries (SSPD_PAIRSET_LOG2,
   // default 2^25 = 256 MiB: ~10M distinct pairs per C2 slot at load 0.3;
   // measured 2^22..2^25 = 4.23..3.90 ms/slot, profiles/r01_ab_pairset.txt).
-  // Pinning it in L2 (SSPD_L2_PERSIST=<MiB>) measured slower.
+  // Pinning it in L2 with an access-policy window measured slower (same file).
   // sharded routers also keep what peers push to them (~2.4x their own new
   // pairs at N=8 on C2): twice the entries from 4 routers up
   uint32_t lg = g->shard && g->shard_args.world >= 4 ? 26 : 25;
@@ -493,20 +493,6 @@ sspd_status ensure_pairset_locked(sspd_grid* g) {
     return fail(SSPD_CUDA_ERROR, "CUDA error: out of memory (pair set)");
   g->pairset_mask = entries - 1;
   CU(cudaMemsetAsync(g->pairset.p, 0xff, entries * 8, g->stream));
-  if (const char* e = std::getenv("SSPD_L2_PERSIST"); e && std::atoi(e) > 0) {
-    cudaDeviceProp prop;
-    CU(cudaGetDeviceProperties(&prop, g->device));
-    const size_t want = std::min<size_t>((size_t)std::atoi(e) << 20, prop.persistingL2CacheMaxSize);
-    CU(cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, want));
-    cudaStreamAttrValue attr{};
-    attr.accessPolicyWindow.base_ptr = g->pairset.p;
-    attr.accessPolicyWindow.num_bytes = std::min<size_t>(entries * 8, prop.accessPolicyMaxWindowSize);
-    attr.accessPolicyWindow.hitRatio =
-        std::min(1.0f, (float)want / (float)attr.accessPolicyWindow.num_bytes);
-    attr.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
-    attr.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
-    CU(cudaStreamSetAttribute(g->stream, cudaStreamAttributeAccessPolicyWindow, &attr));
-  }
   return SSPD_OK;
 }
 
