@@ -199,6 +199,16 @@ sspd_status sspd_track_window(sspd_grid* g, uint32_t k_max);
  * grids.  world = 0 turns sharding off. */
 sspd_status sspd_set_shard(sspd_grid* g, void* dev_inbox_ptrs, uint32_t world, uint32_t rank,
                            uint64_t region_cap);
+/* Relayed sharding (two hops): the scan pushes each new pair only to its
+ * pair owner (a hash of the pair mod world) through inbox table A; the pair
+ * owner runs sspd_shard_relay over what it received (all sources, itself
+ * included), which dedups the routers' union for its share, stamps its own
+ * cells and pushes each pair once to the other cell owners through table B;
+ * cell owners then sspd_shard_receive what arrived (no second dedup needed).
+ * sspd_shard_sent's counters: [0, 32) hop 1, [32, 64) hop 2. */
+sspd_status sspd_set_shard_relay(sspd_grid* g, void* dev_inbox_a, void* dev_inbox_b, uint32_t world,
+                                 uint32_t rank, uint64_t region_cap);
+sspd_status sspd_shard_relay(sspd_grid* g, const uint32_t* dev_pairs, uint64_t n);
 sspd_status sspd_shard_sent(sspd_grid* g, uint64_t** dev_counts);
 sspd_status sspd_shard_receive(sspd_grid* g, const uint32_t* dev_pairs, uint64_t n);
 sspd_status sspd_shard_hot(sspd_grid* g, uint32_t k, uint64_t cutoff, uint32_t** dev_hot_words,

@@ -1267,19 +1267,34 @@ __device__ __forceinline__ uint32_t shard_owner(uint32_t cell, uint32_t ncells, 
 // through the same pair set (a pair several routers saw arrives several
 // times; at N=8 on C2 a router receives ~3 copies per distinct pair), then
 // stamp owned cells only.
+// Relayed routers (two hops, ShardExchange(relay=True)): own pairs go first
+// to a pair owner (MODE 2: pair set, then one push per new pair, no
+// stamping), which dedups the union of the routers' pairs for its share and
+// relays each once to the cell owners (MODE 1 over the received lists, with
+// a second pair set); cell owners stamp what arrives (MODE 4: no pair set --
+// every pair reaches them once).
+enum ShardMode { kShardRecv = 0, kShardOwn = 1, kShardToPairOwner = 2, kShardRecvOnce = 4 };
+
+__device__ __forceinline__ uint32_t pair_owner(uint64_t h, uint32_t world) {
+  return (uint32_t)(h >> 32) % world;
+}
+
 template <int H1MODE, int HIST, int PUSH>
 __global__ void __launch_bounds__(256) scan_shard_kernel(const uint32_t* __restrict__ pairs, uint64_t n,
                                                          const HashTabs* __restrict__ tabs, Geo geo,
                                                          unsigned long long* __restrict__ table, uint64_t table_mask,
                                                          uint32_t* __restrict__ stamps, uint32_t now,
                                                          uint32_t* __restrict__ hist, uint32_t K, ShardArgs sh) {
+  constexpr bool kPushes = PUSH == kShardOwn || PUSH == kShardToPairOwner;
+  constexpr bool kStamps = PUSH != kShardToPairOwner;
+  constexpr bool kDedup = PUSH != kShardRecvOnce;
   __shared__ ScanTables t;
-  __shared__ ListState s_lists[8][PUSH ? 32 : 1];  // per warp (blockDim 256), per owner
+  __shared__ ListState s_lists[8][kPushes ? 32 : 1];  // per warp (blockDim 256), per owner
   load_scan_tables(t, tabs);
   const uint32_t now_slot = HIST ? now % K : 0;
   const uint32_t lane = threadIdx.x & 31;
   ListState* wl = s_lists[threadIdx.x >> 5];
-  if (PUSH)
+  if (kPushes)
     for (uint32_t d = 0; d < sh.world; ++d) list_init(wl[d], lane);
   constexpr int P = 2;
   const uint64_t tid = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -1305,7 +1320,8 @@ __global__ void __launch_bounds__(256) scan_shard_kernel(const uint32_t* __restr
         o[u] = fresh[u] ? pairs[2 * (p0 + u) + 1] : 0u;
       }
     }
-    {
+    uint32_t dmask[P] = {0u, 0u};
+    if (kDedup) {
       uint64_t key[P], h[P];
       unsigned long long v[P];
 #pragma unroll
@@ -1315,12 +1331,14 @@ __global__ void __launch_bounds__(256) scan_shard_kernel(const uint32_t* __restr
         v[u] = fresh[u] ? __ldca(table + pair_slot(h[u], 0, table_mask)) : 0ull;
       }
 #pragma unroll
-      for (int u = 0; u < P; ++u) fresh[u] = fresh[u] && pair_resolve(table, table_mask, key[u], h[u], v[u]);
+      for (int u = 0; u < P; ++u) {
+        fresh[u] = fresh[u] && pair_resolve(table, table_mask, key[u], h[u], v[u]);
+        if (PUSH == kShardToPairOwner && fresh[u]) dmask[u] = 1u << pair_owner(h[u], sh.world);
+      }
     }
-    uint32_t dmask[P] = {0u, 0u};
 #pragma unroll
     for (int u = 0; u < P; ++u) {
-      if (!fresh[u]) continue;
+      if (!kStamps || !fresh[u]) continue;
       uint32_t bucket, col0;
       hash_pair<H1MODE>(t, geo, c[u], o[u], bucket, col0);
       for (uint32_t r0 = 0; r0 < geo.r; r0 += 8) {
@@ -1350,7 +1368,7 @@ __global__ void __launch_bounds__(256) scan_shard_kernel(const uint32_t* __restr
         }
       }
     }
-    if (PUSH) {
+    if (kPushes) {
       // block-reserved list per owner (list_append)
 #pragma unroll
       for (int u = 0; u < P; ++u) {
@@ -1366,7 +1384,7 @@ __global__ void __launch_bounds__(256) scan_shard_kernel(const uint32_t* __restr
       }
     }
   }
-  if (PUSH) {
+  if (kPushes) {
     for (uint32_t d = 0; d < sh.world; ++d) list_pad(wl[d], lane, [&](uint64_t pos, uint2 pr) { deliver(d, pos, pr); });
     __threadfence_system();  // peer stores visible before the exchange's barrier
   }

@@ -156,8 +156,12 @@ struct sspd_grid {
   DevBuf bin_counts, binned;    // binned dedup: per-(region, CTA) counts, partitioned pairs
   DevBuf pairset;               // dedup mode: per-slot set of seen (cip, oip) pairs
   bool shard = false;           // sharded routers (sspd_set_shard): own a 1/world slice of the cells
-  ShardArgs shard_args{};
-  DevBuf shard_sent;            // world u64: pairs pushed to each owner this slot
+  ShardArgs shard_args{};       // one hop: to the cell owners; relayed: hop 1, to the pair owners
+  bool relay = false;           // two hops (sspd_set_shard_relay)
+  ShardArgs shard_b{};          // relayed: hop 2, pair owner -> cell owners
+  DevBuf relayset;              // relayed: the pair owner's per-slot set of pairs it relayed
+  bool relayset_dirty = false;
+  DevBuf shard_sent;            // 2 x 32 u64: pairs pushed to each owner this slot (hop 1, hop 2)
   DevBuf masks;                 // sharded reconstruction: per-survivor bucket masks
   DevBuf* last_tuples = nullptr;  // buffer holding the last reconstruction's r-tuples
   // sspd_reconstruct_async: one queued reconstruction awaiting collect
@@ -828,13 +832,16 @@ sspd_status sspd_scan(sspd_grid* g, const uint32_t* pairs, uint64_t n, int pairs
     if (g->shard) {  // own pairs of a sharded router: stamp owned cells, push to the other owners
       auto* tb = g->pairset.as<unsigned long long>();
       const bool hs = g->K && g->hist_valid;
-#define SSPD_SHARD(H1, HI)                                                                                    \
-  scan_shard_kernel<H1, HI, 1><<<blocks, 256, 0, g->stream>>>(dp, cnt, g->d_tabs, g->geo, tb, g->pairset_mask, \
-                                                              g->stamps, g->now, g->hist, g->K, g->shard_args)
-      if (pow2 && hs) SSPD_SHARD(0, 1);
-      else if (pow2) SSPD_SHARD(0, 0);
-      else if (hs) SSPD_SHARD(1, 1);
-      else SSPD_SHARD(1, 0);
+#define SSPD_SHARD(H1, HI, MODE)                                                                                 \
+  scan_shard_kernel<H1, HI, MODE><<<blocks, 256, 0, g->stream>>>(dp, cnt, g->d_tabs, g->geo, tb, g->pairset_mask, \
+                                                                 g->stamps, g->now, g->hist, g->K, g->shard_args)
+      if (g->relay) {  // hop 1: new pairs to their pair owners, nothing stamped yet
+        if (pow2) SSPD_SHARD(0, 0, kShardToPairOwner);
+        else SSPD_SHARD(1, 0, kShardToPairOwner);
+      } else if (pow2 && hs) SSPD_SHARD(0, 1, kShardOwn);
+      else if (pow2) SSPD_SHARD(0, 0, kShardOwn);
+      else if (hs) SSPD_SHARD(1, 1, kShardOwn);
+      else SSPD_SHARD(1, 0, kShardOwn);
 #undef SSPD_SHARD
       g->pairset_dirty = true;
       return;
@@ -1014,7 +1021,11 @@ sspd_status sspd_advance(sspd_grid* g, uint32_t slots) {
   s = pairset_reset_locked(g);  // the pair set only deduplicates within a slot
   if (s) return s;
   if (g->newpairs_count.p) CU(cudaMemsetAsync(g->newpairs_count.p, 0, 8, g->stream));
-  if (g->shard) CU(cudaMemsetAsync(g->shard_sent.p, 0, 32 * 8, g->stream));
+  if (g->shard) CU(cudaMemsetAsync(g->shard_sent.p, 0, 64 * 8, g->stream));
+  if (g->relayset_dirty) {
+    CU(cudaMemsetAsync(g->relayset.p, 0xff, g->relayset.bytes, g->stream));
+    g->relayset_dirty = false;
+  }
   g->scanned_in_slot = 0;
   g->list_pad_slots = 0;
   for (uint32_t i = 0; i < slots; ++i) {
@@ -1432,11 +1443,24 @@ sspd_status sspd_set_shard(sspd_grid* g, void* dev_inbox_ptrs, uint32_t world, u
     return fail(SSPD_INVALID_ARGUMENT, "set_shard: turn the other exchange hooks off first");
   sspd_status s = commit_locked(g);
   if (s) return s;
-  if (g->shard_sent.ensure(32 * 8) != cudaSuccess) return fail(SSPD_CUDA_ERROR, "CUDA error: out of memory");
-  CU(cudaMemsetAsync(g->shard_sent.p, 0, 32 * 8, g->stream));
+  if (g->shard_sent.ensure(64 * 8) != cudaSuccess) return fail(SSPD_CUDA_ERROR, "CUDA error: out of memory");
+  CU(cudaMemsetAsync(g->shard_sent.p, 0, 64 * 8, g->stream));
   g->shard_args = ShardArgs{static_cast<uint2* const*>(dev_inbox_ptrs), g->shard_sent.as<unsigned long long>(),
                             world, rank, region_cap};
   g->shard = true;
+  g->relay = false;
+  return SSPD_OK;
+}
+
+sspd_status sspd_set_shard_relay(sspd_grid* g, void* dev_inbox_a, void* dev_inbox_b, uint32_t world, uint32_t rank,
+                                 uint64_t region_cap) {
+  sspd_status s = sspd_set_shard(g, dev_inbox_a, world, rank, region_cap);
+  if (s || world == 0) return s;
+  std::lock_guard<std::mutex> lk(g->mu);
+  if (world > 1 && !dev_inbox_b) return fail(SSPD_INVALID_ARGUMENT, "set_shard_relay: need both inbox tables");
+  g->shard_b = ShardArgs{static_cast<uint2* const*>(dev_inbox_b), g->shard_sent.as<unsigned long long>() + 32, world,
+                         rank, region_cap};
+  g->relay = true;
   return SSPD_OK;
 }
 
@@ -1461,14 +1485,51 @@ sspd_status sspd_shard_receive(sspd_grid* g, const uint32_t* dev_pairs, uint64_t
   const unsigned blocks = grid_blocks(g, (n + 3) / 4, 256, SSPD_SCAN_BLOCKS_PER_SM);
   auto* tb = g->pairset.as<unsigned long long>();
   Prof p(g, "scan", n);
-#define SSPD_SHARD(H1, HI)                                                                                  \
-  scan_shard_kernel<H1, HI, 0><<<blocks, 256, 0, g->stream>>>(dev_pairs, n, g->d_tabs, g->geo, tb, g->pairset_mask, \
-                                                              g->stamps, g->now, g->hist, g->K, g->shard_args)
-  if (pow2 && hist) SSPD_SHARD(0, 1);
-  else if (pow2) SSPD_SHARD(0, 0);
-  else if (hist) SSPD_SHARD(1, 1);
-  else SSPD_SHARD(1, 0);
+#define SSPD_SHARD(H1, HI, MODE)                                                                             \
+  scan_shard_kernel<H1, HI, MODE><<<blocks, 256, 0, g->stream>>>(dev_pairs, n, g->d_tabs, g->geo, tb,          \
+                                                                 g->pairset_mask, g->stamps, g->now, g->hist, g->K, \
+                                                                 g->shard_args)
+  if (g->relay) {  // hop 2: each pair arrives once from its pair owner
+    if (pow2 && hist) SSPD_SHARD(0, 1, kShardRecvOnce);
+    else if (pow2) SSPD_SHARD(0, 0, kShardRecvOnce);
+    else if (hist) SSPD_SHARD(1, 1, kShardRecvOnce);
+    else SSPD_SHARD(1, 0, kShardRecvOnce);
+  } else if (pow2 && hist) SSPD_SHARD(0, 1, kShardRecv);
+  else if (pow2) SSPD_SHARD(0, 0, kShardRecv);
+  else if (hist) SSPD_SHARD(1, 1, kShardRecv);
+  else SSPD_SHARD(1, 0, kShardRecv);
 #undef SSPD_SHARD
+  return check_launch();
+}
+
+sspd_status sspd_shard_relay(sspd_grid* g, const uint32_t* dev_pairs, uint64_t n) {
+  if (n == 0) return SSPD_OK;
+  std::lock_guard<std::mutex> lk(g->mu);
+  DeviceGuard dg(g->device);
+  if (!g->shard || !g->relay) return fail(SSPD_INVALID_ARGUMENT, "shard_relay: not a relayed sharded grid");
+  sspd_status ps = ensure_pairset_locked(g);  // sizes the relay set too
+  if (ps) return ps;
+  if (!g->relayset.p) {  // same size as the pair set: the pair owner's share of the routers' union
+    if (g->relayset.ensure((g->pairset_mask + 1) * 8) != cudaSuccess)
+      return fail(SSPD_CUDA_ERROR, "CUDA error: out of memory (relay set)");
+    CU(cudaMemsetAsync(g->relayset.p, 0xff, g->relayset.bytes, g->stream));
+  }
+  g->pristine = false;
+  g->relayset_dirty = true;
+  const bool pow2 = (g->eta & (g->eta - 1)) == 0 && g->eta <= (1u << 31);
+  const bool hist = g->K && g->hist_valid;
+  const unsigned blocks = grid_blocks(g, (n + 3) / 4, 256, SSPD_SCAN_BLOCKS_PER_SM);
+  auto* tb = g->relayset.as<unsigned long long>();
+  const uint64_t mask = (g->relayset.bytes / 8) - 1;
+  Prof p(g, "scan", n);
+#define SSPD_RELAY(H1, HI)                                                                                    \
+  scan_shard_kernel<H1, HI, kShardOwn><<<blocks, 256, 0, g->stream>>>(dev_pairs, n, g->d_tabs, g->geo, tb, mask, \
+                                                                      g->stamps, g->now, g->hist, g->K, g->shard_b)
+  if (pow2 && hist) SSPD_RELAY(0, 1);
+  else if (pow2) SSPD_RELAY(0, 0);
+  else if (hist) SSPD_RELAY(1, 1);
+  else SSPD_RELAY(1, 0);
+#undef SSPD_RELAY
   return check_launch();
 }
 

@@ -308,6 +308,13 @@ class Grid:
     def set_shard(self, dev_inbox_ptrs: int, world: int, rank: int, region_cap: int):
         check(self._L.sspd_set_shard(self._h, C.c_void_p(dev_inbox_ptrs), world, rank, region_cap))
 
+    def set_shard_relay(self, dev_inbox_a: int, dev_inbox_b: int, world: int, rank: int, region_cap: int):
+        check(self._L.sspd_set_shard_relay(self._h, C.c_void_p(dev_inbox_a), C.c_void_p(dev_inbox_b), world, rank,
+                                           region_cap))
+
+    def shard_relay(self, dev_ptr: int, n_pairs: int):
+        check(self._L.sspd_shard_relay(self._h, C.c_void_p(dev_ptr), n_pairs))
+
     def shard_sent_ptr(self) -> int:
         """Device u64[world]: pairs this router pushed to each owner this slot."""
         p = C.c_void_p()

@@ -823,3 +823,95 @@ def test_reconstruct_async_pipelines_slots(gpu):
     with pytest.raises(gpu.InvalidArgument, match="nothing queued"):
         g2 = gpu.Grid(seed=1, **DESK)
         g2.reconstruct_collect()
+
+
+def _reconstruct_merged(gpu, grids, k, theta):
+    """The sharded reconstruction with the collectives done in-process: OR of
+    hot bits, AND of survivor masks (dist.ShardExchange.reconstruct)."""
+    import torch
+
+    from paper_1803_11036_b200 import dist as PD
+
+    hot = []
+    for g in grids:
+        p, n = g.shard_hot(k, theta)
+        hot.append(PD.device_view(p, n, 0))
+    merged = hot[0].clone()
+    for h in hot[1:]:
+        merged |= h
+    for h in hot:
+        h.copy_(merged)
+    torch.cuda.synchronize()
+    sel = [g.shard_select(k, theta) for g in grids]
+    assert len({ns for ns, _, _ in sel}) == 1
+    if sel[0][0]:
+        masks = [PD.device_view(p, w, 0) for _, p, w in sel]
+        anded = masks[0].clone()
+        for m in masks[1:]:
+            anded &= m
+        for m in masks:
+            m.copy_(anded)
+        torch.cuda.synchronize()
+    return [g.shard_finish(theta) for g in grids]
+
+
+@pytest.mark.parametrize("world", [1, 3, 4])
+def test_relayed_sharded_routers_on_one_device(gpu, world):
+    """Two-hop sharding: pairs go to their pair owner, which dedups the
+    routers' union and relays each once to the cell owners.  Reports equal the
+    oracle's union-min merge and owned cells are bit-exact, every slot."""
+    import torch
+
+    from paper_1803_11036_b200 import dist as PD
+
+    geo = DESK
+    cap = 1 << 18
+    grids = [gpu.Grid(seed=0x5b, **geo) for _ in range(world)]
+    in_a = [torch.zeros(world * cap * 2, dtype=torch.int32, device="cuda") for _ in range(world)]
+    in_b = [torch.zeros(world * cap * 2, dtype=torch.int32, device="cuda") for _ in range(world)]
+    ta = torch.tensor([b.data_ptr() for b in in_a], dtype=torch.int64, device="cuda")
+    tb = torch.tensor([b.data_ptr() for b in in_b], dtype=torch.int64, device="cuda")
+    for r, g in enumerate(grids):
+        g.track_window(5)
+        g.set_shard_relay(ta.data_ptr(), tb.data_ptr(), world, r, cap)
+    o = O.OracleGrid(seed=0x5b, **geo)
+    rng = O.Mt64(0x5b)
+    ncells = geo["r"] << geo["q"]
+    shared = rng.pairs(2000)  # pairs several routers see in the same slot
+    for s in range(5):
+        for r, g in enumerate(grids):
+            p = np.concatenate([rng.pairs(3000), shared[r * 300: r * 300 + 1500]])
+            for h in range(2 if r == 0 else 1):
+                cip = 0x0A000000 + h
+                p = np.concatenate([p, np.stack([np.full(90, cip, np.uint32), rng.draw(90).astype(np.uint32)], 1)])
+            g.scan_batch(torch.from_numpy(p.view(np.int32)).cuda())
+            o.scan(p)
+        torch.cuda.synchronize()
+        sent = [PD.device_view(g.shard_sent_ptr(), 128, 0).view(torch.int64).tolist() for g in grids]
+        for po, g in enumerate(grids):  # hop 1 -> relay (every source, the owner itself included)
+            box = in_a[po].view(world, cap, 2)
+            for src in range(world):
+                if sent[src][po]:
+                    assert sent[src][po] <= cap
+                    g.shard_relay(box[src].data_ptr(), sent[src][po])
+        torch.cuda.synchronize()
+        sent = [PD.device_view(g.shard_sent_ptr(), 128, 0).view(torch.int64).tolist() for g in grids]
+        for dst, g in enumerate(grids):  # hop 2 -> cell owners
+            box = in_b[dst].view(world, cap, 2)
+            for src in range(world):
+                if src != dst and sent[src][32 + dst]:
+                    assert sent[src][32 + dst] <= cap
+                    g.shard_receive(box[src].data_ptr(), sent[src][32 + dst])
+        torch.cuda.synchronize()
+        reps = _reconstruct_merged(gpu, grids, 5, 128.0)
+        ref = o.reconstruct(5, 128.0)
+        for rep in reps:
+            assert dets_equal(rep, ref), s
+        cells = o.cells()
+        for r, g in enumerate(grids):
+            lo = -(-r * ncells // world) * geo["eta"]
+            hi = -(-(r + 1) * ncells // world) * geo["eta"]
+            assert np.array_equal(g.cells()[lo:hi], cells[lo:hi]), (s, r)
+        for g in grids:
+            g.advance_slot()
+        o.advance()
