@@ -14,11 +14,12 @@ router uses.  Three exchange formats give the same grid:
           so the exchange overlaps the scan;
   PAIRS   the same lists, all-gathered after the scan;
   BITMAP  the slot's touched bitmap (1 bit per recorder), OR-all-reduced.
-  SHARD   each router owns 1/N of the cells and stamps only those: the scan
-          pushes each new pair to the owners of its other cells (P2P over
-          NVLink), hot bits are OR-merged and each survivor's in-window
-          bucket masks AND-merged at reconstruction (ShardExchange); per-router
-          stamping then scales with 1/N of the routers' union of pairs.
+  SHARD   each router owns 1/N of the cells and stamps only those; new pairs
+          reach the owners of their cells over NVLink, relayed through a
+          pair owner that dedups the routers' union (ShardExchange); hot bits
+          are OR-merged and each survivor's in-window bucket masks AND-merged
+          at reconstruction.  Per-router stamping then scales with 1/N of the
+          routers' union of pairs.
 
 merge_stamps_max is the literal all-reduce(max) of the full stamp grid, kept as
 the baseline.  Every variant equals merge_rseas(node grids, kUnionMin) of the
@@ -194,54 +195,90 @@ class ShardExchange:
     routers").
 
     Router `rank` owns the cells c with c * world // (r * 2^q) == rank and
-    stamps only those.  Its scan stores each pair new to it into region
-    `rank` of the inbox of every other owner of the pair's cells (P2P stores
-    into symmetric memory, double-buffered by slot parity as in PushExchange).
-    merge(): an all-gather of the per-owner push counts is the barrier; each
-    router then scans what was pushed to it (owned cells only).
+    keeps exact stamps only there.  relay=True (the default) routes pairs in
+    two hops through symmetric-memory inboxes (P2P stores over NVLink, double
+    buffered by slot parity as in PushExchange):
+
+      scan    each pair new to a router goes to its pair owner
+              (a hash of the pair mod world; inboxes A);
+      merge   an all-gather of the hop-1 counts is the barrier; every pair
+              owner dedups what it received (the routers' union, for its
+              share), stamps its own cells and pushes each pair once to the
+              other cell owners (inboxes B); a second all-gather; every
+              router stamps what was relayed to it.
+
+    relay=False pushes straight from the scan to every other cell owner (one
+    hop; a pair several routers saw then reaches its owners several times).
+    Measured on one GPU with all routers' work in lockstep
+    (profiles/r01_shard_sim.md): a router's slot at N=8 is 4.3 ms relayed,
+    6.4 ms one-hop, 11.7 ms with the replicated PAIRS exchange.
+
     reconstruct(): OR-all-reduce of the routers' hot bits (r * 2^q bits), the
     same joins on every router, AND-all-reduce of the per-survivor bucket
     masks (n_surv * eta bits), popcount -- the reports equal reconstruct on the
     union-min merged grid.  region_cap must cover the pairs a router scans per
-    slot (a router pushes each new pair at most once per owner); a count past
-    it raises instead of dropping touches.
+    slot plus list padding (kernels.cuh list_pad); a count past it raises.
     """
 
-    def __init__(self, grid, region_cap: int, group=None):
+    def __init__(self, grid, region_cap: int, group=None, relay: bool = True):
         import torch.distributed._symmetric_memory as symm_mem
 
         self.world = dist.get_world_size(group)
         self.rank = dist.get_rank(group)
         self.cap = int(region_cap)
         self.group = group
+        self.relay = relay
         dev = torch.device(f"cuda:{grid.device}")
         name = group.group_name if group is not None else dist.group.WORLD.group_name
-        self.inbox, self.handles = [], []
+        self.inbox, self.handles = [], []  # [parity][hop]
         for _ in range(2):
-            buf = symm_mem.empty(self.world * self.cap * 2, dtype=torch.int32, device=dev)
-            self.inbox.append(buf)
-            self.handles.append(symm_mem.rendezvous(buf, name))
+            bufs, hs = [], []
+            for _ in range(2 if relay else 1):
+                buf = symm_mem.empty(self.world * self.cap * 2, dtype=torch.int32, device=dev)
+                bufs.append(buf)
+                hs.append(symm_mem.rendezvous(buf, name))
+            self.inbox.append(bufs)
+            self.handles.append(hs)
         self.parity = 0
         grid._exchange = SHARD
         grid._shard = self
         self._arm(grid)
 
     def _arm(self, grid):
-        grid.set_shard(self.handles[self.parity].buffer_ptrs_dev, self.world, self.rank, self.cap)
+        hs = self.handles[self.parity]
+        if self.relay:
+            grid.set_shard_relay(hs[0].buffer_ptrs_dev, hs[1].buffer_ptrs_dev, self.world, self.rank, self.cap)
+        else:
+            grid.set_shard(hs[0].buffer_ptrs_dev, self.world, self.rank, self.cap)
 
-    def merge(self, grid):
-        grid.synchronize()  # this router's pushes are complete (the kernel fences them)
+    def _counts(self, grid, hop: int):
+        """sent[src][dst] of hop 0 or 1, all-gathered (also the barrier)."""
+        grid.synchronize()  # this router's stores are complete (the kernels fence them)
         dev = torch.device(f"cuda:{grid.device}")
-        mine = device_view(grid.shard_sent_ptr(), 2 * self.world, grid.device).view(torch.int64)
-        mine = mine[: self.world].clone()
+        mine = device_view(grid.shard_sent_ptr(), 128, grid.device).view(torch.int64)
+        mine = mine[32 * hop: 32 * hop + self.world].clone()
         allsent = torch.empty(self.world * self.world, dtype=torch.int64, device=dev)
-        dist.all_gather_into_tensor(allsent, mine, group=self.group)  # also the barrier
+        dist.all_gather_into_tensor(allsent, mine, group=self.group)
         sent = allsent.view(self.world, self.world).tolist()
         torch.cuda.synchronize(grid.device)
         over = max(max(row) for row in sent)
         if over > self.cap:
             raise RuntimeError(f"shard exchange: {over} pairs for one owner exceed region_cap {self.cap}")
-        box = self.inbox[self.parity].view(self.world, self.cap, 2)
+        return sent
+
+    def merge(self, grid):
+        bufs = self.inbox[self.parity]
+        if self.relay:
+            sent = self._counts(grid, 0)
+            box = bufs[0].view(self.world, self.cap, 2)
+            for src in range(self.world):  # the routers' pairs routed here, this router's own included
+                if sent[src][self.rank]:
+                    grid.shard_relay(box[src].data_ptr(), sent[src][self.rank])
+            sent = self._counts(grid, 1)
+            box = bufs[1].view(self.world, self.cap, 2)
+        else:
+            sent = self._counts(grid, 0)
+            box = bufs[0].view(self.world, self.cap, 2)
         for src in range(self.world):
             if src != self.rank and sent[src][self.rank]:
                 grid.shard_receive(box[src].data_ptr(), sent[src][self.rank])
