@@ -2,15 +2,18 @@
 """Throughput of the sliding super point detector hot path on B200.
 
 One step = one time slice (slot) of BASELINE.json's config C2: scan the slot's
-pairs into the RSEA grid, fold the slot's touches into the stamps, find hot
+pairs into the RSEA grid (stamps and window ring updated in place), find hot
 estimators, reconstruct the super points (levels 2..r-1 + finalize, reports
-back on the host), advance the slot.  At N GPUs each GPU is one edge router
-scanning its own shard of the slot (weak scaling) and the routers merge by
-union-min (OR of the slot's touched bitmaps, see paper_1803_11036_b200/dist.py)
-before reconstruction.
+back on the host), advance the slot.  Slots pipeline: a slot's
+reconstruction is collected after the next slot's scan is queued.  At N GPUs
+each GPU is one edge router scanning its own shard of the slot (weak scaling)
+and the routers merge by union-min before reconstruction (default: cells
+sharded among the routers, pairs relayed over NVLink; see
+paper_1803_11036_b200/dist.py and --merge).
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
-                  [--config c2|c1] [--no-cpu-baseline]
+                  [--config c2|c1] [--no-cpu-baseline] [--no-e2e] [--merge ...]
+                  [--stamp-width 8|16|32] [--window k] [--q/--eta/--theta ...]
 
 Prints ONE JSON line (rank 0).  `--impl reference` times the reference's own
 CPU implementation (oracle/_ref, compiled from /root/reference/proj) on the
@@ -254,7 +257,7 @@ def main():
                          "unavailable): distinct pairs pushed over NVLink during the scan (push), the "
                          "same lists all-gathered after the scan (pairs), OR of touched bitmaps, "
                          "the literal all-reduce(max) of the full stamp grid, or cells sharded among "
-                         "routers with pairs pushed to their owners (shard)")
+                         "routers with pairs relayed to their owners through pair owners (shard)")
     ap.add_argument("--stamp-width", type=int, default=32, choices=[8, 16, 32],
                     help="bits per recorder stamp (C4): 8/16 keep R_k (k <= window) and the reports "
                          "exact, 32 also the full distances")
