@@ -604,8 +604,9 @@ def main():
                              "push": "union-min: distinct pairs pushed to peers over NVLink during the scan",
                              "bitmap": "union-min: OR all-reduce of the slot's touched bitmaps",
                              "stamps": "union-min: NCCL all-reduce(max) of the full stamp grid",
-                             "shard": "union-min over cells sharded among routers: new pairs pushed to "
-                                      "their cells' owners, hot bits OR- and survivor masks AND-reduced",
+                             "shard": "union-min over cells sharded among routers: new pairs relayed over "
+                                      "NVLink through pair owners to their cells' owners, hot bits OR- and "
+                                      "survivor masks AND-reduced",
                              "auto": "none (single router)"}[merge_used],
                    "parallelism": f"{world} routers, one per GPU",
                    "l2": l2_note},
