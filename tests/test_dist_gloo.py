@@ -159,7 +159,7 @@ def test_pair_list_exchange(world):
     assert all(out[r] for r in range(world))
 
 
-def _shard_worker(rank, world, port, slots, out):
+def _shard_worker(rank, world, port, slots, out, relay=False):
     """The sharded union-min algebra (dist.py ShardExchange) on numpy grids:
     each router owns cells c with c * world // ncells == rank, stamps its own
     pairs' owned recorders, sends each pair to the owners of its other cells,
@@ -200,25 +200,34 @@ def _shard_worker(rank, world, port, slots, out):
             cells, b = touches(int(cip), int(oip))
             merged[cells, b] = now
         own = everyone[rank]
+        if relay:
+            # hop 1: every new pair to its pair owner; the pair owner dedups
+            # the union of what it got (its own share included)
+            hop1 = [[] for _ in range(world)]
+            for cip, oip in {(int(a), int(b)) for a, b in own}:
+                hop1[hash((cip, oip)) % world].append((cip, oip))
+            objs = [None] * world
+            dist.all_gather_object(objs, hop1)
+            own = sorted({pr for src in range(world) for pr in objs[src][rank]})
         outbox = [[] for _ in range(world)]
         for cip, oip in own:
             cells, b = touches(int(cip), int(oip))
             for c in cells:
                 if owner[c] == rank:
                     stamps[c, b] = now
-                else:
-                    outbox[owner[c]].append((int(cip), int(oip)))
-        # the exchange: every router receives the pairs pushed to it
+            for d in {int(owner[c]) for c in cells} - {rank}:  # once per owner (the kernel's dmask)
+                outbox[d].append((int(cip), int(oip)))
+        # the exchange: every router receives the pairs pushed (relayed) to it
         objs = [None] * world
         dist.all_gather_object(objs, outbox)
-        for src in range(world):
-            if src == rank:
-                continue
-            for cip, oip in set(objs[src][rank]):
-                cells, b = touches(cip, oip)
-                for c in cells:
-                    if owner[c] == rank:
-                        stamps[c, b] = now
+        received = [pr for src in range(world) if src != rank for pr in objs[src][rank]]
+        if relay:  # each pair reaches a cell owner once, from its pair owner
+            ok = ok and len(received) == len(set(received))
+        for cip, oip in set(received):
+            cells, b = touches(cip, oip)
+            for c in cells:
+                if owner[c] == rank:
+                    stamps[c, b] = now
         mine = owner == rank
         ok = ok and np.array_equal(stamps[mine], merged[mine])
         # hot sets: per-owner R_k, OR-merged
@@ -248,9 +257,10 @@ def _shard_worker(rank, world, port, slots, out):
     dist.destroy_process_group()
 
 
+@pytest.mark.parametrize("relay", [False, True], ids=["one_hop", "relayed"])
 @pytest.mark.parametrize("world", [2, 3])
-def test_sharded_union_min_algebra(world):
+def test_sharded_union_min_algebra(world, relay):
     mgr = mp.Manager()
     out = mgr.dict()
-    mp.spawn(_shard_worker, args=(world, free_port(), 4, out), nprocs=world, join=True)
+    mp.spawn(_shard_worker, args=(world, free_port(), 4, out, relay), nprocs=world, join=True)
     assert all(out[r] for r in range(world))
