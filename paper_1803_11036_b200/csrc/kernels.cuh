@@ -1,13 +1,21 @@
 // kernels.cuh -- sm_100a kernels for the sliding super point detector.
 //
-// Data layout in HBM (see DESIGN.md "Layout"):
+// Data layout in HBM (see DESIGN.md section 3):
 //   stamps  u32[r * 2^q * eta]   (row, column, bucket) order, like the
-//                                 reference's cells_ (rsea.hpp:105-112)
+//                                 reference's cells_ (rsea.hpp:105-112);
+//                                 u8/u16 codes on narrow-stamp grids
 //   touched u32[ceil(n/32)]      this slot's touched recorders, 1 bit each
 //   hist    u32[K * r * 2^q]     per-cell count of buckets whose latest touch
 //                                 is slot s, ring-indexed by s mod K (optional)
 // A recorder's reference distance is min(now - stamp, 0xFFFF); stamp 0 is
 // never-seen and `now` starts at 65535.
+//
+// Contents, in order: hashing and the pair stream; the scans (bitmap,
+// direct, pair-set dedup with the exchange lists) and binning; commit,
+// counts and the window ring; hot sets and the reconstruction chain
+// (programmatic dependent launches); exact ground truth; conversions, merge
+// and equality; sharded routers (own / relay / receive scans, survivor
+// masks); narrow stamps.
 #pragma once
 
 #include <cstdint>
