@@ -533,6 +533,16 @@ def main():
                     "bytes_per_unit": bytes_per_unit, "units_per_launch": units_per_launch,
                     "launch_ms": round(per_launch_ms, 4),
                     "peak_source": "MEASURED_PEAKS.json hbm_gbs" if "hbm_gbs" in peaks else "fallback"}
+            if dom == "scan" and cfg["pool"] == 0:
+                # uniform pairs (C1): every pair does r random touches, the pattern of the
+                # random-access probe (tools/fetch_probe.cu, profiles/r01_access_probe.txt:
+                # red.max / atom.max / ld+atom into 640 MB, at most 5.06 Gpkt/s at r = 5) -- the
+                # scan's ceiling is that, not the streaming copy peak
+                ceiling = 5060.0
+                scan_mpkts = units_per_launch / (per_launch_ms / 1e3) / 1e6
+                roof["random_access"] = {"ceiling_mpkts": ceiling, "scan_mpkts": round(scan_mpkts, 1),
+                                         "frac": round(scan_mpkts / ceiling, 3),
+                                         "source": "tools/fetch_probe.cu best of red, atom and ld+atom into 640 MB, r=5 (profiles/r01_access_probe.txt)"}
     kernels_share = {k2: round(v["ms"] / ms, 4) for k2, v in prof.items()}
 
     # Detection accuracy of the last timed slot against the generator's
