@@ -209,6 +209,11 @@ sspd_status sspd_set_shard(sspd_grid* g, void* dev_inbox_ptrs, uint32_t world, u
 sspd_status sspd_set_shard_relay(sspd_grid* g, void* dev_inbox_a, void* dev_inbox_b, uint32_t world,
                                  uint32_t rank, uint64_t region_cap);
 sspd_status sspd_shard_relay(sspd_grid* g, const uint32_t* dev_pairs, uint64_t n);
+/* sspd_shard_relay over n_regions inbox regions in ONE launch: region i holds
+ * counts[i] (host array) pairs at dev_base + 2 * i * region_stride words.
+ * (One launch pads each warp's list blocks once instead of once per region.) */
+sspd_status sspd_shard_relay_regions(sspd_grid* g, const uint32_t* dev_base, uint64_t region_stride,
+                                     const uint64_t* counts, uint32_t n_regions);
 sspd_status sspd_shard_sent(sspd_grid* g, uint64_t** dev_counts);
 sspd_status sspd_shard_receive(sspd_grid* g, const uint32_t* dev_pairs, uint64_t n);
 sspd_status sspd_shard_hot(sspd_grid* g, uint32_t k, uint64_t cutoff, uint32_t** dev_hot_words,

@@ -52,6 +52,7 @@ SIGNATURES = {
     "sspd_set_shard": (C.c_int, [grid_p, C.c_void_p, C.c_uint32, C.c_uint32, C.c_uint64]),
     "sspd_set_shard_relay": (C.c_int, [grid_p, C.c_void_p, C.c_void_p, C.c_uint32, C.c_uint32, C.c_uint64]),
     "sspd_shard_relay": (C.c_int, [grid_p, C.c_void_p, C.c_uint64]),
+    "sspd_shard_relay_regions": (C.c_int, [grid_p, C.c_void_p, C.c_uint64, u64p, C.c_uint32]),
     "sspd_shard_sent": (C.c_int, [grid_p, C.POINTER(C.c_void_p)]),
     "sspd_shard_receive": (C.c_int, [grid_p, C.c_void_p, C.c_uint64]),
     "sspd_shard_hot": (C.c_int, [grid_p, C.c_uint32, C.c_uint64, C.POINTER(C.c_void_p), u64p]),

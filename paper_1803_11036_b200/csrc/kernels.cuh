@@ -1283,6 +1283,16 @@ __device__ __forceinline__ uint32_t shard_owner(uint32_t cell, uint32_t ncells, 
 // every pair reaches them once).
 enum ShardMode { kShardRecv = 0, kShardOwn = 1, kShardToPairOwner = 2, kShardRecvOnce = 4 };
 
+// Several inbox regions scanned as one input (one launch, so each warp pads
+// its list blocks once, not once per region): logical pair i lies in segment
+// s with start[s] <= i < start[s + 1], at pairs + 2 * (s * stride + i - start[s]).
+struct ShardSegs {
+  uint64_t stride;
+  uint32_t nseg;  // 0: one contiguous input
+  uint32_t unused;
+  uint64_t start[33];
+};
+
 __device__ __forceinline__ uint32_t pair_owner(uint64_t h, uint32_t world) {
   return (uint32_t)(h >> 32) % world;
 }
@@ -1292,7 +1302,8 @@ __global__ void __launch_bounds__(256) scan_shard_kernel(const uint32_t* __restr
                                                          const HashTabs* __restrict__ tabs, Geo geo,
                                                          unsigned long long* __restrict__ table, uint64_t table_mask,
                                                          uint32_t* __restrict__ stamps, uint32_t now,
-                                                         uint32_t* __restrict__ hist, uint32_t K, ShardArgs sh) {
+                                                         uint32_t* __restrict__ hist, uint32_t K, ShardArgs sh,
+                                                         ShardSegs segs = ShardSegs{}) {
   constexpr bool kPushes = PUSH == kShardOwn || PUSH == kShardToPairOwner;
   constexpr bool kStamps = PUSH != kShardToPairOwner;
   constexpr bool kDedup = PUSH != kShardRecvOnce;
@@ -1316,7 +1327,21 @@ __global__ void __launch_bounds__(256) scan_shard_kernel(const uint32_t* __restr
     uint32_t c[P], o[P];
     bool fresh[P];
     const uint64_t p0 = g * P;
-    if (vec && p0 + P <= n) {
+    if (segs.nseg) {
+#pragma unroll
+      for (int u = 0; u < P; ++u) {
+        const uint64_t i = p0 + u;
+        fresh[u] = i < n;
+        c[u] = o[u] = 0u;
+        if (fresh[u]) {
+          uint32_t sg = 0;
+          while (i >= segs.start[sg + 1]) ++sg;
+          const uint2 v = *reinterpret_cast<const uint2*>(pairs + 2 * (sg * segs.stride + (i - segs.start[sg])));
+          c[u] = v.x;
+          o[u] = v.y;
+        }
+      }
+    } else if (vec && p0 + P <= n) {
       const uint4 a = ld_stream_u4(pairs + 2 * p0);
       c[0] = a.x; o[0] = a.y; c[1] = a.z; o[1] = a.w;
       fresh[0] = fresh[1] = true;

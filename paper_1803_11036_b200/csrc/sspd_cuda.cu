@@ -1502,9 +1502,34 @@ sspd_status sspd_shard_receive(sspd_grid* g, const uint32_t* dev_pairs, uint64_t
   return check_launch();
 }
 
+namespace {
+sspd_status shard_relay_locked(sspd_grid* g, const uint32_t* dev_pairs, uint64_t n, const ShardSegs& segs);
+}
+
 sspd_status sspd_shard_relay(sspd_grid* g, const uint32_t* dev_pairs, uint64_t n) {
-  if (n == 0) return SSPD_OK;
   std::lock_guard<std::mutex> lk(g->mu);
+  return shard_relay_locked(g, dev_pairs, n, ShardSegs{});
+}
+
+sspd_status sspd_shard_relay_regions(sspd_grid* g, const uint32_t* dev_base, uint64_t region_stride,
+                                     const uint64_t* counts, uint32_t n_regions) {
+  if (n_regions > 32) return fail(SSPD_INVALID_ARGUMENT, "shard_relay_regions: at most 32 regions");
+  ShardSegs segs{};
+  segs.stride = region_stride;
+  segs.nseg = n_regions;
+  segs.start[0] = 0;
+  for (uint32_t i = 0; i < n_regions; ++i) {
+    if (counts[i] > region_stride) return fail(SSPD_INVALID_ARGUMENT, "shard_relay_regions: count past the region");
+    segs.start[i + 1] = segs.start[i] + counts[i];
+  }
+  for (uint32_t i = n_regions + 1; i < 33; ++i) segs.start[i] = ~0ull;  // the segment search never runs past nseg
+  std::lock_guard<std::mutex> lk(g->mu);
+  return shard_relay_locked(g, dev_base, segs.start[n_regions], segs);
+}
+
+namespace {
+sspd_status shard_relay_locked(sspd_grid* g, const uint32_t* dev_pairs, uint64_t n, const ShardSegs& segs) {
+  if (n == 0) return SSPD_OK;
   DeviceGuard dg(g->device);
   if (!g->shard || !g->relay) return fail(SSPD_INVALID_ARGUMENT, "shard_relay: not a relayed sharded grid");
   sspd_status ps = ensure_pairset_locked(g);  // sizes the relay set too
@@ -1524,7 +1549,8 @@ sspd_status sspd_shard_relay(sspd_grid* g, const uint32_t* dev_pairs, uint64_t n
   Prof p(g, "scan", n);
 #define SSPD_RELAY(H1, HI)                                                                                    \
   scan_shard_kernel<H1, HI, kShardOwn><<<blocks, 256, 0, g->stream>>>(dev_pairs, n, g->d_tabs, g->geo, tb, mask, \
-                                                                      g->stamps, g->now, g->hist, g->K, g->shard_b)
+                                                                      g->stamps, g->now, g->hist, g->K, g->shard_b, \
+                                                                      segs)
   if (pow2 && hist) SSPD_RELAY(0, 1);
   else if (pow2) SSPD_RELAY(0, 0);
   else if (hist) SSPD_RELAY(1, 1);
@@ -1532,6 +1558,7 @@ sspd_status sspd_shard_relay(sspd_grid* g, const uint32_t* dev_pairs, uint64_t n
 #undef SSPD_RELAY
   return check_launch();
 }
+}  // namespace
 
 sspd_status sspd_shard_hot(sspd_grid* g, uint32_t k, uint64_t cutoff, uint32_t** dev_hot_words, uint64_t* n_words) {
   std::lock_guard<std::mutex> lk(g->mu);

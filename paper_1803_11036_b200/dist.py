@@ -210,7 +210,7 @@ class ShardExchange:
     relay=False pushes straight from the scan to every other cell owner (one
     hop; a pair several routers saw then reaches its owners several times).
     Measured on one GPU with all routers' work in lockstep
-    (profiles/r01_shard_sim.md): a router's slot at N=8 is 4.3 ms relayed,
+    (profiles/r01_shard_sim.md): a router's slot at N=8 is 4.0 ms relayed,
     6.4 ms one-hop, 11.7 ms with the replicated PAIRS exchange.
 
     reconstruct(): OR-all-reduce of the routers' hot bits (r * 2^q bits), the
@@ -270,10 +270,8 @@ class ShardExchange:
         bufs = self.inbox[self.parity]
         if self.relay:
             sent = self._counts(grid, 0)
-            box = bufs[0].view(self.world, self.cap, 2)
-            for src in range(self.world):  # the routers' pairs routed here, this router's own included
-                if sent[src][self.rank]:
-                    grid.shard_relay(box[src].data_ptr(), sent[src][self.rank])
+            # the routers' pairs routed here (this router's own included), all regions in one launch
+            grid.shard_relay_regions(bufs[0].data_ptr(), self.cap, [sent[src][self.rank] for src in range(self.world)])
             sent = self._counts(grid, 1)
             box = bufs[1].view(self.world, self.cap, 2)
         else:

@@ -315,6 +315,12 @@ class Grid:
     def shard_relay(self, dev_ptr: int, n_pairs: int):
         check(self._L.sspd_shard_relay(self._h, C.c_void_p(dev_ptr), n_pairs))
 
+    def shard_relay_regions(self, dev_base: int, region_stride: int, counts):
+        """Relay several inbox regions (region i: counts[i] pairs at pair
+        offset i * region_stride from dev_base) in one launch."""
+        arr = (C.c_uint64 * len(counts))(*[int(x) for x in counts])
+        check(self._L.sspd_shard_relay_regions(self._h, C.c_void_p(dev_base), region_stride, arr, len(counts)))
+
     def shard_sent_ptr(self) -> int:
         """Device u64[world]: pairs this router pushed to each owner this slot."""
         p = C.c_void_p()

@@ -889,11 +889,14 @@ def test_relayed_sharded_routers_on_one_device(gpu, world):
         torch.cuda.synchronize()
         sent = [PD.device_view(g.shard_sent_ptr(), 128, 0).view(torch.int64).tolist() for g in grids]
         for po, g in enumerate(grids):  # hop 1 -> relay (every source, the owner itself included)
-            box = in_a[po].view(world, cap, 2)
-            for src in range(world):
-                if sent[src][po]:
-                    assert sent[src][po] <= cap
-                    g.shard_relay(box[src].data_ptr(), sent[src][po])
+            if po % 2:  # both entry points: one region at a time, and all regions in one launch
+                box = in_a[po].view(world, cap, 2)
+                for src in range(world):
+                    if sent[src][po]:
+                        assert sent[src][po] <= cap
+                        g.shard_relay(box[src].data_ptr(), sent[src][po])
+            else:
+                g.shard_relay_regions(in_a[po].data_ptr(), cap, [sent[src][po] for src in range(world)])
         torch.cuda.synchronize()
         sent = [PD.device_view(g.shard_sent_ptr(), 128, 0).view(torch.int64).tolist() for g in grids]
         for dst, g in enumerate(grids):  # hop 2 -> cell owners

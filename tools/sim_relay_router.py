@@ -94,19 +94,13 @@ def main():
         sb = [None] * N
         for po in range(1, N):
             h = grid(po)
-            box = in_a[po].view(N, cap, 2)
-            for src in range(N):
-                if sa[src][po]:
-                    h.shard_relay(box[src].data_ptr(), sa[src][po])
+            h.shard_relay_regions(in_a[po].data_ptr(), cap, [sa[src][po] for src in range(N)])
             sb[po] = sent(h)
             h.close()
             del h
         torch.cuda.synchronize()
         t2 = ev()
-        box = in_a[0].view(N, cap, 2)
-        for src in range(N):
-            if sa[src][0]:
-                r0.shard_relay(box[src].data_ptr(), sa[src][0])
+        r0.shard_relay_regions(in_a[0].data_ptr(), cap, [sa[src][0] for src in range(N)])
         t3 = ev()
         sb[0] = sent(r0)
         t4 = ev()
