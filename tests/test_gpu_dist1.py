@@ -4,7 +4,6 @@ memory rendezvous and the peer table for PUSH, the all-gathers of PAIRS,
 the OR all-reduce of BITMAP, the stamp all-reduce), so the calls and buffer
 views are exercised on a real device; the algebra of 2- and 3-router
 exchanges is covered by tests/test_dist_gloo.py."""
-import os
 import socket
 
 import numpy as np
