@@ -66,6 +66,16 @@ const char* sspd_last_error(void);
 /* Number of visible devices this library can run on (sm_100). */
 sspd_status sspd_device_count(int* n);
 
+/* ---- device memory, for hosts that wire routers together in one process
+ * (the C++ run_detection over several GPUs, csrc/host/routers.cpp) ---- */
+sspd_status sspd_device_alloc(int device, uint64_t bytes, void** ptr);
+sspd_status sspd_device_free(int device, void* ptr);
+/* Pairwise peer access among the listed devices (NVLink loads/stores). */
+sspd_status sspd_enable_peer_access(int n_devices, const int* devices);
+/* Synchronous copy on the grid's stream: host -> device (to_device != 0) or
+ * device -> host. */
+sspd_status sspd_grid_copy(sspd_grid* g, void* dst, const void* src, uint64_t bytes, int to_device);
+
 /* ---- grid lifetime: Rsea::Rsea (rsea.hpp:54; rsea.cpp:18-27) ---- */
 /* Validates like validate_config(cfg, eta, 1, 1.0) (hashing.cpp:63-87) and
  * fails with "Rsea: <first diagnostic>".  All recorders start never-seen. */

@@ -514,6 +514,51 @@ const char* sspd_last_error(void) { return g_err.c_str(); }
 
 uint64_t sspd_launch_count(void) { return g_launches.load(); }
 
+sspd_status sspd_device_alloc(int device, uint64_t bytes, void** ptr) {
+  *ptr = nullptr;
+  DeviceGuard dg(device);
+  if (cudaMalloc(ptr, std::max<uint64_t>(bytes, 16)) != cudaSuccess) {
+    cudaGetLastError();
+    *ptr = nullptr;
+    return fail(SSPD_CUDA_ERROR, "CUDA error: out of memory allocating " + std::to_string(bytes) + " bytes");
+  }
+  return SSPD_OK;
+}
+
+sspd_status sspd_device_free(int device, void* ptr) {
+  DeviceGuard dg(device);
+  if (ptr) cudaFree(ptr);
+  return SSPD_OK;
+}
+
+sspd_status sspd_enable_peer_access(int n_devices, const int* devices) {
+  for (int i = 0; i < n_devices; ++i)
+    for (int j = 0; j < n_devices; ++j) {
+      if (devices[i] == devices[j]) continue;
+      int can = 0;
+      cudaDeviceCanAccessPeer(&can, devices[i], devices[j]);
+      if (!can) return fail(SSPD_CUDA_ERROR, "no peer access between devices " + std::to_string(devices[i]) +
+                                                 " and " + std::to_string(devices[j]));
+      DeviceGuard dg(devices[i]);
+      const cudaError_t e = cudaDeviceEnablePeerAccess(devices[j], 0);
+      if (e != cudaSuccess && e != cudaErrorPeerAccessAlreadyEnabled)
+        return fail(SSPD_CUDA_ERROR, std::string("CUDA error: ") + cudaGetErrorString(e));
+      cudaGetLastError();
+    }
+  return SSPD_OK;
+}
+
+sspd_status sspd_grid_copy(sspd_grid* g, void* dst, const void* src, uint64_t bytes, int to_device) {
+  std::lock_guard<std::mutex> lk(g->mu);
+  DeviceGuard dg(g->device);
+  if (bytes == 0) return SSPD_OK;
+  CU(cudaMemcpyAsync(dst, src, bytes, to_device ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToHost, g->stream));
+  CU(cudaStreamSynchronize(g->stream));
+  if (to_device) g->h2d_bytes += bytes;
+  else g->d2h_bytes += bytes;
+  return SSPD_OK;
+}
+
 sspd_status sspd_device_count(int* n) {
   int c = 0;
   cudaError_t e = cudaGetDeviceCount(&c);

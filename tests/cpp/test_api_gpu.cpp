@@ -5,6 +5,7 @@
 // compiled reference through its C shim (bit-identical grids, identical
 // report lists and estimates).
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
 #include <random>
 #include <set>
@@ -316,6 +317,33 @@ TEST_CASE("pipeline: strategies and worker counts agree") {
     CHECK(cips_of(a[s]) == cips_of(b[s]));
     REQUIRE(a[s].hosts.size() == b[s].hosts.size());
     for (std::size_t h = 0; h < a[s].hosts.size(); ++h) CHECK(a[s].hosts[h].estimate == b[s].hosts[h].estimate);
+  }
+}
+
+TEST_CASE("union-min over several routers (B200 extension): same reports as one grid") {
+  RunConfig rc = test_config();
+  const auto w = workload(3, 256, 10, rc, 91);
+  const auto shards = split(w.trace, 4, 92);
+  const auto one = run_detection(shards, rc);
+  const auto single_trace = run_detection({w.trace}, rc);
+  for (const char* routers : {"2", "3", "4"}) {
+    setenv("SSPD_ROUTERS", routers, 1);  // several routers on this one device
+    const auto many = run_detection(shards, rc);
+    const auto split_trace = run_detection({w.trace}, rc);
+    unsetenv("SSPD_ROUTERS");
+    REQUIRE(many.size() == one.size());
+    REQUIRE(split_trace.size() == single_trace.size());
+    for (std::size_t s = 0; s < one.size(); ++s) {
+      REQUIRE(many[s].hosts.size() == one[s].hosts.size());
+      CHECK(many[s].slot == one[s].slot);
+      for (std::size_t h = 0; h < one[s].hosts.size(); ++h) {
+        CHECK(many[s].hosts[h].cip == one[s].hosts[h].cip);
+        CHECK(many[s].hosts[h].estimate == one[s].hosts[h].estimate);
+      }
+      REQUIRE(split_trace[s].hosts.size() == single_trace[s].hosts.size());
+      for (std::size_t h = 0; h < single_trace[s].hosts.size(); ++h)
+        CHECK(split_trace[s].hosts[h].estimate == single_trace[s].hosts[h].estimate);
+    }
   }
 }
 
