@@ -20,6 +20,7 @@
 
 #include "sspd/estimator.hpp"
 #include "sspd/hashing.hpp"
+#include "sspd/workload.hpp"
 
 struct sspd_grid;
 
@@ -100,6 +101,9 @@ class Rsea {
   int device() const;
   // Scan pairs already resident on this grid's device (no host copy).
   void scan_device(const IpPair* device_pairs, std::size_t n);
+  // Scan (ts, cip, oip) trace records as they are (ts ignored): no host-side
+  // conversion to pairs (sspd_scan_records).
+  void scan_records(std::span<const TraceRecord> records);
   // Keep per-cell in-window counts for windows up to k incrementally.
   void track_window(uint32_t k);
   // The underlying C-ABI handle (include/sspd_cuda.h).

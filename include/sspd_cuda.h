@@ -70,6 +70,12 @@ sspd_status sspd_device_count(int* n);
  * (the C++ run_detection over several GPUs, csrc/host/routers.cpp) ---- */
 sspd_status sspd_device_alloc(int device, uint64_t bytes, void** ptr);
 sspd_status sspd_device_free(int device, void* ptr);
+/* Device blocks of >= 1 MiB freed by grids (and sspd_device_free) are kept
+ * for reuse -- a grid's create + destroy would otherwise cost tens of ms of
+ * cudaMalloc/cudaFree -- up to $SSPD_CACHE_BYTES per device (default 16 GiB).
+ * This frees them (device < 0: every device); *released (may be NULL) gets
+ * the byte count.  Allocation failures flush the cache by themselves. */
+sspd_status sspd_release_cached(int device, uint64_t* released);
 /* Pairwise peer access among the listed devices (NVLink loads/stores). */
 sspd_status sspd_enable_peer_access(int n_devices, const int* devices);
 /* Synchronous copy on the grid's stream: host -> device (to_device != 0) or
@@ -114,6 +120,11 @@ sspd_status sspd_grid_synchronize(sspd_grid* g);
  * otherwise a host pointer, copied in chunks (async when pinned).  Order- and
  * batch-invariant like the reference. */
 sspd_status sspd_scan(sspd_grid* g, const uint32_t* pairs, uint64_t n, int pairs_on_device);
+/* The same over n (ts, cip, oip) trace records (workload.hpp TraceRecord,
+ * 12 bytes each; ts is ignored -- the caller picks a slot's records): the
+ * records go to the device as they are and are turned into pairs there, so a
+ * time-sorted trace is scanned slot by slot without a host-side copy. */
+sspd_status sspd_scan_records(sspd_grid* g, const uint32_t* records, uint64_t n, int on_device);
 
 /* ---- QUIESCENT phase ---- */
 /* Rsea::advance_slot (rsea.cpp:55-63): O(1), `slots` times. */

@@ -10,7 +10,7 @@ from ._cabi import (CandidateOverflow, CudaError, InvalidArgument, NoDevice, Out
                     PAPER_MAX, UNION_MIN, SspdError, load)
 from .grid import (BASE_NOW, Detection, Grid, device_count, estimate_cardinality, exact_counts,
                    export_snapshot,
-                   hot_cutoff, import_snapshot, launch_count, merge_rseas)
+                   hot_cutoff, import_snapshot, launch_count, merge_rseas, release_cached)
 
 from .pipeline import run_detection, validate_config
 
@@ -19,5 +19,5 @@ __all__ = [
     "BASE_NOW", "CandidateOverflow", "CudaError", "Detection", "Grid", "InvalidArgument",
     "NoDevice", "OutOfRange", "PAPER_MAX", "SspdError", "UNION_MIN", "device_count",
     "estimate_cardinality", "exact_counts", "export_snapshot", "hot_cutoff", "import_snapshot", "launch_count",
-    "load", "merge_rseas",
+    "load", "merge_rseas", "release_cached",
 ]

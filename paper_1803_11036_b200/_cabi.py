@@ -61,8 +61,10 @@ SIGNATURES = {
     "sspd_shard_finish": (C.c_int, [grid_p, C.c_uint64, C.POINTER(Detection_t), C.c_uint64, u64p]),
     "sspd_grid_set_stream": (C.c_int, [grid_p, C.c_void_p]),
     "sspd_grid_stream": (C.c_int, [grid_p, C.POINTER(C.c_void_p)]),
+    "sspd_scan_records": (C.c_int, [grid_p, C.c_void_p, C.c_uint64, C.c_int]),
     "sspd_device_alloc": (C.c_int, [C.c_int, C.c_uint64, C.POINTER(C.c_void_p)]),
     "sspd_device_free": (C.c_int, [C.c_int, C.c_void_p]),
+    "sspd_release_cached": (C.c_int, [C.c_int, C.POINTER(C.c_uint64)]),
     "sspd_enable_peer_access": (C.c_int, [C.c_int, C.POINTER(C.c_int)]),
     "sspd_grid_copy": (C.c_int, [grid_p, C.c_void_p, C.c_void_p, C.c_uint64, C.c_int]),
     "sspd_grid_synchronize": (C.c_int, [grid_p]),

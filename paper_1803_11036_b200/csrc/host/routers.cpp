@@ -72,6 +72,11 @@ void Routers::scan(std::size_t router, std::span<const IpPair> pairs) {
   check(sspd_scan(grids_[router], reinterpret_cast<const uint32_t*>(pairs.data()), pairs.size(), 0));
 }
 
+void Routers::scan_records(std::size_t router, std::span<const TraceRecord> records) {
+  if (records.empty()) return;
+  check(sspd_scan_records(grids_[router], reinterpret_cast<const uint32_t*>(records.data()), records.size(), 0));
+}
+
 std::vector<uint64_t> Routers::sent(std::size_t router) {
   uint64_t* dev = nullptr;
   check(sspd_shard_sent(grids_[router], &dev));

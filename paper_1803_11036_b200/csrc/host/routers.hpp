@@ -31,6 +31,7 @@ class Routers {
 
   std::size_t size() const { return grids_.size(); }
   void scan(std::size_t router, std::span<const IpPair> pairs);
+  void scan_records(std::size_t router, std::span<const TraceRecord> records);
   void merge();  // the two hops
   DetectionReport reconstruct(uint32_t k, double theta);
   void advance();

@@ -220,6 +220,14 @@ void Rsea::scan_batch(std::span<const IpPair> pairs, unsigned workers) {
   mirror_valid_ = false;
 }
 
+void Rsea::scan_records(std::span<const TraceRecord> records) {
+  if (records.empty()) return;
+  sync();
+  check(sspd_scan_records(h_, reinterpret_cast<const uint32_t*>(records.data()), records.size(), 0));
+  std::lock_guard<std::mutex> lk(*mu_);
+  mirror_valid_ = false;
+}
+
 void Rsea::scan_device(const IpPair* device_pairs, std::size_t n) {
   sync();
   check(sspd_scan(h_, reinterpret_cast<const uint32_t*>(device_pairs), n, 1));

@@ -1162,6 +1162,12 @@ __global__ void exact_emit_kernel(const unsigned long long* __restrict__ ckeys, 
 // ---------------------------------------------------------------------------
 // Element-wise helpers.
 
+// (ts, cip, oip) trace records (workload.hpp TraceRecord) -> (cip, oip) pairs.
+__global__ void records_to_pairs_kernel(const uint32_t* __restrict__ rec, uint64_t n, uint2* __restrict__ out) {
+  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x)
+    out[i] = make_uint2(rec[3 * i + 1], rec[3 * i + 2]);
+}
+
 __global__ void fill_u32_kernel(uint32_t* p, uint64_t n, uint32_t v) {
   for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
        i += (uint64_t)gridDim.x * blockDim.x)

@@ -8,12 +8,15 @@
 #include <algorithm>
 #include <atomic>
 #include <cmath>
+#include <condition_variable>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <functional>
 #include <map>
 #include <mutex>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "../../include/sspd_cuda.h"
@@ -92,20 +95,255 @@ struct ProfRec {
   uint64_t units;
 };
 
+// Device block cache.  A paper-geometry grid is ~1 GiB of stamps, pair set
+// and staging, and cudaMalloc + cudaFree of that costs ~70 ms -- more than
+// a whole run_detection of ten 1M-pair slots.  Blocks of >= 1 MiB go back to
+// a per-device cache when freed (best fit within 25%, at most
+// $SSPD_CACHE_BYTES per device, default 16 GiB; flushed when cudaMalloc runs
+// out of memory, and by sspd_release_cached).  cudaFree synchronises the
+// device; a cached free does the same unless the caller knows the block is
+// idle, so a block never changes hands while a kernel still uses it.
+class BlockCache {
+ public:
+  static BlockCache& get() {
+    static BlockCache* c = new BlockCache();  // never destroyed: usable from atexit paths
+    return *c;
+  }
+  cudaError_t alloc(void** p, size_t want) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    const size_t bytes = want < kMin ? want : (want + kMin - 1) / kMin * kMin;
+    {
+      std::lock_guard<std::mutex> lk(mu_);
+      auto& f = free_[dev];
+      auto it = f.lower_bound(bytes);
+      if (it != f.end() && it->first <= bytes + bytes / 4) {
+        *p = it->second;
+        cached_[dev] -= it->first;
+        live_[*p] = {it->first, dev};
+        f.erase(it);
+        return cudaSuccess;
+      }
+    }
+    cudaError_t e = cudaMalloc(p, bytes);
+    if (e == cudaErrorMemoryAllocation) {
+      cudaGetLastError();
+      release(dev);
+      e = cudaMalloc(p, bytes);
+    }
+    if (e != cudaSuccess) {
+      *p = nullptr;
+      return e;
+    }
+    std::lock_guard<std::mutex> lk(mu_);
+    live_[*p] = {bytes, dev};
+    return cudaSuccess;
+  }
+  void free(void* p, bool idle) {
+    if (!p) return;
+    std::unique_lock<std::mutex> lk(mu_);
+    auto it = live_.find(p);
+    if (it == live_.end()) {
+      lk.unlock();
+      cudaFree(p);
+      return;
+    }
+    const auto [bytes, dev] = it->second;
+    live_.erase(it);
+    if (bytes < kMin || cached_[dev] + bytes > cap_) {
+      lk.unlock();
+      cudaFree(p);
+      return;
+    }
+    lk.unlock();
+    if (!idle) cudaDeviceSynchronize();  // what cudaFree would have done
+    lk.lock();
+    free_[dev].emplace(bytes, p);
+    cached_[dev] += bytes;
+  }
+  // Free every cached block of `device` (-1: all devices).
+  void release(int device) {
+    std::vector<std::pair<int, void*>> out;
+    {
+      std::lock_guard<std::mutex> lk(mu_);
+      for (auto& [dev, f] : free_) {
+        if (device >= 0 && dev != device) continue;
+        for (auto& [bytes, p] : f) out.emplace_back(dev, p);
+        f.clear();
+        cached_[dev] = 0;
+      }
+    }
+    int cur = 0;
+    cudaGetDevice(&cur);
+    for (auto& [dev, p] : out) {
+      cudaSetDevice(dev);
+      cudaFree(p);
+    }
+    cudaSetDevice(cur);
+  }
+  uint64_t cached_bytes(int device) {
+    std::lock_guard<std::mutex> lk(mu_);
+    uint64_t t = 0;
+    for (auto& [dev, b] : cached_)
+      if (device < 0 || dev == device) t += b;
+    return t;
+  }
+
+ private:
+  BlockCache() {
+    if (const char* e = std::getenv("SSPD_CACHE_BYTES")) cap_ = std::strtoull(e, nullptr, 10);
+  }
+  static constexpr size_t kMin = size_t{1} << 20;
+  size_t cap_ = size_t{16} << 30;
+  std::mutex mu_;
+  std::map<int, std::multimap<size_t, void*>> free_;
+  std::map<int, size_t> cached_;
+  std::map<void*, std::pair<size_t, int>> live_;
+};
+
+// Pinned host buffers (scan staging of pageable input, small scratch):
+// cudaMallocHost/cudaFreeHost cost milliseconds, so freed buffers are kept
+// for reuse by exact size, up to 1 GiB in all.
+class PinnedCache {
+ public:
+  static PinnedCache& get() {
+    static PinnedCache* c = new PinnedCache();
+    return *c;
+  }
+  cudaError_t alloc(void** p, size_t bytes) {
+    {
+      std::lock_guard<std::mutex> lk(mu_);
+      auto it = free_.find(bytes);
+      if (it != free_.end()) {
+        *p = it->second;
+        cached_ -= bytes;
+        free_.erase(it);
+        live_[*p] = bytes;
+        return cudaSuccess;
+      }
+    }
+    cudaError_t e = cudaMallocHost(p, bytes);
+    if (e != cudaSuccess) {
+      *p = nullptr;
+      return e;
+    }
+    std::lock_guard<std::mutex> lk(mu_);
+    live_[*p] = bytes;
+    return cudaSuccess;
+  }
+  // The caller guarantees no copy still reads or writes the buffer.
+  void free(void* p) {
+    if (!p) return;
+    std::unique_lock<std::mutex> lk(mu_);
+    auto it = live_.find(p);
+    const size_t bytes = it == live_.end() ? 0 : it->second;
+    if (it != live_.end()) live_.erase(it);
+    if (bytes && cached_ + bytes <= (size_t{1} << 30)) {
+      free_.emplace(bytes, p);
+      cached_ += bytes;
+      return;
+    }
+    lk.unlock();
+    cudaFreeHost(p);
+  }
+  uint64_t release() {
+    std::vector<void*> out;
+    uint64_t n = 0;
+    {
+      std::lock_guard<std::mutex> lk(mu_);
+      for (auto& [b, p] : free_) out.push_back(p);
+      free_.clear();
+      n = cached_;
+      cached_ = 0;
+    }
+    for (void* p : out) cudaFreeHost(p);
+    return n;
+  }
+
+ private:
+  std::mutex mu_;
+  std::multimap<size_t, void*> free_;
+  std::map<void*, size_t> live_;
+  size_t cached_ = 0;
+};
+
+// Host worker threads for packing pageable input (scan_locked).  They sleep
+// on a condition variable between regions: OpenMP's spinning workers stole
+// the cores from the caller's own threads (profiles/r01_bench_api.md).
+class HostPool {
+ public:
+  static HostPool& get() {
+    static HostPool* p = new HostPool();
+    return *p;
+  }
+  // fn(t, T) for t in [0, T) on T threads, the caller being thread 0.
+  void run(unsigned T, const std::function<void(unsigned, unsigned)>& fn) {
+    T = std::min<unsigned>(T, static_cast<unsigned>(n_workers_) + 1);
+    if (T <= 1) {
+      fn(0, 1);
+      return;
+    }
+    std::lock_guard<std::mutex> one(call_mu_);  // one region at a time
+    {
+      std::lock_guard<std::mutex> lk(mu_);
+      fn_ = &fn;
+      T_ = T;
+      left_ = T - 1;
+      ++gen_;
+    }
+    cv_.notify_all();
+    fn(0, T);
+    std::unique_lock<std::mutex> lk(mu_);
+    done_.wait(lk, [&] { return left_ == 0; });
+    fn_ = nullptr;
+  }
+
+ private:
+  HostPool() {
+    const unsigned hw = std::max(2u, std::thread::hardware_concurrency());
+    n_workers_ = std::min(15u, hw - 1);
+    for (unsigned i = 0; i < n_workers_; ++i) std::thread([this, i] { loop(i + 1); }).detach();
+  }
+  void loop(unsigned id) {
+    uint64_t seen = 0;
+    std::unique_lock<std::mutex> lk(mu_);
+    for (;;) {
+      cv_.wait(lk, [&] { return gen_ != seen; });
+      seen = gen_;
+      if (id >= T_) continue;
+      const auto* f = fn_;
+      const unsigned T = T_;
+      lk.unlock();
+      (*f)(id, T);
+      lk.lock();
+      if (--left_ == 0) done_.notify_one();
+    }
+  }
+  unsigned n_workers_ = 0;
+  std::mutex call_mu_, mu_;
+  std::condition_variable cv_, done_;
+  const std::function<void(unsigned, unsigned)>* fn_ = nullptr;
+  unsigned T_ = 0, left_ = 0;
+  uint64_t gen_ = 0;
+};
+
+cudaError_t cache_alloc(void** p, size_t bytes) { return BlockCache::get().alloc(p, bytes); }
+void cache_free(void* p, bool idle = false) { BlockCache::get().free(p, idle); }
+
 struct DevBuf {
   void* p = nullptr;
   size_t bytes = 0;
   cudaError_t ensure(size_t want) {
     if (want <= bytes) return cudaSuccess;
-    if (p) cudaFree(p);
+    cache_free(p);
     p = nullptr;
     bytes = 0;
-    cudaError_t e = cudaMalloc(&p, want);
+    cudaError_t e = cache_alloc(&p, want);
     if (e == cudaSuccess) bytes = want;
     return e;
   }
-  void release() {
-    if (p) cudaFree(p);
+  void release(bool idle = false) {
+    cache_free(p, idle);
     p = nullptr;
     bytes = 0;
   }
@@ -146,6 +384,12 @@ struct sspd_grid {
   cudaStream_t copy_stream = nullptr;
   cudaEvent_t ev_copy[2] = {nullptr, nullptr}, ev_used[2] = {nullptr, nullptr};
   DevBuf stage[2];       // host pair staging
+  int stage_next = 0;    // the staging buffer the next host chunk goes to
+  void* host_stage[2] = {nullptr, nullptr};  // pinned: pageable input packed here as pairs
+  uint64_t host_stage_bytes = 0;
+  cudaEvent_t ev_hcopy[2] = {nullptr, nullptr};  // the H2D out of host_stage[i] finished
+  DevBuf stage_pairs[2]; // host trace records: their (cip, oip) pairs
+  DevBuf rec_pairs;      // device trace records: their pairs
   DevBuf counts, hot_cols, hot_rowcnt, hotT, tupA, tupB, misc;
   DevBuf hot_words, hot_chunks;  // parallel hot compaction scratch
   DevBuf meta, surv;            // reconstruction bookkeeping, survivors
@@ -517,7 +761,7 @@ uint64_t sspd_launch_count(void) { return g_launches.load(); }
 sspd_status sspd_device_alloc(int device, uint64_t bytes, void** ptr) {
   *ptr = nullptr;
   DeviceGuard dg(device);
-  if (cudaMalloc(ptr, std::max<uint64_t>(bytes, 16)) != cudaSuccess) {
+  if (cache_alloc(ptr, std::max<uint64_t>(bytes, 16)) != cudaSuccess) {
     cudaGetLastError();
     *ptr = nullptr;
     return fail(SSPD_CUDA_ERROR, "CUDA error: out of memory allocating " + std::to_string(bytes) + " bytes");
@@ -527,7 +771,16 @@ sspd_status sspd_device_alloc(int device, uint64_t bytes, void** ptr) {
 
 sspd_status sspd_device_free(int device, void* ptr) {
   DeviceGuard dg(device);
-  if (ptr) cudaFree(ptr);
+  cache_free(ptr);
+  return SSPD_OK;
+}
+
+sspd_status sspd_release_cached(int device, uint64_t* released) {
+  BlockCache& c = BlockCache::get();
+  if (released) *released = c.cached_bytes(device);
+  c.release(device);
+  const uint64_t pinned = PinnedCache::get().release();
+  if (released) *released += pinned;
   return SSPD_OK;
 }
 
@@ -631,11 +884,12 @@ sspd_status create_impl(int device, uint32_t q, uint32_t r, uint32_t delta, uint
   for (int i = 0; i < 2; ++i) {
     cudaEventCreateWithFlags(&g->ev_copy[i], cudaEventDisableTiming);
     cudaEventCreateWithFlags(&g->ev_used[i], cudaEventDisableTiming);
+    cudaEventCreateWithFlags(&g->ev_hcopy[i], cudaEventDisableTiming);
   }
   if (width != 32) {
     // narrow codes (all 0: nothing seen) and the always-on window ring
     const uint64_t bytes = g->geo.n_rec * (width / 8);
-    if (cudaMalloc(&g->codes, bytes) != cudaSuccess) {
+    if (cache_alloc((void**)&g->codes, bytes) != cudaSuccess) {
       cudaGetLastError();
       return cleanup("CUDA error: out of memory allocating " + std::to_string(bytes) + " bytes of stamps");
     }
@@ -645,7 +899,7 @@ sspd_status create_impl(int device, uint32_t q, uint32_t r, uint32_t delta, uint
     g->code_hi = width == 16 ? 0x7F7Fu : 255u;
     g->epoch0 = g->now;
     g->K = k_max;
-    if (cudaMalloc(&g->hist, (size_t)g->K * g->geo.ncells * 4) != cudaSuccess) {
+    if (cache_alloc((void**)&g->hist, (size_t)g->K * g->geo.ncells * 4) != cudaSuccess) {
       cudaGetLastError();
       return cleanup("CUDA error: out of memory (window ring)");
     }
@@ -653,18 +907,18 @@ sspd_status create_impl(int device, uint32_t q, uint32_t r, uint32_t delta, uint
         cudaMemsetAsync(g->hist, 0, (size_t)g->K * g->geo.ncells * 4, g->stream) != cudaSuccess)
       return cleanup("CUDA error: grid init");
     g->hist_valid = true;
-  } else if (cudaMalloc(&g->stamps, g->geo.n_rec * 4) != cudaSuccess) {
+  } else if (cache_alloc((void**)&g->stamps, g->geo.n_rec * 4) != cudaSuccess) {
     cudaGetLastError();
     return cleanup("CUDA error: out of memory allocating " + std::to_string(g->geo.n_rec * 4) +
                    " bytes of stamps");
   }
-  if (width == 32 && cudaMalloc(&g->touched, g->n_words * 4) != cudaSuccess) {
+  if (width == 32 && cache_alloc((void**)&g->touched, g->n_words * 4) != cudaSuccess) {
     cudaGetLastError();
     return cleanup("CUDA error: out of memory allocating the touched bitmap");
   }
-  if (cudaMalloc(&g->d_tabs, sizeof(HashTabs)) != cudaSuccess) return cleanup("CUDA error: tables");
-  if (cudaMallocHost(&g->pinned_small, 4096) != cudaSuccess ||
-      cudaMallocHost(&g->meta_host, sizeof(ReconMeta)) != cudaSuccess ||
+  if (cache_alloc((void**)&g->d_tabs, sizeof(HashTabs)) != cudaSuccess) return cleanup("CUDA error: tables");
+  if (PinnedCache::get().alloc(&g->pinned_small, 4096) != cudaSuccess ||
+      PinnedCache::get().alloc(reinterpret_cast<void**>(&g->meta_host), sizeof(ReconMeta)) != cudaSuccess ||
       g->meta.ensure(sizeof(ReconMeta)) != cudaSuccess)
     return cleanup("CUDA error: pinned scratch");
   HashTabs h = make_tabs(seed);
@@ -720,19 +974,21 @@ sspd_status sspd_grid_destroy(sspd_grid* g) {
   if (!g) return SSPD_OK;
   {
     DeviceGuard dg(g->device);
-    if (g->stream) cudaStreamSynchronize(g->stream);
-    if (g->copy_stream) cudaStreamSynchronize(g->copy_stream);
-    cudaFree(g->stamps);
-    cudaFree(g->codes);
-    cudaFree(g->touched);
-    cudaFree(g->hist);
-    cudaFree(g->d_tabs);
-    if (g->pinned_small) cudaFreeHost(g->pinned_small);
-    if (g->meta_host) cudaFreeHost(g->meta_host);
-    for (DevBuf* b : {&g->stage[0], &g->stage[1], &g->counts, &g->hot_cols, &g->hot_rowcnt, &g->hotT,
+    // peers may still read this grid (merges, relays): the whole device
+    // idles before its blocks go back to the cache
+    cudaDeviceSynchronize();
+    for (void* p : {(void*)g->stamps, (void*)g->codes, (void*)g->touched, (void*)g->hist, (void*)g->d_tabs})
+      cache_free(p, true);
+    PinnedCache::get().free(g->pinned_small);
+    PinnedCache::get().free(g->meta_host);
+    for (int i = 0; i < 2; ++i) {
+      PinnedCache::get().free(g->host_stage[i]);
+      if (g->ev_hcopy[i]) cudaEventDestroy(g->ev_hcopy[i]);
+    }
+    for (DevBuf* b : {&g->stage[0], &g->stage[1], &g->stage_pairs[0], &g->stage_pairs[1], &g->rec_pairs, &g->counts, &g->hot_cols, &g->hot_rowcnt, &g->hotT,
                       &g->tupA, &g->tupB, &g->misc, &g->meta, &g->surv, &g->pairset, &g->newpairs,
                       &g->newpairs_count, &g->bin_counts, &g->binned, &g->hot_words, &g->hot_chunks})
-      b->release();
+      b->release(true);
     for (auto& r : g->prof) {
       cudaEventDestroy(r.a);
       cudaEventDestroy(r.b);
@@ -769,7 +1025,7 @@ sspd_status sspd_grid_clone(const sspd_grid* src_c, int device, sspd_grid** out)
     g->pristine = src->pristine;
     if (src->K) {
       g->K = src->K;
-      CU(cudaMalloc(&g->hist, (size_t)g->K * g->geo.ncells * 4));
+      CU(cache_alloc((void**)&g->hist, (size_t)g->K * g->geo.ncells * 4));
       if (src->hist_valid) {
         CU(cudaMemcpyPeerAsync(g->hist, dev, src->hist, src->device, (size_t)g->K * g->geo.ncells * 4,
                                g->stream));
@@ -814,11 +1070,36 @@ sspd_status sspd_grid_synchronize(sspd_grid* g) {
   return SSPD_OK;
 }
 
+namespace {
+sspd_status scan_locked(sspd_grid* g, const uint32_t* pairs, uint64_t n, int pairs_on_device, int stride);
+}
+
 sspd_status sspd_scan(sspd_grid* g, const uint32_t* pairs, uint64_t n, int pairs_on_device) {
   if (n == 0) return SSPD_OK;
   if (!pairs) return fail(SSPD_INVALID_ARGUMENT, "scan_batch: null pairs");
   std::lock_guard<std::mutex> lk(g->mu);
   DeviceGuard dg(g->device);
+  return scan_locked(g, pairs, n, pairs_on_device, 2);
+}
+
+sspd_status sspd_scan_records(sspd_grid* g, const uint32_t* records, uint64_t n, int on_device) {
+  if (n == 0) return SSPD_OK;
+  if (!records) return fail(SSPD_INVALID_ARGUMENT, "scan_records: null records");
+  std::lock_guard<std::mutex> lk(g->mu);
+  DeviceGuard dg(g->device);
+  if (on_device) {  // to pairs on the device, then the pair path
+    if (g->rec_pairs.ensure(n * 8) != cudaSuccess) return fail(SSPD_CUDA_ERROR, "CUDA error: out of memory");
+    records_to_pairs_kernel<<<grid_blocks(g, n, 256, 8), 256, 0, g->stream>>>(records, n, g->rec_pairs.as<uint2>());
+    g_launches.fetch_add(1, std::memory_order_relaxed);
+    return scan_locked(g, g->rec_pairs.as<uint32_t>(), n, 1, 2);
+  }
+  return scan_locked(g, records, n, 0, 3);
+}
+
+namespace {
+// stride: u32 words per input item -- 2 for (cip, oip) pairs, 3 for
+// (ts, cip, oip) trace records (host input only; converted per chunk).
+sspd_status scan_locked(sspd_grid* g, const uint32_t* pairs, uint64_t n, int pairs_on_device, int stride) {
   g->pristine = false;
   const bool pow2 = (g->eta & (g->eta - 1)) == 0 && g->eta <= (1u << 31);
   // auto: pairs streamed from the host are PCIe-bound, so stamp them in place
@@ -1019,35 +1300,83 @@ sspd_status sspd_scan(sspd_grid* g, const uint32_t* pairs, uint64_t n, int pairs
   // scan of the one before even for a C1-sized (1M-pair) batch.
   const uint64_t chunk_pairs = std::min<uint64_t>(
       n, std::min<uint64_t>(4ull << 20, std::max<uint64_t>(256ull << 10, (n + 3) / 4)));
+  // Pageable sources: the driver's own staging copies them at ~11 GB/s
+  // (profiles/r01_bench_api.md); instead the host threads pack each chunk
+  // into a pinned buffer -- as 8-byte pairs, so records lose their ts on the
+  // way -- and DMA copies that at full PCIe speed, overlapping the packing
+  // of the next chunk.
+  cudaPointerAttributes attr{};
+  if (cudaPointerGetAttributes(&attr, pairs) != cudaSuccess) cudaGetLastError();
+  const bool pinned = attr.type == cudaMemoryTypeHost;
+  const bool pack = !pinned && n >= (64u << 10);
+  const int dstride = pack ? 2 : stride;  // u32 words per item as copied to the device
   for (int i = 0; i < 2; ++i)
-    if (g->stage[i].ensure(chunk_pairs * 8) != cudaSuccess)
+    if (g->stage[i].ensure(chunk_pairs * 4 * dstride) != cudaSuccess ||
+        (dstride == 3 && g->stage_pairs[i].ensure(chunk_pairs * 8) != cudaSuccess))
       return fail(SSPD_CUDA_ERROR, "CUDA error: out of memory (scan staging)");
+  if (pack && g->host_stage_bytes < chunk_pairs * 8) {
+    for (int i = 0; i < 2; ++i) {
+      CU(cudaEventSynchronize(g->ev_hcopy[i]));
+      PinnedCache::get().free(g->host_stage[i]);
+      g->host_stage[i] = nullptr;
+    }
+    g->host_stage_bytes = 0;
+    for (int i = 0; i < 2; ++i)
+      if (PinnedCache::get().alloc(&g->host_stage[i], chunk_pairs * 8) != cudaSuccess)
+        return fail(SSPD_CUDA_ERROR, "CUDA error: pinned scan staging");
+    g->host_stage_bytes = chunk_pairs * 8;
+  }
+  // Balanced chunks; the staging buffer alternates across calls too, so a
+  // call's first copy overlaps the previous call's last scan (ev_used[b]:
+  // the last scan that read stage[b] -- the copy stream must not overwrite
+  // staging still being read).
+  const uint64_t n_chunks = (n + chunk_pairs - 1) / chunk_pairs;
   uint64_t done = 0;
-  int buf = 0;
-  // the copy stream must not overwrite staging still read by earlier scans
-  CU(cudaEventRecord(g->ev_used[0], g->stream));
-  CU(cudaEventRecord(g->ev_used[1], g->stream));
-  while (done < n) {
-    const uint64_t cnt = std::min(chunk_pairs, n - done);
+  int& buf = g->stage_next;
+  for (uint64_t c = 0; c < n_chunks; ++c) {
+    const uint64_t cnt = n * (c + 1) / n_chunks - done;
+    const uint32_t* src = pairs + (uint64_t)stride * done;
+    if (pack) {
+      CU(cudaEventSynchronize(g->ev_hcopy[buf]));  // the last DMA out of this pinned buffer is done
+      auto* dst = static_cast<uint2*>(g->host_stage[buf]);
+      // ~64K items (0.5-0.8 MB) per thread
+      const unsigned threads = static_cast<unsigned>(std::min<uint64_t>(16, std::max<uint64_t>(1, cnt >> 16)));
+      HostPool::get().run(threads, [&](unsigned t, unsigned T) {
+        const uint64_t a = cnt * t / T, b = cnt * (t + 1) / T;
+        if (stride == 3) {
+          for (uint64_t i = a; i < b; ++i) dst[i] = make_uint2(src[3 * i + 1], src[3 * i + 2]);
+        } else if (b > a) {
+          std::memcpy(dst + a, src + 2 * a, (b - a) * 8);
+        }
+      });
+      src = static_cast<const uint32_t*>(g->host_stage[buf]);
+    }
     CU(cudaStreamWaitEvent(g->copy_stream, g->ev_used[buf], 0));
-    CU(cudaMemcpyAsync(g->stage[buf].p, pairs + 2 * done, cnt * 8, cudaMemcpyHostToDevice, g->copy_stream));
-  g->h2d_bytes += (cnt * 8);
+    CU(cudaMemcpyAsync(g->stage[buf].p, src, cnt * 4 * dstride, cudaMemcpyHostToDevice, g->copy_stream));
+    g->h2d_bytes += cnt * 4 * dstride;
     CU(cudaEventRecord(g->ev_copy[buf], g->copy_stream));
+    if (pack) CU(cudaEventRecord(g->ev_hcopy[buf], g->copy_stream));
     CU(cudaStreamWaitEvent(g->stream, g->ev_copy[buf], 0));
-    launch(g->stage[buf].as<uint32_t>(), cnt);
+    if (dstride == 3) {
+      records_to_pairs_kernel<<<grid_blocks(g, cnt, 256, 8), 256, 0, g->stream>>>(
+          g->stage[buf].as<uint32_t>(), cnt, g->stage_pairs[buf].as<uint2>());
+      g_launches.fetch_add(1, std::memory_order_relaxed);
+      launch(g->stage_pairs[buf].as<uint32_t>(), cnt);
+    } else {
+      launch(g->stage[buf].as<uint32_t>(), cnt);
+    }
     CU(cudaEventRecord(g->ev_used[buf], g->stream));
     done += cnt;
     buf ^= 1;
   }
-  // Pageable sources are consumed by the time cudaMemcpyAsync returns (the
-  // driver stages them), so the call can return at once; pinned ones are
-  // read by DMA later, and the caller may reuse its buffer on return
-  // (scan_batch semantics), so wait for those copies.
-  cudaPointerAttributes attr{};
-  if (cudaPointerGetAttributes(&attr, pairs) != cudaSuccess) cudaGetLastError();
-  if (attr.type == cudaMemoryTypeHost) CU(cudaStreamSynchronize(g->copy_stream));
+  // Pageable sources are consumed by the time the call returns (packed, or
+  // staged by the driver inside cudaMemcpyAsync); pinned ones are read by
+  // DMA later, and the caller may reuse its buffer on return (scan_batch
+  // semantics), so wait for those copies.
+  if (pinned) CU(cudaStreamSynchronize(g->copy_stream));
   return check_launch();
 }
+}  // namespace
 
 sspd_status sspd_commit(sspd_grid* g) {
   if (sspd_status w = wide_only(g, "commit")) return w;
@@ -1813,14 +2142,13 @@ sspd_status sspd_track_window(sspd_grid* g, uint32_t k_max) {
   sspd_status s = commit_locked(g);
   if (s) return s;
   if (g->hist) {
-    CU(cudaStreamSynchronize(g->stream));
-    cudaFree(g->hist);
+    cache_free(g->hist);
     g->hist = nullptr;
   }
   g->K = k_max;
   g->hist_valid = false;
   if (k_max) {
-    if (cudaMalloc(&g->hist, (size_t)k_max * g->geo.ncells * 4) != cudaSuccess) {
+    if (cache_alloc((void**)&g->hist, (size_t)k_max * g->geo.ncells * 4) != cudaSuccess) {
       cudaGetLastError();
       g->K = 0;
       return fail(SSPD_CUDA_ERROR, "CUDA error: out of memory (window ring)");

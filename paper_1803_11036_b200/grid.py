@@ -157,6 +157,26 @@ class Grid:
             return
         check(self._L.sspd_scan(self._h, p.ctypes.data_as(C.c_void_p), p.shape[0], 0))
 
+    def scan_records(self, records):
+        """(n,3) uint32 trace records (ts, cip, oip) -- a host array, or a CUDA
+        tensor on this grid's device; ts is ignored (the caller picks a slot's
+        records).  No host-side conversion to pairs (sspd_scan_records)."""
+        if hasattr(records, "data_ptr") and getattr(records, "is_cuda", False):
+            import torch
+
+            cur = torch.cuda.current_stream(records.device)
+            s = torch.cuda.ExternalStream(self.stream_handle(), device=records.device)
+            if s.cuda_stream != cur.cuda_stream:
+                s.wait_stream(cur)
+            check(self._L.sspd_scan_records(self._h, C.c_void_p(records.data_ptr()), records.numel() // 3, 1))
+            if s.cuda_stream != cur.cuda_stream:
+                cur.wait_stream(s)
+            return
+        r = np.ascontiguousarray(records, dtype=np.uint32).reshape(-1, 3)
+        if r.shape[0] == 0:
+            return
+        check(self._L.sspd_scan_records(self._h, r.ctypes.data_as(C.c_void_p), r.shape[0], 0))
+
     def scan_host_ptr(self, host_ptr: int, n_pairs: int):
         """Host (ideally pinned) buffer of n (cip, oip) pairs; copied in chunks."""
         check(self._L.sspd_scan(self._h, C.c_void_p(host_ptr), n_pairs, 0))
@@ -492,3 +512,11 @@ def exact_counts(segments, min_count: int = 1, distinct_hint: int = 0, device: i
 
 def launch_count() -> int:
     return int(load().sspd_launch_count())
+
+
+def release_cached(device: int = -1) -> int:
+    """Free the device blocks closed grids left for reuse (sspd_release_cached);
+    returns the bytes freed.  Call before handing the memory to torch."""
+    n = C.c_uint64()
+    check(load().sspd_release_cached(device, C.byref(n)))
+    return n.value

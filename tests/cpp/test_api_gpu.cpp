@@ -102,6 +102,23 @@ TEST_CASE("scan_batch is worker-count, batch and permutation invariant") {
   CHECK_THROWS_AS(fresh.scan_batch(pairs, 0), std::invalid_argument);
 }
 
+TEST_CASE("scan_records (B200 extension) equals scan_batch of the records' pairs") {
+  std::mt19937_64 rng(22);
+  std::vector<TraceRecord> recs(1100003);
+  std::vector<IpPair> pairs(recs.size());
+  for (std::size_t i = 0; i < recs.size(); ++i) {
+    recs[i] = {static_cast<uint32_t>(i), static_cast<uint32_t>(rng()), static_cast<uint32_t>(rng() % 5000)};
+    pairs[i] = {recs[i].cip, recs[i].oip};
+  }
+  Rsea a(kCfg, kEta), b(kCfg, kEta);
+  a.scan_batch(pairs, 1);
+  b.scan_records(recs);
+  b.scan_records({});
+  CHECK(a == b);
+  b.scan_records(std::span<const TraceRecord>(recs).subspan(17, 1001));
+  CHECK(a == b);  // repeats within the slot
+}
+
 TEST_CASE("advance_slot: saturated fresh grid, equals element-wise increment") {
   Rsea g(kCfg, kEta);
   g.advance_slot(4);

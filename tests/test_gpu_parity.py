@@ -637,6 +637,36 @@ def test_three_routers_push_exchange_on_one_device(gpu):
             nd.advance()
 
 
+@pytest.mark.parametrize("mode", [(1, -1), (2, -1), (3, -1), (-1, -1)], ids=["direct", "dedup", "binned", "auto"])
+def test_scan_records(gpu, mode):
+    """Trace records scanned as they lie (sspd_scan_records): host arrays
+    split into several staged chunks, ragged device slices, and an empty
+    input -- the same grid as scanning the (cip, oip) pairs."""
+    import torch
+
+    g, o = make_pair(gpu, DESK, 0xA7)
+    g.scan_mode(*mode)
+    rng = O.Mt64(0xA7)
+    for n in [1_200_001, 3, 0]:
+        p = rng.pairs(n)
+        rec = np.empty((n, 3), np.uint32)
+        rec[:, 0] = np.arange(n, dtype=np.uint32)
+        rec[:, 1:] = p
+        g.scan_records(rec)
+        o.scan(p)
+    assert np.array_equal(g.cells(), o.cells())
+    g.advance_slot()
+    o.advance()
+    p = rng.pairs(50_000)
+    rec = np.concatenate([np.full((50_000, 1), 7, np.uint32), p], 1)
+    dev = torch.from_numpy(rec.view(np.int32)).cuda()
+    for off, n in [(1, 1), (2, 5), (9, 4321), (0, 0), (4331, 45_669)]:
+        g.scan_records(dev[off:off + n])
+        o.scan(p[off:off + n])
+    assert np.array_equal(g.cells(), o.cells())
+    assert np.array_equal(g.active_counts(2), o.active_counts(2))
+
+
 @pytest.mark.parametrize("mode", [(1, -1), (2, -1), (-1, -1)], ids=["direct", "dedup", "auto"])
 def test_scan_input_forms(gpu, mode):
     """Ragged and misaligned device slices (the 16-byte vector path and the
