@@ -183,6 +183,25 @@ TEST_CASE("trace I/O round trips and errors") {
   t.pop_back();
   std::stringstream tr(t);
   CHECK_THROWS_WITH_SUBSTR(read_trace(tr, TraceFormat::kBinary), "truncated record at position 2");
+
+  // traces longer than the reader's 65536-record blocks: exact round trip,
+  // and error positions past a block boundary
+  std::vector<TraceRecord> big(200003);
+  for (std::size_t i = 0; i < big.size(); ++i)
+    big[i] = {static_cast<uint32_t>(i / 7), static_cast<uint32_t>(i * 2654435761u), static_cast<uint32_t>(~i)};
+  std::stringstream bs;
+  write_trace(big, bs, TraceFormat::kBinary);
+  CHECK(bs.str().size() == 8 + 12 * big.size());
+  const std::string bytes = bs.str();
+  std::stringstream bin(bytes);
+  CHECK(read_trace(bin, TraceFormat::kBinary) == big);
+  std::stringstream cut(bytes.substr(0, 8 + 12 * 65536 + 5));
+  CHECK_THROWS_WITH_SUBSTR(read_trace(cut, TraceFormat::kBinary), "truncated record at position 65536");
+  std::vector<TraceRecord> back(big);
+  back[131073].ts = 0;
+  std::stringstream rs;
+  write_trace(back, rs, TraceFormat::kBinary);
+  CHECK_THROWS_WITH_SUBSTR(read_trace(rs, TraceFormat::kBinary), "timestamp regression at record 131073");
 }
 
 TEST_CASE("orientation by core-network prefixes") {
