@@ -65,17 +65,25 @@ def run_detection(shards, q=14, r=5, delta=6, seed=0, eta=2048, mu=1.0, k=300, s
     # reconstruction is queued and collected after the next slot's scan
     pipelined = union and not recursive and candidate_cap <= (1 << 26)
     pending = None
+    # time-sorted shards: each slot is a contiguous run of records, scanned
+    # where it lies (sspd_scan_records); otherwise select the slot's records
+    ordered = all(len(so) < 2 or bool(np.all(so[1:] >= so[:-1])) for so in slot_of)
+    bounds = [np.searchsorted(so, np.arange(n_slots + 1, dtype=np.uint64)) if ordered else None
+              for so in slot_of]
     for slot in range(n_slots):
-        parts = [s[so == slot][:, 1:] for s, so in zip(shards, slot_of)]
+        if ordered:
+            parts = [s[b[slot]:b[slot + 1]] for s, b in zip(shards, bounds)]
+        else:
+            parts = [s[so == slot] for s, so in zip(shards, slot_of)]
         if union:
-            batch = np.concatenate(parts) if parts else np.zeros((0, 2), np.uint32)
-            if len(batch):
-                nodes[0].scan_batch(batch)
+            for p in parts:
+                if len(p):
+                    nodes[0].scan_records(p)
             target = nodes[0]
         else:
             for g, p in zip(nodes, parts):
                 if len(p):
-                    g.scan_batch(p)
+                    g.scan_records(p)
             target = merge_rseas(nodes, PAPER_MAX)
             target.candidate_cap = candidate_cap
         if pending is not None:

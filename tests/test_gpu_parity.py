@@ -585,6 +585,14 @@ def test_run_detection_matches_reference_fixture(gpu, label, shards, policy):
     assert len(reps) == want["n_reports"]
     got = [[s, d.cip, d.estimate.hex()] for s, dets in reps for d in dets]
     assert got == want["rows"]
+    if shards > 1:
+        # slot runs scanned where they lie vs records selected per slot (an
+        # unsorted shard takes the selection path): the same reports
+        rng = np.random.default_rng(5)
+        mixed = [p[rng.permutation(len(p))] for p in parts]
+        again = gpu.run_detection(mixed, q=10, r=5, delta=8, seed=0x5eed, eta=256, k=5, theta=128.0,
+                                  policy=policy)
+        assert [[s, d.cip, d.estimate.hex()] for s, dets in again for d in dets] == want["rows"]
 
 
 def test_three_routers_push_exchange_on_one_device(gpu):
