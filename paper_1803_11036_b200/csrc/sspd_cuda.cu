@@ -156,7 +156,13 @@ class BlockCache {
       return;
     }
     lk.unlock();
-    if (!idle) cudaDeviceSynchronize();  // what cudaFree would have done
+    if (!idle) {  // what cudaFree would have done: the block's device idles
+      int cur = 0;
+      cudaGetDevice(&cur);
+      if (cur != dev) cudaSetDevice(dev);
+      cudaDeviceSynchronize();
+      if (cur != dev) cudaSetDevice(cur);
+    }
     lk.lock();
     free_[dev].emplace(bytes, p);
     cached_[dev] += bytes;

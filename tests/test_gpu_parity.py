@@ -956,3 +956,21 @@ def test_relayed_sharded_routers_on_one_device(gpu, world):
         for g in grids:
             g.advance_slot()
         o.advance()
+
+
+def test_block_cache_reuse_and_release(gpu):
+    """Closed grids leave their device blocks in the cache (sspd_release_cached);
+    a new grid of the same geometry reuses them and starts pristine, as a
+    freshly allocated grid does."""
+    g = gpu.Grid(**DESK, seed=0x5EED)
+    g.scan_batch(O.Mt64(3).pairs(50_000))
+    g.close()
+    h, o = make_pair(gpu, DESK, 0x5EED)  # may get g's blocks back: they must read as never seen
+    assert np.array_equal(h.cells(), o.cells())
+    p = O.Mt64(4).pairs(20_000)
+    h.scan_batch(p)
+    o.scan(p)
+    assert np.array_equal(h.cells(), o.cells())
+    h.close()
+    assert gpu.release_cached() > 0
+    assert gpu.release_cached() == 0
