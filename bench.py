@@ -313,7 +313,11 @@ def main():
     from paper_1803_11036_b200 import dist as PD
 
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
+        import datetime
+
+        # a wedged collective fails the run after 5 minutes instead of NCCL's 10
+        dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"),
+                                timeout=datetime.timedelta(seconds=int(os.environ.get("SSPD_DIST_TIMEOUT", "300"))))
     torch.cuda.set_device(local)
     dev = local
     L = P.load()
