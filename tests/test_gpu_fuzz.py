@@ -80,3 +80,50 @@ def test_random_case(gpu, case):
         g.advance_slot(slots=adv)
         for _ in range(adv):
             o.advance()
+
+
+@pytest.mark.timeout(300)
+@pytest.mark.parametrize("case", range(16))
+def test_random_run_detection(gpu, case):
+    """run_detection end to end (pipeline.cpp:16-89) against the oracle's: random
+    geometry, shard count, merge policy, window (k, mu, start), traffic with
+    planted super points, time-sorted shards scanned slot run by slot run."""
+    rng = np.random.default_rng(0x5D37 + case)
+    geo = random_geometry(rng)
+    seed = int(rng.integers(0, 2**63))
+    k = int(rng.integers(1, 7))
+    mu = float(rng.choice([1.0, 2.0, 3.5]))
+    start = int(rng.integers(0, 1000))
+    theta = float(max(1.0, geo["eta"] * rng.uniform(0.3, 0.8)))
+    n_shards = int(rng.integers(1, 5))
+    policy = int(rng.integers(0, 2))
+    mt = O.Mt64(seed & 0xFFFFFFFF)
+    hosts = [int(mt.next()) & 0xFFFFFFFF for _ in range(int(rng.integers(1, 4)))]
+    slots = int(rng.integers(2, 7))
+    recs = []
+    for s in range(slots):
+        parts = [mt.pairs(int(rng.integers(0, 2000)))]
+        for h in hosts:
+            if rng.random() < 0.7:
+                fan = int(rng.integers(1, 2 * geo["eta"] + 2))
+                parts.append(np.stack([np.full(fan, h, np.uint32), mt.draw(fan).astype(np.uint32)], 1))
+        p = np.concatenate(parts)
+        p = p[rng.permutation(len(p))]
+        ts = start + np.floor(s * mu + rng.uniform(0, mu, len(p)) * 0.999).astype(np.uint64)
+        ts.sort()
+        recs.append(np.concatenate([ts.astype(np.uint32)[:, None], p], 1))
+    trace = np.concatenate(recs)
+    owner = rng.integers(0, n_shards, len(trace))
+    shards = [trace[owner == i] for i in range(n_shards)]  # each stays time sorted
+    args = dict(q=geo["q"], r=geo["r"], delta=geo["delta"], seed=seed, eta=geo["eta"], mu=mu, k=k,
+                start=start, theta=theta, policy=policy)
+    try:
+        n_slots, want = O.run_detection(shards, **args)
+    except O.CandidateOverflow:
+        with pytest.raises(gpu.CandidateOverflow):
+            gpu.run_detection(shards, **args)
+        return
+    got = gpu.run_detection(shards, **args)
+    assert len(got) == n_slots
+    assert [(s, d.cip, d.estimate) for s, dets in got for d in dets] == \
+           [(s, d.cip, d.estimate) for s, d in want], (case, geo, n_shards, policy, k, mu)
