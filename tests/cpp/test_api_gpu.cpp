@@ -561,6 +561,21 @@ TEST_CASE("differential: run_detection reports equal the reference (single, 4 sh
   RunConfig rec = rc;
   rec.strategy = Strategy::kRecursive;
   expect_same(run_detection({w.trace}, rec), ref_pipeline({w.trace}, rec));
+  // shards that are not time sorted (the record-by-record walk; sorted shards
+  // take a binary search per slot) and a trace with empty slots
+  auto unsorted = shards;
+  std::mt19937_64 rng(83);
+  for (int i = 0; i < 40; ++i) {
+    auto& s = unsorted[rng() % unsorted.size()];
+    std::swap(s[rng() % s.size()], s[rng() % s.size()]);
+  }
+  expect_same(run_detection(unsorted, rc), ref_pipeline(unsorted, rc));
+  expect_same(run_detection(unsorted, pm), ref_pipeline(unsorted, pm));
+  std::vector<TraceRecord> gappy;
+  for (const TraceRecord& r : w.trace)
+    if (r.ts % 3 != 1) gappy.push_back({r.ts * 2, r.cip, r.oip});
+  expect_same(run_detection({gappy}, rc), ref_pipeline({gappy}, rc));
+  expect_same(run_detection(split(gappy, 3, 85), rc), ref_pipeline(split(gappy, 3, 85), rc));
 }
 
 TEST_CASE("differential: acceptance end-to-end at the paper's parameters") {
