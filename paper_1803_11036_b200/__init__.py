@@ -13,9 +13,10 @@ from .grid import (BASE_NOW, Detection, Grid, device_count, estimate_cardinality
                    hot_cutoff, import_snapshot, launch_count, merge_rseas, release_cached)
 
 from .pipeline import run_detection, validate_config
+from .trace import read_trace, write_trace
 
 __all__ = [
-    "run_detection", "validate_config",
+    "run_detection", "validate_config", "read_trace", "write_trace",
     "BASE_NOW", "CandidateOverflow", "CudaError", "Detection", "Grid", "InvalidArgument",
     "NoDevice", "OutOfRange", "PAPER_MAX", "SspdError", "UNION_MIN", "device_count",
     "estimate_cardinality", "exact_counts", "export_snapshot", "hot_cutoff", "import_snapshot", "launch_count",

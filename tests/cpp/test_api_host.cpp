@@ -184,6 +184,16 @@ TEST_CASE("trace I/O round trips and errors") {
   std::stringstream tr(t);
   CHECK_THROWS_WITH_SUBSTR(read_trace(tr, TraceFormat::kBinary), "truncated record at position 2");
 
+  // parse_ipv4's forms, as trace.py mirrors them (tests/test_trace_io.py)
+  std::stringstream forms("# c\n\n7, 16909060,+1.2.3.4.\n8,1.2.3.4,8.8.8.8\r\n");
+  const std::vector<TraceRecord> want_forms{{7, 16909060u, 16909060u}, {8, 16909060u, 0x08080808u}};
+  CHECK(read_trace(forms, TraceFormat::kText) == want_forms);
+  for (const char* bad : {"1,1.2.3,4\n", "1,1.2.3.256,4\n", "1,1..2.3,4\n", "1,4294967296,4\n", "x,1,2\n",
+                          "7,1.2.3.4.\r,1\n"}) {
+    std::stringstream b(bad);
+    CHECK_THROWS_WITH_SUBSTR(read_trace(b, TraceFormat::kText), "malformed line 1");
+  }
+
   // traces longer than the reader's 65536-record blocks: exact round trip,
   // and error positions past a block boundary
   std::vector<TraceRecord> big(200003);
