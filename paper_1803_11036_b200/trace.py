@@ -64,9 +64,32 @@ def _format_ipv4(ip: int) -> str:
     return f"{ip >> 24}.{ip >> 16 & 255}.{ip >> 8 & 255}.{ip & 255}"
 
 
-def read_trace(src, fmt: str = "binary") -> np.ndarray:
-    """src: a path or a binary file object."""
+def read_trace(src, fmt: str = "binary", mmap: bool = False) -> np.ndarray:
+    """src: a path or a binary file object.  mmap=True (a binary trace at a
+    path): a read-only memory map of the records, checked like a read, so
+    that run_detection / Grid.scan_records pack slot runs straight from the
+    page cache into pinned staging, with no copy of the whole trace."""
     if isinstance(src, (str, os.PathLike)):
+        if mmap and fmt == "binary":
+            size = os.path.getsize(src)
+            with open(src, "rb") as f:
+                head = f.read(8)
+            if size == 0:
+                return np.zeros((0, 3), np.uint32)
+            if len(head) < 8 or head[:4] != MAGIC:
+                raise RuntimeError("trace: bad magic")
+            if int.from_bytes(head[4:8], "little") != VERSION:
+                raise RuntimeError("trace: unsupported version")
+            whole = (size - 8) // 12
+            if whole == 0:
+                if size > 8:
+                    raise RuntimeError("trace: truncated record at position 0")
+                return np.zeros((0, 3), np.uint32)
+            recs = np.memmap(src, dtype="<u4", mode="r", offset=8, shape=(whole, 3))
+            _check_order(recs[:, 0])
+            if (size - 8) % 12:
+                raise RuntimeError(f"trace: truncated record at position {whole}")
+            return recs
         with open(src, "rb") as f:
             return read_trace(f, fmt)
     if fmt == "binary":

@@ -585,6 +585,18 @@ def test_run_detection_matches_reference_fixture(gpu, label, shards, policy):
     assert len(reps) == want["n_reports"]
     got = [[s, d.cip, d.estimate.hex()] for s, dets in reps for d in dets]
     assert got == want["rows"]
+    if shards == 1:
+        # the trace memory-mapped from an SSPT file: slot runs packed from the page cache
+        import tempfile
+
+        with tempfile.TemporaryDirectory() as d:
+            path = os.path.join(d, "t.sspt")
+            gpu.write_trace(trace, path)
+            mapped = gpu.read_trace(path, mmap=True)
+            again = gpu.run_detection([mapped], q=10, r=5, delta=8, seed=0x5eed, eta=256, k=5, theta=128.0,
+                                      policy=policy)
+            del mapped
+        assert [[s, d.cip, d.estimate.hex()] for s, dets in again for d in dets] == want["rows"]
     if shards > 1:
         # slot runs scanned where they lie vs records selected per slot (an
         # unsorted shard takes the selection path): the same reports

@@ -16,8 +16,13 @@ def test_cli_traces_round_trip(work):  # noqa: F811
         "-o", work / "trace.txt")
     binary = T.read_trace(work / "trace.bin")
     text = T.read_trace(work / "trace.txt", "text")
+    mapped = T.read_trace(work / "trace.bin", mmap=True)
     assert binary.shape[1] == 3 and len(binary) > 1000
-    assert np.array_equal(binary, text)
+    assert np.array_equal(binary, text) and np.array_equal(binary, mapped)
+    data = (work / "trace.bin").read_bytes()
+    (work / "cut.bin").write_bytes(data[:-7])
+    with pytest.raises(RuntimeError, match=f"truncated record at position {len(binary) - 1}"):
+        T.read_trace(work / "cut.bin", mmap=True)
     for fmt, name in [("binary", "trace.bin"), ("text", "trace.txt")]:
         out = io.BytesIO()
         T.write_trace(binary, out, fmt)
