@@ -117,13 +117,17 @@ sspd_status sspd_grid_synchronize(sspd_grid* g);
 /* Rsea::scan_batch / Rsea::update (rsea.hpp:71-75; rsea.cpp:29-53).  `pairs`
  * holds n (cip, oip) u32 pairs interleaved (the IpPair layout, rsea.hpp:14-17).
  * pairs_on_device != 0: device pointer on the grid's device, consumed in place;
- * otherwise a host pointer, copied in chunks (async when pinned).  Order- and
- * batch-invariant like the reference. */
+ * otherwise a host pointer, copied in chunks on a copy stream that overlaps
+ * the scan.  Pinned input is copied by DMA as it lies (the call returns once
+ * the copies are done); pageable input (>= 64K pairs) is packed into pinned
+ * staging by host worker threads first.  Order- and batch-invariant like
+ * the reference. */
 sspd_status sspd_scan(sspd_grid* g, const uint32_t* pairs, uint64_t n, int pairs_on_device);
 /* The same over n (ts, cip, oip) trace records (workload.hpp TraceRecord,
- * 12 bytes each; ts is ignored -- the caller picks a slot's records): the
- * records go to the device as they are and are turned into pairs there, so a
- * time-sorted trace is scanned slot by slot without a host-side copy. */
+ * 12 bytes each; ts is ignored -- the caller picks a slot's records).  Device
+ * and pinned records are turned into pairs on the device; pageable ones are
+ * packed as pairs while being staged (8 of every 12 bytes cross PCIe).  A
+ * time-sorted trace is scanned slot run by slot run, with no copy of it. */
 sspd_status sspd_scan_records(sspd_grid* g, const uint32_t* records, uint64_t n, int on_device);
 
 /* ---- QUIESCENT phase ---- */
