@@ -119,7 +119,7 @@ sspd_status sspd_grid_synchronize(sspd_grid* g);
  * pairs_on_device != 0: device pointer on the grid's device, consumed in place;
  * otherwise a host pointer, copied in chunks on a copy stream that overlaps
  * the scan.  Pinned input is copied by DMA as it lies (the call returns once
- * the copies are done); pageable input (>= 64K pairs) is packed into pinned
+ * the copies are done); pageable input (>= 4096 pairs) is packed into pinned
  * staging by host worker threads first.  Order- and batch-invariant like
  * the reference. */
 sspd_status sspd_scan(sspd_grid* g, const uint32_t* pairs, uint64_t n, int pairs_on_device);

@@ -1314,7 +1314,7 @@ sspd_status scan_locked(sspd_grid* g, const uint32_t* pairs, uint64_t n, int pai
   cudaPointerAttributes attr{};
   if (cudaPointerGetAttributes(&attr, pairs) != cudaSuccess) cudaGetLastError();
   const bool pinned = attr.type == cudaMemoryTypeHost;
-  const bool pack = !pinned && n >= (64u << 10);
+  const bool pack = !pinned && n >= 4096;  // tiny batches: the driver's staged copy is as fast
   const int dstride = pack ? 2 : stride;  // u32 words per item as copied to the device
   for (int i = 0; i < 2; ++i)
     if (g->stage[i].ensure(chunk_pairs * 4 * dstride) != cudaSuccess ||
