@@ -451,6 +451,33 @@ TEST_CASE("concurrent SCAN-phase callers (rsea.hpp:49-51) give the serial grid")
   CHECK(shared == serial);
 }
 
+TEST_CASE("concurrent scans into separate grids share the host packing pool") {
+  // pageable batches >= 4096 pairs are packed into pinned staging by one
+  // process-wide worker pool; four threads scanning four grids at once (pairs
+  // and records, several chunks each) must each get its serial grid
+  std::mt19937_64 rng(95);
+  std::vector<TraceRecord> recs(700001);
+  for (auto& r : recs) r = {0, static_cast<uint32_t>(rng()), static_cast<uint32_t>(rng() % 100000)};
+  std::vector<IpPair> pairs(recs.size());
+  for (std::size_t i = 0; i < recs.size(); ++i) pairs[i] = {recs[i].cip, recs[i].oip};
+  Rsea serial(kCfg, kEta);
+  serial.scan_batch(pairs, 1);
+  std::vector<Rsea> grids;
+  for (int t = 0; t < 4; ++t) grids.emplace_back(kCfg, kEta);
+  std::vector<std::thread> th;
+  for (int t = 0; t < 4; ++t)
+    th.emplace_back([&, t] {
+      for (int rep = 0; rep < 3; ++rep) {
+        if (t % 2)
+          grids[t].scan_records(recs);
+        else
+          grids[t].scan_batch(pairs, 1);
+      }
+    });
+  for (auto& x : th) x.join();
+  for (const Rsea& g : grids) CHECK(g == serial);
+}
+
 TEST_CASE("Rsea value semantics: copies are independent, moves keep the state") {
   std::mt19937_64 rng(91);
   Rsea a(kCfg, kEta);
