@@ -4,7 +4,9 @@
 // snapshot {export, info, merge}.  Exit codes: 2 configuration, 3 input,
 // 4 candidate cap.  The reference parses with CLI11 (not vendored); this
 // parser accepts the same spellings ("--k 5" and "--k=5", "-o FILE").
+#include <exception>
 #include <fstream>
+#include <future>
 #include <iostream>
 #include <map>
 #include <set>
@@ -145,10 +147,32 @@ void print_truth(const sspd::GroundTruth& t, std::ostream& o, uint32_t min_count
   }
 }
 
+// One shard per router file.  Files are parsed on their own threads (text
+// parsing and 12-byte record decoding are CPU-bound); "-" is read on this
+// thread, in order.  Errors are rethrown in argument order, so the first bad
+// file named on the command line is the one reported, as with a serial load.
+std::vector<std::vector<sspd::TraceRecord>> load_shards(const std::vector<std::string>& paths,
+                                                        sspd::TraceFormat f) {
+  std::vector<std::future<std::vector<sspd::TraceRecord>>> pending(paths.size());
+  for (std::size_t i = 0; i < paths.size(); ++i)
+    if (paths[i] != "-" && paths.size() > 1)
+      pending[i] = std::async(std::launch::async, [&paths, i, f] { return load_trace(paths[i], f); });
+  std::vector<std::vector<sspd::TraceRecord>> shards(paths.size());
+  std::exception_ptr first;
+  for (std::size_t i = 0; i < paths.size(); ++i) {
+    try {
+      shards[i] = pending[i].valid() ? pending[i].get() : load_trace(paths[i], f);
+    } catch (...) {
+      if (!first) first = std::current_exception();
+    }
+  }
+  if (first) std::rethrow_exception(first);
+  return shards;
+}
+
 int detect(const Args& a, const Common& c) {
   if (a.pos.empty()) throw UsageError("detect: trace file(s) required");
-  std::vector<std::vector<sspd::TraceRecord>> shards;
-  for (const auto& p : a.pos) shards.push_back(load_trace(p, c.trace_format()));
+  const auto shards = load_shards(a.pos, c.trace_format());
   const auto reports = sspd::run_detection(shards, c.rc);
   Out out(out_path(a));
   for (const auto& r : reports)

@@ -71,6 +71,21 @@ def test_exit_codes(work):
     assert p.returncode == 3
 
 
+def test_detect_shard_errors_in_argument_order(work):
+    """Shard files load concurrently; the first bad file named is the one reported."""
+    good = (work / "trace.bin").read_bytes()
+    (work / "trunc.bin").write_bytes(good[:8 + 12 * 3 + 5])
+    (work / "magic.bin").write_bytes(b"XXXX" + good[4:])
+    p = run("detect", work / "trace.bin", work / "trunc.bin", work / "magic.bin", work / "missing.bin",
+            "--desk", "-o", os.devnull, check=False)
+    assert p.returncode == 3 and "truncated record at position 3" in p.stderr, p.stderr
+    p = run("detect", work / "magic.bin", work / "trunc.bin", "--desk", "-o", os.devnull, check=False)
+    assert p.returncode == 3 and "bad magic" in p.stderr and "truncated" not in p.stderr, p.stderr
+    p = run("detect", work / "trace.bin", work / "missing.bin", work / "trunc.bin", "--desk",
+            "-o", os.devnull, check=False)
+    assert p.returncode == 3 and "missing.bin" in p.stderr, p.stderr
+
+
 @pytest.mark.gpu
 def test_detect_and_snapshots(gpu, work):
     run("detect", work / "trace.bin", "--desk", "--k", 5, "--seed", "5eed", "-o", work / "r.csv")
