@@ -9,6 +9,7 @@
 #include <cstring>
 #include <exception>
 #include <new>
+#include <sstream>
 #include <string>
 #include <vector>
 
@@ -245,6 +246,26 @@ size_t ref_synth_trace(const uint32_t* planted, size_t n_planted, uint32_t bg_ho
     recs[3 * i + 2] = res.trace[i].oip;
   }
   return res.trace.size();
+}
+
+// read_trace (workload.cpp:66-96) over an in-memory text or binary trace.
+// Returns 0 and the record count in *n (records filled up to cap_recs), or 3
+// with the reference's message in ref_last_error().
+int ref_read_trace(const char* data, size_t len, int binary, uint32_t* recs, size_t cap_recs,
+                   size_t* n) {
+  try {
+    std::istringstream in(std::string(data, len), std::ios::in | std::ios::binary);
+    const auto t = read_trace(in, binary ? TraceFormat::kBinary : TraceFormat::kText);
+    for (size_t i = 0; i < t.size() && i < cap_recs; ++i) {
+      recs[3 * i] = t[i].ts;
+      recs[3 * i + 1] = t[i].cip;
+      recs[3 * i + 2] = t[i].oip;
+    }
+    *n = t.size();
+    return 0;
+  } catch (const std::exception& e) {
+    return fail(e, 3);
+  }
 }
 
 }  // extern "C"

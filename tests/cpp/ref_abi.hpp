@@ -24,4 +24,6 @@ int ref_run_detection(uint32_t q, uint32_t r, uint32_t delta, uint64_t seed, uin
 size_t ref_synth_trace(const uint32_t* planted, size_t n_planted, uint32_t bg_hosts, double zipf,
                        uint32_t pairs_per_slot, uint32_t max_distinct, uint32_t slots, uint64_t seed,
                        double mu, uint32_t k, uint32_t start, uint32_t* recs, size_t cap_recs);
+int ref_read_trace(const char* data, size_t len, int binary, uint32_t* recs, size_t cap_recs,
+                   size_t* n);
 }

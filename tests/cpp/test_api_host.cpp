@@ -4,6 +4,7 @@
 // test_workload.cpp, acceptance.cpp:353-383); with HAVE_REF the synthetic
 // generator is also checked record-for-record against the compiled reference.
 #include <cmath>
+#include <iostream>
 #include <random>
 #include <set>
 #include <sstream>
@@ -287,6 +288,69 @@ TEST_CASE("synth_trace equals the reference generator record for record") {
     for (size_t i = 0; i < n; ++i)
       REQUIRE((ours[i] == TraceRecord{recs[3 * i], recs[3 * i + 1], recs[3 * i + 2]}));
   }
+}
+
+// The text reader's canonical fast path (workload.cpp, parse_line_canonical)
+// against the reference's reader: random lines, mostly well-formed, with
+// signs, spaces, '\r', long numbers, extra fields and stray dots mixed in.
+// Each trace must give the same records, or fail with the same message.
+TEST_CASE("text read_trace equals the reference reader on random lines") {
+  std::mt19937_64 rng(0x7e47);
+  auto pick = [&rng](uint64_t n) { return rng() % n; };
+  auto number = [&](bool octet) -> std::string {
+    switch (pick(120)) {
+      case 0: return std::to_string(rng());                       // long, may overflow
+      case 1: return "+" + std::to_string(pick(300));
+      case 2: return " " + std::to_string(pick(300));
+      case 3: return "0" + std::to_string(pick(1000));
+      case 4: return std::to_string(pick(300)) + "x";
+      case 5: return "";
+      default: return std::to_string(octet ? pick(256 + 4) : pick(uint64_t{1} << 33));
+    }
+  };
+  auto ip = [&]() -> std::string {
+    if (pick(4) == 0) return number(false);
+    std::string s;
+    const int n = pick(10) == 0 ? 3 + static_cast<int>(pick(3)) : 4;
+    for (int i = 0; i < n; ++i) s += (i ? "." : "") + number(true);
+    if (pick(20) == 0) s += ".";
+    return s;
+  };
+  int parsed = 0;
+  for (int trace = 0; trace < 3000; ++trace) {
+    std::string text;
+    uint32_t ts = 0;
+    const int lines = 1 + static_cast<int>(pick(4));
+    for (int l = 0; l < lines; ++l) {
+      ts += static_cast<uint32_t>(pick(3));
+      std::string line = pick(8) == 0 ? number(false) : std::to_string(ts);
+      line += "," + ip() + "," + ip();
+      if (pick(15) == 0) line += "," + ip();
+      if (pick(15) == 0) line += "\r";
+      if (pick(30) == 0) line = "# comment";
+      if (pick(30) == 0) line.clear();
+      text += line + "\n";
+    }
+    std::string ours_err, ref_err;
+    std::vector<TraceRecord> ours;
+    try {
+      std::stringstream in(text);
+      ours = read_trace(in, TraceFormat::kText);
+    } catch (const std::exception& e) {
+      ours_err = e.what();
+    }
+    std::vector<uint32_t> recs(3 * 16);
+    size_t n = 0;
+    if (ref_read_trace(text.data(), text.size(), 0, recs.data(), 16, &n) != 0) ref_err = ref_last_error();
+    REQUIRE(ours_err == ref_err);
+    if (!ref_err.empty()) continue;
+    REQUIRE(ours.size() == n);
+    for (size_t i = 0; i < n; ++i)
+      REQUIRE((ours[i] == TraceRecord{recs[3 * i], recs[3 * i + 1], recs[3 * i + 2]}));
+    ++parsed;
+  }
+  std::cerr << "  " << parsed << " of 3000 random traces parsed, the rest failed identically\n";
+  CHECK(parsed > 300);
 }
 #endif
 

@@ -138,3 +138,20 @@ def test_detect_and_snapshots(gpu, work):
         want = "".join(f"{s},{d.cip >> 24}.{d.cip >> 16 & 255}.{d.cip >> 8 & 255}.{d.cip & 255},"
                        f"{d.estimate:.6g}\n" for s, d in rows)
         assert text == want
+
+    # three router shards, loaded concurrently: union-min merging gives the single-trace grid,
+    # so the reports are byte-identical to the one-file run (and to the reference's pipeline)
+    head = (work / "trace.bin").read_bytes()[:8]
+    shard_paths = []
+    for i in range(3):
+        path = work / f"shard{i}.bin"
+        path.write_bytes(head + np.ascontiguousarray(trace[i::3]).astype("<u4").tobytes())
+        shard_paths.append(path)
+    run("detect", *shard_paths, "--desk", "--k", 5, "--seed", "5eed", "-o", work / "r3.csv")
+    assert (work / "r3.csv").read_bytes() == (work / "r.csv").read_bytes()
+    if O.ref_available():
+        nrep, rows = O.ref_run_detection([trace[i::3] for i in range(3)], q=10, r=5, delta=8,
+                                         seed=0x5eed, eta=256, k=5, theta=128.0)
+        want3 = "".join(f"{s},{d.cip >> 24}.{d.cip >> 16 & 255}.{d.cip >> 8 & 255}.{d.cip & 255},"
+                        f"{d.estimate:.6g}\n" for s, d in rows)
+        assert (work / "r3.csv").read_text() == want3
