@@ -22,4 +22,13 @@ for fmt in bin text; do
   done
   cmp $W/out_sspd_serial_$fmt.csv $W/out_sspd_$fmt.csv && echo "$fmt: reports identical ($(wc -l < $W/out_sspd_$fmt.csv) rows)"
 done
+# fixed cost of one detect call (CUDA init, grid lifetimes): a 1-slot, 300-record trace
+printf 'slots 1\nbackground hosts=10 zipf=1.1 pairs-per-slot=300 max-distinct=4\n' > $W/tiny
+$B synth $W/tiny --seed 1 -o $W/tiny.bin
+for rep in 1 2 3; do
+  s=$(date +%s%N); $B detect $W/tiny.bin -o /dev/null; e=$(date +%s%N)
+  echo "tiny 1-shard trace run $rep: $(( (e - s) / 1000000 )) ms"
+  s=$(date +%s%N); $B detect $W/tiny.bin $W/tiny.bin $W/tiny.bin $W/tiny.bin -o /dev/null; e=$(date +%s%N)
+  echo "tiny 4-shard trace run $rep: $(( (e - s) / 1000000 )) ms"
+done
 rm -rf $W
