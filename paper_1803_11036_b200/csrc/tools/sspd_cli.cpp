@@ -4,6 +4,8 @@
 // snapshot {export, info, merge}.  Exit codes: 2 configuration, 3 input,
 // 4 candidate cap.  The reference parses with CLI11 (not vendored); this
 // parser accepts the same spellings ("--k 5" and "--k=5", "-o FILE").
+#include <chrono>
+#include <cstdlib>
 #include <exception>
 #include <fstream>
 #include <future>
@@ -172,7 +174,11 @@ std::vector<std::vector<sspd::TraceRecord>> load_shards(const std::vector<std::s
 
 int detect(const Args& a, const Common& c) {
   if (a.pos.empty()) throw UsageError("detect: trace file(s) required");
+  const auto t0 = std::chrono::steady_clock::now();
   const auto shards = load_shards(a.pos, c.trace_format());
+  if (std::getenv("SSPD_PIPELINE_TIMING"))  // same switch as run_detection's phase timings
+    std::cerr << "sspd detect: loaded " << shards.size() << " shard file(s) in "
+              << std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count() << " ms\n";
   const auto reports = sspd::run_detection(shards, c.rc);
   Out out(out_path(a));
   for (const auto& r : reports)

@@ -22,6 +22,11 @@ for fmt in bin text; do
   done
   cmp $W/out_sspd_serial_$fmt.csv $W/out_sspd_$fmt.csv && echo "$fmt: reports identical ($(wc -l < $W/out_sspd_$fmt.csv) rows)"
 done
+# in-process phases of one detect call (loading, then run_detection's own breakdown)
+for fmt in bin text; do
+  ext=$fmt; [ $fmt = text ] && ext=txt
+  SSPD_PIPELINE_TIMING=1 $B detect $W/s0.$ext $W/s1.$ext $W/s2.$ext $W/s3.$ext --format $fmt -o /dev/null
+done
 # fixed cost of one detect call (CUDA init, grid lifetimes): a 1-slot, 300-record trace
 printf 'slots 1\nbackground hosts=10 zipf=1.1 pairs-per-slot=300 max-distinct=4\n' > $W/tiny
 $B synth $W/tiny --seed 1 -o $W/tiny.bin
