@@ -383,6 +383,9 @@ def ref():
         L.ref_estimate.argtypes = [C.c_size_t, C.c_size_t]
         L.ref_validate.argtypes = [C.c_uint32, C.c_uint32, C.c_uint32, C.c_uint32, C.c_uint32,
                                    C.c_double, C.c_char_p, C.c_size_t]
+        L.ref_validate_all.restype = C.c_size_t
+        L.ref_validate_all.argtypes = [C.c_uint32, C.c_uint32, C.c_uint32, C.c_uint32, C.c_uint32,
+                                       C.c_double, C.c_char_p, C.c_size_t]
         L.ref_grid_create.restype = C.c_void_p
         L.ref_grid_create.argtypes = [C.c_uint32, C.c_uint32, C.c_uint32, C.c_uint64,
                                       C.c_uint32]
@@ -513,6 +516,13 @@ class RefGrid:
 
     def __eq__(self, other):
         return bool(ref().ref_grid_equal(self._h, other._h))
+
+
+def ref_validate_all(q, r, delta, eta, k, theta) -> list[str]:
+    """Every message of the compiled reference's validate_config (hashing.cpp:63-87)."""
+    buf = C.create_string_buffer(2048)
+    n = ref().ref_validate_all(q, r, delta, eta, k, theta, buf, len(buf))
+    return buf.value.decode().split("\n") if n else []
 
 
 def ref_run_detection(records, q=14, r=5, delta=6, seed=0, eta=2048, mu=1.0, k=300, start=0,

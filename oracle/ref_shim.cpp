@@ -81,6 +81,65 @@ int ref_validate(uint32_t q, uint32_t r, uint32_t delta, uint32_t eta, uint32_t 
   return static_cast<int>(p.size());
 }
 
+// Every diagnostic validate_config returns (hashing.cpp:63-87), joined by
+// '\n' into msg; returns how many there are.
+size_t ref_validate_all(uint32_t q, uint32_t r, uint32_t delta, uint32_t eta, uint32_t k, double theta,
+                        char* msg, size_t len) {
+  const auto p = validate_config(RhfgConfig{q, r, delta, 0}, eta, k, theta);
+  std::string all;
+  for (size_t i = 0; i < p.size(); ++i) all += (i ? "\n" : "") + p[i];
+  if (msg && len) {
+    std::strncpy(msg, all.c_str(), len - 1);
+    msg[len - 1] = 0;
+  }
+  return p.size();
+}
+
+// parse_ipv4 (workload.cpp:37-58): 0 and *ip, or 1 (invalid_argument),
+// 2 (out_of_range), 3 (other) with what() in ref_last_error().
+int ref_parse_ipv4(const char* text, uint32_t* ip) {
+  try {
+    *ip = parse_ipv4(text);
+    return 0;
+  } catch (const std::invalid_argument& e) {
+    return fail(e, 1);
+  } catch (const std::out_of_range& e) {
+    return fail(e, 2);
+  } catch (const std::exception& e) {
+    return fail(e, 3);
+  }
+}
+void ref_format_ipv4(uint32_t ip, char* out, size_t len) {
+  std::strncpy(out, format_ipv4(ip).c_str(), len - 1);
+  out[len - 1] = 0;
+}
+
+// parse_synth_spec (workload.cpp:302-358) over an in-memory spec.  On success
+// returns 0 and a canonical rendering of the spec in out ("slots bg zipf(%a)
+// pps maxd" then "cip count lo hi" per planted host, one line each); on error
+// 1 (invalid_argument) or 3 with what() in ref_last_error().
+int ref_parse_synth_spec(const char* text, size_t len, char* out, size_t outlen) {
+  try {
+    std::istringstream in(std::string(text, len));
+    const SynthSpec s = parse_synth_spec(in);
+    char line[160];
+    std::snprintf(line, sizeof line, "%u %u %a %u %u\n", s.slots, s.background_hosts, s.zipf_exponent,
+                  s.pairs_per_slot, s.max_distinct_per_host);
+    std::string all = line;
+    for (const auto& p : s.planted) {
+      std::snprintf(line, sizeof line, "%u %u %u %u\n", p.cip, p.count, p.slot_lo, p.slot_hi);
+      all += line;
+    }
+    std::strncpy(out, all.c_str(), outlen - 1);
+    out[outlen - 1] = 0;
+    return 0;
+  } catch (const std::invalid_argument& e) {
+    return fail(e, 1);
+  } catch (const std::exception& e) {
+    return fail(e, 3);
+  }
+}
+
 void* ref_grid_create(uint32_t q, uint32_t r, uint32_t delta, uint64_t seed, uint32_t eta) {
   try {
     return new Rsea(RhfgConfig{q, r, delta, seed}, eta);

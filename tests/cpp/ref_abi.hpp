@@ -26,4 +26,13 @@ size_t ref_synth_trace(const uint32_t* planted, size_t n_planted, uint32_t bg_ho
                        double mu, uint32_t k, uint32_t start, uint32_t* recs, size_t cap_recs);
 int ref_read_trace(const char* data, size_t len, int binary, uint32_t* recs, size_t cap_recs,
                    size_t* n);
+size_t ref_validate_all(uint32_t q, uint32_t r, uint32_t delta, uint32_t eta, uint32_t k, double theta,
+                        char* msg, size_t len);
+int ref_parse_ipv4(const char* text, uint32_t* ip);
+void ref_format_ipv4(uint32_t ip, char* out, size_t len);
+int ref_parse_synth_spec(const char* text, size_t len, char* out, size_t outlen);
+int ref_assemble_ip(uint32_t q, uint32_t r, uint32_t delta, const uint32_t* blocks, uint32_t* ip);
+int ref_blocks_consistent(uint32_t q, uint32_t r, uint32_t delta, uint32_t lo, uint32_t hi);
+size_t ref_hot_cutoff(size_t eta, double theta);
+double ref_estimate(size_t eta, size_t rk);
 }

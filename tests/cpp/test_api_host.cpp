@@ -4,6 +4,7 @@
 // test_workload.cpp, acceptance.cpp:353-383); with HAVE_REF the synthetic
 // generator is also checked record-for-record against the compiled reference.
 #include <cmath>
+#include <cstring>
 #include <iostream>
 #include <random>
 #include <set>
@@ -351,6 +352,221 @@ TEST_CASE("text read_trace equals the reference reader on random lines") {
   }
   std::cerr << "  " << parsed << " of 3000 random traces parsed, the rest failed identically\n";
   CHECK(parsed > 300);
+}
+
+// validate_config's whole message list against the reference (hashing.cpp:63-87)
+// over q 0..18, r 0..8, delta 0..q+1, four eta, k and theta values each:
+// 120,384 cases, every one compared message for message.
+TEST_CASE("validate_config equals the reference on the full grid") {
+  const uint32_t etas[] = {0, 1, 2, 256};
+  const uint32_t ks[] = {0, 1, 65534, 65535};
+  const double thetas[] = {0, 0.5, 1, 1024};
+  size_t cases = 0, flagged = 0;
+  char buf[2048];
+  for (uint32_t q = 0; q <= 18; ++q)
+    for (uint32_t r = 0; r <= 8; ++r)
+      for (uint32_t d = 0; d <= q + 1; ++d)
+        for (uint32_t eta : etas)
+          for (uint32_t k : ks)
+            for (double th : thetas) {
+              const auto ours = validate_config(RhfgConfig{q, r, d, 0}, eta, k, th);
+              const size_t n = ref_validate_all(q, r, d, eta, k, th, buf, sizeof buf);
+              std::string joined;
+              for (size_t i = 0; i < ours.size(); ++i) joined += (i ? "\n" : "") + ours[i];
+              if (ours.size() != n || joined != buf) {
+                std::ostringstream os;
+                os << "q=" << q << " r=" << r << " delta=" << d << " eta=" << eta << " k=" << k
+                   << " theta=" << th << ": ours [" << joined << "] ref [" << buf << "]";
+                FAIL(os.str());
+              }
+              ++cases;
+              flagged += n != 0;
+            }
+  std::cerr << "  " << cases << " configurations, " << flagged << " with diagnostics, 0 differences\n";
+  CHECK(cases == 120384);
+  // the delta=0 case the CLI prints in full (tools/sspd.cpp:65-70)
+  const auto d0 = validate_config(RhfgConfig{14, 5, 0, 0}, 2048, 5, 1024);
+  REQUIRE(d0.size() == 2);
+  CHECK(d0[1] == "address coverage (r-2)*delta+q = 14 < 32");
+}
+
+// assemble_ip / blocks_consistent (hashing.cpp:45-61, hashing.hpp:80-84) on
+// random and adversarial blocks over every geometry validate_config accepts
+// with r <= 12, against the reference.
+TEST_CASE("assemble_ip and blocks_consistent equal the reference") {
+  std::mt19937_64 rng(0xa55e);
+  size_t geos = 0, accepted = 0, total = 0;
+  for (uint32_t q = 1; q <= 16; ++q)
+    for (uint32_t r = 3; r <= 12; ++r)
+      for (uint32_t d = 1; d < q; ++d) {
+        const RhfgConfig cfg{q, r, d, 0};
+        if (!validate_config(cfg, 2, 1, 1).empty()) continue;
+        ++geos;
+        std::vector<uint32_t> b(r - 1);
+        for (int t = 0; t < 400; ++t) {
+          const uint32_t cip = static_cast<uint32_t>(rng());
+          for (uint32_t i = 1; i < r; ++i) {
+            b[i - 1] = ((cip >> (((i - 1) * d) & 31u)) & cfg.column_mask());
+            if (t % 3 == 1) b[i - 1] ^= (rng() % 7 == 0) ? (1u << (rng() % q)) : 0;  // corrupt some
+            if (t % 3 == 2) b[i - 1] = static_cast<uint32_t>(rng()) & cfg.column_mask();
+          }
+          uint32_t ip = 0;
+          const int ref = ref_assemble_ip(q, r, d, b.data(), &ip);
+          const auto ours = assemble_ip(b, cfg);
+          REQUIRE(ours.has_value() == (ref != 0));
+          if (ref) REQUIRE(*ours == ip);
+          accepted += ref != 0;
+          ++total;
+          const uint32_t lo = static_cast<uint32_t>(rng()) & cfg.column_mask();
+          const uint32_t hi = static_cast<uint32_t>(rng()) & cfg.column_mask();
+          REQUIRE(blocks_consistent(lo, hi, cfg) == (ref_blocks_consistent(q, r, d, lo, hi) != 0));
+          const uint32_t hi2 = (lo >> d) | (hi & ~((1u << (q - d)) - 1));
+          REQUIRE(blocks_consistent(lo, hi2, cfg) == (ref_blocks_consistent(q, r, d, lo, hi2) != 0));
+        }
+      }
+  std::cerr << "  " << geos << " geometries, " << total << " block lists (" << accepted << " assembled)\n";
+  CHECK(geos > 300);
+}
+
+// hot_cutoff / estimate_cardinality (estimator.cpp:25-36): the same doubles
+// and size_t bit for bit, over eta 1..4096 and random theta and R_k.
+TEST_CASE("hot_cutoff and estimate_cardinality equal the reference") {
+  std::mt19937_64 rng(0xc0f);
+  std::uniform_real_distribution<double> u(0.0, 1.0);
+  size_t n = 0;
+  for (size_t eta = 1; eta <= 4096; ++eta) {
+    for (double th : {0.0, 1.0, 0.5 * eta, static_cast<double>(eta), 1024.0, 1e9, u(rng) * 4 * eta}) {
+      REQUIRE(hot_cutoff(eta, th) == ref_hot_cutoff(eta, th));
+      ++n;
+    }
+    for (size_t rk : {size_t{0}, size_t{1}, eta - 1, eta, static_cast<size_t>(rng() % eta)}) {
+      const double a = estimate_cardinality(eta, rk), b = ref_estimate(eta, rk);
+      REQUIRE(std::memcmp(&a, &b, sizeof a) == 0);
+      ++n;
+    }
+  }
+  for (size_t eta : {size_t{1} << 16, size_t{1} << 20, size_t{1} << 31})
+    for (int t = 0; t < 2000; ++t) {
+      const double th = u(rng) * 2.0 * static_cast<double>(eta);
+      REQUIRE(hot_cutoff(eta, th) == ref_hot_cutoff(eta, th));
+      const size_t rk = rng() % (eta + 1);
+      const double a = estimate_cardinality(eta, rk), b = ref_estimate(eta, rk);
+      REQUIRE(std::memcmp(&a, &b, sizeof a) == 0);
+      n += 2;
+    }
+  std::cerr << "  " << n << " cutoffs and estimates, bit-identical\n";
+}
+
+// parse_ipv4 / format_ipv4 (workload.cpp:37-64): random strings give the
+// same value, or the same exception type and message.
+TEST_CASE("parse_ipv4 and format_ipv4 equal the reference") {
+  std::mt19937_64 rng(0x1b4);
+  auto pick = [&rng](uint64_t n) { return rng() % n; };
+  const char* alphabet = "0123456789....  +-x\r\tabcdef";
+  size_t ok = 0, n = 0;
+  for (int t = 0; t < 200000; ++t) {
+    std::string s;
+    switch (pick(4)) {
+      case 0:  // dotted quads, sometimes off by one field or octet
+        for (int i = 0, m = 3 + static_cast<int>(pick(3)); i < m; ++i)
+          s += (i ? "." : "") + std::to_string(pick(10) ? pick(256) : pick(100000));
+        break;
+      case 1:
+        s = std::to_string(pick(4) ? pick(uint64_t{1} << 32) : rng());
+        break;
+      default:
+        for (int i = 0, m = static_cast<int>(pick(12)); i < m; ++i) s += alphabet[pick(std::strlen(alphabet))];
+    }
+    int code = 0;
+    uint32_t mine = 0;
+    std::string err;
+    try {
+      mine = parse_ipv4(s);
+    } catch (const std::invalid_argument& e) {
+      code = 1, err = e.what();
+    } catch (const std::out_of_range& e) {
+      code = 2, err = e.what();
+    } catch (const std::exception& e) {
+      code = 3, err = e.what();
+    }
+    uint32_t theirs = 0;
+    const int rc = ref_parse_ipv4(s.c_str(), &theirs);
+    if (rc != code || (rc && err != ref_last_error()) || (!rc && mine != theirs))
+      FAIL("parse_ipv4(\"" + s + "\"): ours " + std::to_string(code) + " " + err + " ref " +
+                             std::to_string(rc) + " " + (rc ? ref_last_error() : ""));
+    ok += rc == 0;
+    ++n;
+  }
+  char buf[32];
+  for (int t = 0; t < 100000; ++t) {
+    const uint32_t ip = t < 16 ? (t & 1 ? ~0u << t : 1u << t) : static_cast<uint32_t>(rng());
+    ref_format_ipv4(ip, buf, sizeof buf);
+    REQUIRE(format_ipv4(ip) == buf);
+  }
+  std::cerr << "  " << n << " strings (" << ok << " parsed), 100000 formatted\n";
+  CHECK(ok > 1000);
+}
+
+// parse_synth_spec (workload.cpp:302-358): random specs give the same spec,
+// or the same message.
+TEST_CASE("parse_synth_spec equals the reference") {
+  std::mt19937_64 rng(0x5bec);
+  auto pick = [&rng](uint64_t n) { return rng() % n; };
+  auto num = [&]() -> std::string {
+    switch (pick(16)) {
+      case 0: return "x";
+      case 1: return "";
+      case 2: return std::to_string(rng());
+      case 3: return "-" + std::to_string(pick(5));
+      case 4: return "1e3";
+      default: return std::to_string(pick(5000));
+    }
+  };
+  size_t ok = 0;
+  for (int t = 0; t < 20000; ++t) {
+    std::string text;
+    for (int l = 0, m = static_cast<int>(pick(6)); l < m; ++l) {
+      switch (pick(8)) {
+        case 0: text += "slots " + num(); break;
+        case 1: text += "background hosts=" + num() + " zipf=" + (pick(2) ? "1.25" : num()) +
+                        " pairs-per-slot=" + num() + " max-distinct=" + num(); break;
+        case 2: text += "background " + std::string(pick(2) ? "hosts" : "zipf=0.9"); break;
+        case 3: text += "super cip=" + std::string(pick(3) ? "10.0.0." + std::to_string(pick(300)) : num()) +
+                        " count=" + num() + (pick(2) ? " from=" + num() : "") + (pick(2) ? " to=" + num() : ""); break;
+        case 4: text += "super count=" + num(); break;
+        case 5: text += pick(2) ? "# comment" : ""; break;
+        case 6: text += "bogus a=b"; break;
+        default: text += "super cip=1.2.3.4 count=" + num() + " extra"; break;
+      }
+      text += pick(10) ? "\n" : "\r\n";
+    }
+    std::string mine, err;
+    int code = 0;
+    try {
+      std::istringstream in(text);
+      const SynthSpec s = parse_synth_spec(in);
+      char line[160];
+      std::snprintf(line, sizeof line, "%u %u %a %u %u\n", s.slots, s.background_hosts, s.zipf_exponent,
+                    s.pairs_per_slot, s.max_distinct_per_host);
+      mine = line;
+      for (const auto& p : s.planted) {
+        std::snprintf(line, sizeof line, "%u %u %u %u\n", p.cip, p.count, p.slot_lo, p.slot_hi);
+        mine += line;
+      }
+    } catch (const std::invalid_argument& e) {
+      code = 1, err = e.what();
+    } catch (const std::exception& e) {
+      code = 3, err = e.what();
+    }
+    std::vector<char> out(1 << 16);
+    const int rc = ref_parse_synth_spec(text.data(), text.size(), out.data(), out.size());
+    if (rc != code || (rc ? err != ref_last_error() : mine != out.data()))
+      FAIL("spec [" + text + "]: ours " + std::to_string(code) + " " + (code ? err : mine) +
+                             " ref " + std::to_string(rc) + " " + (rc ? ref_last_error() : out.data()));
+    ok += rc == 0;
+  }
+  std::cerr << "  20000 random specs (" << ok << " parsed)\n";
+  CHECK(ok > 1000);
 }
 #endif
 

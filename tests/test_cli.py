@@ -155,3 +155,18 @@ def test_detect_and_snapshots(gpu, work):
         want3 = "".join(f"{s},{d.cip >> 24}.{d.cip >> 16 & 255}.{d.cip >> 8 & 255}.{d.cip & 255},"
                         f"{d.estimate:.6g}\n" for s, d in rows)
         assert (work / "r3.csv").read_text() == want3
+
+
+@pytest.mark.skipif(not O.ref_available(), reason="oracle/_ref not built")
+@pytest.mark.parametrize("q,r,delta,eta,k,theta", [
+    (14, 5, 0, 2048, 5, 1024), (14, 2, 0, 1, 0, 0.5), (8, 5, 6, 256, 5, 128), (17, 3, 17, 2048, 65535, 1024)])
+def test_invalid_configuration_message_equals_reference(work, q, r, delta, eta, k, theta):
+    """`sspd detect` prints validate_config's whole list (sspd.cpp:65-70, 401-406),
+    byte for byte the reference's messages, and exits 2 -- delta=0 included
+    (hashing.cpp:74-78 reports the coverage rule for it too)."""
+    p = run("detect", work / "trace.bin", "--q", q, "--r", r, "--delta", delta, "--eta", eta,
+            "--k", k, "--theta", theta, "-o", os.devnull, check=False)
+    want = "error: invalid configuration:" + "".join(
+        "\n  " + m for m in O.ref_validate_all(q, r, delta, eta, k, theta)) + "\n"
+    assert p.returncode == 2
+    assert p.stderr == want

@@ -200,3 +200,23 @@ def test_oracle_vs_compiled_reference_random():
                 assert a == b
             o.advance()
             f.advance(2)
+
+
+@pytest.mark.skipif(not O.ref_available(), reason="oracle/_ref not built")
+def test_python_validate_config_equals_reference():
+    """The Python host mirror's validate_config (paper_1803_11036_b200/pipeline.py)
+    returns the compiled reference's full message list (hashing.cpp:63-87) on the
+    same 120,384-point grid the C++ differential uses (tests/cpp/test_api_host.cpp)."""
+    from paper_1803_11036_b200.pipeline import validate_config
+
+    n = 0
+    for q in range(19):
+        for r in range(9):
+            for d in range(q + 2):
+                for eta in (0, 1, 2, 256):
+                    for k in (0, 1, 65534, 65535):
+                        for th in (0.0, 0.5, 1.0, 1024.0):
+                            assert validate_config(q, r, d, eta, k, th) == \
+                                O.ref_validate_all(q, r, d, eta, k, th), (q, r, d, eta, k, th)
+                            n += 1
+    assert n == 120384
