@@ -4,10 +4,15 @@
 // grid without a usable sm_100 device throws std::runtime_error.
 #pragma once
 
+#include <vector>
+
 namespace sspd {
 
 void set_device(int device);
 int current_device();
 int device_count();
+// CUDA ordinals of the usable (sm_100) devices, ascending; what
+// RunConfig::devices > 1 spreads routers over.
+std::vector<int> device_ordinals();
 
 }  // namespace sspd

@@ -65,6 +65,9 @@ int sspd_abi_version(void);
 const char* sspd_last_error(void);
 /* Number of visible devices this library can run on (sm_100). */
 sspd_status sspd_device_count(int* n);
+/* Their CUDA ordinals, ascending (up to cap of them; *n = how many there
+ * are).  On a mixed box these are not 0..n-1. */
+sspd_status sspd_device_ordinals(int* out, int cap, int* n);
 
 /* ---- device memory, for hosts that wire routers together in one process
  * (the C++ run_detection over several GPUs, csrc/host/routers.cpp) ---- */

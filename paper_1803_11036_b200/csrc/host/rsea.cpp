@@ -45,6 +45,13 @@ int device_count() {
   int n = 0;
   return sspd_device_count(&n) == SSPD_OK ? n : 0;
 }
+std::vector<int> device_ordinals() {
+  std::vector<int> out(64);
+  int n = 0;
+  if (sspd_device_ordinals(out.data(), static_cast<int>(out.size()), &n) != SSPD_OK) return {};
+  out.resize(static_cast<std::size_t>(std::min<int>(n, 64)));
+  return out;
+}
 
 CandidateOverflow::CandidateOverflow(uint32_t level_, std::size_t count_, std::size_t cap)
     : std::runtime_error("candidate buffer cap exceeded at level " + std::to_string(level_) + ": " +

@@ -430,7 +430,11 @@ struct sspd_grid {
   uint64_t scanned_in_slot = 0; // pairs scanned since the last advance (list capacity bound)
   uint64_t list_pad_slots = 0;  // bound on the list blocks' padding since the last advance
   PushArgs push{};              // fused exchange: peer inboxes (export mode 3)
-  void* pinned_small = nullptr;  // 4 KB pinned scratch for counters
+  // 8 KB of pinned memory.  The first 4 KB hold a queued reconstruction's
+  // survivor prefix (2 x 512 u32) from recon_queue until it is collected; the
+  // second 4 KB are scratch for synchronous counter/flag read-backs
+  // (pinned_scratch), which may run while a reconstruction is pending.
+  void* pinned_small = nullptr;
   bool profiling = false;
   int prof_suspend = 0;  // inside a PDL launch chain: one event pair around the chain only
   std::vector<ProfRec> prof;
@@ -524,6 +528,9 @@ sspd_status wide_only(const sspd_grid* g, const char* what) {
                                          std::to_string(g->width) + "-bit stamps (exact for in-window counts "
                                          "with k <= " + std::to_string(g->K) + " only)");
 }
+
+// Counter/flag read-back scratch, disjoint from the survivor prefix.
+void* pinned_scratch(const sspd_grid* g) { return static_cast<char*>(g->pinned_small) + 4096; }
 
 sspd_status no_pending(const sspd_grid* g, const char* what) {
   if (!g->recon_pending) return SSPD_OK;
@@ -818,6 +825,24 @@ sspd_status sspd_grid_copy(sspd_grid* g, void* dst, const void* src, uint64_t by
   return SSPD_OK;
 }
 
+sspd_status sspd_device_ordinals(int* out, int cap, int* n) {
+  int c = 0;
+  *n = 0;
+  if (cudaGetDeviceCount(&c) != cudaSuccess) {
+    cudaGetLastError();
+    return fail(SSPD_NO_DEVICE, "no CUDA device");
+  }
+  for (int d = 0; d < c; ++d) {
+    int major = 0;
+    cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, d);
+    if (major != 10) continue;
+    if (*n < cap && out) out[*n] = d;
+    ++*n;
+  }
+  if (!*n) return fail(SSPD_NO_DEVICE, "no sm_100 device visible");
+  return SSPD_OK;
+}
+
 sspd_status sspd_device_count(int* n) {
   int c = 0;
   cudaError_t e = cudaGetDeviceCount(&c);
@@ -923,7 +948,7 @@ sspd_status create_impl(int device, uint32_t q, uint32_t r, uint32_t delta, uint
     return cleanup("CUDA error: out of memory allocating the touched bitmap");
   }
   if (cache_alloc((void**)&g->d_tabs, sizeof(HashTabs)) != cudaSuccess) return cleanup("CUDA error: tables");
-  if (PinnedCache::get().alloc(&g->pinned_small, 4096) != cudaSuccess ||
+  if (PinnedCache::get().alloc(&g->pinned_small, 8192) != cudaSuccess ||
       PinnedCache::get().alloc(reinterpret_cast<void**>(&g->meta_host), sizeof(ReconMeta)) != cudaSuccess ||
       g->meta.ensure(sizeof(ReconMeta)) != cudaSuccess)
     return cleanup("CUDA error: pinned scratch");
@@ -2124,7 +2149,7 @@ sspd_status sspd_equal(sspd_grid* a, sspd_grid* b, int* equal) {
       return fail(SSPD_CUDA_ERROR, std::string("CUDA error: peer access: ") + cudaGetErrorString(e));
     cudaGetLastError();
   }
-  int* flag = static_cast<int*>(a->pinned_small);
+  int* flag = static_cast<int*>(pinned_scratch(a));
   if (a->misc.ensure(64) != cudaSuccess) return fail(SSPD_CUDA_ERROR, "CUDA error: out of memory");
   CU(cudaMemsetAsync(a->misc.p, 0, 4, a->stream));
   {
@@ -2211,9 +2236,9 @@ sspd_status sspd_grid_new_pairs(sspd_grid* g, uint32_t** dev_pairs, uint64_t* co
   DeviceGuard dg(g->device);
   uint64_t c = 0;
   if (g->newpairs_count.p) {
-    CU(cudaMemcpyAsync(g->pinned_small, g->newpairs_count.p, 8, cudaMemcpyDeviceToHost, g->stream));
+    CU(cudaMemcpyAsync(pinned_scratch(g), g->newpairs_count.p, 8, cudaMemcpyDeviceToHost, g->stream));
     CU(cudaStreamSynchronize(g->stream));
-    c = *static_cast<uint64_t*>(g->pinned_small);
+    c = *static_cast<uint64_t*>(pinned_scratch(g));
   }
   *dev_pairs = g->newpairs.as<uint32_t>();
   *count = c;

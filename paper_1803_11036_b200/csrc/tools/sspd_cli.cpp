@@ -89,6 +89,8 @@ struct Common {
     u32("--alpha", rc.alpha);
     u32("--start", rc.window.start);
     u32("--stamp-width", rc.stamp_bits);
+    u32("--devices", rc.devices);  // routers, one per GPU (RunConfig::devices; §8 f4)
+    if (rc.devices == 0) throw UsageError("--devices must be >= 1");
     if (a.opt.count("--workers")) rc.workers = static_cast<unsigned>(std::stoul(a.opt.at("--workers")));
     if (a.opt.count("--mu")) rc.window.mu = std::stod(a.opt.at("--mu"));
     if (a.opt.count("--theta")) rc.theta = std::stod(a.opt.at("--theta"));
@@ -356,7 +358,8 @@ void usage() {
   std::cerr << "usage: sspd <detect|oracle|eval|synth|snapshot {export|info|merge}> [options]\n"
                "  common: --eta --q --r --delta --k --mu --theta --seed HEX --alpha --workers --start\n"
                "          --merge-policy min|paper-max --strategy recursive|leveled --desk --format bin|text\n"
-               "          --device N (GPU ordinal) --stamp-width 8|16|32 (narrow stamps, union-min only)\n";
+               "          --device N (GPU ordinal) --stamp-width 8|16|32 (narrow stamps, union-min only)\n"
+               "          --devices N (detect: one router per GPU over N GPUs; default 1)\n";
 }
 
 }  // namespace

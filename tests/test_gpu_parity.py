@@ -875,6 +875,41 @@ def test_reconstruct_async_pipelines_slots(gpu):
         g2.reconstruct_collect()
 
 
+def test_counter_readbacks_leave_a_queued_reconstruction_intact(gpu):
+    """bench.py's N>1 order: reconstruct_async, the next slot's scan with the
+    pair list exported, new_pairs_ptr() and ==, then reconstruct_collect.  The
+    counter/flag read-backs use their own pinned scratch, so the collected
+    survivors (cip, R_k) are the queued slot's, equal to the oracle's."""
+    import torch
+
+    g, o = make_pair(gpu, DESK, 0xA11A)
+    g.track_window(30)
+    g.set_exchange(2)
+    other, _ = make_pair(gpu, DESK, 0xA11A)
+    rng = O.Mt64(0xA11A)
+    for s in range(4):
+        parts = [rng.pairs(4000)]
+        for h in range(3):
+            parts.append(np.stack([np.full(300, 0x0C000000 + 7 * h + s, np.uint32),
+                                   rng.draw(300).astype(np.uint32)], 1))
+        p = np.concatenate(parts)
+        g.scan_batch(torch.from_numpy(p.view(np.int32)).cuda())
+        o.scan(p)
+        g.reconstruct_async(30, 128.0)
+        want = o.reconstruct(30, 128.0)
+        assert len(want) >= 3
+        nxt = rng.pairs(5000)
+        g.advance_slot()
+        o.advance()
+        g.scan_batch(torch.from_numpy(nxt.view(np.int32)).cuda())  # export on: counts new pairs
+        o.scan(nxt)
+        _, n = g.new_pairs_ptr()
+        assert n >= len(np.unique(nxt, axis=0))
+        assert not (g == other)
+        assert dets_equal(g.reconstruct_collect(), want), s
+        assert np.array_equal(g.cells(), o.cells())
+
+
 def _reconstruct_merged(gpu, grids, k, theta):
     """The sharded reconstruction with the collectives done in-process: OR of
     hot bits, AND of survivor masks (dist.ShardExchange.reconstruct)."""
