@@ -39,6 +39,7 @@ SIGNATURES = {
     "sspd_abi_version": (C.c_int, []),
     "sspd_last_error": (C.c_char_p, []),
     "sspd_device_count": (C.c_int, [C.POINTER(C.c_int)]),
+    "sspd_device_ordinals": (C.c_int, [C.POINTER(C.c_int), C.c_int, C.POINTER(C.c_int)]),
     "sspd_grid_create": (C.c_int, [C.c_int, C.c_uint32, C.c_uint32, C.c_uint32, C.c_uint64,
                                    C.c_uint32, C.POINTER(grid_p)]),
     "sspd_grid_clone": (C.c_int, [grid_p, C.c_int, C.POINTER(grid_p)]),

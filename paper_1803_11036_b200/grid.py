@@ -55,6 +55,14 @@ def device_count() -> int:
     return n.value
 
 
+def device_ordinals() -> list[int]:
+    """CUDA ordinals of the visible sm_100 devices (sspd_device_ordinals)."""
+    out = (C.c_int * 64)()
+    n = C.c_int()
+    check(load().sspd_device_ordinals(out, 64, C.byref(n)))
+    return list(out[:min(n.value, 64)])
+
+
 def _u32(a):
     return a.ctypes.data_as(_cabi.u32p)
 
