@@ -45,9 +45,9 @@ CONFIGS = {
                pairs_per_slot=100_000_000, trace_slots=10, hosts=1 << 21, pool=16, zipf=1.1,
                n_super=110, fanout=4096),
     # configs[0]: the reference's CPU-runnable case (reference default geometry).
-    "c1": dict(workload="C1: 1 router/GPU, uniform (cip,oip) pairs, 10 slots x 1e6 pairs + 20 "
-                        "planted supers x 2048 per slot, reference default table q14 r5 delta6 "
-                        "eta2048", q=14, r=5, delta=6, eta=2048, seed=0x5eed, k=5, theta=1024.0,
+    "c1": dict(workload="C1: 1 router/GPU, 10 slots x 1e6 (cip,oip) pairs: 20 planted supers x "
+                        "2048 distinct oips, the rest uniform; reference default table q14 r5 "
+                        "delta6 eta2048", q=14, r=5, delta=6, eta=2048, seed=0x5eed, k=5, theta=1024.0,
                pairs_per_slot=1_000_000, trace_slots=10, hosts=1, pool=0, zipf=1.1,
                n_super=20, fanout=2048),
 }
@@ -69,6 +69,29 @@ class SynthParams(C.Structure):
 def synth_params(cfg, rank, world):
     return SynthParams(cfg["seed"] ^ 0xC2C2, cfg["hosts"], cfg["pool"], cfg["n_super"],
                        cfg["fanout"], cfg["pairs_per_slot"] * world, rank, world)
+
+
+B200_L2_BYTES = 126 << 20  # what torch reports for a B200 (L2_cache_size)
+
+
+def l2_policy(cfg):
+    """(flush?, note): the timing rule's L2 statement for this workload.  C2's
+    800 MB slot is larger than L2; C1's 8 MB slot is not, so every GPU step
+    starts with a 2xL2 write inside the timed region."""
+    slot_bytes = cfg["pairs_per_slot"] * 8
+    if slot_bytes < 2 * B200_L2_BYTES:
+        return True, (f"GPU L2 ({B200_L2_BYTES >> 20} MiB) flushed before every step by a "
+                      f"{2 * B200_L2_BYTES >> 20} MiB write inside the timed region; slot input "
+                      f"{slot_bytes / 1e6:g} MB")
+    return False, (f"inputs larger than L2: {slot_bytes / 1e6:g} MB per slot vs "
+                   f"{B200_L2_BYTES >> 20} MiB GPU L2, no flush")
+
+
+def config_of(cfg):
+    """The `config` object both arms print, identical for the same workload
+    (implementation details go under `setup`)."""
+    return {"workload": cfg["workload"], "pairs_per_step_per_gpu": cfg["pairs_per_slot"],
+            "window_k": cfg["k"], "theta": cfg["theta"], "l2": l2_policy(cfg)[1]}
 
 
 def zipf_cdf(L, cfg):
@@ -194,7 +217,7 @@ def run_reference(cfg, steps, warmup, pairs_cap, time_budget_s, workers=None):
 
     # the workload comes from the host-only generator (no CUDA runtime in
     # this process): the same traces the device generator makes
-    S = C.CDLL(os.path.join(ROOT, "paper_1803_11036_b200", "lib", "libsspd_synth.so"))
+    S = C.CDLL(os.path.join(ROOT, "oracle", "libsynth_host.so"))
     if workers is None:
         workers = env_int("SSPD_REF_WORKERS", os.cpu_count() or 1)
     t0 = time.time()
@@ -290,8 +313,9 @@ def main():
             "n_gpus": args.gpus, "steps": r["steps_timed"], "warmup": args.warmup,
             "ms_per_step": round(r["step_ms"], 3), "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "u32/u16 integer", "data": "synthetic",
-            "config": {"workload": cfg["workload"], "sample": f"{r['pairs_per_step']} pairs per step",
-                       "parallelism": "host OpenMP"},
+            "config": config_of(cfg),
+            "setup": {"sample": f"{r['pairs_per_step']} pairs per step", "parallelism": "host OpenMP",
+                      "recorders": "u16 distances (the reference's Recorder)"},
             "gbps_800B": round(r["value"] * 1e6 * PKT_BYTES * 8 / 1e9, 3),
             "reconstruct_ms": round(r["reconstruct_ms"], 3),
             "phases_ms": {"scan": round(r["scan_ms"], 3), "reconstruct": round(r["reconstruct_ms"], 3),
@@ -370,16 +394,10 @@ def main():
     # Timing rule: inputs larger than L2, else flush L2 between steps.  C2's
     # slot is 800 MB; C1's is 8 MB, so C1 steps start by writing a 2x-L2
     # buffer (inside the timed region: it is charged to the step).
-    l2_bytes = torch.cuda.get_device_properties(dev).L2_cache_size
-    slot_bytes = n_local * 8
+    l2_bytes = max(torch.cuda.get_device_properties(dev).L2_cache_size, B200_L2_BYTES)
     flush = None
-    if slot_bytes < 2 * l2_bytes:
+    if l2_policy(cfg)[0]:
         flush = torch.empty(2 * l2_bytes // 4, dtype=torch.int32, device=f"cuda:{dev}")
-        l2_note = (f"L2 ({l2_bytes >> 20} MiB) flushed before every step by a {2 * l2_bytes >> 20} MiB "
-                   f"write inside the timed region; slot input {slot_bytes / 1e6:g} MB")
-    else:
-        l2_note = (f"inputs larger than L2: {slot_bytes / 1e6:g} MB per slot vs "
-                   f"{l2_bytes >> 20} MiB L2, no flush")
 
     # Slots pipeline: slot i's reconstruction is queued (sspd_reconstruct_async)
     # and its reports collected after slot i+1's scan is queued, so the GPU
@@ -612,8 +630,8 @@ def main():
         # GTX 950 at the paper parameters -- the C1 geometry
         "vs_baseline": round(value / 109.0, 2) if args.config == "c1" else None,
         "dtype": {8: "u8 stamps", 16: "u16 stamps", 32: "u32"}[args.stamp_width], "data": "synthetic",
-        "config": {"workload": cfg["workload"], "pairs_per_step_per_gpu": n_local,
-                   "window_k": k, "theta": theta, "stamp_bits": args.stamp_width,
+        "config": config_of(cfg),
+        "setup": {"stamp_bits": args.stamp_width,
                    "merge": {"pairs": "union-min: all-gather of each router's distinct pairs per slot",
                              "push": "union-min: distinct pairs pushed to peers over NVLink during the scan",
                              "bitmap": "union-min: OR all-reduce of the slot's touched bitmaps",
@@ -622,8 +640,7 @@ def main():
                                       "NVLink through pair owners to their cells' owners, hot bits OR- and "
                                       "survivor masks AND-reduced",
                              "auto": "none (single router)"}[merge_used],
-                   "parallelism": f"{world} routers, one per GPU",
-                   "l2": l2_note},
+                   "parallelism": f"{world} routers, one per GPU"},
         "gbps_800B": round(value * 1e6 * PKT_BYTES * 8 / 1e9, 1),
         # the paper's form: Mpkt/s * 800 * 8 / 1024, i.e. 109 Mpkt/s -> 681.25
         "gbps_800B_paper": round(value * PKT_BYTES * 8 / 1024, 1),

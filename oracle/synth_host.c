@@ -1,7 +1,10 @@
-/* Host-only build of the synthetic trace generator (synth.h), with no CUDA
- * runtime, for callers that must not load the device library -- e.g. the
- * reference arm of bench.py, which generates the same traces for the CPU
- * reference.  Same arithmetic as the device kernel, bit for bit. */
+/* Host-only build of the product's synthetic trace generator
+ * (paper_1803_11036_b200/csrc/synth.h), with no CUDA runtime, for the CPU
+ * legs of bench.py (--impl reference, cpu_baseline), which feed the compiled
+ * reference the same traces the device generator makes.  TEST/BENCH
+ * INFRASTRUCTURE: built into oracle/libsynth_host.so; the product never
+ * loads it.  Same arithmetic as the device kernel, bit for bit
+ * (tests/test_synth.py). */
 #include <math.h>
 #include <stdint.h>
 #include <stdlib.h>

@@ -7,6 +7,7 @@
 #include <algorithm>
 #include <cstdlib>
 #include <cstring>
+#include <iostream>
 #include <random>
 #include <set>
 #include <sstream>
@@ -17,6 +18,7 @@
 #include "sspd/rsea.hpp"
 #include "sspd/snapshot.hpp"
 #include "sspd/split.hpp"
+#include "sspd_cuda.h"
 #ifdef HAVE_REF
 #include "ref_abi.hpp"
 #endif
@@ -633,6 +635,68 @@ TEST_CASE("differential: acceptance end-to-end at the paper's parameters") {
   }
   CHECK(fpr / reps.size() <= 0.05);
   expect_same(reps, ref_pipeline({w.trace}, rc));
+}
+
+// Config C1 at its stated size (bench.py --config c1): 10 slots x
+// 1e6 pairs (uniform, with 20 planted supers x 2048 distinct oips first),
+// the reference defaults q14 r5 delta6 eta2048, k=5, theta=1024.  Through
+// sspd::run_detection against the compiled reference (pipeline.cpp:16-89):
+// every slot's full grid (167,772,160 recorders), all 81,920 R_k and every
+// report; then the probe-less (pipelined) run against ref_run_detection.
+TEST_CASE("differential: C1 at full size, every slot's grid, R_k and reports") {
+  RunConfig rc;
+  rc.cfg = RhfgConfig{14, 5, 6, 0x5eed};
+  rc.eta = 2048;
+  rc.window.k = 5;
+  rc.theta = 1024;
+  constexpr uint32_t kSlots = 10;
+  constexpr uint64_t kPairs = 1'000'000;
+  sspd_synth_params_t sp{0x5eedULL ^ 0xC2C2, 1, 0, 20, 2048, kPairs, 0, 1};
+  std::vector<uint64_t> cdf(1);
+  REQUIRE(sspd_synth_zipf_cdf(1, 1.1, cdf.data()) == SSPD_OK);
+  std::vector<TraceRecord> trace;
+  trace.reserve(kSlots * kPairs);
+  std::vector<std::vector<uint32_t>> slot_pairs(kSlots, std::vector<uint32_t>(2 * kPairs));
+  for (uint32_t s = 0; s < kSlots; ++s) {
+    REQUIRE(sspd_synth_host(&sp, cdf.data(), s, 0, kPairs, slot_pairs[s].data()) == SSPD_OK);
+    for (uint64_t j = 0; j < kPairs; ++j) trace.push_back({s, slot_pairs[s][2 * j], slot_pairs[s][2 * j + 1]});
+  }
+  const unsigned workers = std::max(1u, std::thread::hardware_concurrency());
+  void* ref = ref_grid_create(14, 5, 6, 0x5eed, 2048);
+  const size_t n_rec = ref_grid_size(ref);
+  REQUIRE(n_rec == 167772160u);
+  std::vector<uint16_t> want(n_rec);
+  const size_t n_cells = size_t{5} << 14;
+  std::vector<uint32_t> rk(n_cells);
+  uint64_t probed = 0, cells_ok = 0, rk_ok = 0;
+  const auto reps = run_detection({trace}, rc, [&](uint64_t slot, const Rsea& grid) {
+    ref_scan(ref, slot_pairs[slot].data(), kPairs, workers);
+    ref_get_cells(ref, want.data());
+    const auto got = grid.cells();
+    cells_ok += got.size() == want.size() && std::equal(got.begin(), got.end(), want.begin());
+    REQUIRE(sspd_active_counts(grid.handle(), rc.window.k, rk.data()) == SSPD_OK);
+    bool same = true;
+    for (size_t c = 0; c < n_cells && same; ++c) {
+      uint32_t n = 0;
+      for (size_t b = 0; b < rc.eta; ++b) n += want[c * rc.eta + b] < rc.window.k;
+      same = n == rk[c];
+    }
+    rk_ok += same;
+    ++probed;
+    ref_advance(ref, workers);
+  });
+  ref_grid_destroy(ref);
+  CHECK(probed == kSlots);
+  CHECK(cells_ok == kSlots);
+  CHECK(rk_ok == kSlots);
+  const RefRows want_reps = ref_pipeline({trace}, rc);
+  expect_same(reps, want_reps);
+  expect_same(run_detection({trace}, rc), want_reps);  // no probe: the pipelined path
+  size_t hosts = 0;
+  for (const auto& r : reps) hosts += r.hosts.size();
+  std::cerr << "  C1: " << kSlots << " slots x " << kPairs << " pairs, " << hosts
+            << " reports, grids / R_k / reports identical every slot\n";
+  CHECK(hosts >= 20 * kSlots);
 }
 #endif
 

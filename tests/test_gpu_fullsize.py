@@ -3,7 +3,8 @@ an 80 GiB stamp grid on the device, 40 GiB of u16 recorders in the reference).
 
 The compiled reference (oracle/_ref, OpenMP on all host cores) replays the
 same slots: 3 slots of C2 traffic (Zipf background + injected scanners/DDoS
-victims, from the repository's generator) at a bounded 8e6 pairs per slot.
+victims, from the repository's generator) at the full 1e8 pairs per slot:
+bench.py's own trace slots 0-2 (same generator parameters).
 Compared bit-exactly: per-cell R_k for several k over all 327,680
 estimators, the hot sets, the reported super points and estimates, and the
 full recorder contents of a random sample of 256 estimators (16.8M
@@ -21,7 +22,7 @@ from oracle import oracle as O
 pytestmark = [pytest.mark.gpu, pytest.mark.slow]
 
 GEO = dict(q=16, r=5, delta=6, seed=0x5eed, eta=1 << 16)
-PAIRS = 8_000_000
+PAIRS = 100_000_000
 K, THETA = 5, 1024.0
 
 

@@ -10,7 +10,7 @@ import pytest
 import paper_1803_11036_b200 as P
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-SYNTH = os.path.join(ROOT, "paper_1803_11036_b200", "lib", "libsspd_synth.so")
+SYNTH = os.path.join(ROOT, "oracle", "libsynth_host.so")
 
 
 class Params(C.Structure):
