@@ -44,6 +44,16 @@ CONFIGS = {
                q=16, r=5, delta=6, eta=1 << 16, seed=0x5eed, k=5, theta=1024.0,
                pairs_per_slot=100_000_000, trace_slots=10, hosts=1 << 21, pool=16, zipf=1.1,
                n_super=110, fanout=4096),
+    # C2 with SURVEY §8(d)'s upper pool bound: 64 distinct opposites per
+    # background host (~4x the distinct pairs per slot).  theta and the
+    # injected fanout scale 4x so the window's background stays below the hot
+    # cutoff (distinct pairs per window << theta * 2^q); the pair set doubles.
+    "c2p64": dict(workload="C2 with 64-entry opposite pools: 1 router/GPU, 1e9-pair Zipf(1.1) trace (10 "
+                           "slots x 1e8 pairs), 100 scanners + 10 DDoS victims at 4*theta injected, "
+                           "theta 4096, full-HBM table q16 r5 delta6 eta65536 (80 GiB u32 stamps)",
+                  q=16, r=5, delta=6, eta=1 << 16, seed=0x5eed, k=5, theta=4096.0,
+                  pairs_per_slot=100_000_000, trace_slots=10, hosts=1 << 21, pool=64, zipf=1.1,
+                  n_super=110, fanout=16384, pairset_log2=26),
     # configs[0]: the reference's CPU-runnable case (reference default geometry).
     "c1": dict(workload="C1: 1 router/GPU, 10 slots x 1e6 (cip,oip) pairs: 20 planted supers x "
                         "2048 distinct oips, the rest uniform; reference default table q14 r5 "
@@ -352,6 +362,8 @@ def main():
     torch.cuda.set_stream(stream)
 
     # --- setup (untimed): grid, trace resident in HBM, pinned host copy ------
+    if cfg.get("pairset_log2"):
+        os.environ.setdefault("SSPD_PAIRSET_LOG2", str(cfg["pairset_log2"]))
     g = P.Grid(cfg["q"], cfg["r"], cfg["delta"], cfg["seed"], cfg["eta"], device=dev,
                width=args.stamp_width, k_max=cfg["k"])
     g.set_stream(stream.cuda_stream)
@@ -478,9 +490,11 @@ def main():
     g.profile(True)
     g.profile_reset()
     launches0 = P.launch_count()
+    fresh0 = g.fresh_pairs()
     clk = ClockSampler(dev).__enter__()
     ms, recon, reps = timed_loop(args.steps, slot, False, clk)
     launches = P.launch_count() - launches0
+    fresh = g.fresh_pairs() - fresh0  # pairs new to their slot (pipelined dedup scan's device counter)
     slot += args.steps
     prof = {}
     for name in ("bin", "scan", "commit", "hist_counts", "count", "reconstruct", "hot_compact", "level2",
@@ -538,20 +552,25 @@ def main():
             achieved = bytes_per_unit * units_per_launch / (per_launch_ms / 1e3) / 1e9
             # DRAM bytes per launch of the same kernel at the same config, from
             # the committed ncu --set full capture (bench cannot run ncu itself)
-            traffic = None
-            try:
-                with open(os.path.join(ROOT, "profiles", "r01_traffic.json")) as f:
-                    t = json.load(f).get(args.config, {}).get(dom)
-                if t and t["units_per_launch"] == units_per_launch:
-                    traffic = t["dram_bytes_per_launch"]
-            except Exception:
-                traffic = None
+            traffic, tsrc = None, None
+            for rnd in ("r02", "r01"):  # the newest capture of this kernel at this config
+                try:
+                    with open(os.path.join(ROOT, "profiles", f"{rnd}_traffic.json")) as f:
+                        t = json.load(f).get(args.config, {}).get(dom)
+                except Exception:
+                    t = None
+                if t and t["units_per_launch"] == units_per_launch and (
+                        rnd != "r01" or args.config != "c2"):  # r01's C2 capture is the replaced kernel
+                    traffic, tsrc = t, f"profiles/{rnd}_traffic.json"
+                    break
+            tb = traffic["dram_bytes_per_launch"] if traffic else None
             roof = {"kernel": dom, "bound": "hbm", "achieved": round(achieved, 1), "peak": hbm,
-                    "unit": "GB/s", "frac": round(achieved / hbm, 4), "traffic": traffic,
+                    "unit": "GB/s", "frac": round(achieved / hbm, 4), "traffic": tb,
                     # what DRAM actually moved per launch at this launch time (the dedup scan
                     # skips the repeated pairs' work, so traffic < algorithmic bytes)
-                    "traffic_gbs": (round(traffic / (per_launch_ms / 1e3) / 1e9, 1)
-                                    if traffic else None),
+                    "traffic_gbs": round(tb / (per_launch_ms / 1e3) / 1e9, 1) if tb else None,
+                    "dram_frac": round(tb / (per_launch_ms / 1e3) / 1e9 / hbm, 4) if tb else None,
+                    "traffic_source": tsrc,
                     "bytes_per_unit": bytes_per_unit, "units_per_launch": units_per_launch,
                     "launch_ms": round(per_launch_ms, 4),
                     "peak_source": "MEASURED_PEAKS.json hbm_gbs" if "hbm_gbs" in peaks else "fallback"}
@@ -565,6 +584,33 @@ def main():
                 roof["random_access"] = {"ceiling_mpkts": ceiling, "scan_mpkts": round(scan_mpkts, 1),
                                          "frac": round(scan_mpkts / ceiling, 3),
                                          "source": "tools/fetch_probe.cu best of red, atom and ld+atom into 640 MB, r=5 (profiles/r01_access_probe.txt)"}
+            elif dom == "scan" and prof[dom]["launches"] and fresh:
+                # Zipf traffic (C2): only the pairs new to their slot stamp their r recorders
+                # (random sector read-modify-writes); the rest cost one pair-set probe, of which
+                # the L2 misses are the other random DRAM accesses (ncu, via the traffic file).
+                # Ceiling: random returning atomics into an 80 GB table, the best of 4/8/16
+                # CTAs/SM in tools/fetch_probe.cu (profiles/r01_access_probe.txt "atom" column:
+                # 4.00 Gpkt/s x r=5 = 20.0 G accesses/s).
+                launch_s = per_launch_ms / 1e3
+                fresh_pl = fresh / prof[dom]["launches"]
+                rmw = fresh_pl * r
+                miss = None
+                if traffic and traffic.get("l2_read_miss_sectors") is not None:
+                    # read misses minus the streamed pairs' own sectors
+                    miss = max(0.0, traffic["l2_read_miss_sectors"] - units_per_launch * 8 / 32)
+                total = rmw + (miss or 0.0)
+                ceiling = 20.0e9
+                roof["fresh_pairs_per_launch"] = int(fresh_pl)
+                roof["dram_bytes_per_fresh_pair"] = round(tb / fresh_pl, 1) if tb else None
+                roof["random_access"] = {
+                    "stamp_rmw_per_s": round(rmw / launch_s / 1e9, 3),
+                    "probe_l2_miss_per_s": round(miss / launch_s / 1e9, 3) if miss is not None else None,
+                    "total_per_s": round(total / launch_s / 1e9, 3), "unit": "G accesses/s",
+                    "ceiling_per_s": ceiling / 1e9, "frac": round(total / launch_s / ceiling, 3),
+                    "source": "fresh pairs: device counter of the pipelined dedup scan (sspd_grid_fresh_pairs); "
+                              "probe misses: ncu lts read-miss sectors of the same kernel minus the pair "
+                              "stream's; ceiling: tools/fetch_probe.cu atom into 80 GB "
+                              "(profiles/r01_access_probe.txt)"}
     kernels_share = {k2: round(v["ms"] / ms, 4) for k2, v in prof.items()}
 
     # Detection accuracy of the last timed slot against the generator's

@@ -290,6 +290,10 @@ sspd_status sspd_grid_new_pairs(sspd_grid* g, uint32_t** dev_pairs, uint64_t* co
  * every mode, and modes may be mixed within a slot.  Narrow-stamp grids run
  * mode 0 as 1 and mode 3 as 2. */
 sspd_status sspd_scan_mode(sspd_grid* g, int mode, int filter);
+/* Pairs found new to their slot by the pipelined dedup scan (the C2 path),
+ * summed since the grid was created: the pair set's inserts plus probes that
+ * hit the probe limit.  Diagnostic (bench.py's per-launch fresh pairs). */
+sspd_status sspd_grid_fresh_pairs(sspd_grid* g, uint64_t* count);
 
 /* ---- synthetic traces (shape of synth_trace,
  * workload.cpp:215-300), bit-identical on host and device ---- */

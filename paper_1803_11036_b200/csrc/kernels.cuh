@@ -40,6 +40,13 @@ struct Geo {
   uint64_t n_rec;        // ncells * eta
 };
 
+// Window-ring row of a stamp `age` = now - old slots back (1 <= age < K):
+// (now - age) mod K from now_slot = now mod K, without a division (a runtime
+// `% K` is a MUFU.RCP + fix-up sequence on every first touch).
+__device__ __forceinline__ uint32_t ring_back(uint32_t now_slot, uint32_t age, uint32_t K) {
+  return now_slot >= age ? now_slot - age : now_slot + K - age;
+}
+
 // floor(n / d) for n < 2^40 (recorder indices) and any 32-bit d >= 1:
 // shift for powers of two, else a Granlund-Montgomery multiply.
 struct Div40 {
@@ -235,7 +242,7 @@ __global__ void __launch_bounds__(256) scan_direct_kernel(const uint32_t* __rest
           const uint32_t old = atomicMax(stamps + idx[u], now);
           if (old < now) {
             atomicAdd(hist + (uint64_t)now_slot * geo.ncells + cell[u], 1u);
-            if (old + K > now) atomicSub(hist + (uint64_t)(old % K) * geo.ncells + cell[u], 1u);
+            if (old + K > now) atomicSub(hist + (uint64_t)ring_back(now_slot, now - old, K) * geo.ncells + cell[u], 1u);
           }
         } else {
           asm volatile("red.relaxed.gpu.global.max.u32 [%0], %1;" ::"l"(stamps + idx[u]), "r"(now) : "memory");
@@ -322,7 +329,7 @@ __device__ __forceinline__ void stamp_pair(const ScanTables& t, const Geo& geo, 
       const uint64_t idx = (uint64_t)cell[u] * geo.eta + bucket;
       if (HIST && old[u] < now) {
         atomicAdd(hist + (uint64_t)now_slot * geo.ncells + cell[u], 1u);
-        if (old[u] + K > now) atomicSub(hist + (uint64_t)(old[u] % K) * geo.ncells + cell[u], 1u);
+        if (old[u] + K > now) atomicSub(hist + (uint64_t)ring_back(now_slot, now - old[u], K) * geo.ncells + cell[u], 1u);
       }
       if (BITS) red_or(touched + (idx >> 5), 1u << (idx & 31));
     }
@@ -517,7 +524,7 @@ __global__ void __launch_bounds__(256, SSPD_DEDUP_MINB) scan_dedup_kernel(const 
           if (row >= geo.r || old[u][row] >= now) continue;
           const uint32_t cell = row << geo.q | row_col(geo, row, c[u], col0[u]);
           atomicAdd(hist + (uint64_t)now_slot * geo.ncells + cell, 1u);
-          if (old[u][row] + K > now) atomicSub(hist + (uint64_t)(old[u][row] % K) * geo.ncells + cell, 1u);
+          if (old[u][row] + K > now) atomicSub(hist + (uint64_t)ring_back(now_slot, now - old[u][row], K) * geo.ncells + cell, 1u);
         }
       }
       continue;
@@ -535,6 +542,171 @@ __global__ void __launch_bounds__(256, SSPD_DEDUP_MINB) scan_dedup_kernel(const 
           if (p != push.rank) push.peers[p][(uint64_t)push.rank * push.region_cap + pos] = pr;
     });
   if (PUSH) __threadfence_system();  // peer stores visible before the exchange's barrier
+}
+
+// PIPELINED DEDUP SCAN (the default C2 path: window ring on, no bitmap, no
+// exchange list, r <= 8).  Same results as scan_dedup_kernel<.., HIST=1,
+// BITS=0, EXPORT=0>; the difference is WHEN each fresh pair's r stamp
+// atomics run: a thread's fresh pairs of group i are hashed as soon as their
+// probes resolve, and their atomics are issued one iteration later, together
+// with group i+1's pair-set probes, so the atomics' round trip is not on the
+// critical path of one group:
+//   iteration i: load pairs(i) -> probe(i) | atomics(i-1) -> resolve(i)
+//                -> ring(i-1) -> hash(i)
+// Requesting the recorder lines early (prefetch.global.L2 variants, or a
+// cp.async.bulk.prefetch) measured 23-24% SLOWER than none at C2
+// (profiles/r02_ab_pipe.md), so nothing is prefetched.
+// HINT 1: L2 eviction priorities -- the random stamp atomics evict_first
+// (each stamp line is used once per slot), the pair-set probes
+// evict_last (head pairs repeat all slot long), the streamed pairs
+// evict_first -- so the stamps' 47M lines per C2 slot do not push the
+// pair set's hot lines out of L2.
+__device__ __forceinline__ uint64_t l2_policy_first() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ uint64_t l2_policy_last() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ uint32_t atom_max_hint(uint32_t* p, uint32_t v, uint64_t pol) {
+  uint32_t old;
+  asm volatile("atom.relaxed.gpu.global.max.L2::cache_hint.u32 %0, [%1], %2, %3;"
+               : "=r"(old) : "l"(p), "r"(v), "l"(pol) : "memory");
+  return old;
+}
+__device__ __forceinline__ unsigned long long ld_ca_hint(const unsigned long long* p, uint64_t pol) {
+  unsigned long long v;
+  asm volatile("ld.global.ca.L2::cache_hint.u64 %0, [%1], %2;" : "=l"(v) : "l"(p), "l"(pol));
+  return v;
+}
+__device__ __forceinline__ uint4 ld_stream_u4_hint(const void* p, uint64_t pol) {
+  uint4 v;
+  asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v4.u32 {%0,%1,%2,%3}, [%4], %5;"
+               : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+               : "l"(p), "l"(pol));
+  return v;
+}
+
+// pair_resolve with the pair-set cache policy on its probes
+__device__ __forceinline__ bool pair_resolve_hint(unsigned long long* __restrict__ table, uint64_t mask, uint64_t key,
+                                                  uint64_t h, unsigned long long v, uint64_t pol) {
+  if (key == kEmptyKey) return true;
+  for (int i = 0;;) {
+    const uint64_t slot = pair_slot(h, i, mask);
+    if (v == key) return false;
+    if (v == kEmptyKey) {
+      const unsigned long long old = atomicCAS(table + slot, kEmptyKey, key);  // (atom.cas takes no cache hint)
+      if (old == kEmptyKey) return true;
+      if (old == key) return false;
+    }
+    if (++i >= kProbeLimit) return true;
+    v = ld_ca_hint(table + pair_slot(h, i, mask), pol);
+  }
+}
+
+// R: rows at compile time (5, the reference default), or 0 = geo.r <= 8.
+#ifndef SSPD_PIPE_MINB
+#define SSPD_PIPE_MINB 4
+#endif
+template <int H1MODE, int HINT, int R>
+__global__ void __launch_bounds__(256, SSPD_PIPE_MINB) scan_dedup_pipe_kernel(
+    const uint32_t* __restrict__ pairs, uint64_t n, const HashTabs* __restrict__ tabs, Geo geo,
+    unsigned long long* __restrict__ table, uint64_t table_mask, uint32_t* __restrict__ stamps, uint32_t now,
+    uint32_t* __restrict__ hist, uint32_t K, unsigned long long* __restrict__ fresh_count) {
+  __shared__ ScanTables t;
+  load_scan_tables(t, tabs);
+  const uint32_t now_slot = now % K;
+  const uint64_t tid = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const uint64_t nthreads = (uint64_t)gridDim.x * blockDim.x;
+  const bool vec = (reinterpret_cast<uintptr_t>(pairs) & 15u) == 0;
+  const uint64_t pol_stamp = HINT ? l2_policy_first() : 0, pol_set = HINT ? l2_policy_last() : 0;
+  constexpr int P = 2;
+  constexpr uint32_t RM = R ? R : 8;  // unrolled row count
+  const uint32_t nr = R ? R : geo.r;
+  const uint64_t ngroups = (n + P - 1) / P;
+  uint32_t n_fresh = 0;
+  // the previous group's fresh pairs: cip, bucket, row-0 column
+  uint32_t pc[P], pb[P], p0[P];
+  bool pv[P];
+#pragma unroll
+  for (int u = 0; u < P; ++u) pv[u] = false;
+  // one extra round per thread drains the last group's pending stamps
+  for (uint64_t g = tid; g < ngroups + nthreads; g += nthreads) {
+    const bool have = g < ngroups;
+    uint32_t c[P], o[P];
+    bool valid[P];
+    const uint64_t q0 = g * P;
+    if (have && vec && q0 + P <= n) {
+      const uint4 a = HINT ? ld_stream_u4_hint(pairs + 2 * q0, pol_stamp) : ld_stream_u4(pairs + 2 * q0);
+      c[0] = a.x; o[0] = a.y; c[1] = a.z; o[1] = a.w;
+      valid[0] = valid[1] = true;
+    } else {
+#pragma unroll
+      for (int u = 0; u < P; ++u) {
+        valid[u] = have && q0 + u < n;
+        c[u] = valid[u] ? pairs[2 * (q0 + u)] : 0u;
+        o[u] = valid[u] ? pairs[2 * (q0 + u) + 1] : 0u;
+      }
+    }
+    uint64_t key[P], h[P];
+    unsigned long long v[P];
+#pragma unroll
+    for (int u = 0; u < P; ++u) {
+      key[u] = (uint64_t)c[u] << 32 | o[u];
+      h[u] = pair_slot_hash(key[u]);
+      unsigned long long* slot0 = table + pair_slot(h[u], 0, table_mask);
+      v[u] = valid[u] ? (HINT ? ld_ca_hint(slot0, pol_set) : __ldca(slot0)) : 0ull;
+    }
+    // the previous group's stamps, in flight together with this group's probes
+    uint32_t old[P][RM];
+#pragma unroll
+    for (int u = 0; u < P; ++u) {
+      if (!pv[u]) continue;
+#pragma unroll
+      for (uint32_t row = 0; row < RM; ++row)
+        if (row < nr) {
+          uint32_t* sp = stamps + (uint64_t)(row << geo.q | row_col(geo, row, pc[u], p0[u])) * geo.eta + pb[u];
+          old[u][row] = HINT ? atom_max_hint(sp, now, pol_stamp) : atomicMax(sp, now);
+        }
+    }
+    bool fresh[P];
+#pragma unroll
+    for (int u = 0; u < P; ++u)
+      fresh[u] = valid[u] && (HINT ? pair_resolve_hint(table, table_mask, key[u], h[u], v[u], pol_set)
+                                   : pair_resolve(table, table_mask, key[u], h[u], v[u]));
+    // window ring moves for the previous group's first touches
+#pragma unroll
+    for (int u = 0; u < P; ++u) {
+      if (!pv[u]) continue;
+#pragma unroll
+      for (uint32_t row = 0; row < RM; ++row) {
+        if (row >= nr || old[u][row] >= now) continue;
+        const uint32_t cell = row << geo.q | row_col(geo, row, pc[u], p0[u]);
+        atomicAdd(hist + (uint64_t)now_slot * geo.ncells + cell, 1u);
+        if (old[u][row] + K > now)
+          atomicSub(hist + (uint64_t)ring_back(now_slot, now - old[u][row], K) * geo.ncells + cell, 1u);
+      }
+    }
+    // this group's fresh pairs become pending
+#pragma unroll
+    for (int u = 0; u < P; ++u) {
+      pv[u] = fresh[u];
+      n_fresh += fresh[u];
+      if (!fresh[u]) continue;
+      pc[u] = c[u];
+      hash_pair<H1MODE>(t, geo, c[u], o[u], pb[u], p0[u]);
+    }
+  }
+  // pairs new to this slot (pair-set inserts plus probe-limit misses): one
+  // atomic per warp
+  if (fresh_count) {
+#pragma unroll
+    for (int off = 16; off; off >>= 1) n_fresh += __shfl_xor_sync(0xffffffffu, n_fresh, off);
+    if ((threadIdx.x & 31) == 0 && n_fresh) atomicAdd(fresh_count, (unsigned long long)n_fresh);
+  }
 }
 
 // BINNING (partition pairs by pair-set region before a dedup scan).  Two
@@ -631,7 +803,7 @@ __device__ __forceinline__ void commit_word(uint32_t bits, uint64_t rec0, uint32
         stamps[rec] = now;
         const uint32_t cell = (uint32_t)by_eta.div(rec);
         atomicAdd(hist + (uint64_t)now_slot * ncells + cell, 1u);
-        if (old + K > now) atomicSub(hist + (uint64_t)(old % K) * ncells + cell, 1u);
+        if (old + K > now) atomicSub(hist + (uint64_t)ring_back(now_slot, now - old, K) * ncells + cell, 1u);
       }
     } else {
       stamps[rec] = now;  // idempotent: a recorder touched this slot reads `now`
@@ -1402,7 +1574,7 @@ __global__ void __launch_bounds__(256) scan_shard_kernel(const uint32_t* __restr
           for (uint32_t j = 0; j < 8; ++j) {
             if (old[j] >= now) continue;
             atomicAdd(hist + (uint64_t)now_slot * geo.ncells + cell[j], 1u);
-            if (old[j] + K > now) atomicSub(hist + (uint64_t)(old[j] % K) * geo.ncells + cell[j], 1u);
+            if (old[j] + K > now) atomicSub(hist + (uint64_t)ring_back(now_slot, now - old[j], K) * geo.ncells + cell[j], 1u);
           }
         }
       }
@@ -1538,7 +1710,7 @@ __device__ __forceinline__ void narrow_ring(uint32_t old, uint32_t cell, const N
   atomicAdd(hist + (uint64_t)now_slot * geo.ncells + cell, 1u);
   if (old >= nc.lo) {
     const uint32_t age = nc.now - old;
-    if (age < K) atomicSub(hist + (uint64_t)((now - age) % K) * geo.ncells + cell, 1u);
+    if (age < K) atomicSub(hist + (uint64_t)ring_back(now_slot, age, K) * geo.ncells + cell, 1u);
   }
 }
 

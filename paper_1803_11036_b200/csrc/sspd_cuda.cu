@@ -451,6 +451,11 @@ struct sspd_grid {
   // L2 (C2 at 40 GiB: 4.19 vs 4.76 ms/slot, profiles/r01_ab_narrow_preload.md);
   // SSPD_NARROW_PRELOAD=0 turns it off
   bool narrow_preload = true;
+  // Pipelined dedup scan (kernels.cuh scan_dedup_pipe_kernel) for the
+  // window-ring path: -1 off (scan_dedup_kernel), 0 on, 1 on with L2
+  // eviction priorities.  $SSPD_DEDUP_PIPE overrides (A/B runs).
+  int dedup_pipe = 0;
+  DevBuf fresh_count;  // u64: pairs new to their slot, summed over the pipelined scans
   uint32_t code_now() const { return code_lo + (now - epoch0); }
   std::mutex mu;
 };
@@ -561,6 +566,20 @@ sspd_status launch_pdl(sspd_grid* g, void (*kernel)(KArgs...), unsigned grid, un
   g_launches.fetch_add(1, std::memory_order_relaxed);
   const cudaError_t e = cudaLaunchKernelEx(&cfg, kernel, static_cast<KArgs>(args)...);
   if (e != cudaSuccess) return fail(SSPD_CUDA_ERROR, std::string("CUDA launch: ") + cudaGetErrorString(e));
+  return SSPD_OK;
+}
+
+// The touched bitmap (1 bit per recorder: 2.7 GB at C2) exists only once a
+// bitmap scan, a recorded exchange or sspd_grid_touched needs it; the dedup
+// and direct scans never do.
+sspd_status ensure_touched_locked(sspd_grid* g) {
+  if (g->touched) return SSPD_OK;
+  if (cache_alloc((void**)&g->touched, g->n_words * 4) != cudaSuccess) {
+    cudaGetLastError();
+    g->touched = nullptr;
+    return fail(SSPD_CUDA_ERROR, "CUDA error: out of memory allocating the touched bitmap");
+  }
+  CU(cudaMemsetAsync(g->touched, 0, g->n_words * 4, g->stream));
   return SSPD_OK;
 }
 
@@ -754,6 +773,10 @@ sspd_status ensure_pairset_locked(sspd_grid* g) {
     return fail(SSPD_CUDA_ERROR, "CUDA error: out of memory (pair set)");
   g->pairset_mask = entries - 1;
   CU(cudaMemsetAsync(g->pairset.p, 0xff, entries * 8, g->stream));
+  if (!g->fresh_count.p) {
+    if (g->fresh_count.ensure(8) != cudaSuccess) return fail(SSPD_CUDA_ERROR, "CUDA error: out of memory");
+    CU(cudaMemsetAsync(g->fresh_count.p, 0, 8, g->stream));
+  }
   return SSPD_OK;
 }
 
@@ -895,6 +918,7 @@ sspd_status create_impl(int device, uint32_t q, uint32_t r, uint32_t delta, uint
   g->width = width;
   if (const char* f = std::getenv("SSPD_SCAN_FILTER")) g->scan_filter = std::atoi(f) != 0;
   if (const char* f = std::getenv("SSPD_NARROW_PRELOAD")) g->narrow_preload = std::atoi(f) != 0;
+  if (const char* f = std::getenv("SSPD_DEDUP_PIPE")) g->dedup_pipe = std::atoi(f);
   // Device-resident pairs: deferred bitmap, measured faster than direct
   // stamping at both geometries (profiles/r01_ab_scan_modes.txt).
   if (const char* m = std::getenv("SSPD_SCAN_MODE")) {
@@ -943,10 +967,6 @@ sspd_status create_impl(int device, uint32_t q, uint32_t r, uint32_t delta, uint
     return cleanup("CUDA error: out of memory allocating " + std::to_string(g->geo.n_rec * 4) +
                    " bytes of stamps");
   }
-  if (width == 32 && cache_alloc((void**)&g->touched, g->n_words * 4) != cudaSuccess) {
-    cudaGetLastError();
-    return cleanup("CUDA error: out of memory allocating the touched bitmap");
-  }
   if (cache_alloc((void**)&g->d_tabs, sizeof(HashTabs)) != cudaSuccess) return cleanup("CUDA error: tables");
   if (PinnedCache::get().alloc(&g->pinned_small, 8192) != cudaSuccess ||
       PinnedCache::get().alloc(reinterpret_cast<void**>(&g->meta_host), sizeof(ReconMeta)) != cudaSuccess ||
@@ -956,8 +976,7 @@ sspd_status create_impl(int device, uint32_t q, uint32_t r, uint32_t delta, uint
   if (cudaMemcpyAsync(g->d_tabs, &h, sizeof h, cudaMemcpyHostToDevice, g->stream) != cudaSuccess)
     return cleanup("CUDA error: table upload");
   // All recorders never seen: stamp 0.
-  if (width == 32 && (cudaMemsetAsync(g->stamps, 0, g->geo.n_rec * 4, g->stream) != cudaSuccess ||
-                      cudaMemsetAsync(g->touched, 0, g->n_words * 4, g->stream) != cudaSuccess))
+  if (width == 32 && cudaMemsetAsync(g->stamps, 0, g->geo.n_rec * 4, g->stream) != cudaSuccess)
     return cleanup("CUDA error: grid init");
   if (cudaStreamSynchronize(g->stream) != cudaSuccess) return cleanup("CUDA error: grid init sync");
   *out = g;
@@ -1018,7 +1037,8 @@ sspd_status sspd_grid_destroy(sspd_grid* g) {
     }
     for (DevBuf* b : {&g->stage[0], &g->stage[1], &g->stage_pairs[0], &g->stage_pairs[1], &g->rec_pairs, &g->counts, &g->hot_cols, &g->hot_rowcnt, &g->hotT,
                       &g->tupA, &g->tupB, &g->misc, &g->meta, &g->surv, &g->pairset, &g->newpairs,
-                      &g->newpairs_count, &g->bin_counts, &g->binned, &g->hot_words, &g->hot_chunks})
+                      &g->newpairs_count, &g->bin_counts, &g->binned, &g->hot_words, &g->hot_chunks, &g->relayset,
+                      &g->shard_sent, &g->masks, &g->fresh_count})
       b->release(true);
     for (auto& r : g->prof) {
       cudaEventDestroy(r.a);
@@ -1179,6 +1199,8 @@ sspd_status scan_locked(sspd_grid* g, const uint32_t* pairs, uint64_t n, int pai
     }
   }
   g->scanned_in_slot += n;
+  if (!g->shard && g->width == 32 && (bits || (!direct && !dedup)))
+    if (sspd_status ts = ensure_touched_locked(g)) return ts;
   if (dedup || g->shard) {
     sspd_status ps = ensure_pairset_locked(g);
     if (ps) return ps;
@@ -1247,7 +1269,24 @@ sspd_status scan_locked(sspd_grid* g, const uint32_t* pairs, uint64_t n, int pai
                                                                    g->pairset_mask, g->stamps, g->now,      \
                                                                    g->hist, g->K, g->touched, np, nc)
       const bool ex = g->export_pairs;
-      if (ex && g->push.world > 1) {
+      if (!ex && hist && !bits && g->geo.r <= 8 && (g->dedup_pipe == 0 || g->dedup_pipe == 1)) {
+#define SSPD_PIPE(H1, HI, R)                                                                                 \
+  scan_dedup_pipe_kernel<H1, HI, R><<<blocks, 256, 0, g->stream>>>(dp, cnt, g->d_tabs, g->geo, tb,              \
+                                                                   g->pairset_mask, g->stamps, g->now, g->hist,  \
+                                                                   g->K, g->fresh_count.as<unsigned long long>())
+        const bool r5 = g->geo.r == 5, hint = g->dedup_pipe == 1;
+        switch ((pow2 ? 0 : 4) + (hint ? 2 : 0) + (r5 ? 1 : 0)) {
+          case 0: SSPD_PIPE(0, 0, 0); break;
+          case 1: SSPD_PIPE(0, 0, 5); break;
+          case 2: SSPD_PIPE(0, 1, 0); break;
+          case 3: SSPD_PIPE(0, 1, 5); break;
+          case 4: SSPD_PIPE(1, 0, 0); break;
+          case 5: SSPD_PIPE(1, 0, 5); break;
+          case 6: SSPD_PIPE(1, 1, 0); break;
+          default: SSPD_PIPE(1, 1, 5); break;
+        }
+#undef SSPD_PIPE
+      } else if (ex && g->push.world > 1) {
         if (pow2 && hist)
           scan_dedup_kernel<0, 1, 0, 1, 1><<<blocks, 256, 0, g->stream>>>(dp, cnt, g->d_tabs, g->geo, tb,
                                                                           g->pairset_mask, g->stamps, g->now,
@@ -1414,6 +1453,7 @@ sspd_status sspd_commit(sspd_grid* g) {
   std::lock_guard<std::mutex> lk(g->mu);
   DeviceGuard dg(g->device);
   g->pristine = false;
+  if (!g->touched) return SSPD_OK;  // no bitmap yet: nothing recorded or merged into one
   g->pending = true;  // the caller may have OR-merged remote touches in
   return commit_locked(g);
 }
@@ -2216,6 +2256,9 @@ sspd_status sspd_set_exchange(sspd_grid* g, int mode) {
   if (mode != 0)
     if (sspd_status w = wide_only(g, "set_exchange")) return w;
   std::lock_guard<std::mutex> lk(g->mu);
+  DeviceGuard dg(g->device);
+  if (mode == 1)
+    if (sspd_status ts = ensure_touched_locked(g)) return ts;
   g->record_touched = mode == 1;
   g->export_pairs = mode == 2;
   return SSPD_OK;
@@ -2245,6 +2288,19 @@ sspd_status sspd_grid_new_pairs(sspd_grid* g, uint32_t** dev_pairs, uint64_t* co
   return SSPD_OK;
 }
 
+sspd_status sspd_grid_fresh_pairs(sspd_grid* g, uint64_t* count) {
+  std::lock_guard<std::mutex> lk(g->mu);
+  DeviceGuard dg(g->device);
+  uint64_t c = 0;
+  if (g->fresh_count.p) {
+    CU(cudaMemcpyAsync(pinned_scratch(g), g->fresh_count.p, 8, cudaMemcpyDeviceToHost, g->stream));
+    CU(cudaStreamSynchronize(g->stream));
+    c = *static_cast<uint64_t*>(pinned_scratch(g));
+  }
+  *count = c;
+  return SSPD_OK;
+}
+
 sspd_status sspd_scan_mode(sspd_grid* g, int mode, int filter) {
   std::lock_guard<std::mutex> lk(g->mu);
   DeviceGuard dg(g->device);
@@ -2259,6 +2315,7 @@ sspd_status sspd_grid_touched(sspd_grid* g, uint32_t** dev_bits, uint64_t* words
   if (sspd_status w = wide_only(g, "grid_touched")) return w;
   std::lock_guard<std::mutex> lk(g->mu);
   DeviceGuard dg(g->device);
+  if (sspd_status ts = ensure_touched_locked(g)) return ts;
   CU(cudaStreamSynchronize(g->stream));
   *dev_bits = g->touched;
   *words = g->n_words;

@@ -389,6 +389,12 @@ class Grid:
                 return [Detection(c, e, r) for c, r, e in rows]
             self._report_buf = (_cabi.Detection_t * n.value)()
 
+    def fresh_pairs(self) -> int:
+        """Pairs the pipelined dedup scan found new to their slot, since creation."""
+        n = C.c_uint64()
+        check(self._L.sspd_grid_fresh_pairs(self._h, C.byref(n)))
+        return n.value
+
     def scan_mode(self, mode: int = -1, filter: int = -1):
         """Scan strategy (include/sspd_cuda.h sspd_scan_mode): 0 = deferred bitmap,
         1 = direct stamping, 2 = direct behind the per-slot pair set, 3 = 2 after
