@@ -364,28 +364,37 @@ def main():
     # --- setup (untimed): grid, trace resident in HBM, pinned host copy ------
     if cfg.get("pairset_log2"):
         os.environ.setdefault("SSPD_PAIRSET_LOG2", str(cfg["pairset_log2"]))
-    g = P.Grid(cfg["q"], cfg["r"], cfg["delta"], cfg["seed"], cfg["eta"], device=dev,
-               width=args.stamp_width, k_max=cfg["k"])
-    g.set_stream(stream.cuda_stream)
-    g.scan_mode({"auto": -1, "bitmap": 0, "direct": 1, "dedup": 2, "binned": 3}[args.scan_mode], args.filter)
+    def new_grid(shard=None):
+        gr = P.Grid(cfg["q"], cfg["r"], cfg["delta"], cfg["seed"], cfg["eta"], device=dev,
+                    width=args.stamp_width, k_max=cfg["k"], shard=shard)
+        gr.set_stream(stream.cuda_stream)
+        gr.scan_mode({"auto": -1, "bitmap": 0, "direct": 1, "dedup": 2, "binned": 3}[args.scan_mode], args.filter)
+        return gr
+
     merge_used = args.merge
-    if world > 1 and args.merge != "stamps":
-        cap = min(cfg["pairs_per_slot"], 32 << 20)
+    if world > 1 and args.merge in ("auto", "shard"):
+        # cells sharded among the routers: each router's grid
+        # holds only the cells it owns (sspd_grid_create_sharded), so N routers
+        # hold an N-times larger table; pair lists if symmetric memory is missing
         # a router pushes each of its new pairs at most once per owner, plus the
         # padding of its warps' last list blocks (kernels.cuh list_pad) per launch
         shard_cap = cfg["pairs_per_slot"] + 40 * torch.cuda.get_device_properties(local).multi_processor_count * 4 * 8 * 64
-        if args.merge == "auto":
-            try:  # cells sharded among the routers; pair lists if symmetric memory is missing
-                PD.prepare(g, PD.SHARD, region_cap=shard_cap)
-                merge_used = "shard"
-            except Exception as e:  # symmetric memory unavailable: lists after the scan
-                print(f"[bench] shard exchange unavailable ({type(e).__name__}: {e}); using pairs",
-                      file=sys.stderr)
-                PD.prepare(g, PD.PAIRS)
-                merge_used = "pairs"
-        else:
-            PD.prepare(g, {"pairs": PD.PAIRS, "push": PD.PUSH, "bitmap": PD.BITMAP, "shard": PD.SHARD}[args.merge],
-                       region_cap=shard_cap if args.merge == "shard" else cap)
+        try:
+            g = new_grid(shard=(world, rank))
+            PD.prepare(g, PD.SHARD, region_cap=shard_cap)
+            merge_used = "shard"
+        except Exception as e:
+            if args.merge == "shard":
+                raise
+            print(f"[bench] shard exchange unavailable ({type(e).__name__}: {e}); using pairs", file=sys.stderr)
+            g = new_grid()
+            PD.prepare(g, PD.PAIRS)
+            merge_used = "pairs"
+    else:
+        g = new_grid()
+        if world > 1 and args.merge != "stamps":
+            cap = min(cfg["pairs_per_slot"], 32 << 20)
+            PD.prepare(g, {"pairs": PD.PAIRS, "push": PD.PUSH, "bitmap": PD.BITMAP}[args.merge], region_cap=cap)
     cdf = torch.from_numpy(zipf_cdf(L, cfg).view(np.int64)).to(f"cuda:{dev}")
     sp = synth_params(cfg, rank, world)
     n_local = cfg["pairs_per_slot"]

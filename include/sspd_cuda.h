@@ -101,6 +101,19 @@ sspd_status sspd_grid_create(int device, uint32_t q, uint32_t r, uint32_t delta,
 sspd_status sspd_grid_create_narrow(int device, uint32_t q, uint32_t r, uint32_t delta,
                                     uint64_t seed, uint32_t eta, uint32_t width,
                                     uint32_t k_max, sspd_grid** out);
+/* A sharded router's PARTIAL grid: only the cells router `rank` of `world`
+ * owns (cell c belongs to c * world / (r * 2^q)) get stamps on `device`,
+ * so N routers hold an N-times larger table between them.  k_max > 0 also
+ * tracks the window ring.  Scans need sspd_set_shard(_relay) with the same
+ * world and rank first; distances are readable for the owned recorders only
+ * (sspd_grid_owned); calls that need every cell (clone, merge, equal,
+ * reconstruct, finalize, hot_sets, active_counts, the other exchange hooks)
+ * fail with SSPD_INVALID_ARGUMENT. */
+sspd_status sspd_grid_create_sharded(int device, uint32_t q, uint32_t r, uint32_t delta, uint64_t seed,
+                                     uint32_t eta, uint32_t k_max, uint32_t world, uint32_t rank,
+                                     sspd_grid** out);
+/* Recorders [rec_lo, rec_hi) held by this grid (everything unless partial). */
+sspd_status sspd_grid_owned(const sspd_grid* g, uint64_t* rec_lo, uint64_t* rec_hi);
 /* Stamp width (8, 16, 32) and tracked window (0 = none). */
 sspd_status sspd_grid_stamp_width(const sspd_grid* g, uint32_t* width, uint32_t* k_max);
 /* Copy constructor (Rsea is copyable: snapshot.cpp:127, pipeline.cpp:39):
@@ -242,8 +255,28 @@ sspd_status sspd_shard_relay(sspd_grid* g, const uint32_t* dev_pairs, uint64_t n
  * (One launch pads each warp's list blocks once instead of once per region.) */
 sspd_status sspd_shard_relay_regions(sspd_grid* g, const uint32_t* dev_base, uint64_t region_stride,
                                      const uint64_t* counts, uint32_t n_regions);
+/* The same with the counts read by the kernel from DEVICE memory (no host
+ * round trip in the slot): region i holds dev_counts[i * count_stride] pairs,
+ * e.g. this router's column of the all-gathered `sent` counters.  A count
+ * past region_stride is clamped and flagged (sspd_shard_overflow). */
+sspd_status sspd_shard_relay_regions_dev(sspd_grid* g, const uint32_t* dev_base, uint64_t region_stride,
+                                         const uint64_t* dev_counts, uint64_t count_stride, uint32_t n_regions);
 sspd_status sspd_shard_sent(sspd_grid* g, uint64_t** dev_counts);
 sspd_status sspd_shard_receive(sspd_grid* g, const uint32_t* dev_pairs, uint64_t n);
+/* sspd_shard_receive over n_regions inbox regions in one launch, counts in
+ * device memory as above; region skip_region (this router's own) is empty. */
+sspd_status sspd_shard_receive_regions_dev(sspd_grid* g, const uint32_t* dev_base, uint64_t region_stride,
+                                           const uint64_t* dev_counts, uint64_t count_stride, uint32_t n_regions,
+                                           uint32_t skip_region);
+/* 1 if a device-counted region ran past its stride since the last call. */
+sspd_status sspd_shard_overflow(sspd_grid* g, int* overflowed);
+/* dst[w] = OR (op 0) or AND (op 1) over srcs[0..n_src)[w], w < words, in one
+ * kernel on `device` (stream NULL = the legacy default stream).  srcs is a
+ * host array of device pointers -- peers' buffers over NVLink (peer access or
+ * symmetric memory) -- so routers merge hot bits and survivor masks without a
+ * host round trip.  dst may not alias a source another device still reads. */
+sspd_status sspd_reduce_words(int device, const uint32_t* const* srcs, uint32_t n_src, uint64_t words, int op,
+                              uint32_t* dst, void* cuda_stream);
 sspd_status sspd_shard_hot(sspd_grid* g, uint32_t k, uint64_t cutoff, uint32_t** dev_hot_words,
                            uint64_t* n_words);
 sspd_status sspd_shard_select(sspd_grid* g, uint32_t k, uint64_t cutoff, uint64_t cap, uint64_t* n_surv,

@@ -48,6 +48,9 @@ SIGNATURES = {
     "sspd_grid_create_narrow": (C.c_int, [C.c_int, C.c_uint32, C.c_uint32, C.c_uint32, C.c_uint64,
                                           C.c_uint32, C.c_uint32, C.c_uint32, C.POINTER(grid_p)]),
     "sspd_grid_stamp_width": (C.c_int, [grid_p, u32p, u32p]),
+    "sspd_grid_create_sharded": (C.c_int, [C.c_int, C.c_uint32, C.c_uint32, C.c_uint32, C.c_uint64,
+                                           C.c_uint32, C.c_uint32, C.c_uint32, C.c_uint32, C.POINTER(grid_p)]),
+    "sspd_grid_owned": (C.c_int, [grid_p, u64p, u64p]),
     "sspd_reconstruct_async": (C.c_int, [grid_p, C.c_uint32, C.c_uint64, C.c_uint64]),
     "sspd_reconstruct_collect": (C.c_int, [grid_p, C.POINTER(Detection_t), C.c_uint64, u64p, u32p, u64p]),
     "sspd_set_shard": (C.c_int, [grid_p, C.c_void_p, C.c_uint32, C.c_uint32, C.c_uint64]),
@@ -56,6 +59,12 @@ SIGNATURES = {
     "sspd_shard_relay_regions": (C.c_int, [grid_p, C.c_void_p, C.c_uint64, u64p, C.c_uint32]),
     "sspd_shard_sent": (C.c_int, [grid_p, C.POINTER(C.c_void_p)]),
     "sspd_shard_receive": (C.c_int, [grid_p, C.c_void_p, C.c_uint64]),
+    "sspd_shard_relay_regions_dev": (C.c_int, [grid_p, C.c_void_p, C.c_uint64, C.c_void_p, C.c_uint64, C.c_uint32]),
+    "sspd_shard_receive_regions_dev": (C.c_int, [grid_p, C.c_void_p, C.c_uint64, C.c_void_p, C.c_uint64,
+                                                 C.c_uint32, C.c_uint32]),
+    "sspd_shard_overflow": (C.c_int, [grid_p, C.POINTER(C.c_int)]),
+    "sspd_reduce_words": (C.c_int, [C.c_int, C.POINTER(C.c_void_p), C.c_uint32, C.c_uint64, C.c_int, C.c_void_p,
+                                    C.c_void_p]),
     "sspd_shard_hot": (C.c_int, [grid_p, C.c_uint32, C.c_uint64, C.POINTER(C.c_void_p), u64p]),
     "sspd_shard_select": (C.c_int, [grid_p, C.c_uint32, C.c_uint64, C.c_uint64, u64p, C.POINTER(C.c_void_p), u64p,
                                     u32p, u64p]),

@@ -37,7 +37,9 @@ Routers::Routers(const RhfgConfig& cfg, uint32_t eta, uint32_t k_max, std::size_
   try {
     const uint64_t inbox_bytes = n * region_cap * 8;
     for (std::size_t i = 0; i < n; ++i) {
-      check(sspd_grid_create_narrow(devices[i], cfg.q, cfg.r, cfg.delta, cfg.seed, eta, 32, k_max, &grids_[i]));
+      // a partial grid: only router i's cells (n == 1: all of them)
+      check(sspd_grid_create_sharded(devices[i], cfg.q, cfg.r, cfg.delta, cfg.seed, eta, k_max,
+                                     static_cast<uint32_t>(n), static_cast<uint32_t>(i), &grids_[i]));
       check(sspd_device_alloc(devices[i], inbox_bytes, &in_a_[i]));
       check(sspd_device_alloc(devices[i], inbox_bytes, &in_b_[i]));
       check(sspd_device_alloc(devices[i], n * sizeof(void*), &table_a_[i]));
@@ -57,7 +59,21 @@ Routers::Routers(const RhfgConfig& cfg, uint32_t eta, uint32_t k_max, std::size_
 
 Routers::~Routers() { release(); }
 
+uint32_t* Routers::scratch(uint64_t words) {
+  if (words > scratch_words_) {
+    if (scratch_) check(sspd_device_free(dev_[0], scratch_));
+    scratch_ = nullptr;
+    scratch_words_ = 0;
+    check(sspd_device_alloc(dev_[0], words * 4, &scratch_));
+    scratch_words_ = words;
+  }
+  return static_cast<uint32_t*>(scratch_);
+}
+
 void Routers::release() {
+  if (scratch_) sspd_device_free(dev_[0], scratch_);
+  scratch_ = nullptr;
+  scratch_words_ = 0;
   for (std::size_t i = 0; i < grids_.size(); ++i) {
     if (grids_[i]) sspd_grid_destroy(grids_[i]);
     for (void* p : {in_a_[i], in_b_[i], table_a_[i], table_b_[i]})
@@ -114,16 +130,21 @@ void Routers::merge() {
 DetectionReport Routers::reconstruct(uint32_t k, double theta) {
   const std::size_t n = grids_.size();
   const uint64_t cutoff = hot_cutoff(eta_, theta);
-  // hot bits: OR over the routers
+  // hot bits: OR over the routers, one kernel on router 0's device reading
+  // every router's bits over NVLink, then each router takes the merged copy
+  // (sspd_shard_hot returns with each router's bits complete)
   std::vector<uint32_t*> hot(n);
   uint64_t words = 0;
   for (std::size_t i = 0; i < n; ++i) check(sspd_shard_hot(grids_[i], k, cutoff, &hot[i], &words));
-  std::vector<uint32_t> merged(words, 0), part(words);
-  for (std::size_t i = 0; i < n; ++i) {
-    check(sspd_grid_copy(grids_[i], part.data(), hot[i], words * 4, 0));
-    for (uint64_t w = 0; w < words; ++w) merged[w] |= part[w];
-  }
-  for (std::size_t i = 0; i < n; ++i) check(sspd_grid_copy(grids_[i], hot[i], merged.data(), words * 4, 1));
+  std::vector<void*> stream(n);
+  for (std::size_t i = 0; i < n; ++i) check(sspd_grid_stream(grids_[i], &stream[i]));
+  uint32_t* merged = scratch(words);
+  std::vector<const uint32_t*> srcs(hot.begin(), hot.end());
+  check(sspd_reduce_words(dev_[0], srcs.data(), static_cast<uint32_t>(n), words, 0, merged, stream[0]));
+  check(sspd_grid_synchronize(grids_[0]));  // every router's bits read before any is overwritten
+  const uint32_t* one[1] = {merged};
+  for (std::size_t i = 0; i < n; ++i)  // queued before shard_select on the router's own stream
+    check(sspd_reduce_words(dev_[i], one, 1, words, 0, hot[i], stream[i]));
   // the same joins everywhere; survivor masks: AND over the routers
   uint64_t n_surv = 0, mwords = 0, ovf_count = 0;
   uint32_t ovf_level = 0;
@@ -134,13 +155,12 @@ DetectionReport Routers::reconstruct(uint32_t k, double theta) {
     if (st == SSPD_CANDIDATE_OVERFLOW) throw CandidateOverflow(ovf_level, ovf_count, cap_);
     check(st);
   }
-  if (n_surv) {
-    std::vector<uint32_t> anded(mwords, ~0u), mp(mwords);
-    for (std::size_t i = 0; i < n; ++i) {
-      check(sspd_grid_copy(grids_[i], mp.data(), masks[i], mwords * 4, 0));
-      for (uint64_t w = 0; w < mwords; ++w) anded[w] &= mp[w];
-    }
-    check(sspd_grid_copy(grids_[0], masks[0], anded.data(), mwords * 4, 1));  // router 0 reports
+  if (n_surv) {  // AND over the routers into router 0's masks (it reports)
+    uint32_t* anded = scratch(mwords);
+    std::vector<const uint32_t*> msrcs(masks.begin(), masks.end());
+    check(sspd_reduce_words(dev_[0], msrcs.data(), static_cast<uint32_t>(n), mwords, 1, anded, stream[0]));
+    const uint32_t* one[1] = {anded};
+    check(sspd_reduce_words(dev_[0], one, 1, mwords, 1, masks[0], stream[0]));  // then shard_finish, same stream
   }
   // router 0 holds the merged masks: it reports
   std::vector<sspd_detection> buf(1024);

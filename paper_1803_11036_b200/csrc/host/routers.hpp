@@ -8,7 +8,10 @@
 // share, stamp their own cells and relay each pair once to the other cell
 // owners; cell owners stamp what arrives.  Reconstruction ORs the routers'
 // hot bits and ANDs the survivors' bucket masks (include/sspd_cuda.h,
-// "sharded routers").  The reports equal the union-min merged grid's.
+// "sharded routers") with one device kernel over the routers' buffers, read
+// over NVLink (sspd_reduce_words).  Each router's grid is partial: it
+// allocates only its own cells (sspd_grid_create_sharded), so N GPUs hold an
+// N-times larger table.  The reports equal the union-min merged grid's.
 #pragma once
 
 #include <cstdint>
@@ -47,6 +50,9 @@ class Routers {
   std::vector<sspd_grid*> grids_;
   std::vector<void*> in_a_, in_b_;        // router i's inboxes (N regions of region_cap pairs)
   std::vector<void*> table_a_, table_b_;  // per router: device arrays of every router's inbox
+  void* scratch_ = nullptr;               // on router 0's device: merged hot bits / masks
+  uint64_t scratch_words_ = 0;
+  uint32_t* scratch(uint64_t words);
 };
 
 }  // namespace sspd::detail

@@ -38,6 +38,10 @@ struct Geo {
   uint32_t low_mask;     // 2^(q-delta) - 1: overlap of adjacent blocks
   uint32_t ncells;       // r * 2^q
   uint64_t n_rec;        // ncells * eta
+  // cells [own_lo, own_hi) have stamps on this device: all of them, except
+  // on a partial grid of a sharded router (sspd_grid_create_sharded), whose
+  // stamp pointer is then based so that cell c's recorders stay at c * eta
+  uint32_t own_lo, own_hi;
 };
 
 // Window-ring row of a stamp `age` = now - old slots back (1 <= age < K):
@@ -263,7 +267,10 @@ __global__ void __launch_bounds__(256) scan_direct_kernel(const uint32_t* __rest
 // only ever redundant work, never a lost touch.  New pairs stamp their r
 // recorders like scan_direct_kernel.
 constexpr uint64_t kEmptyKey = ~0ull;
-constexpr int kProbeLimit = 8;
+#ifndef SSPD_PROBE_LIMIT
+#define SSPD_PROBE_LIMIT 8
+#endif
+constexpr int kProbeLimit = SSPD_PROBE_LIMIT;
 
 // The pair set is split into kPairBins regions; a key's region is the top
 // bits of its hash and its slot within the region the low bits, with linear
@@ -273,9 +280,28 @@ constexpr int kProbeLimit = 8;
 constexpr int kPairBinBits = 6;
 constexpr int kPairBins = 1 << kPairBinBits;
 
-__device__ __forceinline__ uint64_t pair_slot_hash(uint64_t key) {
+// A hash of the whole key (exact ground-truth sets).
+__device__ __forceinline__ uint64_t pair_mix_hash(uint64_t key) {
   uint64_t h = key * 0x9e3779b97f4a7c15ull;
   return h ^ (h >> 29);
+}
+
+// Slot hash of the per-slot pair sets.  SSPD_PAIR_GROUP: every bit but the
+// low 4 from the cip alone, the low 4 from the oip, so a host's pairs share
+// one 16-slot (128 B) line of the set -- the Zipf head's ~3M repeating pairs
+// then live in ~0.2M L2 lines instead of ~3M (one tag each) among the tail's.
+#ifndef SSPD_PAIR_GROUP
+#define SSPD_PAIR_GROUP 0
+#endif
+__device__ __forceinline__ uint64_t pair_slot_hash(uint64_t key) {
+  if (SSPD_PAIR_GROUP) {
+    uint64_t z = (key >> 32) + 0x9e3779b97f4a7c15ull;
+    z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ull;
+    z = (z ^ (z >> 27)) * 0x94d049bb133111ebull;
+    z ^= z >> 31;
+    return (z & ~15ull) | ((uint32_t)key * 0x9E3779B1u >> 28);
+  }
+  return pair_mix_hash(key);
 }
 
 __device__ __forceinline__ uint32_t pair_bin(uint64_t h) { return (uint32_t)(h >> (64 - kPairBinBits)); }
@@ -554,8 +580,10 @@ __global__ void __launch_bounds__(256, SSPD_DEDUP_MINB) scan_dedup_kernel(const 
 //   iteration i: load pairs(i) -> probe(i) | atomics(i-1) -> resolve(i)
 //                -> ring(i-1) -> hash(i)
 // Requesting the recorder lines early (prefetch.global.L2 variants, or a
-// cp.async.bulk.prefetch) measured 23-24% SLOWER than none at C2
-// (profiles/r02_ab_pipe.md), so nothing is prefetched.
+// cp.async.bulk.prefetch) measured 23-24% SLOWER than none at C2, and an
+// L2-resident front set of pairs seen twice (probed first, evict_last) 1.9-2x
+// slower: the extra dependent round trip for every pair outweighs the misses
+// it saves (profiles/r02_ab_pipe.md); nothing is prefetched or fronted.
 // HINT 1: L2 eviction priorities -- the random stamp atomics evict_first
 // (each stamp line is used once per slot), the pair-set probes
 // evict_last (head pairs repeat all slot long), the streamed pairs
@@ -607,9 +635,56 @@ __device__ __forceinline__ bool pair_resolve_hint(unsigned long long* __restrict
   }
 }
 
+// SECTOR PROBES (SSPD_PIPE_SECT): the pair set read 32 B at a time -- the
+// 4 slots of the sector holding a key's home slot in ONE 256-bit load
+// (LDG.E.ENL2.256) -- so a collision inside the sector costs no dependent
+// round trip; sectors are then probed in order, and empty slots are claimed
+// in slot order, so concurrent inserters of one key agree.  (Exact: "seen"
+// only on a key match; a probe limit reads as fresh.)
+struct Sect {
+  unsigned long long k[4];
+};
+__device__ __forceinline__ Sect ld_sect(const unsigned long long* p) {
+  Sect s;
+  asm volatile("ld.global.ca.v4.u64 {%0,%1,%2,%3}, [%4];"
+               : "=l"(s.k[0]), "=l"(s.k[1]), "=l"(s.k[2]), "=l"(s.k[3])
+               : "l"(p));
+  return s;
+}
+__device__ __forceinline__ uint64_t sect_base(uint64_t h, int i, uint64_t mask) {
+  return pair_slot(h & ~3ull, 4 * i, mask);  // region base | ((h & ~3) + 4i) & region mask
+}
+constexpr int kSectLimit = 4;
+__device__ __forceinline__ bool sect_resolve(unsigned long long* __restrict__ table, uint64_t mask, uint64_t key,
+                                             uint64_t h, Sect v) {
+  if (key == kEmptyKey) return true;
+  for (int i = 0;;) {
+    const uint64_t base = sect_base(h, i, mask);
+#pragma unroll
+    for (int j = 0; j < 4; ++j)
+      if (v.k[j] == key) return false;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      if (v.k[j] != kEmptyKey) continue;
+      const unsigned long long old = atomicCAS(table + base + j, kEmptyKey, key);
+      if (old == kEmptyKey) return true;
+      if (old == key) return false;
+    }
+    if (++i >= kSectLimit) return true;
+    v = ld_sect(table + sect_base(h, i, mask));
+  }
+}
+
+#ifndef SSPD_PIPE_SECT
+#define SSPD_PIPE_SECT 0
+#endif
+
 // R: rows at compile time (5, the reference default), or 0 = geo.r <= 8.
 #ifndef SSPD_PIPE_MINB
 #define SSPD_PIPE_MINB 4
+#endif
+#ifndef SSPD_PIPE_PPT
+#define SSPD_PIPE_PPT 2  // pairs per thread per iteration (1, 2 or 4)
 #endif
 template <int H1MODE, int HINT, int R>
 __global__ void __launch_bounds__(256, SSPD_PIPE_MINB) scan_dedup_pipe_kernel(
@@ -623,7 +698,7 @@ __global__ void __launch_bounds__(256, SSPD_PIPE_MINB) scan_dedup_pipe_kernel(
   const uint64_t nthreads = (uint64_t)gridDim.x * blockDim.x;
   const bool vec = (reinterpret_cast<uintptr_t>(pairs) & 15u) == 0;
   const uint64_t pol_stamp = HINT ? l2_policy_first() : 0, pol_set = HINT ? l2_policy_last() : 0;
-  constexpr int P = 2;
+  constexpr int P = SSPD_PIPE_PPT;
   constexpr uint32_t RM = R ? R : 8;  // unrolled row count
   const uint32_t nr = R ? R : geo.r;
   const uint64_t ngroups = (n + P - 1) / P;
@@ -639,10 +714,13 @@ __global__ void __launch_bounds__(256, SSPD_PIPE_MINB) scan_dedup_pipe_kernel(
     uint32_t c[P], o[P];
     bool valid[P];
     const uint64_t q0 = g * P;
-    if (have && vec && q0 + P <= n) {
-      const uint4 a = HINT ? ld_stream_u4_hint(pairs + 2 * q0, pol_stamp) : ld_stream_u4(pairs + 2 * q0);
-      c[0] = a.x; o[0] = a.y; c[1] = a.z; o[1] = a.w;
-      valid[0] = valid[1] = true;
+    if (P >= 2 && have && vec && q0 + P <= n) {
+#pragma unroll
+      for (int u = 0; u < P; u += 2) {
+        const uint4 a = HINT ? ld_stream_u4_hint(pairs + 2 * (q0 + u), pol_stamp) : ld_stream_u4(pairs + 2 * (q0 + u));
+        c[u] = a.x; o[u] = a.y; c[u + 1] = a.z; o[u + 1] = a.w;
+        valid[u] = valid[u + 1] = true;
+      }
     } else {
 #pragma unroll
       for (int u = 0; u < P; ++u) {
@@ -653,12 +731,18 @@ __global__ void __launch_bounds__(256, SSPD_PIPE_MINB) scan_dedup_pipe_kernel(
     }
     uint64_t key[P], h[P];
     unsigned long long v[P];
+    Sect sv[SSPD_PIPE_SECT ? P : 1];
 #pragma unroll
     for (int u = 0; u < P; ++u) {
       key[u] = (uint64_t)c[u] << 32 | o[u];
       h[u] = pair_slot_hash(key[u]);
-      unsigned long long* slot0 = table + pair_slot(h[u], 0, table_mask);
-      v[u] = valid[u] ? (HINT ? ld_ca_hint(slot0, pol_set) : __ldca(slot0)) : 0ull;
+      if (SSPD_PIPE_SECT) {
+        if (valid[u]) sv[u] = ld_sect(table + sect_base(h[u], 0, table_mask));
+        v[u] = 0ull;
+      } else {
+        unsigned long long* slot0 = table + pair_slot(h[u], 0, table_mask);
+        v[u] = valid[u] ? (HINT ? ld_ca_hint(slot0, pol_set) : __ldca(slot0)) : 0ull;
+      }
     }
     // the previous group's stamps, in flight together with this group's probes
     uint32_t old[P][RM];
@@ -674,9 +758,13 @@ __global__ void __launch_bounds__(256, SSPD_PIPE_MINB) scan_dedup_pipe_kernel(
     }
     bool fresh[P];
 #pragma unroll
-    for (int u = 0; u < P; ++u)
-      fresh[u] = valid[u] && (HINT ? pair_resolve_hint(table, table_mask, key[u], h[u], v[u], pol_set)
-                                   : pair_resolve(table, table_mask, key[u], h[u], v[u]));
+    for (int u = 0; u < P; ++u) {
+      if (SSPD_PIPE_SECT)
+        fresh[u] = valid[u] && sect_resolve(table, table_mask, key[u], h[u], sv[SSPD_PIPE_SECT ? u : 0]);
+      else
+        fresh[u] = valid[u] && (HINT ? pair_resolve_hint(table, table_mask, key[u], h[u], v[u], pol_set)
+                                     : pair_resolve(table, table_mask, key[u], h[u], v[u]));
+    }
     // window ring moves for the previous group's first touches
 #pragma unroll
     for (int u = 0; u < P; ++u) {
@@ -849,6 +937,10 @@ __global__ void __launch_bounds__(256) count_kernel(const uint32_t* __restrict__
   const uint64_t nwarps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
   const bool vec = (geo.eta & 3u) == 0;
   for (uint64_t cell = warp; cell < geo.ncells; cell += nwarps) {
+    if (cell < geo.own_lo || cell >= geo.own_hi) {  // another router's cell: nothing here
+      if (lane == 0) counts[cell] = 0;
+      continue;
+    }
     const uint32_t* est = stamps + cell * geo.eta;
     uint32_t c = 0;
     if (vec) {
@@ -892,6 +984,7 @@ __global__ void __launch_bounds__(256) hist_rebuild_kernel(const uint32_t* __res
   const uint64_t warp = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const uint64_t nwarps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
   for (uint64_t cell = warp; cell < geo.ncells; cell += nwarps) {
+    if (cell < geo.own_lo || cell >= geo.own_hi) continue;
     const uint32_t* est = stamps + cell * geo.eta;
     for (uint32_t i = lane; i < geo.eta; i += 32) {
       const uint32_t s = est[i];
@@ -1272,7 +1365,7 @@ __global__ void __launch_bounds__(256) finalize_count_kernel(const uint32_t* __r
 __device__ __forceinline__ bool exact_pair_new(unsigned long long* __restrict__ pset, uint64_t pmask, uint64_t key,
                                                unsigned int* __restrict__ flags) {
   if (key == kEmptyKey) return atomicExch(&flags[1], 1u) == 0u;  // the one key equal to the marker
-  const uint64_t h = pair_slot_hash(key);
+  const uint64_t h = pair_mix_hash(key);
   for (uint64_t i = 0; i <= pmask; ++i) {
     const uint64_t slot = (h + i) & pmask;
     const unsigned long long v = pset[slot];
@@ -1467,8 +1560,15 @@ enum ShardMode { kShardRecv = 0, kShardOwn = 1, kShardToPairOwner = 2, kShardRec
 struct ShardSegs {
   uint64_t stride;
   uint32_t nseg;  // 0: one contiguous input
-  uint32_t unused;
+  uint32_t skip;  // dev_counts: a segment read as empty (the router's own region), else ~0u
   uint64_t start[33];
+  // Counts read by the kernel instead (no host round trip): segment i holds
+  // dev_counts[i * count_stride] pairs -- e.g. a column of the all-gathered
+  // per-router `sent` counters.  A count past `stride` is clamped and sets
+  // *ovf (the caller checks it when it next synchronises).
+  const unsigned long long* dev_counts;
+  uint64_t count_stride;
+  uint32_t* ovf;
 };
 
 __device__ __forceinline__ uint32_t pair_owner(uint64_t h, uint32_t world) {
@@ -1487,7 +1587,27 @@ __global__ void __launch_bounds__(256) scan_shard_kernel(const uint32_t* __restr
   constexpr bool kDedup = PUSH != kShardRecvOnce;
   __shared__ ScanTables t;
   __shared__ ListState s_lists[8][kPushes ? 32 : 1];  // per warp (blockDim 256), per owner
-  load_scan_tables(t, tabs);
+  __shared__ uint64_t s_start[33];                     // segment starts (host or device counts)
+  if (segs.nseg && threadIdx.x == 0) {
+    uint64_t acc = 0;
+    s_start[0] = 0;
+    for (uint32_t i = 0; i < segs.nseg; ++i) {
+      uint64_t c;
+      if (segs.dev_counts) {
+        c = i == segs.skip ? 0ull : segs.dev_counts[i * segs.count_stride];
+        if (c > segs.stride) {
+          if (segs.ovf) atomicOr(segs.ovf, 1u);
+          c = segs.stride;
+        }
+      } else {
+        c = segs.start[i + 1] - segs.start[i];
+      }
+      acc += c;
+      s_start[i + 1] = acc;
+    }
+  }
+  load_scan_tables(t, tabs);  // (its __syncthreads also publishes s_start)
+  if (segs.nseg) n = s_start[segs.nseg];
   const uint32_t now_slot = HIST ? now % K : 0;
   const uint32_t lane = threadIdx.x & 31;
   ListState* wl = s_lists[threadIdx.x >> 5];
@@ -1513,8 +1633,8 @@ __global__ void __launch_bounds__(256) scan_shard_kernel(const uint32_t* __restr
         c[u] = o[u] = 0u;
         if (fresh[u]) {
           uint32_t sg = 0;
-          while (i >= segs.start[sg + 1]) ++sg;
-          const uint2 v = *reinterpret_cast<const uint2*>(pairs + 2 * (sg * segs.stride + (i - segs.start[sg])));
+          while (i >= s_start[sg + 1]) ++sg;
+          const uint2 v = *reinterpret_cast<const uint2*>(pairs + 2 * (sg * segs.stride + (i - s_start[sg])));
           c[u] = v.x;
           o[u] = v.y;
         }
@@ -1631,6 +1751,40 @@ __global__ void __launch_bounds__(256) shard_mask_kernel(const uint32_t* __restr
       }
     }
     masks[item] = m;
+  }
+}
+
+// dst = OR / AND over up to 32 source word arrays (peer memory allowed), 16 B
+// at a time where every pointer is aligned.
+struct ReduceSrcs {
+  const uint32_t* p[32];
+};
+template <int AND>
+__global__ void __launch_bounds__(256) reduce_words_kernel(ReduceSrcs srcs, uint32_t n_src, uint64_t words,
+                                                           uint32_t* __restrict__ dst, int vec) {
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  const uint64_t tid = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (vec) {
+    for (uint64_t i = tid; i < words / 4; i += stride) {
+      uint4 acc = AND ? make_uint4(~0u, ~0u, ~0u, ~0u) : make_uint4(0u, 0u, 0u, 0u);
+      for (uint32_t s = 0; s < n_src; ++s) {
+        const uint4 v = __ldcv(reinterpret_cast<const uint4*>(srcs.p[s]) + i);  // peers' fresh data
+        if (AND) acc.x &= v.x, acc.y &= v.y, acc.z &= v.z, acc.w &= v.w;
+        else acc.x |= v.x, acc.y |= v.y, acc.z |= v.z, acc.w |= v.w;
+      }
+      reinterpret_cast<uint4*>(dst)[i] = acc;
+    }
+    for (uint64_t i = words / 4 * 4 + tid; i < words; i += stride) {
+      uint32_t acc = AND ? ~0u : 0u;
+      for (uint32_t s = 0; s < n_src; ++s) acc = AND ? (acc & __ldcv(srcs.p[s] + i)) : (acc | __ldcv(srcs.p[s] + i));
+      dst[i] = acc;
+    }
+    return;
+  }
+  for (uint64_t i = tid; i < words; i += stride) {
+    uint32_t acc = AND ? ~0u : 0u;
+    for (uint32_t s = 0; s < n_src; ++s) acc = AND ? (acc & __ldcv(srcs.p[s] + i)) : (acc | __ldcv(srcs.p[s] + i));
+    dst[i] = acc;
   }
 }
 

@@ -412,6 +412,7 @@ struct sspd_grid {
   DevBuf relayset;              // relayed: the pair owner's per-slot set of pairs it relayed
   bool relayset_dirty = false;
   DevBuf shard_sent;            // 2 x 32 u64: pairs pushed to each owner this slot (hop 1, hop 2)
+  DevBuf shard_ovf;             // u32: a device-counted region ran past its stride
   DevBuf masks;                 // sharded reconstruction: per-survivor bucket masks
   DevBuf* last_tuples = nullptr;  // buffer holding the last reconstruction's r-tuples
   // sspd_reconstruct_async: one queued reconstruction awaiting collect
@@ -435,6 +436,12 @@ struct sspd_grid {
   // second 4 KB are scratch for synchronous counter/flag read-backs
   // (pinned_scratch), which may run while a reconstruction is pending.
   void* pinned_small = nullptr;
+  // partial grid (sspd_grid_create_sharded): only cells [geo.own_lo,
+  // geo.own_hi) are allocated, at stamps_alloc; `stamps` is based so that
+  // recorder i of an owned cell is still stamps[i]
+  bool partial = false;
+  uint32_t part_world = 1, part_rank = 0;
+  uint32_t* stamps_alloc = nullptr;
   bool profiling = false;
   int prof_suspend = 0;  // inside a PDL launch chain: one event pair around the chain only
   std::vector<ProfRec> prof;
@@ -527,6 +534,14 @@ struct Prof {
 
 // Entry points that need the full 32-bit stamps (distances, merges,
 // exchanges) refuse narrow grids instead of returning inexact data.
+// Calls that need every cell's stamps on this grid.
+sspd_status whole_only(const sspd_grid* g, const char* what) {
+  if (!g->partial) return SSPD_OK;
+  return fail(SSPD_INVALID_ARGUMENT, std::string(what) + ": a sharded router's partial grid holds only cells " +
+                                         std::to_string(g->geo.own_lo) + ".." + std::to_string(g->geo.own_hi - 1) +
+                                         " (use the shard calls)");
+}
+
 sspd_status wide_only(const sspd_grid* g, const char* what) {
   if (g->width == 32) return SSPD_OK;
   return fail(SSPD_INVALID_ARGUMENT, std::string(what) + ": not available on a grid with " +
@@ -888,7 +903,8 @@ sspd_status sspd_device_count(int* n) {
 namespace {
 
 sspd_status create_impl(int device, uint32_t q, uint32_t r, uint32_t delta, uint64_t seed, uint32_t eta,
-                        uint32_t width, uint32_t k_max, sspd_grid** out) {
+                        uint32_t width, uint32_t k_max, sspd_grid** out, uint32_t part_world = 1,
+                        uint32_t part_rank = 0) {
   *out = nullptr;
   const std::string prob = first_problem(q, r, delta, eta);
   if (!prob.empty()) return fail(SSPD_INVALID_ARGUMENT, "Rsea: " + prob);
@@ -914,6 +930,13 @@ sspd_status create_impl(int device, uint32_t q, uint32_t r, uint32_t delta, uint
   g->geo.low_mask = (1u << (q - delta)) - 1u;
   g->geo.ncells = r << q;
   g->geo.n_rec = (uint64_t)g->geo.ncells * eta;
+  // owned cells: those with shard_owner(c) == rank, i.e. c * world / ncells == rank
+  g->geo.own_lo = (uint32_t)(((uint64_t)part_rank * g->geo.ncells + part_world - 1) / part_world);
+  g->geo.own_hi = (uint32_t)(((uint64_t)(part_rank + 1) * g->geo.ncells + part_world - 1) / part_world);
+  g->partial = part_world > 1;
+  g->part_world = part_world;
+  g->part_rank = part_rank;
+  const uint64_t own_rec = (uint64_t)(g->geo.own_hi - g->geo.own_lo) * eta;
   g->by_eta = Div40::make(eta);
   g->width = width;
   if (const char* f = std::getenv("SSPD_SCAN_FILTER")) g->scan_filter = std::atoi(f) != 0;
@@ -962,10 +985,12 @@ sspd_status create_impl(int device, uint32_t q, uint32_t r, uint32_t delta, uint
         cudaMemsetAsync(g->hist, 0, (size_t)g->K * g->geo.ncells * 4, g->stream) != cudaSuccess)
       return cleanup("CUDA error: grid init");
     g->hist_valid = true;
-  } else if (cache_alloc((void**)&g->stamps, g->geo.n_rec * 4) != cudaSuccess) {
+  } else if (cache_alloc((void**)&g->stamps_alloc, own_rec * 4) != cudaSuccess) {
     cudaGetLastError();
-    return cleanup("CUDA error: out of memory allocating " + std::to_string(g->geo.n_rec * 4) +
-                   " bytes of stamps");
+    g->stamps_alloc = nullptr;
+    return cleanup("CUDA error: out of memory allocating " + std::to_string(own_rec * 4) + " bytes of stamps");
+  } else {
+    g->stamps = g->stamps_alloc - (uint64_t)g->geo.own_lo * eta;
   }
   if (cache_alloc((void**)&g->d_tabs, sizeof(HashTabs)) != cudaSuccess) return cleanup("CUDA error: tables");
   if (PinnedCache::get().alloc(&g->pinned_small, 8192) != cudaSuccess ||
@@ -976,7 +1001,7 @@ sspd_status create_impl(int device, uint32_t q, uint32_t r, uint32_t delta, uint
   if (cudaMemcpyAsync(g->d_tabs, &h, sizeof h, cudaMemcpyHostToDevice, g->stream) != cudaSuccess)
     return cleanup("CUDA error: table upload");
   // All recorders never seen: stamp 0.
-  if (width == 32 && cudaMemsetAsync(g->stamps, 0, g->geo.n_rec * 4, g->stream) != cudaSuccess)
+  if (width == 32 && cudaMemsetAsync(g->stamps_alloc, 0, own_rec * 4, g->stream) != cudaSuccess)
     return cleanup("CUDA error: grid init");
   if (cudaStreamSynchronize(g->stream) != cudaSuccess) return cleanup("CUDA error: grid init sync");
   *out = g;
@@ -988,6 +1013,28 @@ sspd_status create_impl(int device, uint32_t q, uint32_t r, uint32_t delta, uint
 sspd_status sspd_grid_create(int device, uint32_t q, uint32_t r, uint32_t delta, uint64_t seed, uint32_t eta,
                              sspd_grid** out) {
   return create_impl(device, q, r, delta, seed, eta, 32, 0, out);
+}
+
+sspd_status sspd_grid_create_sharded(int device, uint32_t q, uint32_t r, uint32_t delta, uint64_t seed,
+                                     uint32_t eta, uint32_t k_max, uint32_t world, uint32_t rank, sspd_grid** out) {
+  *out = nullptr;
+  if (world < 1 || world > 32 || rank >= world)
+    return fail(SSPD_INVALID_ARGUMENT, "create_sharded: need 1 <= world <= 32 and rank < world");
+  if (k_max > 65534) return fail(SSPD_INVALID_ARGUMENT, "k must be in [1, 65534], got " + std::to_string(k_max));
+  sspd_status s = create_impl(device, q, r, delta, seed, eta, 32, 0, out, world, rank);
+  if (s || !k_max) return s;
+  s = sspd_track_window(*out, k_max);
+  if (s) {
+    sspd_grid_destroy(*out);
+    *out = nullptr;
+  }
+  return s;
+}
+
+sspd_status sspd_grid_owned(const sspd_grid* g, uint64_t* rec_lo, uint64_t* rec_hi) {
+  *rec_lo = (uint64_t)g->geo.own_lo * g->eta;
+  *rec_hi = (uint64_t)g->geo.own_hi * g->eta;
+  return SSPD_OK;
 }
 
 sspd_status sspd_grid_create_narrow(int device, uint32_t q, uint32_t r, uint32_t delta, uint64_t seed, uint32_t eta,
@@ -1027,7 +1074,7 @@ sspd_status sspd_grid_destroy(sspd_grid* g) {
     // peers may still read this grid (merges, relays): the whole device
     // idles before its blocks go back to the cache
     cudaDeviceSynchronize();
-    for (void* p : {(void*)g->stamps, (void*)g->codes, (void*)g->touched, (void*)g->hist, (void*)g->d_tabs})
+    for (void* p : {(void*)g->stamps_alloc, (void*)g->codes, (void*)g->touched, (void*)g->hist, (void*)g->d_tabs})
       cache_free(p, true);
     PinnedCache::get().free(g->pinned_small);
     PinnedCache::get().free(g->meta_host);
@@ -1038,7 +1085,7 @@ sspd_status sspd_grid_destroy(sspd_grid* g) {
     for (DevBuf* b : {&g->stage[0], &g->stage[1], &g->stage_pairs[0], &g->stage_pairs[1], &g->rec_pairs, &g->counts, &g->hot_cols, &g->hot_rowcnt, &g->hotT,
                       &g->tupA, &g->tupB, &g->misc, &g->meta, &g->surv, &g->pairset, &g->newpairs,
                       &g->newpairs_count, &g->bin_counts, &g->binned, &g->hot_words, &g->hot_chunks, &g->relayset,
-                      &g->shard_sent, &g->masks, &g->fresh_count})
+                      &g->shard_sent, &g->shard_ovf, &g->masks, &g->fresh_count})
       b->release(true);
     for (auto& r : g->prof) {
       cudaEventDestroy(r.a);
@@ -1058,6 +1105,7 @@ sspd_status sspd_grid_destroy(sspd_grid* g) {
 }
 
 sspd_status sspd_grid_clone(const sspd_grid* src_c, int device, sspd_grid** out) {
+  if (sspd_status w = whole_only(src_c, "clone")) return w;
   auto* src = const_cast<sspd_grid*>(src_c);
   if (sspd_status w = wide_only(src, "Rsea copy")) return w;
   std::lock_guard<std::mutex> lk(src->mu);
@@ -1151,6 +1199,9 @@ namespace {
 // stride: u32 words per input item -- 2 for (cip, oip) pairs, 3 for
 // (ts, cip, oip) trace records (host input only; converted per chunk).
 sspd_status scan_locked(sspd_grid* g, const uint32_t* pairs, uint64_t n, int pairs_on_device, int stride) {
+  if (g->partial && !g->shard)
+    return fail(SSPD_INVALID_ARGUMENT, "scan: a sharded router's partial grid scans through the shard exchange "
+                                       "(sspd_set_shard / sspd_set_shard_relay first)");
   g->pristine = false;
   const bool pow2 = (g->eta & (g->eta - 1)) == 0 && g->eta <= (1u << 31);
   // auto: pairs streamed from the host are PCIe-bound, so stamp them in place
@@ -1270,8 +1321,10 @@ sspd_status scan_locked(sspd_grid* g, const uint32_t* pairs, uint64_t n, int pai
                                                                    g->hist, g->K, g->touched, np, nc)
       const bool ex = g->export_pairs;
       if (!ex && hist && !bits && g->geo.r <= 8 && (g->dedup_pipe == 0 || g->dedup_pipe == 1)) {
+        // one resident wave of the pipelined kernel (its own occupancy)
+        const unsigned pblocks = grid_blocks(g, (cnt + 3) / 4, 256, SSPD_PIPE_MINB);
 #define SSPD_PIPE(H1, HI, R)                                                                                 \
-  scan_dedup_pipe_kernel<H1, HI, R><<<blocks, 256, 0, g->stream>>>(dp, cnt, g->d_tabs, g->geo, tb,              \
+  scan_dedup_pipe_kernel<H1, HI, R><<<pblocks, 256, 0, g->stream>>>(dp, cnt, g->d_tabs, g->geo, tb,              \
                                                                    g->pairset_mask, g->stamps, g->now, g->hist,  \
                                                                    g->K, g->fresh_count.as<unsigned long long>())
         const bool r5 = g->geo.r == 5, hint = g->dedup_pipe == 1;
@@ -1449,6 +1502,7 @@ sspd_status scan_locked(sspd_grid* g, const uint32_t* pairs, uint64_t n, int pai
 }  // namespace
 
 sspd_status sspd_commit(sspd_grid* g) {
+  if (sspd_status w = whole_only(g, "commit")) return w;
   if (sspd_status w = wide_only(g, "commit")) return w;
   std::lock_guard<std::mutex> lk(g->mu);
   DeviceGuard dg(g->device);
@@ -1505,6 +1559,9 @@ sspd_status sspd_get_distances(sspd_grid* g, uint16_t* host_out, uint64_t offset
   if (sspd_status w = wide_only(g, "cells")) return w;
   if (offset > g->geo.n_rec || count > g->geo.n_rec - offset)
     return fail(SSPD_OUT_OF_RANGE, "cells: range out of bounds");
+  if (g->partial && count &&
+      (offset < (uint64_t)g->geo.own_lo * g->eta || offset + count > (uint64_t)g->geo.own_hi * g->eta))
+    return whole_only(g, "cells");
   std::lock_guard<std::mutex> lk(g->mu);
   DeviceGuard dg(g->device);
   sspd_status s = commit_locked(g);
@@ -1531,6 +1588,9 @@ sspd_status sspd_put_distances(sspd_grid* g, const uint16_t* host_in, uint64_t o
   if (sspd_status w = wide_only(g, "cells")) return w;
   if (offset > g->geo.n_rec || count > g->geo.n_rec - offset)
     return fail(SSPD_OUT_OF_RANGE, "cells: range out of bounds");
+  if (g->partial && count &&
+      (offset < (uint64_t)g->geo.own_lo * g->eta || offset + count > (uint64_t)g->geo.own_hi * g->eta))
+    return whole_only(g, "cells");
   std::lock_guard<std::mutex> lk(g->mu);
   DeviceGuard dg(g->device);
   sspd_status s = commit_locked(g);
@@ -1558,6 +1618,7 @@ sspd_status sspd_put_distances(sspd_grid* g, const uint16_t* host_in, uint64_t o
 }
 
 sspd_status sspd_active_counts(sspd_grid* g, uint32_t k, uint32_t* host_out) {
+  if (sspd_status w = whole_only(g, "active_counts")) return w;
   std::lock_guard<std::mutex> lk(g->mu);
   DeviceGuard dg(g->device);
   sspd_status s = counts_locked(g, k);
@@ -1569,6 +1630,7 @@ sspd_status sspd_active_counts(sspd_grid* g, uint32_t k, uint32_t* host_out) {
 }
 
 sspd_status sspd_hot_sets(sspd_grid* g, uint32_t k, uint64_t cutoff, uint32_t* cols_out, uint32_t* row_counts) {
+  if (sspd_status w = whole_only(g, "hot_sets")) return w;
   std::lock_guard<std::mutex> lk(g->mu);
   DeviceGuard dg(g->device);
   std::vector<uint32_t> rc;
@@ -1590,6 +1652,7 @@ sspd_status sspd_hot_sets(sspd_grid* g, uint32_t k, uint64_t cutoff, uint32_t* c
 
 sspd_status sspd_finalize(sspd_grid* g, const uint32_t* tuples, uint64_t n, uint32_t k, uint64_t cutoff,
                           uint8_t* accepted, uint32_t* cips, uint32_t* r_ks) {
+  if (sspd_status w = whole_only(g, "finalize_candidate")) return w;
   if (g->r > 64) return fail(SSPD_INVALID_ARGUMENT, "finalize_candidate: r > 64 unsupported");
   std::lock_guard<std::mutex> lk(g->mu);
   DeviceGuard dg(g->device);
@@ -1792,9 +1855,10 @@ extern "C" {
 
 sspd_status sspd_reconstruct(sspd_grid* g, uint32_t k, uint64_t cutoff, uint64_t cap, sspd_detection* out,
                              uint64_t out_cap, uint64_t* n_out, uint32_t* ovf_level, uint64_t* ovf_count) {
+  *n_out = 0;
+  if (sspd_status w = whole_only(g, "reconstruct")) return w;
   std::lock_guard<std::mutex> lk(g->mu);
   DeviceGuard dg(g->device);
-  *n_out = 0;
   if (sspd_status s = no_pending(g, "reconstruct")) return s;
   if (g->r > 64) return fail(SSPD_INVALID_ARGUMENT, "reconstruct: r > 64 unsupported");
   if (g->shard && g->shard_args.world > 1)
@@ -1818,6 +1882,7 @@ sspd_status sspd_reconstruct(sspd_grid* g, uint32_t k, uint64_t cutoff, uint64_t
 }
 
 sspd_status sspd_reconstruct_async(sspd_grid* g, uint32_t k, uint64_t cutoff, uint64_t cap) {
+  if (sspd_status w = whole_only(g, "reconstruct")) return w;
   std::lock_guard<std::mutex> lk(g->mu);
   DeviceGuard dg(g->device);
   if (sspd_status s = no_pending(g, "reconstruct_async")) return s;
@@ -1878,6 +1943,9 @@ sspd_status sspd_set_shard(sspd_grid* g, void* dev_inbox_ptrs, uint32_t world, u
   if (sspd_status w = wide_only(g, "set_shard")) return w;
   std::lock_guard<std::mutex> lk(g->mu);
   DeviceGuard dg(g->device);
+  if (g->partial && (world != g->part_world || rank != g->part_rank))
+    return fail(SSPD_INVALID_ARGUMENT, "set_shard: this partial grid was created for router " +
+                                           std::to_string(g->part_rank) + " of " + std::to_string(g->part_world));
   if (world == 0) {
     g->shard = false;
     return SSPD_OK;
@@ -1888,8 +1956,10 @@ sspd_status sspd_set_shard(sspd_grid* g, void* dev_inbox_ptrs, uint32_t world, u
     return fail(SSPD_INVALID_ARGUMENT, "set_shard: turn the other exchange hooks off first");
   sspd_status s = commit_locked(g);
   if (s) return s;
-  if (g->shard_sent.ensure(64 * 8) != cudaSuccess) return fail(SSPD_CUDA_ERROR, "CUDA error: out of memory");
+  if (g->shard_sent.ensure(64 * 8) != cudaSuccess || g->shard_ovf.ensure(4) != cudaSuccess)
+    return fail(SSPD_CUDA_ERROR, "CUDA error: out of memory");
   CU(cudaMemsetAsync(g->shard_sent.p, 0, 64 * 8, g->stream));
+  CU(cudaMemsetAsync(g->shard_ovf.p, 0, 4, g->stream));
   g->shard_args = ShardArgs{static_cast<uint2* const*>(dev_inbox_ptrs), g->shard_sent.as<unsigned long long>(),
                             world, rank, region_cap};
   g->shard = true;
@@ -1916,9 +1986,81 @@ sspd_status sspd_shard_sent(sspd_grid* g, uint64_t** dev_counts) {
   return SSPD_OK;
 }
 
+namespace {
+sspd_status shard_receive_locked(sspd_grid* g, const uint32_t* dev_pairs, uint64_t n, const ShardSegs& segs);
+}
+
 sspd_status sspd_shard_receive(sspd_grid* g, const uint32_t* dev_pairs, uint64_t n) {
   if (n == 0) return SSPD_OK;
   std::lock_guard<std::mutex> lk(g->mu);
+  return shard_receive_locked(g, dev_pairs, n, ShardSegs{});
+}
+
+namespace {
+// Device-counted segments (kernels.cuh ShardSegs::dev_counts): launched with
+// a grid sized for the regions' capacity; the kernel reads the counts.
+ShardSegs dev_segs(sspd_grid* g, uint64_t region_stride, const uint64_t* dev_counts, uint64_t count_stride,
+                   uint32_t n_regions, uint32_t skip) {
+  ShardSegs segs{};
+  segs.stride = region_stride;
+  segs.nseg = n_regions;
+  segs.skip = skip;
+  segs.dev_counts = reinterpret_cast<const unsigned long long*>(dev_counts);
+  segs.count_stride = count_stride;
+  segs.ovf = g->shard_ovf.as<uint32_t>();
+  return segs;
+}
+}  // namespace
+
+sspd_status sspd_shard_receive_regions_dev(sspd_grid* g, const uint32_t* dev_base, uint64_t region_stride,
+                                           const uint64_t* dev_counts, uint64_t count_stride, uint32_t n_regions,
+                                           uint32_t skip_region) {
+  if (n_regions == 0 || n_regions > 32 || !dev_counts)
+    return fail(SSPD_INVALID_ARGUMENT, "shard_receive_regions: 1..32 regions and device counts");
+  std::lock_guard<std::mutex> lk(g->mu);
+  if (!g->shard) return fail(SSPD_INVALID_ARGUMENT, "shard_receive: not a sharded grid");
+  return shard_receive_locked(g, dev_base, region_stride * n_regions,
+                              dev_segs(g, region_stride, dev_counts, count_stride, n_regions, skip_region));
+}
+
+sspd_status sspd_reduce_words(int device, const uint32_t* const* srcs, uint32_t n_src, uint64_t words, int op,
+                              uint32_t* dst, void* cuda_stream) {
+  if (n_src == 0 || n_src > 32 || (op != 0 && op != 1) || !dst)
+    return fail(SSPD_INVALID_ARGUMENT, "reduce_words: 1..32 sources, op 0 (OR) or 1 (AND)");
+  if (words == 0) return SSPD_OK;
+  DeviceGuard dg(device);
+  ReduceSrcs rs{};
+  bool aligned = (reinterpret_cast<uintptr_t>(dst) & 15u) == 0;
+  for (uint32_t i = 0; i < n_src; ++i) {
+    if (!srcs[i]) return fail(SSPD_INVALID_ARGUMENT, "reduce_words: null source");
+    rs.p[i] = srcs[i];
+    aligned = aligned && (reinterpret_cast<uintptr_t>(srcs[i]) & 15u) == 0;
+  }
+  int sms = 148;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
+  const uint64_t items = aligned ? (words + 3) / 4 : words;
+  const unsigned blocks = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>((items + 255) / 256, (uint64_t)sms * 4));
+  auto st = static_cast<cudaStream_t>(cuda_stream);
+  g_launches.fetch_add(1, std::memory_order_relaxed);
+  if (op) reduce_words_kernel<1><<<blocks, 256, 0, st>>>(rs, n_src, words, dst, aligned ? 1 : 0);
+  else reduce_words_kernel<0><<<blocks, 256, 0, st>>>(rs, n_src, words, dst, aligned ? 1 : 0);
+  return check_launch();
+}
+
+sspd_status sspd_shard_overflow(sspd_grid* g, int* overflowed) {
+  std::lock_guard<std::mutex> lk(g->mu);
+  DeviceGuard dg(g->device);
+  *overflowed = 0;
+  if (!g->shard_ovf.p) return SSPD_OK;
+  CU(cudaMemcpyAsync(pinned_scratch(g), g->shard_ovf.p, 4, cudaMemcpyDeviceToHost, g->stream));
+  CU(cudaMemsetAsync(g->shard_ovf.p, 0, 4, g->stream));
+  CU(cudaStreamSynchronize(g->stream));
+  *overflowed = *static_cast<int*>(pinned_scratch(g)) != 0;
+  return SSPD_OK;
+}
+
+namespace {
+sspd_status shard_receive_locked(sspd_grid* g, const uint32_t* dev_pairs, uint64_t n, const ShardSegs& segs) {
   DeviceGuard dg(g->device);
   if (!g->shard) return fail(SSPD_INVALID_ARGUMENT, "shard_receive: not a sharded grid");
   sspd_status s = ensure_pairset_locked(g);
@@ -1933,7 +2075,7 @@ sspd_status sspd_shard_receive(sspd_grid* g, const uint32_t* dev_pairs, uint64_t
 #define SSPD_SHARD(H1, HI, MODE)                                                                             \
   scan_shard_kernel<H1, HI, MODE><<<blocks, 256, 0, g->stream>>>(dev_pairs, n, g->d_tabs, g->geo, tb,          \
                                                                  g->pairset_mask, g->stamps, g->now, g->hist, g->K, \
-                                                                 g->shard_args)
+                                                                 g->shard_args, segs)
   if (g->relay) {  // hop 2: each pair arrives once from its pair owner
     if (pow2 && hist) SSPD_SHARD(0, 1, kShardRecvOnce);
     else if (pow2) SSPD_SHARD(0, 0, kShardRecvOnce);
@@ -1946,6 +2088,7 @@ sspd_status sspd_shard_receive(sspd_grid* g, const uint32_t* dev_pairs, uint64_t
 #undef SSPD_SHARD
   return check_launch();
 }
+}  // namespace
 
 namespace {
 sspd_status shard_relay_locked(sspd_grid* g, const uint32_t* dev_pairs, uint64_t n, const ShardSegs& segs);
@@ -1970,6 +2113,16 @@ sspd_status sspd_shard_relay_regions(sspd_grid* g, const uint32_t* dev_base, uin
   for (uint32_t i = n_regions + 1; i < 33; ++i) segs.start[i] = ~0ull;  // the segment search never runs past nseg
   std::lock_guard<std::mutex> lk(g->mu);
   return shard_relay_locked(g, dev_base, segs.start[n_regions], segs);
+}
+
+sspd_status sspd_shard_relay_regions_dev(sspd_grid* g, const uint32_t* dev_base, uint64_t region_stride,
+                                         const uint64_t* dev_counts, uint64_t count_stride, uint32_t n_regions) {
+  if (n_regions == 0 || n_regions > 32 || !dev_counts)
+    return fail(SSPD_INVALID_ARGUMENT, "shard_relay_regions: 1..32 regions and device counts");
+  std::lock_guard<std::mutex> lk(g->mu);
+  if (!g->shard_ovf.p) return fail(SSPD_INVALID_ARGUMENT, "shard_relay: not a relayed sharded grid");
+  return shard_relay_locked(g, dev_base, region_stride * n_regions,
+                            dev_segs(g, region_stride, dev_counts, count_stride, n_regions, ~0u));
 }
 
 namespace {
@@ -2111,6 +2264,9 @@ sspd_status sspd_merge(const sspd_grid* const* grids_c, uint64_t n, int policy, 
     if (sspd_status w = wide_only(grids[i], "merge_rseas")) return w;
   if (sspd_status w = wide_only(out, "merge_rseas")) return w;
   for (uint64_t i = 0; i < n; ++i)
+    if (sspd_status w = whole_only(grids[i], "merge_rseas")) return w;
+  if (sspd_status w = whole_only(out, "merge_rseas")) return w;
+  for (uint64_t i = 0; i < n; ++i)
     if (!compatible(grids[i], grids[0]))
       return fail(SSPD_INVALID_ARGUMENT, "merge_rseas: incompatible snapshots (seed/q/r/delta/eta differ)");
   if (!compatible(out, grids[0]))
@@ -2170,6 +2326,8 @@ sspd_status sspd_merge(const sspd_grid* const* grids_c, uint64_t n, int policy, 
 }
 
 sspd_status sspd_equal(sspd_grid* a, sspd_grid* b, int* equal) {
+  if (sspd_status w = whole_only(a, "==")) return w;
+  if (sspd_status w = whole_only(b, "==")) return w;
   *equal = 0;
   if (sspd_status w = wide_only(a, "operator==")) return w;
   if (sspd_status w = wide_only(b, "operator==")) return w;
@@ -2235,6 +2393,7 @@ sspd_status sspd_track_window(sspd_grid* g, uint32_t k_max) {
 }
 
 sspd_status sspd_grid_stamps(sspd_grid* g, uint32_t** dev_stamps, uint64_t* words) {
+  if (sspd_status w = whole_only(g, "grid_stamps")) return w;
   if (sspd_status w = wide_only(g, "grid_stamps")) return w;
   std::lock_guard<std::mutex> lk(g->mu);
   DeviceGuard dg(g->device);
@@ -2253,8 +2412,10 @@ sspd_status sspd_grid_stamps(sspd_grid* g, uint32_t** dev_stamps, uint64_t* word
 }
 
 sspd_status sspd_set_exchange(sspd_grid* g, int mode) {
-  if (mode != 0)
+  if (mode != 0) {
     if (sspd_status w = wide_only(g, "set_exchange")) return w;
+    if (sspd_status w = whole_only(g, "set_exchange")) return w;
+  }
   std::lock_guard<std::mutex> lk(g->mu);
   DeviceGuard dg(g->device);
   if (mode == 1)
@@ -2265,6 +2426,7 @@ sspd_status sspd_set_exchange(sspd_grid* g, int mode) {
 }
 
 sspd_status sspd_set_push(sspd_grid* g, void* dev_peer_ptrs, uint32_t world, uint32_t rank, uint64_t region_cap) {
+  if (sspd_status w = whole_only(g, "set_push")) return w;
   if (world > 1)
     if (sspd_status w = wide_only(g, "set_push")) return w;
   std::lock_guard<std::mutex> lk(g->mu);

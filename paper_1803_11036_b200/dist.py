@@ -218,7 +218,17 @@ class ShardExchange:
     masks (n_surv * eta bits), popcount -- the reports equal reconstruct on the
     union-min merged grid.  region_cap must cover the pairs a router scans per
     slot plus list padding (kernels.cuh list_pad); a count past it raises.
+
+    No host round trip inside merge(): the per-router counts are all-gathered
+    on the device and the relay/receive kernels read them from device memory
+    (sspd_shard_*_regions_dev); stream order (the grid's stream joined to
+    torch's around each collective) is the only synchronisation.  The hot-bit
+    OR and the mask AND run as ONE kernel per router over the peers'
+    symmetric-memory copies (sspd_reduce_words over NVLink) after a device
+    barrier of the symmetric-memory handle; buffers alternate by slot parity.
     """
+
+    MASK_WORDS = 1 << 22  # symmetric mask buffer (16 MiB); more survivors fall back to NCCL
 
     def __init__(self, grid, region_cap: int, group=None, relay: bool = True):
         import torch.distributed._symmetric_memory as symm_mem
@@ -240,6 +250,15 @@ class ShardExchange:
             self.inbox.append(bufs)
             self.handles.append(hs)
         self.parity = 0
+        # per parity: symmetric copies of the hot bits and of the survivor masks
+        hot_words = grid.r * (((1 << grid.q) + 31) // 32)
+        self.hot_sym, self.mask_sym = [], []
+        for _ in range(2):
+            hb = symm_mem.empty(hot_words, dtype=torch.int32, device=dev)
+            mb = symm_mem.empty(self.MASK_WORDS, dtype=torch.int32, device=dev)
+            self.hot_sym.append((hb, symm_mem.rendezvous(hb, name)))
+            self.mask_sym.append((mb, symm_mem.rendezvous(mb, name)))
+        self._keep = []  # count tensors the queued kernels still read
         grid._exchange = SHARD
         grid._shard = self
         self._arm(grid)
@@ -251,47 +270,68 @@ class ShardExchange:
         else:
             grid.set_shard(hs[0].buffer_ptrs_dev, self.world, self.rank, self.cap)
 
-    def _counts(self, grid, hop: int):
-        """sent[src][dst] of hop 0 or 1, all-gathered (also the barrier)."""
-        grid.synchronize()  # this router's stores are complete (the kernels fence them)
+    def _streams(self, grid):
         dev = torch.device(f"cuda:{grid.device}")
+        return torch.cuda.current_stream(dev), torch.cuda.ExternalStream(grid.stream_handle(), device=dev)
+
+    def _counts(self, grid, hop: int) -> torch.Tensor:
+        """sent[src][dst] of hop 0 or 1, all-gathered on the device (also the
+        barrier: every router's pushes precede its contribution in stream
+        order, and the kernels fence them system-wide).  Row-major
+        [src * world + dst]; no host copy."""
+        cur, gs = self._streams(grid)
+        cur.wait_stream(gs)  # this router's scan/relay kernels, then the collective
         mine = device_view(grid.shard_sent_ptr(), 128, grid.device).view(torch.int64)
         mine = mine[32 * hop: 32 * hop + self.world].clone()
-        allsent = torch.empty(self.world * self.world, dtype=torch.int64, device=dev)
+        allsent = torch.empty(self.world * self.world, dtype=torch.int64, device=mine.device)
         dist.all_gather_into_tensor(allsent, mine, group=self.group)
-        sent = allsent.view(self.world, self.world).tolist()
-        torch.cuda.synchronize(grid.device)
-        over = max(max(row) for row in sent)
-        if over > self.cap:
-            raise RuntimeError(f"shard exchange: {over} pairs for one owner exceed region_cap {self.cap}")
-        return sent
+        gs.wait_stream(cur)  # the next kernels read the gathered counts
+        self._keep.append(allsent)
+        return allsent
 
     def merge(self, grid):
+        self._keep = []
         bufs = self.inbox[self.parity]
+        col = lambda t: t.data_ptr() + 8 * self.rank  # noqa: E731 -- counts [src][rank], stride world
         if self.relay:
             sent = self._counts(grid, 0)
             # the routers' pairs routed here (this router's own included), all regions in one launch
-            grid.shard_relay_regions(bufs[0].data_ptr(), self.cap, [sent[src][self.rank] for src in range(self.world)])
+            grid.shard_relay_regions_dev(bufs[0].data_ptr(), self.cap, col(sent), self.world, self.world)
             sent = self._counts(grid, 1)
-            box = bufs[1].view(self.world, self.cap, 2)
+            box = bufs[1]
         else:
             sent = self._counts(grid, 0)
-            box = bufs[0].view(self.world, self.cap, 2)
-        for src in range(self.world):
-            if src != self.rank and sent[src][self.rank]:
-                grid.shard_receive(box[src].data_ptr(), sent[src][self.rank])
-        grid.synchronize()
+            box = bufs[0]
+        # every other router's region of this router's inbox, one launch
+        grid.shard_receive_regions_dev(box.data_ptr(), self.cap, col(sent), self.world, self.world, self.rank)
         self.parity ^= 1
         self._arm(grid)
 
+    def _reduce_peers(self, grid, src_ptr: int, words: int, sym, op: str):
+        """In place: the words at src_ptr become the OR/AND over all routers',
+        read from the peers' symmetric copies by one kernel."""
+        buf, h = sym
+        cur, gs = self._streams(grid)
+        cur.wait_stream(gs)
+        buf[:words].copy_(device_view(src_ptr, words, grid.device))
+        h.barrier(channel=self.parity)  # every router's copy is in place
+        from .grid import reduce_words
+        reduce_words(grid.device, list(h.buffer_ptrs), words, op, src_ptr, cur.cuda_stream)
+        gs.wait_stream(cur)
+
     def reconstruct(self, grid, k: int, theta: float):
+        p = self.parity
         ptr, n = grid.shard_hot(k, theta)
-        or_allreduce_(device_view(ptr, n, grid.device), self.group)
-        torch.cuda.synchronize(grid.device)
+        if grid.shard_overflow():
+            raise RuntimeError(f"shard exchange: pairs for one owner exceed region_cap {self.cap}")
+        self._reduce_peers(grid, ptr, n, self.hot_sym[p], "or")
         ns, mptr, words = grid.shard_select(k, theta)
         if ns:
-            and_allreduce_(device_view(mptr, words, grid.device), self.group)
-            torch.cuda.synchronize(grid.device)
+            if words <= self.MASK_WORDS:
+                self._reduce_peers(grid, mptr, words, self.mask_sym[p], "and")
+            else:
+                and_allreduce_(device_view(mptr, words, grid.device), self.group)
+                torch.cuda.synchronize(grid.device)
         return grid.shard_finish(theta)
 
 

@@ -71,14 +71,22 @@ class Grid:
     """An RSEA grid resident on one B200 (Rsea, rsea.hpp:52-114)."""
 
     def __init__(self, q: int = 14, r: int = 5, delta: int = 6, seed: int = 0,
-                 eta: int = 2048, device: int = 0, _handle=None, width: int = 32, k_max: int = 0):
+                 eta: int = 2048, device: int = 0, _handle=None, width: int = 32, k_max: int = 0,
+                 shard: tuple[int, int] | None = None):
         """width 8/16 (with the window k_max): a narrow-stamp grid, exact for
-        R_k with k <= k_max and the reports (sspd_grid_create_narrow)."""
+        R_k with k <= k_max and the reports (sspd_grid_create_narrow).
+        shard=(world, rank): a sharded router's partial grid holding only the
+        cells it owns (sspd_grid_create_sharded)."""
         self._L = load()
         self.q, self.r, self.delta, self.seed, self.eta = q, r, delta, seed, eta
         if _handle is None:
             h = C.c_void_p()
-            if width == 32 and not k_max:
+            if shard is not None:
+                if width != 32:
+                    raise ValueError("a sharded router's grid has 32-bit stamps")
+                check(self._L.sspd_grid_create_sharded(device, q, r, delta, seed, eta, k_max, shard[0],
+                                                       shard[1], C.byref(h)))
+            elif width == 32 and not k_max:
                 check(self._L.sspd_grid_create(device, q, r, delta, seed, eta, C.byref(h)))
             else:
                 check(self._L.sspd_grid_create_narrow(device, q, r, delta, seed, eta, width, k_max,
@@ -209,6 +217,18 @@ class Grid:
         n = self.recorder_count()
         out = np.empty(n, dtype=np.uint16)
         check(self._L.sspd_get_distances(self._h, out.ctypes.data_as(_cabi.u16p), 0, n))
+        return out
+
+    def owned(self) -> tuple[int, int]:
+        """Recorders [lo, hi) this grid holds (all of them unless partial)."""
+        lo, hi = C.c_uint64(), C.c_uint64()
+        check(self._L.sspd_grid_owned(self._h, C.byref(lo), C.byref(hi)))
+        return lo.value, hi.value
+
+    def cells_range(self, offset: int, count: int) -> np.ndarray:
+        """Recorders [offset, offset + count) as u16 distances."""
+        out = np.empty(count, dtype=np.uint16)
+        check(self._L.sspd_get_distances(self._h, out.ctypes.data_as(_cabi.u16p), offset, count))
         return out
 
     def set_cells(self, values: np.ndarray, offset: int = 0):
@@ -348,6 +368,25 @@ class Grid:
         offset i * region_stride from dev_base) in one launch."""
         arr = (C.c_uint64 * len(counts))(*[int(x) for x in counts])
         check(self._L.sspd_shard_relay_regions(self._h, C.c_void_p(dev_base), region_stride, arr, len(counts)))
+
+    def shard_relay_regions_dev(self, dev_base: int, region_stride: int, dev_counts: int, count_stride: int,
+                                n_regions: int):
+        """shard_relay_regions with region i's count read by the kernel from
+        device memory at dev_counts[i * count_stride] (u64): no host round trip."""
+        check(self._L.sspd_shard_relay_regions_dev(self._h, C.c_void_p(dev_base), region_stride,
+                                                   C.c_void_p(dev_counts), count_stride, n_regions))
+
+    def shard_receive_regions_dev(self, dev_base: int, region_stride: int, dev_counts: int, count_stride: int,
+                                  n_regions: int, skip_region: int):
+        """Receive n_regions inbox regions in one launch, counts in device memory."""
+        check(self._L.sspd_shard_receive_regions_dev(self._h, C.c_void_p(dev_base), region_stride,
+                                                     C.c_void_p(dev_counts), count_stride, n_regions, skip_region))
+
+    def shard_overflow(self) -> bool:
+        """Did a device-counted region run past its stride (since the last call)?"""
+        f = C.c_int()
+        check(self._L.sspd_shard_overflow(self._h, C.byref(f)))
+        return bool(f.value)
 
     def shard_sent_ptr(self) -> int:
         """Device u64[world]: pairs this router pushed to each owner this slot."""
@@ -522,6 +561,14 @@ def exact_counts(segments, min_count: int = 1, distinct_hint: int = 0, device: i
         if n.value <= cap:
             return {int(c): int(k) for c, k in zip(cips[:n.value], counts[:n.value])}
         cap = int(n.value)
+
+
+def reduce_words(device: int, srcs: list[int], words: int, op: str, dst: int, stream: int = 0):
+    """dst = OR ("or") / AND ("and") of the u32 arrays at the device pointers
+    srcs (peers' buffers allowed), one kernel (sspd_reduce_words)."""
+    arr = (C.c_void_p * len(srcs))(*[C.c_void_p(int(p)) for p in srcs])
+    check(load().sspd_reduce_words(device, arr, len(srcs), words, {"or": 0, "and": 1}[op], C.c_void_p(dst),
+                                   C.c_void_p(stream)))
 
 
 def launch_count() -> int:

@@ -800,7 +800,8 @@ def test_sharded_routers_on_one_device(gpu, world):
 
     geo = DESK
     cap = 1 << 16
-    grids = [gpu.Grid(seed=0x5a, **geo) for _ in range(world)]
+    # partial grids (sspd_grid_create_sharded): each router allocates only its cells
+    grids = [gpu.Grid(seed=0x5a, shard=(world, r) if world > 1 else None, **geo) for r in range(world)]
     inboxes = [torch.zeros(world * cap * 2, dtype=torch.int32, device="cuda") for _ in range(world)]
     table = torch.tensor([b.data_ptr() for b in inboxes], dtype=torch.int64, device="cuda")
     for r, g in enumerate(grids):
@@ -826,7 +827,8 @@ def test_sharded_routers_on_one_device(gpu, world):
         for r, g in enumerate(grids):
             lo = -(-r * ncells // world) * geo["eta"]
             hi = -(-(r + 1) * ncells // world) * geo["eta"]
-            assert np.array_equal(g.cells()[lo:hi], cells[lo:hi]), (s, r)
+            assert g.owned() == (lo, hi)
+            assert np.array_equal(g.cells_range(lo, hi - lo), cells[lo:hi]), (s, r)
         for g in grids:
             g.advance_slot()
         o.advance()
@@ -910,6 +912,23 @@ def test_counter_readbacks_leave_a_queued_reconstruction_intact(gpu):
         assert np.array_equal(g.cells(), o.cells())
 
 
+def test_partial_grid_refuses_whole_grid_calls(gpu):
+    """A sharded router's partial grid allocates only its cells and refuses
+    what needs all of them (include/sspd_cuda.h sspd_grid_create_sharded)."""
+    g = gpu.Grid(seed=1, shard=(4, 1), k_max=5, **DESK)
+    ncells = DESK["r"] << DESK["q"]
+    lo, hi = g.owned()
+    assert (lo, hi) == (-(-ncells // 4) * DESK["eta"], -(-2 * ncells // 4) * DESK["eta"])
+    assert (g.cells_range(lo, hi - lo) == 0xFFFF).all()
+    for call in (g.cells, lambda: g.reconstruct_leveled(5, 128.0), lambda: g.active_counts(5),
+                 lambda: g.hot_sets(5, 128.0), g.copy, lambda: g.set_exchange(2),
+                 lambda: g.scan_batch(np.zeros((4, 2), np.uint32)), lambda: g.cells_range(lo - 1, 2)):
+        with pytest.raises(gpu.InvalidArgument):
+            call()
+    with pytest.raises(gpu.InvalidArgument, match="router 1 of 4"):
+        g.set_shard(0, 4, 2, 16)
+
+
 def _reconstruct_merged(gpu, grids, k, theta):
     """The sharded reconstruction with the collectives done in-process: OR of
     hot bits, AND of survivor masks (dist.ShardExchange.reconstruct)."""
@@ -951,7 +970,7 @@ def test_relayed_sharded_routers_on_one_device(gpu, world):
 
     geo = DESK
     cap = 1 << 18
-    grids = [gpu.Grid(seed=0x5b, **geo) for _ in range(world)]
+    grids = [gpu.Grid(seed=0x5b, shard=(world, r) if world > 1 else None, **geo) for r in range(world)]
     in_a = [torch.zeros(world * cap * 2, dtype=torch.int32, device="cuda") for _ in range(world)]
     in_b = [torch.zeros(world * cap * 2, dtype=torch.int32, device="cuda") for _ in range(world)]
     ta = torch.tensor([b.data_ptr() for b in in_a], dtype=torch.int64, device="cuda")
@@ -999,7 +1018,8 @@ def test_relayed_sharded_routers_on_one_device(gpu, world):
         for r, g in enumerate(grids):
             lo = -(-r * ncells // world) * geo["eta"]
             hi = -(-(r + 1) * ncells // world) * geo["eta"]
-            assert np.array_equal(g.cells()[lo:hi], cells[lo:hi]), (s, r)
+            assert g.owned() == (lo, hi)
+            assert np.array_equal(g.cells_range(lo, hi - lo), cells[lo:hi]), (s, r)
         for g in grids:
             g.advance_slot()
         o.advance()
@@ -1021,3 +1041,106 @@ def test_block_cache_reuse_and_release(gpu):
     h.close()
     assert gpu.release_cached() > 0
     assert gpu.release_cached() == 0
+
+
+@pytest.mark.parametrize("world", [2, 4])
+def test_relayed_routers_with_device_counts_and_peer_reduce(gpu, world):
+    """dist.ShardExchange's device-driven slot, the routers on one device:
+    the per-router `sent` counters gathered into one device array (the
+    all-gather), relay and receive launched with the counts read by the
+    kernels (sspd_shard_*_regions_dev, no host round trip), hot bits OR- and
+    survivor masks AND-merged by sspd_reduce_words over the routers' copies.
+    Reports equal the oracle's union-min merge, owned cells bit-exact."""
+    import torch
+
+    from paper_1803_11036_b200 import dist as PD
+    from paper_1803_11036_b200.grid import reduce_words
+
+    geo = DESK
+    cap = 1 << 18
+    grids = [gpu.Grid(seed=0x5c, shard=(world, r), k_max=5, **geo) for r in range(world)]
+    in_a = [torch.zeros(world * cap * 2, dtype=torch.int32, device="cuda") for _ in range(world)]
+    in_b = [torch.zeros(world * cap * 2, dtype=torch.int32, device="cuda") for _ in range(world)]
+    ta = torch.tensor([b.data_ptr() for b in in_a], dtype=torch.int64, device="cuda")
+    tb = torch.tensor([b.data_ptr() for b in in_b], dtype=torch.int64, device="cuda")
+    for r, g in enumerate(grids):
+        g.set_shard_relay(ta.data_ptr(), tb.data_ptr(), world, r, cap)
+    o = O.OracleGrid(seed=0x5c, **geo)
+    rng = O.Mt64(0x5c)
+    ncells = geo["r"] << geo["q"]
+    shared = rng.pairs(2000)
+
+    def gathered(hop):  # [src * world + dst], as dist.ShardExchange._counts all-gathers it
+        torch.cuda.synchronize()
+        rows = [PD.device_view(g.shard_sent_ptr(), 128, 0).view(torch.int64)[32 * hop: 32 * hop + world]
+                for g in grids]
+        out = torch.cat(rows).contiguous()
+        torch.cuda.synchronize()  # the grids' streams read it next
+        return out
+
+    for s in range(4):
+        for r, g in enumerate(grids):
+            p = np.concatenate([rng.pairs(3000), shared[r * 300: r * 300 + 1500]])
+            cip = 0x0A000000 + (s % 2)
+            p = np.concatenate([p, np.stack([np.full(150, cip, np.uint32), rng.draw(150).astype(np.uint32)], 1)])
+            g.scan_batch(torch.from_numpy(p.view(np.int32)).cuda())
+            o.scan(p)
+        sent = gathered(0)
+        for po, g in enumerate(grids):
+            g.shard_relay_regions_dev(in_a[po].data_ptr(), cap, sent.data_ptr() + 8 * po, world, world)
+        sent2 = gathered(1)
+        for dst, g in enumerate(grids):
+            g.shard_receive_regions_dev(in_b[dst].data_ptr(), cap, sent2.data_ptr() + 8 * dst, world, world, dst)
+        torch.cuda.synchronize()
+        assert not any(g.shard_overflow() for g in grids)
+        # reconstruction: peer-reduce kernels instead of host or torch OR/AND
+        hot = [g.shard_hot(5, 128.0) for g in grids]
+        n = hot[0][1]
+        merged = torch.empty(n, dtype=torch.int32, device="cuda")
+        reduce_words(0, [p for p, _ in hot], n, "or", merged.data_ptr())
+        torch.cuda.synchronize()
+        for p, _ in hot:
+            reduce_words(0, [merged.data_ptr()], n, "or", p)
+        torch.cuda.synchronize()
+        sel = [g.shard_select(5, 128.0) for g in grids]
+        if sel[0][0]:
+            w = sel[0][2]
+            anded = torch.empty(w, dtype=torch.int32, device="cuda")
+            reduce_words(0, [p for _, p, _ in sel], w, "and", anded.data_ptr())
+            torch.cuda.synchronize()
+            for _, p, _ in sel:
+                reduce_words(0, [anded.data_ptr()], w, "and", p)
+            torch.cuda.synchronize()
+        ref = o.reconstruct(5, 128.0)
+        assert {0x0A000000 + (s % 2)} <= {d.cip for d in ref}
+        for g in grids:
+            assert dets_equal(g.shard_finish(128.0), ref), s
+        cells = o.cells()
+        for r, g in enumerate(grids):
+            lo, hi = g.owned()
+            assert np.array_equal(g.cells_range(lo, hi - lo), cells[lo:hi]), (s, r)
+        for g in grids:
+            g.advance_slot()
+        o.advance()
+
+
+def test_reduce_words_matches_numpy(gpu):
+    """sspd_reduce_words: OR / AND over up to 32 sources, aligned and
+    misaligned, word counts not a multiple of 4."""
+    import torch
+
+    from paper_1803_11036_b200.grid import reduce_words
+
+    rng = np.random.default_rng(3)
+    for n_src, words, off in [(1, 7, 0), (3, 1000, 0), (5, 4097, 1), (32, 333, 3)]:
+        host = rng.integers(0, 2**32, size=(n_src, words + 4), dtype=np.uint64).astype(np.uint32)
+        dev = torch.from_numpy(host.view(np.int32)).cuda()
+        srcs = [dev[i, off:].data_ptr() for i in range(n_src)]
+        for op in ("or", "and"):
+            out = torch.zeros(words + 1, dtype=torch.int32, device="cuda")
+            reduce_words(0, srcs, words, op, out[1:].data_ptr() if off else out.data_ptr())
+            torch.cuda.synchronize()
+            got = (out[1:] if off else out[:words]).cpu().numpy().view(np.uint32)[:words]
+            sl = host[:, off:off + words]
+            want = np.bitwise_or.reduce(sl, axis=0) if op == "or" else np.bitwise_and.reduce(sl, axis=0)
+            assert np.array_equal(got, want), (n_src, words, off, op)
