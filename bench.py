@@ -595,31 +595,32 @@ def main():
                                          "source": "tools/fetch_probe.cu best of red, atom and ld+atom into 640 MB, r=5 (profiles/r01_access_probe.txt)"}
             elif dom == "scan" and prof[dom]["launches"] and fresh:
                 # Zipf traffic (C2): only the pairs new to their slot stamp their r recorders
-                # (random sector read-modify-writes); the rest cost one pair-set probe, of which
-                # the L2 misses are the other random DRAM accesses (ncu, via the traffic file).
-                # Ceiling: random returning atomics into an 80 GB table, the best of 4/8/16
-                # CTAs/SM in tools/fetch_probe.cu (profiles/r01_access_probe.txt "atom" column:
-                # 4.00 Gpkt/s x r=5 = 20.0 G accesses/s).
+                # (random sector read-modify-writes); the rest cost one pair-set probe, whose L2
+                # misses are the other random DRAM accesses.  The kernel's DRAM accesses come
+                # from the ncu capture of the same kernel (64 B per read fill, 32 B per written
+                # sector) at this launch time; the ceiling is the best random-access rate
+                # tools/fetch_probe.cu measured on a B200 (profiles/r01_access_probe.txt:
+                # 4-byte loads into a 40 GB table at 16 CTAs/SM, 8.94 Gpkt/s x 5 = 44.7 G/s;
+                # returning atomics reach 20 G/s at any table size).
                 launch_s = per_launch_ms / 1e3
                 fresh_pl = fresh / prof[dom]["launches"]
-                rmw = fresh_pl * r
-                miss = None
-                if traffic and traffic.get("l2_read_miss_sectors") is not None:
-                    # read misses minus the streamed pairs' own sectors
-                    miss = max(0.0, traffic["l2_read_miss_sectors"] - units_per_launch * 8 / 32)
-                total = rmw + (miss or 0.0)
-                ceiling = 20.0e9
                 roof["fresh_pairs_per_launch"] = int(fresh_pl)
                 roof["dram_bytes_per_fresh_pair"] = round(tb / fresh_pl, 1) if tb else None
-                roof["random_access"] = {
-                    "stamp_rmw_per_s": round(rmw / launch_s / 1e9, 3),
-                    "probe_l2_miss_per_s": round(miss / launch_s / 1e9, 3) if miss is not None else None,
-                    "total_per_s": round(total / launch_s / 1e9, 3), "unit": "G accesses/s",
-                    "ceiling_per_s": ceiling / 1e9, "frac": round(total / launch_s / ceiling, 3),
-                    "source": "fresh pairs: device counter of the pipelined dedup scan (sspd_grid_fresh_pairs); "
-                              "probe misses: ncu lts read-miss sectors of the same kernel minus the pair "
-                              "stream's; ceiling: tools/fetch_probe.cu atom into 80 GB "
-                              "(profiles/r01_access_probe.txt)"}
+                ra = {"stamp_rmw_per_s": round(fresh_pl * r / launch_s / 1e9, 3), "unit": "G accesses/s",
+                      "ceiling_per_s": 44.7,
+                      "source": "fresh pairs: device counter of the pipelined dedup scan (sspd_grid_fresh_pairs); "
+                                "DRAM accesses: ncu dram__bytes_read/64 + dram__bytes_write/32 of the same kernel "
+                                f"({tsrc}); ceiling: tools/fetch_probe.cu best random-load rate "
+                                "(profiles/r01_access_probe.txt)"}
+                if traffic:
+                    acc = traffic["dram_read"] / 64 + traffic["dram_write"] / 32
+                    ra["dram_accesses_per_s"] = round(acc / launch_s / 1e9, 3)
+                    ra["frac"] = round(acc / launch_s / 44.7e9, 3)
+                    if traffic.get("l2_read_miss_sectors") is not None:
+                        # read misses (32 B sectors) minus the streamed pairs' own: the probes'
+                        ra["probe_miss_sectors_per_launch"] = int(
+                            max(0.0, traffic["l2_read_miss_sectors"] - units_per_launch * 8 / 32))
+                roof["random_access"] = ra
     kernels_share = {k2: round(v["ms"] / ms, 4) for k2, v in prof.items()}
 
     # Detection accuracy of the last timed slot against the generator's

@@ -583,7 +583,7 @@ __global__ void __launch_bounds__(256, SSPD_DEDUP_MINB) scan_dedup_kernel(const 
 // cp.async.bulk.prefetch) measured 23-24% SLOWER than none at C2, and an
 // L2-resident front set of pairs seen twice (probed first, evict_last) 1.9-2x
 // slower: the extra dependent round trip for every pair outweighs the misses
-// it saves (profiles/r02_ab_pipe.md); nothing is prefetched or fronted.
+// it saves (profiles/r02_ab_scan.md); nothing is prefetched or fronted.
 // HINT 1: L2 eviction priorities -- the random stamp atomics evict_first
 // (each stamp line is used once per slot), the pair-set probes
 // evict_last (head pairs repeat all slot long), the streamed pairs

@@ -698,6 +698,26 @@ TEST_CASE("differential: C1 at full size, every slot's grid, R_k and reports") {
             << " reports, grids / R_k / reports identical every slot\n";
   CHECK(hosts >= 20 * kSlots);
 }
+
+// A window the ring cannot budget (K > eta/4): run_detection
+// tracks no ring and counts over the stamps instead -- the reference's
+// largest legal k at its default geometry, whose ring would need
+// 4 B x 65534 x 5 x 2^14 = 21 GB.  Reports equal the reference's.
+TEST_CASE("differential: run_detection at k = 65534 without a window ring") {
+  RunConfig rc;
+  rc.cfg = RhfgConfig{14, 5, 6, 0x5eed};
+  rc.eta = 2048;
+  rc.theta = 1024;
+  rc.window.k = 65534;
+  const auto w = workload(3, 1500, 4, rc, 123);
+  expect_same(run_detection({w.trace}, rc), ref_pipeline({w.trace}, rc));
+  RunConfig desk = test_config();
+  desk.window.k = 65534;
+  const auto wd = workload(3, 256, 6, desk, 124);
+  expect_same(run_detection({wd.trace}, desk), ref_pipeline({wd.trace}, desk));
+  const auto shards = split(wd.trace, 3, 125);
+  expect_same(run_detection(shards, desk), ref_pipeline(shards, desk));
+}
 #endif
 
 CHECK_MAIN
