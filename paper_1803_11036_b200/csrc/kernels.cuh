@@ -239,19 +239,23 @@ __global__ void __launch_bounds__(256) scan_direct_kernel(const uint32_t* __rest
         idx[u] = (uint64_t)cell[u] * geo.eta + bucket;
         cur[u] = (row < geo.r) ? (FILTER ? __ldca(stamps + idx[u]) : 0u) : now;
       }
+      uint32_t old[4];
 #pragma unroll
-      for (int u = 0; u < 4; ++u) {
+      for (int u = 0; u < 4; ++u) {  // issue the group's atomics before consuming any old value
+        old[u] = now;
         if (cur[u] == now) continue;
-        if (HIST) {
-          const uint32_t old = atomicMax(stamps + idx[u], now);
-          if (old < now) {
-            atomicAdd(hist + (uint64_t)now_slot * geo.ncells + cell[u], 1u);
-            if (old + K > now) atomicSub(hist + (uint64_t)ring_back(now_slot, now - old, K) * geo.ncells + cell[u], 1u);
-          }
-        } else {
-          asm volatile("red.relaxed.gpu.global.max.u32 [%0], %1;" ::"l"(stamps + idx[u]), "r"(now) : "memory");
-        }
+        if (HIST) old[u] = atomicMax(stamps + idx[u], now);
+        else asm volatile("red.relaxed.gpu.global.max.u32 [%0], %1;" ::"l"(stamps + idx[u]), "r"(now) : "memory");
         if (BITS) red_or(touched + (idx[u] >> 5), 1u << (idx[u] & 31));
+      }
+      if (HIST) {
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          if (old[u] >= now) continue;
+          atomicAdd(hist + (uint64_t)now_slot * geo.ncells + cell[u], 1u);
+          if (old[u] + K > now)
+            atomicSub(hist + (uint64_t)ring_back(now_slot, now - old[u], K) * geo.ncells + cell[u], 1u);
+        }
       }
     }
   });
