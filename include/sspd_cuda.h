@@ -327,6 +327,13 @@ sspd_status sspd_scan_mode(sspd_grid* g, int mode, int filter);
  * summed since the grid was created: the pair set's inserts plus probes that
  * hit the probe limit.  Diagnostic (bench.py's per-launch fresh pairs). */
 sspd_status sspd_grid_fresh_pairs(sspd_grid* g, uint64_t* count);
+/* The CHECKED build (lib/libsspd_cuda_checked.so, -DSSPD_CHECKED): bounds
+ * checks on every data-dependent stamp / code / window-ring index and the
+ * ring's no-underflow invariant (kernels.cuh "CHECKED BUILD").  Waits for the
+ * device, returns the first failing kernels.cuh line and the failure count,
+ * optionally resetting both.  The product library returns
+ * SSPD_INVALID_ARGUMENT. */
+sspd_status sspd_checked_status(int device, uint32_t* first_line, uint64_t* failures, int reset);
 
 /* ---- synthetic traces (shape of synth_trace,
  * workload.cpp:215-300), bit-identical on host and device ---- */

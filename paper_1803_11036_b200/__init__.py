@@ -8,7 +8,7 @@ multi-router runs.
 """
 from ._cabi import (CandidateOverflow, CudaError, InvalidArgument, NoDevice, OutOfRange,
                     PAPER_MAX, UNION_MIN, SspdError, load)
-from .grid import (BASE_NOW, Detection, Grid, device_count, device_ordinals, estimate_cardinality, exact_counts,
+from .grid import (BASE_NOW, Detection, Grid, checked_status, device_count, device_ordinals, estimate_cardinality, exact_counts,
                    export_snapshot,
                    hot_cutoff, import_snapshot, launch_count, merge_rseas, release_cached)
 
@@ -18,7 +18,7 @@ from .trace import read_trace, write_trace
 __all__ = [
     "run_detection", "validate_config", "read_trace", "write_trace",
     "BASE_NOW", "CandidateOverflow", "CudaError", "Detection", "Grid", "InvalidArgument",
-    "NoDevice", "OutOfRange", "PAPER_MAX", "SspdError", "UNION_MIN", "device_count", "device_ordinals",
+    "NoDevice", "OutOfRange", "PAPER_MAX", "SspdError", "UNION_MIN", "checked_status", "device_count", "device_ordinals",
     "estimate_cardinality", "exact_counts", "export_snapshot", "hot_cutoff", "import_snapshot", "launch_count",
     "load", "merge_rseas", "release_cached",
 ]

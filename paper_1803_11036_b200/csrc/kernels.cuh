@@ -81,6 +81,55 @@ struct Div40 {
   }
 };
 
+// CHECKED BUILD (-DSSPD_CHECKED, lib/libsspd_cuda_checked.so; compute-
+// sanitizer is closed on this pool): every data-dependent index into the
+// stamps, narrow codes and window ring is bounds-checked against the grid
+// (including a partial grid's own cells), and every window-ring decrement
+// asserts the count it takes from is positive -- the ring's invariant.  A
+// failed check records the first failing source line and a count in device
+// globals (read by sspd_checked_status) and skips the access.  The product
+// build compiles all of it away.
+#ifdef SSPD_CHECKED
+__device__ unsigned int g_chk_line;
+__device__ unsigned long long g_chk_count;
+__device__ __forceinline__ bool chk_fail(unsigned line) {
+  atomicCAS(&g_chk_line, 0u, line);
+  atomicAdd(&g_chk_count, 1ull);
+  return false;
+}
+#define SSPD_OK_OR_SKIP(cond) ((cond) ? true : chk_fail(__LINE__))
+#else
+#define SSPD_OK_OR_SKIP(cond) true
+#endif
+
+// Recorder (cell, bucket) of an owned cell.
+__device__ __forceinline__ bool rec_ok(const Geo& geo, uint64_t cell, uint32_t bucket) {
+  return cell >= geo.own_lo && cell < geo.own_hi && bucket < geo.eta;
+}
+// Window-ring moves: +1 for the slot now, -1 for the slot a recorder leaves.
+__device__ __forceinline__ void ring_add(uint32_t* hist, uint32_t slot, uint32_t ncells, uint32_t cell, uint32_t K,
+                                         unsigned line) {
+#ifdef SSPD_CHECKED
+  if (!(slot < K && cell < ncells)) {
+    chk_fail(line);
+    return;
+  }
+#endif
+  atomicAdd(hist + (uint64_t)slot * ncells + cell, 1u);
+}
+__device__ __forceinline__ void ring_sub(uint32_t* hist, uint32_t slot, uint32_t ncells, uint32_t cell, uint32_t K,
+                                         unsigned line) {
+#ifdef SSPD_CHECKED
+  if (!(slot < K && cell < ncells)) {
+    chk_fail(line);
+    return;
+  }
+  if (atomicSub(hist + (uint64_t)slot * ncells + cell, 1u) == 0u) chk_fail(line);  // count went below zero
+#else
+  atomicSub(hist + (uint64_t)slot * ncells + cell, 1u);
+#endif
+}
+
 // x86 semantics of the reference's 32-bit shifts by computed amounts
 // (hashing.hpp:70 can shift by >= 32 for large r): the count is masked.
 __device__ __forceinline__ uint32_t shr32(uint32_t x, uint32_t s) { return x >> (s & 31u); }
@@ -237,7 +286,8 @@ __global__ void __launch_bounds__(256) scan_direct_kernel(const uint32_t* __rest
         const uint32_t row = r0 + u;
         cell[u] = row << geo.q | row_col(geo, row, cip, col0);
         idx[u] = (uint64_t)cell[u] * geo.eta + bucket;
-        cur[u] = (row < geo.r) ? (FILTER ? __ldca(stamps + idx[u]) : 0u) : now;
+        const bool live = row < geo.r && SSPD_OK_OR_SKIP(rec_ok(geo, cell[u], bucket));
+        cur[u] = live ? (FILTER ? __ldca(stamps + idx[u]) : 0u) : now;
       }
       uint32_t old[4];
 #pragma unroll
@@ -252,9 +302,9 @@ __global__ void __launch_bounds__(256) scan_direct_kernel(const uint32_t* __rest
 #pragma unroll
         for (int u = 0; u < 4; ++u) {
           if (old[u] >= now) continue;
-          atomicAdd(hist + (uint64_t)now_slot * geo.ncells + cell[u], 1u);
+          ring_add(hist, now_slot, geo.ncells, cell[u], K, __LINE__);
           if (old[u] + K > now)
-            atomicSub(hist + (uint64_t)ring_back(now_slot, now - old[u], K) * geo.ncells + cell[u], 1u);
+            ring_sub(hist, ring_back(now_slot, now - old[u], K), geo.ncells, cell[u], K, __LINE__);
         }
       }
     }
@@ -347,7 +397,7 @@ __device__ __forceinline__ void stamp_pair(const ScanTables& t, const Geo& geo, 
       const uint32_t row = r0 + u;
       cell[u] = row << geo.q | row_col(geo, row, cip, col0);
       old[u] = now;
-      if (row < geo.r) {
+      if (row < geo.r && SSPD_OK_OR_SKIP(rec_ok(geo, cell[u], bucket))) {
         uint32_t* p = stamps + (uint64_t)cell[u] * geo.eta + bucket;
         if (HIST) old[u] = atomicMax(p, now);
         else asm volatile("red.relaxed.gpu.global.max.u32 [%0], %1;" ::"l"(p), "r"(now) : "memory");
@@ -358,8 +408,8 @@ __device__ __forceinline__ void stamp_pair(const ScanTables& t, const Geo& geo, 
       if (r0 + u >= geo.r) break;
       const uint64_t idx = (uint64_t)cell[u] * geo.eta + bucket;
       if (HIST && old[u] < now) {
-        atomicAdd(hist + (uint64_t)now_slot * geo.ncells + cell[u], 1u);
-        if (old[u] + K > now) atomicSub(hist + (uint64_t)ring_back(now_slot, now - old[u], K) * geo.ncells + cell[u], 1u);
+        ring_add(hist, now_slot, geo.ncells, cell[u], K, __LINE__);
+        if (old[u] + K > now) ring_sub(hist, ring_back(now_slot, now - old[u], K), geo.ncells, cell[u], K, __LINE__);
       }
       if (BITS) red_or(touched + (idx >> 5), 1u << (idx & 31));
     }
@@ -540,11 +590,14 @@ __global__ void __launch_bounds__(256, SSPD_DEDUP_MINB) scan_dedup_kernel(const 
         if (!fresh[u]) continue;
         hash_pair<H1MODE>(t, geo, c[u], o[u], bucket[u], col0[u]);
 #pragma unroll
-        for (uint32_t row = 0; row < 8; ++row)
-          if (row < geo.r)
+        for (uint32_t row = 0; row < 8; ++row) {
+          old[u][row] = now;
+          if (row < geo.r &&
+              SSPD_OK_OR_SKIP(rec_ok(geo, row << geo.q | row_col(geo, row, c[u], col0[u]), bucket[u])))
             old[u][row] = atomicMax(stamps + (uint64_t)(row << geo.q | row_col(geo, row, c[u], col0[u])) * geo.eta +
                                         bucket[u],
                                     now);
+        }
       }
 #pragma unroll
       for (int u = 0; u < P; ++u) {
@@ -553,8 +606,8 @@ __global__ void __launch_bounds__(256, SSPD_DEDUP_MINB) scan_dedup_kernel(const 
         for (uint32_t row = 0; row < 8; ++row) {
           if (row >= geo.r || old[u][row] >= now) continue;
           const uint32_t cell = row << geo.q | row_col(geo, row, c[u], col0[u]);
-          atomicAdd(hist + (uint64_t)now_slot * geo.ncells + cell, 1u);
-          if (old[u][row] + K > now) atomicSub(hist + (uint64_t)ring_back(now_slot, now - old[u][row], K) * geo.ncells + cell, 1u);
+          ring_add(hist, now_slot, geo.ncells, cell, K, __LINE__);
+          if (old[u][row] + K > now) ring_sub(hist, ring_back(now_slot, now - old[u][row], K), geo.ncells, cell, K, __LINE__);
         }
       }
       continue;
@@ -756,8 +809,11 @@ __global__ void __launch_bounds__(256, SSPD_PIPE_MINB) scan_dedup_pipe_kernel(
 #pragma unroll
       for (uint32_t row = 0; row < RM; ++row)
         if (row < nr) {
-          uint32_t* sp = stamps + (uint64_t)(row << geo.q | row_col(geo, row, pc[u], p0[u])) * geo.eta + pb[u];
-          old[u][row] = HINT ? atom_max_hint(sp, now, pol_stamp) : atomicMax(sp, now);
+          const uint32_t cell = row << geo.q | row_col(geo, row, pc[u], p0[u]);
+          uint32_t* sp = stamps + (uint64_t)cell * geo.eta + pb[u];
+          old[u][row] = now;
+          if (SSPD_OK_OR_SKIP(rec_ok(geo, cell, pb[u])))
+            old[u][row] = HINT ? atom_max_hint(sp, now, pol_stamp) : atomicMax(sp, now);
         }
     }
     bool fresh[P];
@@ -777,9 +833,9 @@ __global__ void __launch_bounds__(256, SSPD_PIPE_MINB) scan_dedup_pipe_kernel(
       for (uint32_t row = 0; row < RM; ++row) {
         if (row >= nr || old[u][row] >= now) continue;
         const uint32_t cell = row << geo.q | row_col(geo, row, pc[u], p0[u]);
-        atomicAdd(hist + (uint64_t)now_slot * geo.ncells + cell, 1u);
+        ring_add(hist, now_slot, geo.ncells, cell, K, __LINE__);
         if (old[u][row] + K > now)
-          atomicSub(hist + (uint64_t)ring_back(now_slot, now - old[u][row], K) * geo.ncells + cell, 1u);
+          ring_sub(hist, ring_back(now_slot, now - old[u][row], K), geo.ncells, cell, K, __LINE__);
       }
     }
     // this group's fresh pairs become pending
@@ -894,8 +950,8 @@ __device__ __forceinline__ void commit_word(uint32_t bits, uint64_t rec0, uint32
       if (old != now) {
         stamps[rec] = now;
         const uint32_t cell = (uint32_t)by_eta.div(rec);
-        atomicAdd(hist + (uint64_t)now_slot * ncells + cell, 1u);
-        if (old + K > now) atomicSub(hist + (uint64_t)ring_back(now_slot, now - old, K) * ncells + cell, 1u);
+        ring_add(hist, now_slot, ncells, cell, K, __LINE__);
+        if (old + K > now) ring_sub(hist, ring_back(now_slot, now - old, K), ncells, cell, K, __LINE__);
       }
     } else {
       stamps[rec] = now;  // idempotent: a recorder touched this slot reads `now`
@@ -1321,7 +1377,10 @@ __global__ void __launch_bounds__(256) finalize_count_kernel(const uint32_t* __r
     const uint32_t c0 = (uint32_t)(item % chunks) * kChunk;
     const uint32_t c1 = min(c0 + kChunk, geo.eta);
     __syncthreads();
-    if (threadIdx.x < geo.r) s_cols[threadIdx.x] = tuples[(uint64_t)surv_idx[sidx] * geo.r + threadIdx.x];
+    if (threadIdx.x < geo.r) {
+      s_cols[threadIdx.x] = tuples[(uint64_t)surv_idx[sidx] * geo.r + threadIdx.x];
+      if (!SSPD_OK_OR_SKIP(s_cols[threadIdx.x] <= geo.col_mask)) s_cols[threadIdx.x] = 0;
+    }
     __syncthreads();
     uint32_t cnt = 0;
     if (kmode == 0) {
@@ -1682,13 +1741,14 @@ __global__ void __launch_bounds__(256) scan_shard_kernel(const uint32_t* __restr
         for (uint32_t j = 0; j < 8; ++j) {  // owned touches: atomics issued together
           const uint32_t row = r0 + j;
           old[j] = now;
-          if (row >= geo.r) continue;
           cell[j] = row << geo.q | row_col(geo, row, c[u], col0);
+          if (row >= geo.r) continue;
           const uint32_t owner = shard_owner(cell[j], geo.ncells, sh.world);
           if (owner != sh.rank) {
             dmask[u] |= 1u << owner;
             continue;
           }
+          if (!SSPD_OK_OR_SKIP(rec_ok(geo, cell[j], bucket))) continue;
           uint32_t* p = stamps + (uint64_t)cell[j] * geo.eta + bucket;
           if (HIST) old[j] = atomicMax(p, now);
           else asm volatile("red.relaxed.gpu.global.max.u32 [%0], %1;" ::"l"(p), "r"(now) : "memory");
@@ -1697,8 +1757,8 @@ __global__ void __launch_bounds__(256) scan_shard_kernel(const uint32_t* __restr
 #pragma unroll
           for (uint32_t j = 0; j < 8; ++j) {
             if (old[j] >= now) continue;
-            atomicAdd(hist + (uint64_t)now_slot * geo.ncells + cell[j], 1u);
-            if (old[j] + K > now) atomicSub(hist + (uint64_t)ring_back(now_slot, now - old[j], K) * geo.ncells + cell[j], 1u);
+            ring_add(hist, now_slot, geo.ncells, cell[j], K, __LINE__);
+            if (old[j] + K > now) ring_sub(hist, ring_back(now_slot, now - old[j], K), geo.ncells, cell[j], K, __LINE__);
           }
         }
       }
@@ -1748,6 +1808,7 @@ __global__ void __launch_bounds__(256) shard_mask_kernel(const uint32_t* __restr
       for (uint32_t row = 0; row < geo.r && m; ++row) {
         const uint32_t cell = row << geo.q | cols[row];
         if (shard_owner(cell, geo.ncells, world) != rank) continue;
+        if (!SSPD_OK_OR_SKIP(rec_ok(geo, cell, w * 32 + nb - 1))) continue;
         const uint32_t* e = stamps + (uint64_t)cell * geo.eta + w * 32;
         uint32_t bits = 0;
         for (uint32_t j = 0; j < nb; ++j) bits |= (uint32_t)(e[j] > thr) << j;
@@ -1865,10 +1926,10 @@ __device__ __forceinline__ void narrow_ring(uint32_t old, uint32_t cell, const N
                                            uint32_t now_slot, const Geo& geo, uint32_t* __restrict__ hist,
                                            uint32_t K) {
   if (old >= nc.now) return;  // already stamped this slot
-  atomicAdd(hist + (uint64_t)now_slot * geo.ncells + cell, 1u);
+  ring_add(hist, now_slot, geo.ncells, cell, K, __LINE__);
   if (old >= nc.lo) {
     const uint32_t age = nc.now - old;
-    if (age < K) atomicSub(hist + (uint64_t)ring_back(now_slot, age, K) * geo.ncells + cell, 1u);
+    if (age < K) ring_sub(hist, ring_back(now_slot, age, K), geo.ncells, cell, K, __LINE__);
   }
 }
 
@@ -1927,6 +1988,7 @@ __global__ void __launch_bounds__(256) scan_narrow_kernel(const uint32_t* __rest
 #pragma unroll
         for (uint32_t row = 0; row < 8; ++row) {
           if (row >= geo.r) break;
+          (void)SSPD_OK_OR_SKIP(rec_ok(geo, row << geo.q | row_col(geo, row, c[u], col0[u]), bucket[u]));
           T* p = codes + (uint64_t)(row << geo.q | row_col(geo, row, c[u], col0[u])) * geo.eta + bucket[u];
           if constexpr (sizeof(T) == 2 && !PRELOAD) old[u][row] = narrow_max(p, nc.now);
           else if constexpr (sizeof(T) == 2) old[u][row] = __ldcg(reinterpret_cast<const unsigned short*>(p));
@@ -1977,6 +2039,7 @@ __global__ void __launch_bounds__(256) scan_narrow_kernel(const uint32_t* __rest
         hash_pair<H1MODE>(t, geo, c[u], o[u], bucket, col0);
         for (uint32_t row = 0; row < geo.r; ++row) {
           const uint32_t cell = row << geo.q | row_col(geo, row, c[u], col0);
+          (void)SSPD_OK_OR_SKIP(rec_ok(geo, cell, bucket));
           T* p = codes + (uint64_t)cell * geo.eta + bucket;
           uint32_t old;
           if constexpr (sizeof(T) == 2) old = narrow_max(p, nc.now);

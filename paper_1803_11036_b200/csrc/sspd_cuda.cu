@@ -2450,6 +2450,30 @@ sspd_status sspd_grid_new_pairs(sspd_grid* g, uint32_t** dev_pairs, uint64_t* co
   return SSPD_OK;
 }
 
+sspd_status sspd_checked_status(int device, uint32_t* first_line, uint64_t* failures, int reset) {
+  *first_line = 0;
+  *failures = 0;
+#ifdef SSPD_CHECKED
+  DeviceGuard dg(device);
+  CU(cudaDeviceSynchronize());
+  CU(cudaMemcpyFromSymbol(first_line, g_chk_line, sizeof(uint32_t)));
+  unsigned long long n = 0;
+  CU(cudaMemcpyFromSymbol(&n, g_chk_count, sizeof n));
+  *failures = n;
+  if (reset) {
+    const uint32_t z = 0;
+    const unsigned long long z8 = 0;
+    CU(cudaMemcpyToSymbol(g_chk_line, &z, sizeof z));
+    CU(cudaMemcpyToSymbol(g_chk_count, &z8, sizeof z8));
+  }
+  return SSPD_OK;
+#else
+  (void)device;
+  (void)reset;
+  return fail(SSPD_INVALID_ARGUMENT, "checked_status: not a checked build (lib/libsspd_cuda_checked.so)");
+#endif
+}
+
 sspd_status sspd_grid_fresh_pairs(sspd_grid* g, uint64_t* count) {
   std::lock_guard<std::mutex> lk(g->mu);
   DeviceGuard dg(g->device);

@@ -571,6 +571,14 @@ def reduce_words(device: int, srcs: list[int], words: int, op: str, dst: int, st
                                    C.c_void_p(stream)))
 
 
+def checked_status(device: int = 0, reset: bool = True) -> tuple[int, int]:
+    """(first failing kernels.cuh line, failures) of the checked build's device
+    bounds/invariant checks; raises InvalidArgument on the product build."""
+    line, n = C.c_uint32(), C.c_uint64()
+    check(load().sspd_checked_status(device, C.byref(line), C.byref(n), 1 if reset else 0))
+    return line.value, n.value
+
+
 def launch_count() -> int:
     return int(load().sspd_launch_count())
 

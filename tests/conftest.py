@@ -28,3 +28,16 @@ def gpu():
     import paper_1803_11036_b200 as P
     assert P.device_count() >= 1
     return P
+
+
+@pytest.fixture(autouse=True)
+def _checked_build_clean(request):
+    """Under SSPD_CHECKED_ASSERT=1 (tests/test_gpu_checked.py runs the GPU
+    suites on lib/libsspd_cuda_checked.so): after every GPU test, no device
+    bounds check or window-ring invariant may have failed."""
+    yield
+    if os.environ.get("SSPD_CHECKED_ASSERT") != "1" or "gpu" not in request.keywords:
+        return
+    import paper_1803_11036_b200 as P
+    line, n = P.checked_status(0, reset=True)
+    assert n == 0, f"{n} device check failure(s), first at kernels.cuh:{line}"
