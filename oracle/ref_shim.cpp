@@ -95,6 +95,33 @@ size_t ref_validate_all(uint32_t q, uint32_t r, uint32_t delta, uint32_t eta, ui
   return p.size();
 }
 
+// export_snapshot (snapshot.cpp:36-68) of a reference grid: the whole
+// stream's bytes into out (cap bytes); returns the size, or 0 on error.
+size_t ref_export_snapshot(void* g, uint32_t k, uint32_t theta, uint64_t slot, uint32_t node_id, char* out,
+                           size_t cap) {
+  try {
+    const auto* rs = static_cast<Rsea*>(g);
+    SnapshotMeta m;
+    m.seed = rs->cfg().seed;
+    m.q = rs->cfg().q;
+    m.r = rs->cfg().r;
+    m.delta = rs->cfg().delta;
+    m.eta = rs->eta();
+    m.k = k;
+    m.theta = theta;
+    m.slot = slot;
+    m.node_id = node_id;
+    std::ostringstream os(std::ios::out | std::ios::binary);
+    export_snapshot(*rs, m, os);
+    const std::string b = os.str();
+    if (b.size() <= cap) std::memcpy(out, b.data(), b.size());
+    return b.size();
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return 0;
+  }
+}
+
 // parse_ipv4 (workload.cpp:37-58): 0 and *ip, or 1 (invalid_argument),
 // 2 (out_of_range), 3 (other) with what() in ref_last_error().
 int ref_parse_ipv4(const char* text, uint32_t* ip) {

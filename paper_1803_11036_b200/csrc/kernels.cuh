@@ -735,6 +735,19 @@ __device__ __forceinline__ bool sect_resolve(unsigned long long* __restrict__ ta
 #ifndef SSPD_PIPE_SECT
 #define SSPD_PIPE_SECT 0
 #endif
+// SSPD_PIPE_LDPF: load (not prefetch) each fresh pair's recorders when it is
+// hashed, so its deferred atomics hit L2 (the ld-then-atomic pattern
+// tools/fetch_probe.cu measured fastest; prefetch.global.L2 measured slow):
+// 1 = loads whose values are never read, 2 = values carried to the next
+// iteration and folded into a sink before the atomics.
+#ifndef SSPD_PIPE_LDPF
+#define SSPD_PIPE_LDPF 0
+#endif
+__device__ __forceinline__ uint32_t ld_cg_volatile(const uint32_t* p) {
+  uint32_t v;
+  asm volatile("ld.global.cg.u32 %0, [%1];" : "=r"(v) : "l"(p));
+  return v;
+}
 
 // R: rows at compile time (5, the reference default), or 0 = geo.r <= 8.
 #ifndef SSPD_PIPE_MINB
@@ -763,6 +776,8 @@ __global__ void __launch_bounds__(256, SSPD_PIPE_MINB) scan_dedup_pipe_kernel(
   // the previous group's fresh pairs: cip, bucket, row-0 column
   uint32_t pc[P], pb[P], p0[P];
   bool pv[P];
+  uint32_t ldv[SSPD_PIPE_LDPF == 2 ? P : 1][SSPD_PIPE_LDPF == 2 ? RM : 1];
+  uint32_t sink = 0;
 #pragma unroll
   for (int u = 0; u < P; ++u) pv[u] = false;
   // one extra round per thread drains the last group's pending stamps
@@ -806,6 +821,10 @@ __global__ void __launch_bounds__(256, SSPD_PIPE_MINB) scan_dedup_pipe_kernel(
 #pragma unroll
     for (int u = 0; u < P; ++u) {
       if (!pv[u]) continue;
+      if (SSPD_PIPE_LDPF == 2)
+#pragma unroll
+        for (uint32_t row = 0; row < RM; ++row)
+          if (row < nr) sink ^= ldv[SSPD_PIPE_LDPF == 2 ? u : 0][SSPD_PIPE_LDPF == 2 ? row : 0];
 #pragma unroll
       for (uint32_t row = 0; row < RM; ++row)
         if (row < nr) {
@@ -846,8 +865,17 @@ __global__ void __launch_bounds__(256, SSPD_PIPE_MINB) scan_dedup_pipe_kernel(
       if (!fresh[u]) continue;
       pc[u] = c[u];
       hash_pair<H1MODE>(t, geo, c[u], o[u], pb[u], p0[u]);
+      if (SSPD_PIPE_LDPF)
+#pragma unroll
+        for (uint32_t row = 0; row < RM; ++row)
+          if (row < nr) {
+            const uint32_t v = ld_cg_volatile(stamps + (uint64_t)(row << geo.q | row_col(geo, row, pc[u], p0[u])) *
+                                                           geo.eta + pb[u]);
+            if (SSPD_PIPE_LDPF == 2) ldv[SSPD_PIPE_LDPF == 2 ? u : 0][SSPD_PIPE_LDPF == 2 ? row : 0] = v;
+          }
     }
   }
+  if (SSPD_PIPE_LDPF == 2 && sink == 0x9e3779b9u && now == 0u && fresh_count) *fresh_count = sink;  // keep the loads
   // pairs new to this slot (pair-set inserts plus probe-limit misses): one
   // atomic per warp
   if (fresh_count) {

@@ -26,6 +26,8 @@ size_t ref_synth_trace(const uint32_t* planted, size_t n_planted, uint32_t bg_ho
                        double mu, uint32_t k, uint32_t start, uint32_t* recs, size_t cap_recs);
 int ref_read_trace(const char* data, size_t len, int binary, uint32_t* recs, size_t cap_recs,
                    size_t* n);
+size_t ref_export_snapshot(void* g, uint32_t k, uint32_t theta, uint64_t slot, uint32_t node_id, char* out,
+                           size_t cap);
 size_t ref_validate_all(uint32_t q, uint32_t r, uint32_t delta, uint32_t eta, uint32_t k, double theta,
                         char* msg, size_t len);
 int ref_parse_ipv4(const char* text, uint32_t* ip);

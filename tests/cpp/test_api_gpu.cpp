@@ -718,6 +718,48 @@ TEST_CASE("differential: run_detection at k = 65534 without a window ring") {
   const auto shards = split(wd.trace, 3, 125);
   expect_same(run_detection(shards, desk), ref_pipeline(shards, desk));
 }
+
+// export_snapshot byte for byte against the reference's (snapshot.cpp:36-68):
+// the same scans and advances into our device grid and the compiled
+// reference's grid, the same meta -> identical 56-byte header and u16 payload;
+// and each import of the other's bytes reproduces the grid.
+TEST_CASE("differential: export_snapshot bytes equal the reference's") {
+  for (const RhfgConfig& cfg : {RhfgConfig{10, 5, 8, 0x5eed}, RhfgConfig{14, 5, 6, 0xabc}}) {
+    const uint32_t eta = cfg.q == 10 ? 256 : 2048;
+    Rsea g(cfg, eta);
+    void* r = ref_grid_create(cfg.q, cfg.r, cfg.delta, cfg.seed, eta);
+    std::mt19937_64 rng(cfg.seed);
+    for (int step = 0; step < 4; ++step) {
+      std::vector<IpPair> p(40000);
+      for (auto& x : p) x = {static_cast<uint32_t>(rng() % 5000), static_cast<uint32_t>(rng())};
+      g.scan_batch(p, 1);
+      ref_scan(r, reinterpret_cast<const uint32_t*>(p.data()), p.size(), 4);
+      if (step < 3) {
+        g.advance_slot(1);
+        ref_advance(r, 4);
+      }
+    }
+    SnapshotMeta m;
+    m.k = 5;
+    m.theta = 128;
+    m.slot = 3;
+    m.node_id = 7;
+    std::ostringstream ours(std::ios::out | std::ios::binary);
+    export_snapshot(g, m, ours);
+    const std::string a = ours.str();
+    std::string b(a.size() + 64, '\0');
+    const size_t n = ref_export_snapshot(r, 5, 128, 3, 7, b.data(), b.size());
+    REQUIRE(n == a.size());
+    b.resize(n);
+    CHECK(a.size() == kSnapshotHeaderSize + snapshot_payload_size(eta, cfg.r, cfg.q));
+    CHECK(a == b);
+    std::istringstream back(b, std::ios::in | std::ios::binary);
+    const ImportedSnapshot imp = import_snapshot(back);
+    CHECK(imp.rsea == g);
+    CHECK(imp.meta.node_id == 7u);
+    ref_grid_destroy(r);
+  }
+}
 #endif
 
 CHECK_MAIN

@@ -170,3 +170,17 @@ def test_invalid_configuration_message_equals_reference(work, q, r, delta, eta, 
         "\n  " + m for m in O.ref_validate_all(q, r, delta, eta, k, theta)) + "\n"
     assert p.returncode == 2
     assert p.stderr == want
+
+
+@pytest.mark.gpu
+def test_detect_devices_option_matches_one_router(gpu, work):
+    """`sspd detect --devices N` runs N routers (partial grids, relays, peer
+    reduces; several share a GPU when the box has fewer) and prints the
+    one-router report byte for byte; --devices 0 is a usage error."""
+    run("detect", work / "trace.bin", "--desk", "--k", 5, "--seed", "5eed", "-o", work / "r1.csv")
+    for n in (2, 3):
+        run("detect", work / "trace.bin", "--desk", "--k", 5, "--seed", "5eed", "--devices", n,
+            "-o", work / f"r{n}.csv")
+        assert (work / f"r{n}.csv").read_bytes() == (work / "r1.csv").read_bytes()
+    p = run("detect", work / "trace.bin", "--desk", "--devices", 0, "-o", os.devnull, check=False)
+    assert p.returncode == 1
