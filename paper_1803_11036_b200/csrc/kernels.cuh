@@ -711,12 +711,28 @@ __device__ __forceinline__ Sect ld_sect(const unsigned long long* p) {
 __device__ __forceinline__ uint64_t sect_base(uint64_t h, int i, uint64_t mask) {
   return pair_slot(h & ~3ull, 4 * i, mask);  // region base | ((h & ~3) + 4i) & region mask
 }
+// SSPD_PIPE_SECT 2 -- HOST GROUPS: a cip's pairs share a 32-slot group (two
+// 128 B lines, 8 sectors; group index from the cip alone), a pair's first
+// sector from its oip; probes walk the group's sectors.  The Zipf head's
+// ~3M repeating pairs then sit in ~0.2M groups (~0.4M L2 lines) instead of
+// ~3M lines among the tail's, at one sector load per probe.
+__device__ __forceinline__ uint64_t host_group_hash(uint64_t key) {
+  uint64_t z = (key >> 32) + 0x9e3779b97f4a7c15ull;
+  z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ull;
+  z = (z ^ (z >> 27)) * 0x94d049bb133111ebull;
+  z ^= z >> 31;
+  return (z & ~31ull) | ((uint64_t)((uint32_t)key * 0x9E3779B1u >> 29) << 2);
+}
+__device__ __forceinline__ uint64_t group_sect_base(uint64_t h, int i, uint64_t mask) {
+  return (h & ~31ull & mask) | ((((h >> 2) + (uint64_t)i) & 7ull) << 2);
+}
 constexpr int kSectLimit = 4;
+template <int GROUP = 0>
 __device__ __forceinline__ bool sect_resolve(unsigned long long* __restrict__ table, uint64_t mask, uint64_t key,
                                              uint64_t h, Sect v) {
   if (key == kEmptyKey) return true;
   for (int i = 0;;) {
-    const uint64_t base = sect_base(h, i, mask);
+    const uint64_t base = GROUP ? group_sect_base(h, i, mask) : sect_base(h, i, mask);
 #pragma unroll
     for (int j = 0; j < 4; ++j)
       if (v.k[j] == key) return false;
@@ -728,7 +744,7 @@ __device__ __forceinline__ bool sect_resolve(unsigned long long* __restrict__ ta
       if (old == key) return false;
     }
     if (++i >= kSectLimit) return true;
-    v = ld_sect(table + sect_base(h, i, mask));
+    v = ld_sect(table + (GROUP ? group_sect_base(h, i, mask) : sect_base(h, i, mask)));
   }
 }
 
@@ -807,9 +823,11 @@ __global__ void __launch_bounds__(256, SSPD_PIPE_MINB) scan_dedup_pipe_kernel(
 #pragma unroll
     for (int u = 0; u < P; ++u) {
       key[u] = (uint64_t)c[u] << 32 | o[u];
-      h[u] = pair_slot_hash(key[u]);
+      h[u] = SSPD_PIPE_SECT == 2 ? host_group_hash(key[u]) : pair_slot_hash(key[u]);
       if (SSPD_PIPE_SECT) {
-        if (valid[u]) sv[u] = ld_sect(table + sect_base(h[u], 0, table_mask));
+        if (valid[u])
+          sv[u] = ld_sect(table + (SSPD_PIPE_SECT == 2 ? group_sect_base(h[u], 0, table_mask)
+                                                       : sect_base(h[u], 0, table_mask)));
         v[u] = 0ull;
       } else {
         unsigned long long* slot0 = table + pair_slot(h[u], 0, table_mask);
@@ -839,7 +857,8 @@ __global__ void __launch_bounds__(256, SSPD_PIPE_MINB) scan_dedup_pipe_kernel(
 #pragma unroll
     for (int u = 0; u < P; ++u) {
       if (SSPD_PIPE_SECT)
-        fresh[u] = valid[u] && sect_resolve(table, table_mask, key[u], h[u], sv[SSPD_PIPE_SECT ? u : 0]);
+        fresh[u] = valid[u] && sect_resolve<SSPD_PIPE_SECT == 2>(table, table_mask, key[u], h[u],
+                                                                 sv[SSPD_PIPE_SECT ? u : 0]);
       else
         fresh[u] = valid[u] && (HINT ? pair_resolve_hint(table, table_mask, key[u], h[u], v[u], pol_set)
                                      : pair_resolve(table, table_mask, key[u], h[u], v[u]));
