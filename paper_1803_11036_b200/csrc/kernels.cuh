@@ -751,6 +751,21 @@ __device__ __forceinline__ bool sect_resolve(unsigned long long* __restrict__ ta
 #ifndef SSPD_PIPE_SECT
 #define SSPD_PIPE_SECT 0
 #endif
+// SSPD_PIPE_CPASYNC: each thread copies its NEXT group's pairs (16 B) into its
+// own shared-memory slot with cp.async (LDGSTS) while it works on the current
+// one, so the pair stream's DRAM latency leaves the per-iteration chain
+// without holding registers; warp-private double buffer, no CTA barrier.
+#ifndef SSPD_PIPE_CPASYNC
+#define SSPD_PIPE_CPASYNC 0
+#endif
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
+  const uint32_t sa = (uint32_t)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(sa), "l"(gmem) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
+
 // SSPD_PIPE_LDPF: load (not prefetch) each fresh pair's recorders when it is
 // hashed, so its deferred atomics hit L2 (the ld-then-atomic pattern
 // tools/fetch_probe.cu measured fastest; prefetch.global.L2 measured slow):
@@ -797,12 +812,31 @@ __global__ void __launch_bounds__(256, SSPD_PIPE_MINB) scan_dedup_pipe_kernel(
 #pragma unroll
   for (int u = 0; u < P; ++u) pv[u] = false;
   // one extra round per thread drains the last group's pending stamps
-  for (uint64_t g = tid; g < ngroups + nthreads; g += nthreads) {
+  constexpr bool kCp = SSPD_PIPE_CPASYNC && P == 2;
+  __shared__ uint4 s_next[kCp ? 2 : 1][kCp ? 256 : 1];
+  auto full_group = [&](uint64_t gg) { return gg < ngroups && vec && gg * P + P <= n; };
+  if (kCp) {
+    if (full_group(tid)) cp_async16(&s_next[0][threadIdx.x], pairs + 2 * (tid * P));
+    cp_async_commit();
+  }
+  uint32_t it = 0;
+  for (uint64_t g = tid; g < ngroups + nthreads; g += nthreads, ++it) {
     const bool have = g < ngroups;
     uint32_t c[P], o[P];
     bool valid[P];
     const uint64_t q0 = g * P;
-    if (P >= 2 && have && vec && q0 + P <= n) {
+    if (kCp) {
+      // queue the next group's copy, then wait for this one's
+      if (full_group(g + nthreads))
+        cp_async16(&s_next[(it + 1) & 1][threadIdx.x], pairs + 2 * ((g + nthreads) * P));
+      cp_async_commit();
+      cp_async_wait<1>();
+    }
+    if (kCp && full_group(g)) {
+      const uint4 a = s_next[it & 1][threadIdx.x];
+      c[0] = a.x; o[0] = a.y; c[P - 1] = a.z; o[P - 1] = a.w;
+      valid[0] = valid[P - 1] = true;
+    } else if (P >= 2 && have && vec && q0 + P <= n) {
 #pragma unroll
       for (int u = 0; u < P; u += 2) {
         const uint4 a = HINT ? ld_stream_u4_hint(pairs + 2 * (q0 + u), pol_stamp) : ld_stream_u4(pairs + 2 * (q0 + u));
