@@ -9,9 +9,14 @@ time); router 0 is timed on
   + receive (stamp what the pair owners relayed to it)
   + reconstruction on its own hot bits.
 
-Collective / NVLink time is not included.  Geometry as sim_shard_router.py.
+Collective / NVLink time is not included.  Round 2: every router's grid is
+PARTIAL (only its cells, sspd_grid_create_sharded), so the full C2 geometry
+(eta 2^16) fits -- router 0 plus one helper at a time -- and router 0's relay
+and receive take their counts from device memory in one launch each
+(sspd_shard_relay_regions_dev / sspd_shard_receive_regions_dev), as
+dist.ShardExchange runs them.
 
-    python tools/sim_relay_router.py [--routers 8]
+    python tools/sim_relay_router.py [--routers 8] [--eta 65536]
 """
 import argparse
 import ctypes as C
@@ -31,10 +36,11 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--routers", type=int, default=8)
     ap.add_argument("--slots", type=int, default=4)
+    ap.add_argument("--eta", type=int, default=1 << 16)
     args = ap.parse_args()
     N = args.routers
     cfg = dict(B.CONFIGS["c2"])
-    cfg["eta"] = 1 << 15
+    cfg["eta"] = args.eta
     L = P.load()
     dev = 0
     torch.cuda.set_device(dev)
@@ -56,7 +62,8 @@ def main():
                                           C.c_void_p(buf.data_ptr()), C.c_void_p(stream.cuda_stream)))
 
     def grid(rank):
-        g = P.Grid(cfg["q"], cfg["r"], cfg["delta"], cfg["seed"], cfg["eta"], device=dev, k_max=k)
+        g = P.Grid(cfg["q"], cfg["r"], cfg["delta"], cfg["seed"], cfg["eta"], device=dev, k_max=k,
+                   shard=(N, rank) if N > 1 else None)
         g.set_stream(stream.cuda_stream)
         g.set_shard_relay(ta.data_ptr(), tb.data_ptr(), N, rank, cap)
         return g
@@ -98,26 +105,24 @@ def main():
             sb[po] = sent(h)
             h.close()
             del h
+        counts_a = torch.tensor([sa[src][0] for src in range(N)], dtype=torch.int64, device="cuda")
         torch.cuda.synchronize()
         t2 = ev()
-        r0.shard_relay_regions(in_a[0].data_ptr(), cap, [sa[src][0] for src in range(N)])
+        r0.shard_relay_regions_dev(in_a[0].data_ptr(), cap, counts_a.data_ptr(), 1, N)
         t3 = ev()
         sb[0] = sent(r0)
+        got = sum(sb[src][32] for src in range(1, N))
+        counts_b = torch.tensor([sb[src][32] for src in range(N)], dtype=torch.int64, device="cuda")
+        torch.cuda.synchronize()
         t4 = ev()
-        box = in_b[0].view(N, cap, 2)
-        got = 0
-        for src in range(1, N):
-            c = sb[src][32]
-            assert c <= cap, (src, c, cap)
-            got += c
-            if c:
-                r0.shard_receive(box[src].data_ptr(), c)
+        r0.shard_receive_regions_dev(in_b[0].data_ptr(), cap, counts_b.data_ptr(), 1, N, 0)
         t5 = ev()
         r0.shard_hot(k, theta)
         r0.shard_select(k, theta)
         r0.shard_finish(theta)
         t6 = ev()
         torch.cuda.synchronize()
+        assert not r0.shard_overflow(), "a region ran past its capacity"
         relay_in = sum(sa[src][0] for src in range(N))
         rows.append((t0.elapsed_time(t1), t2.elapsed_time(t3), t4.elapsed_time(t5), t5.elapsed_time(t6), relay_in, got))
         print(f"slot {slot}: own {rows[-1][0]:.3f} ms, relay {rows[-1][1]:.3f} ms ({relay_in / 1e6:.1f}M in), receive "
@@ -127,8 +132,8 @@ def main():
     own, relay, recv, rec = (np.mean([r[i] for r in rows]) for i in range(4))
     rin, got = (np.mean([r[i] for r in rows]) / 1e6 for i in (4, 5))
     per = own + relay + recv + rec
-    print(f"# One router of {N} under the RELAYED shard exchange (two hops), timed on one B200 "
-          f"(`tools/sim_relay_router.py`)\n")
+    print(f"# One router of {N} under the RELAYED shard exchange (two hops), partial grids, device-counted "
+          f"relay/receive, eta {cfg['eta']}, timed on one B200 (`tools/sim_relay_router.py`)\n")
     print("| phase | ms per slot |\n|---|---|")
     print(f"| own scan: dedup, push each new pair to its pair owner (no stamping) | {own:.3f} |")
     print(f"| relay: dedup the {rin:.1f}M pairs routed to this pair owner, stamp own cells, push once per owner "
