@@ -127,3 +127,119 @@ def test_random_run_detection(gpu, case):
     assert len(got) == n_slots
     assert [(s, d.cip, d.estimate) for s, dets in got for d in dets] == \
            [(s, d.cip, d.estimate) for s, d in want], (case, geo, n_shards, policy, k, mu)
+
+
+@pytest.mark.timeout(300)
+@pytest.mark.parametrize("case", range(16))
+def test_random_sharded_routers(gpu, case):
+    """Sharded routers on one device over random geometries (include/sspd_cuda.h
+    "sharded routers"; dist.ShardExchange): world 2..5 partial grids, one or
+    two hops, counts from the host or from device memory, hot bits / masks
+    merged by sspd_reduce_words.  Every router's reports equal the oracle's
+    union-min merge and its owned cells are bit-exact, every slot."""
+    import torch
+
+    from paper_1803_11036_b200 import dist as PD
+    from paper_1803_11036_b200.grid import reduce_words
+
+    rng = np.random.default_rng(0x5A4D + case)
+    geo = random_geometry(rng)
+    seed = int(rng.integers(0, 2**63))
+    world = int(rng.integers(2, 6))
+    relay = bool(rng.random() < 0.6)
+    dev_counts = bool(rng.random() < 0.5)
+    k = int(rng.integers(1, 7))
+    theta = float(max(1.0, geo["eta"] * rng.uniform(0.3, 0.8)))
+    cap = 1 << 16
+    grids = [gpu.Grid(seed=seed, shard=(world, r), k_max=k, **geo) for r in range(world)]
+    for g in grids:
+        g.candidate_cap = 1 << 18
+    in_a = [torch.zeros(world * cap * 2, dtype=torch.int32, device="cuda") for _ in range(world)]
+    in_b = [torch.zeros(world * cap * 2, dtype=torch.int32, device="cuda") for _ in range(world)]
+    ta = torch.tensor([b.data_ptr() for b in in_a], dtype=torch.int64, device="cuda")
+    tb = torch.tensor([b.data_ptr() for b in in_b], dtype=torch.int64, device="cuda")
+    for r, g in enumerate(grids):
+        if relay:
+            g.set_shard_relay(ta.data_ptr(), tb.data_ptr(), world, r, cap)
+        else:
+            g.set_shard(ta.data_ptr(), world, r, cap)
+    o = O.OracleGrid(seed=seed, **geo)
+    mt = O.Mt64(seed & 0xFFFFFFFF)
+    hosts = [int(mt.next()) & 0xFFFFFFFF for _ in range(int(rng.integers(1, 4)))]
+
+    def counts(hop):  # [src * world + dst] on the device, as the all-gather leaves them
+        torch.cuda.synchronize()
+        out = torch.cat([PD.device_view(g.shard_sent_ptr(), 128, 0).view(torch.int64)[32 * hop: 32 * hop + world]
+                         for g in grids]).contiguous()
+        torch.cuda.synchronize()
+        return out
+
+    def receive(boxes, hop):
+        sent = counts(hop)
+        host = sent.view(world, world).tolist()
+        for dst, g in enumerate(grids):
+            if dev_counts:
+                g.shard_receive_regions_dev(boxes[dst].data_ptr(), cap, sent.data_ptr() + 8 * dst, world, world, dst)
+            else:
+                box = boxes[dst].view(world, cap, 2)
+                for src in range(world):
+                    if src != dst and host[src][dst]:
+                        g.shard_receive(box[src].data_ptr(), host[src][dst])
+
+    for s in range(int(rng.integers(2, 5))):
+        shared = mt.pairs(int(rng.integers(0, 800)))
+        for r, g in enumerate(grids):
+            parts = [mt.pairs(int(rng.integers(0, 1500))), shared]
+            for h in hosts:
+                if rng.random() < 0.6:
+                    fan = int(rng.integers(1, geo["eta"] + 2))
+                    parts.append(np.stack([np.full(fan, h, np.uint32), mt.draw(fan).astype(np.uint32)], 1))
+            p = np.concatenate(parts)
+            if len(p):
+                g.scan_batch(torch.from_numpy(np.ascontiguousarray(p).view(np.int32)).cuda())
+            o.scan(p)
+        if relay:
+            sent = counts(0)
+            for po, g in enumerate(grids):
+                if dev_counts:
+                    g.shard_relay_regions_dev(in_a[po].data_ptr(), cap, sent.data_ptr() + 8 * po, world, world)
+                else:
+                    g.shard_relay_regions(in_a[po].data_ptr(), cap, sent.view(world, world)[:, po].tolist())
+            receive(in_b, 1)
+        else:
+            receive(in_a, 0)
+        torch.cuda.synchronize()
+        assert not any(g.shard_overflow() for g in grids)
+        hot = [g.shard_hot(k, theta) for g in grids]
+        merged = torch.empty(hot[0][1], dtype=torch.int32, device="cuda")
+        reduce_words(0, [p for p, _ in hot], hot[0][1], "or", merged.data_ptr())
+        torch.cuda.synchronize()
+        for p, _ in hot:
+            reduce_words(0, [merged.data_ptr()], hot[0][1], "or", p)
+        torch.cuda.synchronize()
+        try:
+            want = o.reconstruct(k, theta, cap=1 << 18)
+        except O.CandidateOverflow as e:
+            with pytest.raises(gpu.CandidateOverflow) as got:
+                grids[0].shard_select(k, theta)
+            assert (got.value.level, got.value.count) == (e.level, e.count)
+            return
+        sel = [g.shard_select(k, theta) for g in grids]
+        if sel[0][0]:
+            w = sel[0][2]
+            anded = torch.empty(w, dtype=torch.int32, device="cuda")
+            reduce_words(0, [p for _, p, _ in sel], w, "and", anded.data_ptr())
+            torch.cuda.synchronize()
+            for _, p, _ in sel:
+                reduce_words(0, [anded.data_ptr()], w, "and", p)
+            torch.cuda.synchronize()
+        for g in grids:
+            assert [(d.cip, d.estimate) for d in g.shard_finish(theta)] == \
+                [(d.cip, d.estimate) for d in want], (case, s, geo, world, relay, dev_counts)
+        cells = o.cells()
+        for g in grids:
+            lo, hi = g.owned()
+            assert np.array_equal(g.cells_range(lo, hi - lo), cells[lo:hi]), (case, s)
+        for g in grids:
+            g.advance_slot()
+        o.advance()
