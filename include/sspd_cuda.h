@@ -327,6 +327,12 @@ sspd_status sspd_scan_mode(sspd_grid* g, int mode, int filter);
  * summed since the grid was created: the pair set's inserts plus probes that
  * hit the probe limit.  Diagnostic (bench.py's per-launch fresh pairs). */
 sspd_status sspd_grid_fresh_pairs(sspd_grid* g, uint64_t* count);
+
+/* The pipelined scan's per-slot key set (kernels.cuh scan_cset_kernel), for
+ * tests and diagnostics: its device pointer (u32 entries, NULL before the
+ * first key-set scan) and log2 of its entry count, after the grid's queued
+ * work.  Valid until the next scan or advance. */
+sspd_status sspd_grid_keyset(sspd_grid* g, uint32_t** dev_entries, uint32_t* log2_entries);
 /* The CHECKED build (lib/libsspd_cuda_checked.so, -DSSPD_CHECKED): bounds
  * checks on every data-dependent stamp / code / window-ring index and the
  * ring's no-underflow invariant (kernels.cuh "CHECKED BUILD").  Waits for the

@@ -99,6 +99,7 @@ SIGNATURES = {
     "sspd_set_push": (C.c_int, [grid_p, C.c_void_p, C.c_uint32, C.c_uint32, C.c_uint64]),
     "sspd_scan_mode": (C.c_int, [grid_p, C.c_int, C.c_int]),
     "sspd_grid_fresh_pairs": (C.c_int, [grid_p, u64p]),
+    "sspd_grid_keyset": (C.c_int, [grid_p, C.POINTER(C.c_void_p), u32p]),
     "sspd_checked_status": (C.c_int, [C.c_int, u32p, u64p, C.c_int]),
     "sspd_profile_enable": (C.c_int, [grid_p, C.c_int]),
     "sspd_profile_read": (C.c_int, [grid_p, C.c_char_p, C.POINTER(C.c_double), u64p, u64p]),

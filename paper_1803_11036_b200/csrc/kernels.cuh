@@ -183,24 +183,33 @@ __device__ __forceinline__ void load_scan_tables(ScanTables& t, const HashTabs* 
   __syncthreads();
 }
 
-// Bucket of oip and row-0 column of cip (hash_opposite, hashing.hpp:56-59;
-// rsea.cpp:31-32).
+// Row-0 column of cip (rhfg_from_row0's col0, hashing.hpp:68-69).
+__device__ __forceinline__ uint32_t row0_col(const ScanTables& t, const Geo& geo, uint32_t cip) {
+  return ((uint32_t)t.row0[0][cip & 0xff] ^ t.row0[1][(cip >> 8) & 0xff] ^ t.row0[2][(cip >> 16) & 0xff] ^
+          t.row0[3][cip >> 24]) &
+         geo.col_mask;
+}
+
+// Bucket of oip (hash_opposite, hashing.hpp:56-59).
 template <int H1MODE>
-__device__ __forceinline__ void hash_pair(const ScanTables& t, const Geo& geo, uint32_t cip, uint32_t oip,
-                                          uint32_t& bucket, uint32_t& col0) {
+__device__ __forceinline__ uint32_t h1_bucket(const ScanTables& t, const Geo& geo, uint32_t oip) {
   if (H1MODE == 0) {
     const uint32_t* lo = reinterpret_cast<const uint32_t*>(&t.h1[0][0]);
     const uint32_t h = lo[2 * (0 * 256 + (oip & 0xff))] ^ lo[2 * (1 * 256 + ((oip >> 8) & 0xff))] ^
                        lo[2 * (2 * 256 + ((oip >> 16) & 0xff))] ^ lo[2 * (3 * 256 + (oip >> 24))];
-    bucket = h & (geo.eta - 1u);
-  } else {
-    const uint64_t h = t.h1[0][oip & 0xff] ^ t.h1[1][(oip >> 8) & 0xff] ^ t.h1[2][(oip >> 16) & 0xff] ^
-                       t.h1[3][oip >> 24];
-    bucket = (uint32_t)(h % geo.eta);
+    return h & (geo.eta - 1u);
   }
-  col0 = ((uint32_t)t.row0[0][cip & 0xff] ^ t.row0[1][(cip >> 8) & 0xff] ^ t.row0[2][(cip >> 16) & 0xff] ^
-          t.row0[3][cip >> 24]) &
-         geo.col_mask;
+  const uint64_t h = t.h1[0][oip & 0xff] ^ t.h1[1][(oip >> 8) & 0xff] ^ t.h1[2][(oip >> 16) & 0xff] ^
+                     t.h1[3][oip >> 24];
+  return (uint32_t)(h % geo.eta);
+}
+
+// Bucket of oip and row-0 column of cip (rsea.cpp:31-32).
+template <int H1MODE>
+__device__ __forceinline__ void hash_pair(const ScanTables& t, const Geo& geo, uint32_t cip, uint32_t oip,
+                                          uint32_t& bucket, uint32_t& col0) {
+  bucket = h1_bucket<H1MODE>(t, geo, oip);
+  col0 = row0_col(t, geo, cip);
 }
 
 // Column of row `row` (rhfg_from_row0, hashing.hpp:68-71).
@@ -931,6 +940,326 @@ __global__ void __launch_bounds__(256, SSPD_PIPE_MINB) scan_dedup_pipe_kernel(
   if (SSPD_PIPE_LDPF == 2 && sink == 0x9e3779b9u && now == 0u && fresh_count) *fresh_count = sink;  // keep the loads
   // pairs new to this slot (pair-set inserts plus probe-limit misses): one
   // atomic per warp
+  if (fresh_count) {
+#pragma unroll
+    for (int off = 16; off; off >>= 1) n_fresh += __shfl_xor_sync(0xffffffffu, n_fresh, off);
+    if ((threadIdx.x & 31) == 0 && n_fresh) atomicAdd(fresh_count, (unsigned long long)n_fresh);
+  }
+}
+
+// COMPACT KEY SET SCAN (the default C2 path when eta <= 2^16: window ring
+// on, no bitmap, no exchange list, r <= 8).  Same results as the pipelined
+// dedup scan above; what changes is the per-slot set.
+//  * The key is (cip, bucket(oip)), not (cip, oip): the r recorders a pair
+//    stamps are (row, col_row(cip), bucket) (rsea.cpp:31-36), so two pairs
+//    with one key stamp the same recorders and the second is redundant.
+//    With eta <= 2^16 the key has 48 bits.
+//  * x = perm48(key) is a bijection of 48-bit values.  Its top lg bits are
+//    the key's home slot in a 2^lg-entry table; the other 48 - lg <= 24
+//    bits (the remainder) are stored with the probe distance d in one u32:
+//    entry = (d + 1) << 24 | remainder, 0 = empty.  An entry at slot s
+//    therefore names exactly one key (home = s - d, remainder), so a match
+//    is exact: "seen" is never wrong, and every miss path (probe limit)
+//    reads as fresh, which only costs redundant stamps.
+//  * 4 B per entry instead of 8: at lg = 24 the table is 64 MiB, and the
+//    ~9.4M keys of a C2 slot load it to 0.56.  The table plus the stamp
+//    atomics' own L2 footprint fit the 126 MB L2, where the 256 MiB table of
+//    8-byte keys did not (~52M of its 100M probes per slot missed L2 to
+//    DRAM, profiles/r02_ab_scan.md).  Linear probing walks 8 entries per 32 B
+//    sector, so a collision rarely costs a second line.
+// Concurrent inserters of one key walk the same slots and compare the same
+// expected entry: one CAS wins, the others read it back as "seen".
+#ifndef SSPD_CSET_PROBE_LIMIT
+#define SSPD_CSET_PROBE_LIMIT 32
+#endif
+#ifndef SSPD_CSET_BW
+#define SSPD_CSET_BW 4  // entries per probe bucket: 1 (linear probing by slot), 4 or 8
+#endif
+constexpr uint32_t kCsetMinLog2 = 24, kCsetMaxLog2 = 30;
+// first size 2^24 (64 MiB); the host grows it while a slot's keys load it
+// past kCsetMaxLoad (sspd_cuda.cu cset_slot_end_locked).  With 4-entry
+// buckets the smallest set that holds the keys is the fastest (C2: 2^24 at
+// load 0.56 beat 2^25 and 2^26; C2 with 64-entry pools: 2^24 at 0.92 still
+// beat 2^25, profiles/r02_ab_keyset.md), so growth only keeps the table
+// clear of the overflow cliff.
+constexpr uint32_t kCsetStartLog2 = 24;
+constexpr double kCsetMaxLoad = 0.75;
+
+#ifndef SSPD_CSET_PERM
+#define SSPD_CSET_PERM 0  // 1: one odd multiply (Fibonacci hashing: the home is the product's top bits)
+#endif
+__device__ __forceinline__ uint64_t cset_perm48(uint64_t x) {
+  constexpr uint64_t M = (1ull << 48) - 1;
+  if (SSPD_CSET_PERM == 1) return (x * 0x9E3779B97F4Bull) & M;
+  x = (x * 0x9E3779B97F4Bull) & M;  // odd multipliers and xor-shifts: each step is invertible mod 2^48
+  x ^= x >> 23;
+  x = (x * 0xC2B2AE3D27D5ull) & M;
+  x ^= x >> 25;
+  x = (x * 0x165667B19E37ull) & M;
+  x ^= x >> 24;
+  return x;
+}
+
+__device__ __forceinline__ bool cset_resolve(uint32_t* __restrict__ table, uint32_t mask, uint32_t home,
+                                             uint32_t rem, uint32_t v) {
+  for (uint32_t d = 0;;) {
+    const uint32_t want = (d + 1) << 24 | rem;
+    if (v == want) return false;
+    if (v == 0u) {
+      const uint32_t old = atomicCAS(table + ((home + d) & mask), 0u, want);
+      if (old == 0u) return true;
+      if (old == want) return false;
+    }
+    if (++d >= SSPD_CSET_PROBE_LIMIT) return true;
+    v = __ldca(table + ((home + d) & mask));
+  }
+}
+
+__device__ __forceinline__ uint32_t ld_ca_hint_u32(const uint32_t* p, uint64_t pol) {
+  uint32_t v;
+  asm volatile("ld.global.ca.L2::cache_hint.u32 %0, [%1], %2;" : "=r"(v) : "l"(p), "l"(pol));
+  return v;
+}
+
+// BUCKETS (BW = 4 or 8 entries, one 16 B / 32 B load): the home is a
+// bucket, a key sits anywhere in it (empties claimed in slot order), and a
+// full bucket overflows into the next.  One load resolves nearly every probe
+// (at load 0.28, P(more than 4 keys in a 4-entry bucket) < 1%), so a warp no
+// longer waits for its longest linear-probe chain.  The entry stores the
+// bucket displacement: entry = (d + 1) << rb | remainder, with rb = 48 -
+// log2(buckets) remainder bits.
+// Linear runs of full buckets have a long tail: at load 0.56 a sequential
+// insert of 9.4M keys displaces a few hundred keys past 8 buckets, none past
+// 17; at 0.75 none past 53 (2^24 entries).  48 fits the displacement field at
+// every size (lg >= 24: 32 - rb >= 6 bits) and only the rare long run walks it.
+#ifndef SSPD_CSET_BUCKET_LIMIT
+#define SSPD_CSET_BUCKET_LIMIT 48
+#endif
+constexpr uint32_t kCsetBucketLimit = SSPD_CSET_BUCKET_LIMIT;
+#ifndef SSPD_CSET_FAR_NOINLINE
+#define SSPD_CSET_FAR_NOINLINE 1  // 1: buckets past the home one out of line; 2: past the 8th in a loop of their own
+#endif
+template <int BW>
+struct CBucket {
+  uint32_t e[BW];
+};
+template <int BW, int HINT>
+__device__ __forceinline__ CBucket<BW> ld_bucket(const uint32_t* p, uint64_t pol) {
+  CBucket<BW> b;
+  if (BW == 4) {
+    if (HINT)
+      asm volatile("ld.global.ca.L2::cache_hint.v4.u32 {%0,%1,%2,%3}, [%4], %5;"
+                   : "=r"(b.e[0]), "=r"(b.e[1]), "=r"(b.e[2]), "=r"(b.e[3]) : "l"(p), "l"(pol));
+    else
+      asm volatile("ld.global.ca.v4.u32 {%0,%1,%2,%3}, [%4];"
+                   : "=r"(b.e[0]), "=r"(b.e[1]), "=r"(b.e[2]), "=r"(b.e[3]) : "l"(p));
+  } else {
+    uint64_t w[4];
+    if (HINT)
+      asm volatile("ld.global.ca.L2::cache_hint.v4.u64 {%0,%1,%2,%3}, [%4], %5;"
+                   : "=l"(w[0]), "=l"(w[1]), "=l"(w[2]), "=l"(w[3]) : "l"(p), "l"(pol));
+    else
+      asm volatile("ld.global.ca.v4.u64 {%0,%1,%2,%3}, [%4];" : "=l"(w[0]), "=l"(w[1]), "=l"(w[2]), "=l"(w[3]) : "l"(p));
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      b.e[2 * j] = (uint32_t)w[j];
+      b.e[2 * j + 1] = (uint32_t)(w[j] >> 32);
+    }
+  }
+  return b;
+}
+// Buckets d >= 1 of a probe.  Out of line (SSPD_CSET_FAR_NOINLINE 1): a
+// 48-bucket walk inlined into the probe loop cost the common one-bucket probe
+// 35% at C2 (4.32 vs 3.19 ms), and an 8-bucket inline walk overflowed a few
+// hundred keys per slot; the call's saved registers (ptxas reports them as
+// spills) are only touched on this rare path (profiles/r02_ab_keyset.md A/B 4).
+template <int BW, int HINT>
+__device__ __noinline__ bool cset_resolve_far(uint32_t* __restrict__ table, uint32_t bmask, uint32_t hb,
+                                              uint32_t rem, uint32_t rb, uint64_t pol) {
+  for (uint32_t d = 1; d < kCsetBucketLimit; ++d) {
+    const CBucket<BW> v = ld_bucket<BW, HINT>(table + (uint64_t)((hb + d) & bmask) * BW, pol);
+    const uint32_t want = (d + 1) << rb | rem;
+    uint32_t* base = table + (uint64_t)((hb + d) & bmask) * BW;
+#pragma unroll
+    for (int j = 0; j < BW; ++j)
+      if (v.e[j] == want) return false;
+#pragma unroll
+    for (int j = 0; j < BW; ++j) {
+      if (v.e[j] != 0u) continue;
+      const uint32_t old = atomicCAS(base + j, 0u, want);
+      if (old == 0u) return true;
+      if (old == want) return false;
+    }
+  }
+  return true;
+}
+
+template <int BW, int HINT>
+__device__ __forceinline__ bool cset_resolve_bucket(uint32_t* __restrict__ table, uint32_t bmask, uint32_t hb,
+                                                    uint32_t rem, uint32_t rb, CBucket<BW> v, uint64_t pol) {
+  if (SSPD_CSET_FAR_NOINLINE == 1) {
+    const uint32_t want = 1u << rb | rem;
+    uint32_t* base = table + (uint64_t)hb * BW;
+#pragma unroll
+    for (int j = 0; j < BW; ++j)
+      if (v.e[j] == want) return false;
+#pragma unroll
+    for (int j = 0; j < BW; ++j) {
+      if (v.e[j] != 0u) continue;
+      const uint32_t old = atomicCAS(base + j, 0u, want);
+      if (old == 0u) return true;
+      if (old == want) return false;
+    }
+    return cset_resolve_far<BW, HINT>(table, bmask, hb, rem, rb, pol);
+  }
+  for (uint32_t d = 0;;) {
+    const uint32_t want = (d + 1) << rb | rem;
+    uint32_t* base = table + (uint64_t)((hb + d) & bmask) * BW;
+#pragma unroll
+    for (int j = 0; j < BW; ++j)
+      if (v.e[j] == want) return false;
+#pragma unroll
+    for (int j = 0; j < BW; ++j) {
+      if (v.e[j] != 0u) continue;
+      const uint32_t old = atomicCAS(base + j, 0u, want);
+      if (old == 0u) return true;
+      if (old == want) return false;
+    }
+    if (++d >= (SSPD_CSET_FAR_NOINLINE == 2 ? 8u : kCsetBucketLimit)) break;
+    v = ld_bucket<BW, HINT>(table + (uint64_t)((hb + d) & bmask) * BW, pol);
+  }
+  if (SSPD_CSET_FAR_NOINLINE != 2) return true;
+  // mode 2: the first 8 buckets as above, the rare longer walk in a loop of its own
+#pragma unroll 1
+  for (uint32_t d = 8; d < kCsetBucketLimit; ++d) {
+    v = ld_bucket<BW, HINT>(table + (uint64_t)((hb + d) & bmask) * BW, pol);
+    const uint32_t want = (d + 1) << rb | rem;
+    uint32_t* base = table + (uint64_t)((hb + d) & bmask) * BW;
+#pragma unroll
+    for (int j = 0; j < BW; ++j)
+      if (v.e[j] == want) return false;
+#pragma unroll
+    for (int j = 0; j < BW; ++j) {
+      if (v.e[j] != 0u) continue;
+      const uint32_t old = atomicCAS(base + j, 0u, want);
+      if (old == 0u) return true;
+      if (old == want) return false;
+    }
+  }
+  return true;
+}
+
+// Pipelined exactly like scan_dedup_pipe_kernel: iteration i loads and
+// probes group i while group i-1's stamp atomics are in flight.
+// HINT 1: the set's probes evict_last, the stamps and the pair stream
+// evict_first.
+template <int H1MODE, int HINT, int R, int BW>
+__global__ void __launch_bounds__(256, SSPD_PIPE_MINB) scan_cset_kernel(
+    const uint32_t* __restrict__ pairs, uint64_t n, const HashTabs* __restrict__ tabs, Geo geo,
+    uint32_t* __restrict__ table, uint32_t lg, uint32_t* __restrict__ stamps, uint32_t now,
+    uint32_t* __restrict__ hist, uint32_t K, unsigned long long* __restrict__ fresh_count) {
+  __shared__ ScanTables t;
+  load_scan_tables(t, tabs);
+  const uint32_t now_slot = now % K;
+  const uint64_t tid = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const uint64_t nthreads = (uint64_t)gridDim.x * blockDim.x;
+  const bool vec = (reinterpret_cast<uintptr_t>(pairs) & 15u) == 0;
+  const uint64_t pol_first = HINT ? l2_policy_first() : 0, pol_last = HINT ? l2_policy_last() : 0;
+  constexpr uint32_t LB = BW == 8 ? 3 : BW == 4 ? 2 : 0;
+  const uint32_t rb = 48u - (lg - LB), mask = (1u << (lg - LB)) - 1u;
+  constexpr int P = SSPD_PIPE_PPT;
+  constexpr uint32_t RM = R ? R : 8;
+  const uint32_t nr = R ? R : geo.r;
+  const uint64_t ngroups = (n + P - 1) / P;
+  uint32_t n_fresh = 0;
+  uint32_t pc[P], pb[P], p0[P];  // the previous group's fresh pairs: cip, bucket, row-0 column
+  bool pv[P];
+#pragma unroll
+  for (int u = 0; u < P; ++u) pv[u] = false;
+  // one extra round per thread drains the last group's pending stamps
+  for (uint64_t g = tid; g < ngroups + nthreads; g += nthreads) {
+    const bool have = g < ngroups;
+    uint32_t c[P], o[P];
+    bool valid[P];
+    const uint64_t q0 = g * P;
+    if (P >= 2 && have && vec && q0 + P <= n) {
+#pragma unroll
+      for (int u = 0; u < P; u += 2) {
+        const uint4 a = HINT ? ld_stream_u4_hint(pairs + 2 * (q0 + u), pol_first) : ld_stream_u4(pairs + 2 * (q0 + u));
+        c[u] = a.x; o[u] = a.y; c[u + 1] = a.z; o[u + 1] = a.w;
+        valid[u] = valid[u + 1] = true;
+      }
+    } else {
+#pragma unroll
+      for (int u = 0; u < P; ++u) {
+        valid[u] = have && q0 + u < n;
+        c[u] = valid[u] ? pairs[2 * (q0 + u)] : 0u;
+        o[u] = valid[u] ? pairs[2 * (q0 + u) + 1] : 0u;
+      }
+    }
+    uint32_t b[P], home[P], rem[P], v[P];
+    constexpr int BWL = BW == 1 ? 4 : BW;  // bucket type (unused when BW == 1)
+    CBucket<BWL> vb[BW == 1 ? 1 : P];
+#pragma unroll
+    for (int u = 0; u < P; ++u) {
+      b[u] = h1_bucket<H1MODE>(t, geo, o[u]);
+      const uint64_t x = cset_perm48((uint64_t)c[u] << 16 | b[u]);
+      home[u] = (uint32_t)(x >> rb);
+      rem[u] = (uint32_t)x & ((1u << rb) - 1u);
+      if constexpr (BW == 1) {
+        v[u] = valid[u] ? (HINT ? ld_ca_hint_u32(table + home[u], pol_last) : __ldca(table + home[u])) : 0u;
+      } else {
+        if (valid[u]) vb[u] = ld_bucket<BWL, HINT>(table + (uint64_t)home[u] * BW, pol_last);
+      }
+    }
+    // the previous group's stamps, in flight together with this group's probes
+    uint32_t old[P][RM];
+#pragma unroll
+    for (int u = 0; u < P; ++u) {
+      if (!pv[u]) continue;
+#pragma unroll
+      for (uint32_t row = 0; row < RM; ++row)
+        if (row < nr) {
+          const uint32_t cell = row << geo.q | row_col(geo, row, pc[u], p0[u]);
+          uint32_t* sp = stamps + (uint64_t)cell * geo.eta + pb[u];
+          old[u][row] = now;
+          if (SSPD_OK_OR_SKIP(rec_ok(geo, cell, pb[u])))
+            old[u][row] = HINT ? atom_max_hint(sp, now, pol_first) : atomicMax(sp, now);
+        }
+    }
+    bool fresh[P];
+#pragma unroll
+    for (int u = 0; u < P; ++u) {
+      if constexpr (BW == 1)
+        fresh[u] = valid[u] && cset_resolve(table, mask, home[u], rem[u], v[u]);
+      else
+        fresh[u] = valid[u] && cset_resolve_bucket<BWL, HINT>(table, mask, home[u], rem[u], rb, vb[u], pol_last);
+    }
+    // window ring moves for the previous group's first touches
+#pragma unroll
+    for (int u = 0; u < P; ++u) {
+      if (!pv[u]) continue;
+#pragma unroll
+      for (uint32_t row = 0; row < RM; ++row) {
+        if (row >= nr || old[u][row] >= now) continue;
+        const uint32_t cell = row << geo.q | row_col(geo, row, pc[u], p0[u]);
+        ring_add(hist, now_slot, geo.ncells, cell, K, __LINE__);
+        if (old[u][row] + K > now)
+          ring_sub(hist, ring_back(now_slot, now - old[u][row], K), geo.ncells, cell, K, __LINE__);
+      }
+    }
+    // this group's fresh pairs become pending
+#pragma unroll
+    for (int u = 0; u < P; ++u) {
+      pv[u] = fresh[u];
+      n_fresh += fresh[u];
+      if (!fresh[u]) continue;
+      pc[u] = c[u];
+      pb[u] = b[u];
+      p0[u] = row0_col(t, geo, c[u]);
+    }
+  }
+  // keys new to this slot (set inserts plus probe-limit misses): one atomic per warp
   if (fresh_count) {
 #pragma unroll
     for (int off = 16; off; off >>= 1) n_fresh += __shfl_xor_sync(0xffffffffu, n_fresh, off);

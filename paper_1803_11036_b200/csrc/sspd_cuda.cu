@@ -463,6 +463,23 @@ struct sspd_grid {
   // eviction priorities.  $SSPD_DEDUP_PIPE overrides (A/B runs).
   int dedup_pipe = 0;
   DevBuf fresh_count;  // u64: pairs new to their slot, summed over the pipelined scans
+  // Compact key set (kernels.cuh scan_cset_kernel): 2^cset_lg u32 entries
+  // keyed by (cip, bucket), the default for the pipelined path when
+  // eta <= 2^16.  $SSPD_CSET=0 turns it off, $SSPD_CSET_LOG2 sizes it.
+  int use_cset = 1;
+  int cset_hint = 1;            // L2 priorities in the key-set scan ($SSPD_CSET_HINT=0: off)
+  DevBuf cset;
+  uint32_t cset_lg = 0;         // log2 entries of the (next) allocation
+  bool cset_dirty = false;
+  bool cset_fixed = false;      // $SSPD_CSET_LOG2 given: no growth
+  // growth: the fresh-key counter is copied to pinned memory at each slot
+  // end and read one advance later (no host wait), so the set is sized from
+  // the keys a slot actually produced
+  unsigned long long* cset_pin = nullptr;
+  cudaEvent_t cset_ev = nullptr;
+  bool cset_ev_pending = false;
+  uint64_t cset_seen_total = 0;
+  uint32_t cset_seen_now = 0, cset_pin_now = 0;
   uint32_t code_now() const { return code_lo + (now - epoch0); }
   std::mutex mu;
 };
@@ -616,9 +633,10 @@ sspd_status commit_locked(sspd_grid* g) {
 // The pair set may only skip a pair whose recorders still read `now`; any
 // write to the stamps other than a scan invalidates it.
 sspd_status pairset_reset_locked(sspd_grid* g) {
-  if (!g->pairset_dirty) return SSPD_OK;
-  CU(cudaMemsetAsync(g->pairset.p, 0xff, (g->pairset_mask + 1) * 8, g->stream));
-  g->pairset_dirty = false;
+  if (!g->pairset_dirty && !g->cset_dirty) return SSPD_OK;
+  if (g->pairset.p) CU(cudaMemsetAsync(g->pairset.p, 0xff, (g->pairset_mask + 1) * 8, g->stream));
+  if (g->cset_dirty) CU(cudaMemsetAsync(g->cset.p, 0, (4ull << g->cset_lg), g->stream));
+  g->pairset_dirty = g->cset_dirty = false;
   return SSPD_OK;
 }
 
@@ -795,6 +813,63 @@ sspd_status ensure_pairset_locked(sspd_grid* g) {
   return SSPD_OK;
 }
 
+// The compact key set, allocated on first use: 2^24 entries (64 MiB) keep
+// a C2 slot's ~9.4M keys at load 0.56; $SSPD_CSET_LOG2 in [24, 30].
+sspd_status ensure_cset_locked(sspd_grid* g) {
+  if (!g->fresh_count.p) {
+    if (g->fresh_count.ensure(8) != cudaSuccess) return fail(SSPD_CUDA_ERROR, "CUDA error: out of memory");
+    CU(cudaMemsetAsync(g->fresh_count.p, 0, 8, g->stream));
+  }
+  if (g->cset.p) return SSPD_OK;
+  if (!g->cset_lg) {
+    g->cset_lg = kCsetStartLog2;
+    if (const char* e = std::getenv("SSPD_CSET_LOG2")) {
+      g->cset_lg = std::min<uint32_t>(kCsetMaxLog2, std::max<uint32_t>(kCsetMinLog2, (uint32_t)std::atoi(e)));
+      g->cset_fixed = true;
+    }
+  }
+  if (g->cset.ensure(4ull << g->cset_lg) != cudaSuccess)
+    return fail(SSPD_CUDA_ERROR, "CUDA error: out of memory (key set)");
+  CU(cudaMemsetAsync(g->cset.p, 0, 4ull << g->cset_lg, g->stream));
+  return SSPD_OK;
+}
+
+// At a slot end (before the set is cleared): read the fresh-key count the
+// previous slot end copied out, if that copy has landed, and grow the set for
+// the coming slots when a slot's keys loaded it past kCsetMaxLoad; then copy
+// this slot end's count.  Growth reallocates (the cleared set starts empty).
+sspd_status cset_slot_end_locked(sspd_grid* g) {
+  if (!g->cset.p || g->cset_fixed) return SSPD_OK;
+  if (!g->cset_pin) {
+    if (PinnedCache::get().alloc(reinterpret_cast<void**>(&g->cset_pin), 64) != cudaSuccess)
+      return fail(SSPD_CUDA_ERROR, "CUDA error: out of pinned memory");
+    CU(cudaEventCreateWithFlags(&g->cset_ev, cudaEventDisableTiming));
+  }
+  if (g->cset_ev_pending) {
+    if (cudaEventQuery(g->cset_ev) != cudaSuccess) return SSPD_OK;  // not landed yet: try at the next slot end
+    g->cset_ev_pending = false;
+    const uint64_t total = *g->cset_pin;
+    if (g->cset_seen_now && g->cset_pin_now > g->cset_seen_now) {
+      const uint64_t per_slot = (total - g->cset_seen_total) / (g->cset_pin_now - g->cset_seen_now);
+      const uint64_t cap = 1ull << g->cset_lg;
+      if ((double)per_slot > kCsetMaxLoad * (double)cap && g->cset_lg < kCsetMaxLog2) {
+        uint32_t lg = g->cset_lg;
+        while (lg < kCsetMaxLog2 && (double)per_slot > kCsetMaxLoad * (double)(1ull << lg)) ++lg;
+        g->cset.release();
+        g->cset_lg = lg;
+        g->cset_dirty = false;
+      }
+    }
+    g->cset_seen_total = total;
+    g->cset_seen_now = g->cset_pin_now;
+  }
+  CU(cudaMemcpyAsync(g->cset_pin, g->fresh_count.p, 8, cudaMemcpyDeviceToHost, g->stream));
+  CU(cudaEventRecord(g->cset_ev, g->stream));
+  g->cset_ev_pending = true;
+  g->cset_pin_now = g->now + 1;  // the count covers every slot before now + 1
+  return SSPD_OK;
+}
+
 bool compatible(const sspd_grid* a, const sspd_grid* b) {
   return a->seed == b->seed && a->q == b->q && a->r == b->r && a->delta == b->delta && a->eta == b->eta;
 }
@@ -942,6 +1017,8 @@ sspd_status create_impl(int device, uint32_t q, uint32_t r, uint32_t delta, uint
   if (const char* f = std::getenv("SSPD_SCAN_FILTER")) g->scan_filter = std::atoi(f) != 0;
   if (const char* f = std::getenv("SSPD_NARROW_PRELOAD")) g->narrow_preload = std::atoi(f) != 0;
   if (const char* f = std::getenv("SSPD_DEDUP_PIPE")) g->dedup_pipe = std::atoi(f);
+  if (const char* f = std::getenv("SSPD_CSET")) g->use_cset = std::atoi(f);
+  if (const char* f = std::getenv("SSPD_CSET_HINT")) g->cset_hint = std::atoi(f);
   // Device-resident pairs: deferred bitmap, measured faster than direct
   // stamping at both geometries (profiles/r01_ab_scan_modes.txt).
   if (const char* m = std::getenv("SSPD_SCAN_MODE")) {
@@ -1077,6 +1154,8 @@ sspd_status sspd_grid_destroy(sspd_grid* g) {
     for (void* p : {(void*)g->stamps_alloc, (void*)g->codes, (void*)g->touched, (void*)g->hist, (void*)g->d_tabs})
       cache_free(p, true);
     PinnedCache::get().free(g->pinned_small);
+    if (g->cset_pin) PinnedCache::get().free(g->cset_pin);
+    if (g->cset_ev) cudaEventDestroy(g->cset_ev);
     PinnedCache::get().free(g->meta_host);
     for (int i = 0; i < 2; ++i) {
       PinnedCache::get().free(g->host_stage[i]);
@@ -1085,7 +1164,7 @@ sspd_status sspd_grid_destroy(sspd_grid* g) {
     for (DevBuf* b : {&g->stage[0], &g->stage[1], &g->stage_pairs[0], &g->stage_pairs[1], &g->rec_pairs, &g->counts, &g->hot_cols, &g->hot_rowcnt, &g->hotT,
                       &g->tupA, &g->tupB, &g->misc, &g->meta, &g->surv, &g->pairset, &g->newpairs,
                       &g->newpairs_count, &g->bin_counts, &g->binned, &g->hot_words, &g->hot_chunks, &g->relayset,
-                      &g->shard_sent, &g->shard_ovf, &g->masks, &g->fresh_count})
+                      &g->shard_sent, &g->shard_ovf, &g->masks, &g->fresh_count, &g->cset})
       b->release(true);
     for (auto& r : g->prof) {
       cudaEventDestroy(r.a);
@@ -1252,7 +1331,13 @@ sspd_status scan_locked(sspd_grid* g, const uint32_t* pairs, uint64_t n, int pai
   g->scanned_in_slot += n;
   if (!g->shard && g->width == 32 && (bits || (!direct && !dedup)))
     if (sspd_status ts = ensure_touched_locked(g)) return ts;
-  if (dedup || g->shard) {
+  // the pipelined dedup path, and within it the compact key set (eta <= 2^16)
+  const bool pipe = dedup && !g->shard && !g->export_pairs && hist && !bits && g->width == 32 && g->geo.r <= 8 &&
+                    (g->dedup_pipe == 0 || g->dedup_pipe == 1);
+  const bool cset = pipe && g->use_cset && g->geo.eta <= 65536u;
+  if (cset) {
+    if (sspd_status cs = ensure_cset_locked(g)) return cs;
+  } else if (dedup || g->shard) {
     sspd_status ps = ensure_pairset_locked(g);
     if (ps) return ps;
   }
@@ -1320,7 +1405,28 @@ sspd_status scan_locked(sspd_grid* g, const uint32_t* pairs, uint64_t n, int pai
                                                                    g->pairset_mask, g->stamps, g->now,      \
                                                                    g->hist, g->K, g->touched, np, nc)
       const bool ex = g->export_pairs;
-      if (!ex && hist && !bits && g->geo.r <= 8 && (g->dedup_pipe == 0 || g->dedup_pipe == 1)) {
+      if (cset) {
+        const unsigned pblocks = grid_blocks(g, (cnt + 3) / 4, 256, SSPD_PIPE_MINB);
+        auto* ct = g->cset.as<uint32_t>();
+        auto* fc = g->fresh_count.as<unsigned long long>();
+#define SSPD_CSETK(H1, HI, R)                                                                                    \
+  scan_cset_kernel<H1, HI, R, SSPD_CSET_BW><<<pblocks, 256, 0, g->stream>>>(dp, cnt, g->d_tabs, g->geo, ct,         \
+                                                                           g->cset_lg, g->stamps, g->now, g->hist, \
+                                                                           g->K, fc)
+        const bool r5 = g->geo.r == 5, hint = g->cset_hint != 0;
+        switch ((pow2 ? 0 : 4) + (hint ? 2 : 0) + (r5 ? 1 : 0)) {
+          case 0: SSPD_CSETK(0, 0, 0); break;
+          case 1: SSPD_CSETK(0, 0, 5); break;
+          case 2: SSPD_CSETK(0, 1, 0); break;
+          case 3: SSPD_CSETK(0, 1, 5); break;
+          case 4: SSPD_CSETK(1, 0, 0); break;
+          case 5: SSPD_CSETK(1, 0, 5); break;
+          case 6: SSPD_CSETK(1, 1, 0); break;
+          default: SSPD_CSETK(1, 1, 5); break;
+        }
+#undef SSPD_CSETK
+        g->cset_dirty = true;
+      } else if (!ex && hist && !bits && g->geo.r <= 8 && (g->dedup_pipe == 0 || g->dedup_pipe == 1)) {
         // one resident wave of the pipelined kernel (its own occupancy)
         const unsigned pblocks = grid_blocks(g, (cnt + 3) / 4, 256, SSPD_PIPE_MINB);
 #define SSPD_PIPE(H1, HI, R)                                                                                 \
@@ -1517,6 +1623,10 @@ sspd_status sspd_advance(sspd_grid* g, uint32_t slots) {
   DeviceGuard dg(g->device);
   sspd_status s = commit_locked(g);
   if (s) return s;
+  if (g->cset_dirty) {
+    s = cset_slot_end_locked(g);
+    if (s) return s;
+  }
   s = pairset_reset_locked(g);  // the pair set only deduplicates within a slot
   if (s) return s;
   if (g->newpairs_count.p) CU(cudaMemsetAsync(g->newpairs_count.p, 0, 8, g->stream));
@@ -2484,6 +2594,15 @@ sspd_status sspd_grid_fresh_pairs(sspd_grid* g, uint64_t* count) {
     c = *static_cast<uint64_t*>(pinned_scratch(g));
   }
   *count = c;
+  return SSPD_OK;
+}
+
+sspd_status sspd_grid_keyset(sspd_grid* g, uint32_t** dev_entries, uint32_t* log2_entries) {
+  std::lock_guard<std::mutex> lk(g->mu);
+  DeviceGuard dg(g->device);
+  CU(cudaStreamSynchronize(g->stream));
+  if (dev_entries) *dev_entries = g->cset.as<uint32_t>();
+  if (log2_entries) *log2_entries = g->cset.p ? g->cset_lg : 0;
   return SSPD_OK;
 }
 

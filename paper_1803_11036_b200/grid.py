@@ -434,6 +434,16 @@ class Grid:
         check(self._L.sspd_grid_fresh_pairs(self._h, C.byref(n)))
         return n.value
 
+    def keyset(self) -> np.ndarray | None:
+        """The per-slot key set's entries (a host copy; None before the first
+        key-set scan)."""
+        p, lg = C.c_void_p(), C.c_uint32()
+        check(self._L.sspd_grid_keyset(self._h, C.byref(p), C.byref(lg)))
+        if not p.value:
+            return None
+        from .dist import device_view
+        return device_view(p.value, 1 << lg.value, self.device).cpu().numpy().view(np.uint32)
+
     def scan_mode(self, mode: int = -1, filter: int = -1):
         """Scan strategy (include/sspd_cuda.h sspd_scan_mode): 0 = deferred bitmap,
         1 = direct stamping, 2 = direct behind the per-slot pair set, 3 = 2 after
