@@ -972,6 +972,9 @@ __global__ void __launch_bounds__(256, SSPD_PIPE_MINB) scan_dedup_pipe_kernel(
 #ifndef SSPD_CSET_PROBE_LIMIT
 #define SSPD_CSET_PROBE_LIMIT 32
 #endif
+#ifndef SSPD_CSET_PF
+#define SSPD_CSET_PF 0
+#endif
 #ifndef SSPD_CSET_BW
 #define SSPD_CSET_BW 4  // entries per probe bucket: 1 (linear probing by slot), 4 or 8
 #endif
@@ -1176,13 +1179,27 @@ __global__ void __launch_bounds__(256, SSPD_PIPE_MINB) scan_cset_kernel(
   bool pv[P];
 #pragma unroll
   for (int u = 0; u < P; ++u) pv[u] = false;
+  // SSPD_CSET_PF: the next group's 16 B of pairs are loaded one iteration
+  // ahead, so the stream's DRAM latency is off the probe chain
+  constexpr bool kPf = SSPD_CSET_PF && P == 2;
+  auto full_group = [&](uint64_t gg) { return gg < ngroups && vec && gg * P + P <= n; };
+  uint4 nxt = make_uint4(0u, 0u, 0u, 0u);
+  if (kPf && full_group(tid))
+    nxt = HINT ? ld_stream_u4_hint(pairs + 2 * (tid * P), pol_first) : ld_stream_u4(pairs + 2 * (tid * P));
   // one extra round per thread drains the last group's pending stamps
   for (uint64_t g = tid; g < ngroups + nthreads; g += nthreads) {
     const bool have = g < ngroups;
     uint32_t c[P], o[P];
     bool valid[P];
     const uint64_t q0 = g * P;
-    if (P >= 2 && have && vec && q0 + P <= n) {
+    if (kPf && full_group(g)) {
+      const uint4 a = nxt;
+      const uint64_t gn = g + nthreads;
+      if (full_group(gn))
+        nxt = HINT ? ld_stream_u4_hint(pairs + 2 * (gn * P), pol_first) : ld_stream_u4(pairs + 2 * (gn * P));
+      c[0] = a.x; o[0] = a.y; c[P - 1] = a.z; o[P - 1] = a.w;
+      valid[0] = valid[P - 1] = true;
+    } else if (P >= 2 && have && vec && q0 + P <= n) {
 #pragma unroll
       for (int u = 0; u < P; u += 2) {
         const uint4 a = HINT ? ld_stream_u4_hint(pairs + 2 * (q0 + u), pol_first) : ld_stream_u4(pairs + 2 * (q0 + u));
