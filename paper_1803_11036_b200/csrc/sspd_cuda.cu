@@ -858,6 +858,8 @@ sspd_status cset_slot_end_locked(sspd_grid* g) {
         g->cset.release();
         g->cset_lg = lg;
         g->cset_dirty = false;
+        // allocate (and clear) now, at the slot end, not inside the next scan
+        if (sspd_status es = ensure_cset_locked(g)) return es;
       }
     }
     g->cset_seen_total = total;
