@@ -2,7 +2,7 @@
 kernels.cuh "CHECKED BUILD" -- bounds checks on every data-dependent stamp,
 code and window-ring index, and the ring's no-underflow invariant).  This
 pool closes compute-sanitizer, so these checks stand in for its memcheck on
-the data-dependent accesses: every test of test_gpu_parity / _narrow / _fuzz
+the data-dependent accesses: every test of test_gpu_parity / _narrow / _fuzz / _keyset
 runs on the checked kernels, and after each one (tests/conftest.py) no check
 may have failed."""
 import os
@@ -26,8 +26,9 @@ def test_checked_build_reports_itself(gpu):
 @pytest.mark.skipif(not os.path.exists(CHECKED), reason="checked library not built")
 def test_parity_suites_on_checked_kernels(gpu):
     env = dict(os.environ, SSPD_LIB=CHECKED, SSPD_CHECKED_ASSERT="1")
-    p = subprocess.run([sys.executable, "-m", "pytest", "-q", "-m", "gpu", "-p", "no:cacheprovider",
-                        "tests/test_gpu_parity.py", "tests/test_gpu_narrow.py", "tests/test_gpu_fuzz.py"],
+    p = subprocess.run([sys.executable, "-m", "pytest", "-q", "-m", "gpu and not slow", "-p", "no:cacheprovider",
+                        "tests/test_gpu_parity.py", "tests/test_gpu_narrow.py", "tests/test_gpu_fuzz.py",
+                        "tests/test_gpu_keyset.py"],
                        cwd=ROOT, env=env, capture_output=True, text=True, timeout=1800)
     tail = "\n".join((p.stdout + p.stderr).strip().splitlines()[-25:])
     assert p.returncode == 0, tail

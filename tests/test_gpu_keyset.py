@@ -104,6 +104,7 @@ def test_keyset_counts_distinct_keys(gpu, geo):
         g.advance_slot()
 
 
+@pytest.mark.slow
 def test_keyset_overfull_table(gpu):
     """More distinct keys than the 2^24-entry table holds: probes hit the
     limit and read as fresh (redundant stamps only); the grid stays exact."""
@@ -148,6 +149,7 @@ def test_keyset_survives_cells_writes_and_slot_reset(gpu):
         assert np.array_equal(g.cells(), o.cells()), s
 
 
+@pytest.mark.slow
 def test_keyset_grows_with_the_slot_keys(gpu):
     """Slots with more keys than 0.75 x the 2^24 starting entries make the
     host grow the set at a later slot end (reallocated, starting empty); the
@@ -207,7 +209,8 @@ def decode_table(t, bw=4):
     return (hb << np.uint64(rb)) | (e & np.uint64((1 << rb) - 1)), d
 
 
-@pytest.mark.parametrize("n,dup", [(400_000, 3), (6_000_000, 5), (18_000_000, 5)])
+@pytest.mark.parametrize("n,dup", [(400_000, 3), (6_000_000, 5),
+                                   pytest.param(18_000_000, 5, marks=pytest.mark.slow)])
 def test_keyset_table_holds_each_key_once(gpu, n, dup):
     """After a slot the table holds every distinct key of it exactly once:
     decoded entries are unique and equal perm48 of the slot's keys (no key
