@@ -323,9 +323,11 @@ sspd_status sspd_grid_new_pairs(sspd_grid* g, uint32_t** dev_pairs, uint64_t* co
  * every mode, and modes may be mixed within a slot.  Narrow-stamp grids run
  * mode 0 as 1 and mode 3 as 2. */
 sspd_status sspd_scan_mode(sspd_grid* g, int mode, int filter);
-/* Pairs found new to their slot by the pipelined dedup scan (the C2 path),
- * summed since the grid was created: the pair set's inserts plus probes that
- * hit the probe limit.  Diagnostic (bench.py's per-launch fresh pairs). */
+/* Keys found new to their slot by the pipelined dedup scan (the C2 path),
+ * summed since the grid was created: the set's inserts plus probes that hit
+ * the probe limit.  A key is (cip, bucket(oip)) on the key-set scan (eta <=
+ * 2^16) and (cip, oip) otherwise.  Diagnostic (bench.py's per-launch fresh
+ * keys; the key set's growth). */
 sspd_status sspd_grid_fresh_pairs(sspd_grid* g, uint64_t* count);
 
 /* The pipelined scan's per-slot key set (kernels.cuh scan_cset_kernel), for

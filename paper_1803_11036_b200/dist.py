@@ -32,33 +32,100 @@ import torch
 import torch.distributed as dist
 
 
-def or_allreduce_(t: torch.Tensor, group=None) -> torch.Tensor:
-    """In-place bitwise-OR all-reduce of an int32 tensor (NCCL has no OR op).
-
-    Reduce-scatter by all_to_all + a local OR of the received chunks, then
-    all-gather: the 2(N-1)/N per-rank volume of a ring all-reduce.  The same
-    code runs on NCCL (GPU) and gloo (the CPU tests).
-    """
+def _bitwise_allreduce_nccl_(t: torch.Tensor, op: str, group=None) -> torch.Tensor:
+    """Reduce-scatter by all_to_all + a local OR/AND of the received chunks,
+    then all-gather: the 2(N-1)/N per-rank volume of a ring all-reduce.  The
+    collective path for CPU tensors (gloo: the multi-process CPU tests)."""
     world = dist.get_world_size(group)
-    if world == 1:
-        return t
     flat = t.view(-1)
     n = flat.numel()
     per = (n + world - 1) // world
     padded = flat
     if per * world != n:
-        padded = torch.zeros(per * world, dtype=flat.dtype, device=flat.device)
+        padded = torch.full((per * world,), 0 if op == "or" else -1, dtype=flat.dtype, device=flat.device)
         padded[:n].copy_(flat)
     recv = torch.empty_like(padded)
     dist.all_to_all_single(recv, padded, group=group)
     chunks = recv.view(world, per)
     mine = chunks[0].clone()
     for i in range(1, world):
-        mine.bitwise_or_(chunks[i])
+        (mine.bitwise_or_ if op == "or" else mine.bitwise_and_)(chunks[i])
     out = torch.empty_like(padded)
     dist.all_gather_into_tensor(out, mine, group=group)
     flat.copy_(out[:n])
     return t
+
+
+class _PeerStage:
+    """A symmetric-memory staging buffer per (group, device), grown on
+    demand, for bitwise all-reduces by sspd_reduce_words over NVLink."""
+
+    _cache: dict = {}
+
+    @classmethod
+    def get(cls, group, words: int, device: int):
+        import torch.distributed._symmetric_memory as symm_mem
+
+        name = group.group_name if group is not None else dist.group.WORLD.group_name
+        key = (name, device)
+        have = cls._cache.get(key)
+        if have is not None and have[0].numel() >= words:
+            return have
+        buf = symm_mem.empty(max(words, 1 << 20), dtype=torch.int32, device=torch.device(f"cuda:{device}"))
+        have = (buf, symm_mem.rendezvous(buf, name))
+        cls._cache[key] = have
+        return have
+
+
+def _bitwise_allreduce_peer_(t: torch.Tensor, op: str, group=None) -> torch.Tensor:
+    """In place, for a CUDA int32 tensor: every rank stages its words in a
+    symmetric buffer; rank r reduces slice r from all peers' buffers with ONE
+    sspd_reduce_words kernel reading over NVLink (reduce-scatter), then reads
+    every other slice from its owner (all-gather).  Same 2(N-1)/N volume per
+    rank as a ring all-reduce; device barriers order the phases, no host
+    round trip."""
+    from .grid import reduce_words
+
+    world, rank = dist.get_world_size(group), dist.get_rank(group)
+    flat = t.view(-1)
+    n = flat.numel()
+    dev = flat.device.index
+    buf, h = _PeerStage.get(group, n, dev)
+    stream = torch.cuda.current_stream(flat.device).cuda_stream
+    per = ((n + world - 1) // world + 3) // 4 * 4  # 16 B aligned slices
+    lo = [min(n, p * per) for p in range(world)]
+    cnt = [min(n, lo[p] + per) - lo[p] for p in range(world)]
+    buf[:n].copy_(flat)
+    h.barrier(channel=0)  # every rank's words staged
+    if cnt[rank]:
+        reduce_words(dev, [b + 4 * lo[rank] for b in h.buffer_ptrs], cnt[rank], op,
+                     buf.data_ptr() + 4 * lo[rank], stream)
+    h.barrier(channel=1)  # every slice reduced in its owner's buffer
+    for p in range(world):
+        if p != rank and cnt[p]:
+            reduce_words(dev, [h.buffer_ptrs[p] + 4 * lo[p]], cnt[p], op, buf.data_ptr() + 4 * lo[p], stream)
+    flat.copy_(buf[:n])
+    h.barrier(channel=2)  # no peer still reads this buffer when it is next staged
+    return t
+
+
+def or_allreduce_(t: torch.Tensor, group=None) -> torch.Tensor:
+    """In-place bitwise-OR all-reduce of an int32 tensor (NCCL has no OR op):
+    over peer memory for CUDA tensors, by collectives for CPU ones."""
+    if dist.get_world_size(group) == 1:
+        return t
+    if t.is_cuda:
+        return _bitwise_allreduce_peer_(t, "or", group)
+    return _bitwise_allreduce_nccl_(t, "or", group)
+
+
+def and_allreduce_(t: torch.Tensor, group=None) -> torch.Tensor:
+    """In-place bitwise-AND all-reduce of an int32 tensor."""
+    if dist.get_world_size(group) == 1:
+        return t
+    if t.is_cuda:
+        return _bitwise_allreduce_peer_(t, "and", group)
+    return _bitwise_allreduce_nccl_(t, "and", group)
 
 
 class _CudaArray:
@@ -172,13 +239,6 @@ class PushExchange:
             grid.set_exchange(PAIRS)
         self.parity ^= 1
         self._arm(grid)
-
-
-def and_allreduce_(t: torch.Tensor, group=None) -> torch.Tensor:
-    """In-place bitwise-AND all-reduce of an int32 tensor: NOT(OR(NOT x))."""
-    t.bitwise_not_()
-    or_allreduce_(t, group)
-    return t.bitwise_not_()
 
 
 def reconstruct(grid, k: int, theta: float, group=None):

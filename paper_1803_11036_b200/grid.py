@@ -429,7 +429,8 @@ class Grid:
             self._report_buf = (_cabi.Detection_t * n.value)()
 
     def fresh_pairs(self) -> int:
-        """Pairs the pipelined dedup scan found new to their slot, since creation."""
+        """Keys the pipelined dedup scan found new to their slot, since creation:
+        (cip, bucket) keys on the key-set scan (eta <= 2^16), else (cip, oip) pairs."""
         n = C.c_uint64()
         check(self._L.sspd_grid_fresh_pairs(self._h, C.byref(n)))
         return n.value

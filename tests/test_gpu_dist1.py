@@ -62,3 +62,21 @@ def test_exchange_paths_single_rank(gpu, pg, exchange):
             [(d.cip, d.estimate) for d in o.reconstruct(5, 128.0)]
         g.advance_slot()
         o.advance()
+
+
+@pytest.mark.parametrize("op", ["or", "and"])
+def test_peer_bitwise_allreduce_single_rank(gpu, pg, op):
+    """The peer-memory OR/AND all-reduce (symmetric staging buffer, device
+    barriers, sspd_reduce_words over the peers' copies) on a 1-rank group:
+    the reduce of one copy is the identity, over ragged lengths and a
+    length past the staging buffer's first size."""
+    import torch
+
+    from paper_1803_11036_b200 import dist as PD
+
+    for n in (1, 5, 1027, (1 << 20) + 13):
+        x = torch.randint(-2**31, 2**31 - 1, (n,), dtype=torch.int32, device="cuda:0")
+        want = x.clone()
+        PD._bitwise_allreduce_peer_(x, op)
+        torch.cuda.synchronize()
+        assert torch.equal(x, want), n
