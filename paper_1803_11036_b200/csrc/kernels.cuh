@@ -1160,7 +1160,8 @@ template <int H1MODE, int HINT, int R, int BW>
 __global__ void __launch_bounds__(256, SSPD_PIPE_MINB) scan_cset_kernel(
     const uint32_t* __restrict__ pairs, uint64_t n, const HashTabs* __restrict__ tabs, Geo geo,
     uint32_t* __restrict__ table, uint32_t lg, uint32_t* __restrict__ stamps, uint32_t now,
-    uint32_t* __restrict__ hist, uint32_t K, unsigned long long* __restrict__ fresh_count) {
+    uint32_t* __restrict__ hist, uint32_t K, unsigned long long* __restrict__ fresh_count, uint32_t part = 0,
+    uint32_t part_shift = 31) {
   __shared__ ScanTables t;
   load_scan_tables(t, tabs);
   const uint32_t now_slot = now % K;
@@ -1223,6 +1224,10 @@ __global__ void __launch_bounds__(256, SSPD_PIPE_MINB) scan_cset_kernel(
       const uint64_t x = cset_perm48((uint64_t)c[u] << 16 | b[u]);
       home[u] = (uint32_t)(x >> rb);
       rem[u] = (uint32_t)x & ((1u << rb) - 1u);
+      // PASSES: this launch takes only the keys whose home lies in its part
+      // of the table (the top part_log2 bits of the home), so one pass's
+      // probes touch 1/2^part_log2 of the set
+      valid[u] = valid[u] && (home[u] >> part_shift) == part;
       if constexpr (BW == 1) {
         v[u] = valid[u] ? (HINT ? ld_ca_hint_u32(table + home[u], pol_last) : __ldca(table + home[u])) : 0u;
       } else {

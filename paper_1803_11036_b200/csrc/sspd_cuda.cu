@@ -468,6 +468,7 @@ struct sspd_grid {
   // eta <= 2^16.  $SSPD_CSET=0 turns it off, $SSPD_CSET_LOG2 sizes it.
   int use_cset = 1;
   int cset_hint = 1;            // L2 priorities in the key-set scan ($SSPD_CSET_HINT=0: off)
+  uint32_t cset_pass_log2 = 0;  // 2^k passes per batch, each over 1/2^k of the set ($SSPD_CSET_PASSES)
   DevBuf cset;
   uint32_t cset_lg = 0;         // log2 entries of the (next) allocation
   bool cset_dirty = false;
@@ -1021,6 +1022,10 @@ sspd_status create_impl(int device, uint32_t q, uint32_t r, uint32_t delta, uint
   if (const char* f = std::getenv("SSPD_DEDUP_PIPE")) g->dedup_pipe = std::atoi(f);
   if (const char* f = std::getenv("SSPD_CSET")) g->use_cset = std::atoi(f);
   if (const char* f = std::getenv("SSPD_CSET_HINT")) g->cset_hint = std::atoi(f);
+  if (const char* f = std::getenv("SSPD_CSET_PASSES")) {
+    const int v = std::atoi(f);
+    g->cset_pass_log2 = v >= 4 ? 2 : v >= 2 ? 1 : 0;
+  }
   // Device-resident pairs: deferred bitmap, measured faster than direct
   // stamping at both geometries (profiles/r01_ab_scan_modes.txt).
   if (const char* m = std::getenv("SSPD_SCAN_MODE")) {
@@ -1411,10 +1416,15 @@ sspd_status scan_locked(sspd_grid* g, const uint32_t* pairs, uint64_t n, int pai
         const unsigned pblocks = grid_blocks(g, (cnt + 3) / 4, 256, SSPD_PIPE_MINB);
         auto* ct = g->cset.as<uint32_t>();
         auto* fc = g->fresh_count.as<unsigned long long>();
+        // passes over the batch, each probing 1/passes of the set ($SSPD_CSET_PASSES)
+        const uint32_t plog = g->cset_pass_log2;
+        const uint32_t lgb = g->cset_lg - (SSPD_CSET_BW == 8 ? 3 : SSPD_CSET_BW == 4 ? 2 : 0);
+        const uint32_t pshift = plog ? lgb - plog : 31u;
 #define SSPD_CSETK(H1, HI, R)                                                                                    \
+  for (uint32_t part = 0; part < (1u << plog); ++part)                                                            \
   scan_cset_kernel<H1, HI, R, SSPD_CSET_BW><<<pblocks, 256, 0, g->stream>>>(dp, cnt, g->d_tabs, g->geo, ct,         \
                                                                            g->cset_lg, g->stamps, g->now, g->hist, \
-                                                                           g->K, fc)
+                                                                           g->K, fc, part, pshift)
         const bool r5 = g->geo.r == 5, hint = g->cset_hint != 0;
         switch ((pow2 ? 0 : 4) + (hint ? 2 : 0) + (r5 ? 1 : 0)) {
           case 0: SSPD_CSETK(0, 0, 0); break;

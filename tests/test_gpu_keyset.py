@@ -24,16 +24,18 @@ WIDE = dict(q=16, r=8, delta=6, eta=64)
 E16 = dict(q=12, r=5, delta=7, eta=65536)   # the largest eta the set takes (48-bit keys)
 
 
-def _grid(gpu, geo, seed, cset, k=4):
-    old = os.environ.get("SSPD_CSET")
-    os.environ["SSPD_CSET"] = "1" if cset else "0"
+def _grid(gpu, geo, seed, cset, k=4, passes=1):
+    env = {"SSPD_CSET": "1" if cset else "0", "SSPD_CSET_PASSES": str(passes)}
+    old = {key: os.environ.get(key) for key in env}
+    os.environ.update(env)
     try:
         g = gpu.Grid(seed=seed, **geo)
     finally:
-        if old is None:
-            del os.environ["SSPD_CSET"]
-        else:
-            os.environ["SSPD_CSET"] = old
+        for key, v in old.items():
+            if v is None:
+                del os.environ[key]
+            else:
+                os.environ[key] = v
     g.scan_mode(2, -1)
     g.track_window(k)
     return g
@@ -70,10 +72,11 @@ def colliding_traffic(rng, seed, eta, hosts, per_host, n):
     return np.stack([cips[pick_h], oips[pick_h, pick_o]], 1).astype(np.uint32)
 
 
-@pytest.mark.parametrize("cset", [1, 0], ids=["keyset", "pairset"])
+@pytest.mark.parametrize("cset", [(1, 1), (1, 2), (1, 4), (0, 1)], ids=["keyset", "keyset_2pass", "keyset_4pass",
+                                                                    "pairset"])
 @pytest.mark.parametrize("geo", [DESK, PAPER, ODD, WIDE, E16], ids=["desk", "paper", "odd_eta", "wide_r", "eta65536"])
 def test_keyset_scan_bit_exact(gpu, geo, cset):
-    g = _grid(gpu, geo, 0x5eed, cset)
+    g = _grid(gpu, geo, 0x5eed, cset[0], passes=cset[1])
     o = O.OracleGrid(seed=0x5eed, **geo)
     rng = O.Mt64(11)
     for s in range(4):
@@ -88,11 +91,12 @@ def test_keyset_scan_bit_exact(gpu, geo, cset):
         o.advance()
 
 
+@pytest.mark.parametrize("passes", [1, 2])
 @pytest.mark.parametrize("geo", [DESK, PAPER, E16], ids=["desk", "paper", "eta65536"])
-def test_keyset_counts_distinct_keys(gpu, geo):
+def test_keyset_counts_distinct_keys(gpu, geo, passes):
     """The fresh-key counter equals the distinct (cip, bucket) keys of each
     slot: no repeat is missed and no new key is taken for a seen one."""
-    g = _grid(gpu, geo, 0x1234, 1)
+    g = _grid(gpu, geo, 0x1234, 1, passes=passes)
     bucket = bucket_fn(0x1234, geo["eta"])
     rng = O.Mt64(5)
     for s in range(3):
