@@ -1074,8 +1074,10 @@ __device__ __forceinline__ CBucket<BW> ld_bucket(const uint32_t* p, uint64_t pol
 // Buckets d >= 1 of a probe.  Out of line (SSPD_CSET_FAR_NOINLINE 1): a
 // 48-bucket walk inlined into the probe loop cost the common one-bucket probe
 // 35% at C2 (4.32 vs 3.19 ms), and an 8-bucket inline walk overflowed a few
-// hundred keys per slot; the call's saved registers (ptxas reports them as
-// spills) are only touched on this rare path (profiles/r02_ab_keyset.md A/B 4).
+// hundred keys per slot.  The call costs one spilled register in the probe
+// loop (ptxas: 8 B; the SASS has one STL and one LDL per iteration, which
+// hit L1).  Even so this is 1.5% faster at C2 than the spill-free two-stage
+// inline walk (SSPD_CSET_FAR_NOINLINE 2; profiles/r02_ab_keyset.md A/B 4).
 template <int BW, int HINT>
 __device__ __noinline__ bool cset_resolve_far(uint32_t* __restrict__ table, uint32_t bmask, uint32_t hb,
                                               uint32_t rem, uint32_t rb, uint64_t pol) {
