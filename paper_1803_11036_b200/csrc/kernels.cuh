@@ -1035,13 +1035,7 @@ __device__ __forceinline__ uint32_t ld_ca_hint_u32(const uint32_t* p, uint64_t p
 // insert of 9.4M keys displaces a few hundred keys past 8 buckets, none past
 // 17; at 0.75 none past 53 (2^24 entries).  48 fits the displacement field at
 // every size (lg >= 24: 32 - rb >= 6 bits) and only the rare long run walks it.
-#ifndef SSPD_CSET_BUCKET_LIMIT
-#define SSPD_CSET_BUCKET_LIMIT 48
-#endif
-constexpr uint32_t kCsetBucketLimit = SSPD_CSET_BUCKET_LIMIT;
-#ifndef SSPD_CSET_FAR_NOINLINE
-#define SSPD_CSET_FAR_NOINLINE 1  // 1: buckets past the home one out of line; 2: past the 8th in a loop of their own
-#endif
+constexpr uint32_t kCsetBucketLimit = 48;
 template <int BW>
 struct CBucket {
   uint32_t e[BW];
@@ -1071,13 +1065,13 @@ __device__ __forceinline__ CBucket<BW> ld_bucket(const uint32_t* p, uint64_t pol
   }
   return b;
 }
-// Buckets d >= 1 of a probe.  Out of line (SSPD_CSET_FAR_NOINLINE 1): a
-// 48-bucket walk inlined into the probe loop cost the common one-bucket probe
-// 35% at C2 (4.32 vs 3.19 ms), and an 8-bucket inline walk overflowed a few
-// hundred keys per slot.  The call costs one spilled register in the probe
-// loop (ptxas: 8 B; the SASS has one STL and one LDL per iteration, which
-// hit L1).  Even so this is 1.5% faster at C2 than the spill-free two-stage
-// inline walk (SSPD_CSET_FAR_NOINLINE 2; profiles/r02_ab_keyset.md A/B 4).
+// Buckets d >= 1 of a probe, out of line: a 48-bucket walk inlined into the
+// probe loop cost the common one-bucket probe 35% at C2 (4.32 vs 3.19 ms),
+// and an 8-bucket inline walk overflowed a few hundred keys per slot.  The
+// call costs one spilled register in the probe loop (ptxas: 8 B; the SASS
+// has one STL and one LDL per iteration, which hit L1).  Even so this is
+// 1.5% faster at C2 than a spill-free two-stage inline walk
+// (profiles/r02_ab_keyset.md A/B 4; that variant was removed).
 template <int BW, int HINT>
 __device__ __noinline__ bool cset_resolve_far(uint32_t* __restrict__ table, uint32_t bmask, uint32_t hb,
                                               uint32_t rem, uint32_t rb, uint64_t pol) {
@@ -1102,56 +1096,19 @@ __device__ __noinline__ bool cset_resolve_far(uint32_t* __restrict__ table, uint
 template <int BW, int HINT>
 __device__ __forceinline__ bool cset_resolve_bucket(uint32_t* __restrict__ table, uint32_t bmask, uint32_t hb,
                                                     uint32_t rem, uint32_t rb, CBucket<BW> v, uint64_t pol) {
-  if (SSPD_CSET_FAR_NOINLINE == 1) {
-    const uint32_t want = 1u << rb | rem;
-    uint32_t* base = table + (uint64_t)hb * BW;
+  const uint32_t want = 1u << rb | rem;  // displacement 0: the home bucket, already loaded
+  uint32_t* base = table + (uint64_t)hb * BW;
 #pragma unroll
-    for (int j = 0; j < BW; ++j)
-      if (v.e[j] == want) return false;
+  for (int j = 0; j < BW; ++j)
+    if (v.e[j] == want) return false;
 #pragma unroll
-    for (int j = 0; j < BW; ++j) {
-      if (v.e[j] != 0u) continue;
-      const uint32_t old = atomicCAS(base + j, 0u, want);
-      if (old == 0u) return true;
-      if (old == want) return false;
-    }
-    return cset_resolve_far<BW, HINT>(table, bmask, hb, rem, rb, pol);
+  for (int j = 0; j < BW; ++j) {
+    if (v.e[j] != 0u) continue;
+    const uint32_t old = atomicCAS(base + j, 0u, want);
+    if (old == 0u) return true;
+    if (old == want) return false;
   }
-  for (uint32_t d = 0;;) {
-    const uint32_t want = (d + 1) << rb | rem;
-    uint32_t* base = table + (uint64_t)((hb + d) & bmask) * BW;
-#pragma unroll
-    for (int j = 0; j < BW; ++j)
-      if (v.e[j] == want) return false;
-#pragma unroll
-    for (int j = 0; j < BW; ++j) {
-      if (v.e[j] != 0u) continue;
-      const uint32_t old = atomicCAS(base + j, 0u, want);
-      if (old == 0u) return true;
-      if (old == want) return false;
-    }
-    if (++d >= (SSPD_CSET_FAR_NOINLINE == 2 ? 8u : kCsetBucketLimit)) break;
-    v = ld_bucket<BW, HINT>(table + (uint64_t)((hb + d) & bmask) * BW, pol);
-  }
-  if (SSPD_CSET_FAR_NOINLINE != 2) return true;
-  // mode 2: the first 8 buckets as above, the rare longer walk in a loop of its own
-#pragma unroll 1
-  for (uint32_t d = 8; d < kCsetBucketLimit; ++d) {
-    v = ld_bucket<BW, HINT>(table + (uint64_t)((hb + d) & bmask) * BW, pol);
-    const uint32_t want = (d + 1) << rb | rem;
-    uint32_t* base = table + (uint64_t)((hb + d) & bmask) * BW;
-#pragma unroll
-    for (int j = 0; j < BW; ++j)
-      if (v.e[j] == want) return false;
-#pragma unroll
-    for (int j = 0; j < BW; ++j) {
-      if (v.e[j] != 0u) continue;
-      const uint32_t old = atomicCAS(base + j, 0u, want);
-      if (old == 0u) return true;
-      if (old == want) return false;
-    }
-  }
-  return true;
+  return cset_resolve_far<BW, HINT>(table, bmask, hb, rem, rb, pol);
 }
 
 // Pipelined exactly like scan_dedup_pipe_kernel: iteration i loads and

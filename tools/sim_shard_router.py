@@ -1,21 +1,21 @@
-"""One router's slot in an N-router sharded deployment, timed on ONE GPU.
+"""One router's slot in an N-router ONE-HOP sharded deployment, timed on ONE
+GPU (the relayed exchange's counterpart is tools/sim_relay_router.py).
 
-The SHARD exchange (dist.py ShardExchange) cannot be timed here with N GPUs,
-so this runs router 0's share of the work for real and produces its inputs
-with helper grids: routers 1..N-1 scan their shards one after another on the
-same device (pushing into router 0's inbox exactly as their own GPUs would),
-then router 0 is timed on
+The SHARD exchange (dist.py ShardExchange(relay=False)) cannot be timed here
+with N GPUs, so this runs router 0's share of the work for real and produces
+its inputs with helper grids: routers 1..N-1 scan their shards one after
+another on the same device (pushing into router 0's inbox exactly as their
+own GPUs would), then router 0 is timed on
 
-  own scan (dedup, stamp owned cells, push to owners)
-  + receive (stamp what the other routers pushed to it)
+  own scan (dedup, stamp owned cells, push new pairs to the other owners)
+  + receive (the other routers' pushes: dedup against router 0's own keys,
+    stamp owned cells; all regions in one launch, counts from device memory)
   + reconstruction (hot bits / masks merged in-process here; NCCL on N GPUs)
 
-against a single router scanning the same shard into the full table.  The
-collectives' NVLink time is not included (two all-reduces of r*2^q bits and
-n_surv*eta bits per slot).  Geometry: the C2 trace and table shape with
-eta = 2^15 (40 GiB per grid) so that two grids fit on one device.
+Collective / NVLink time is not included.  Round 2: every grid is PARTIAL (only
+its cells, sspd_grid_create_sharded), so the full C2 geometry (eta 2^16) fits.
 
-    python tools/sim_shard_router.py [--routers 8] > profiles/r01_shard_sim.md
+    python tools/sim_shard_router.py [--routers 8] [--eta 65536]
 """
 import argparse
 import ctypes as C
@@ -35,10 +35,11 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--routers", type=int, default=8)
     ap.add_argument("--slots", type=int, default=4)
+    ap.add_argument("--eta", type=int, default=1 << 16)
     args = ap.parse_args()
     N = args.routers
     cfg = dict(B.CONFIGS["c2"])
-    cfg["eta"] = 1 << 15
+    cfg["eta"] = args.eta
     L = P.load()
     dev = 0
     torch.cuda.set_device(dev)
@@ -46,7 +47,7 @@ def main():
     torch.cuda.set_stream(stream)
     cdf = torch.from_numpy(B.zipf_cdf(L, cfg).view(np.int64)).cuda()
     n = cfg["pairs_per_slot"]
-    cap = 24 << 20  # pairs per (destination, source) region: a router's new pairs fit
+    cap = 12 << 20  # pairs per (destination, source) region: a router's new pairs fit
     k, theta = cfg["k"], cfg["theta"]
 
     def shard(rank, slot, out):
@@ -60,7 +61,8 @@ def main():
     table = torch.tensor([b.data_ptr() for b in inboxes], dtype=torch.int64, device="cuda")
 
     def grid(rank):
-        g = P.Grid(cfg["q"], cfg["r"], cfg["delta"], cfg["seed"], cfg["eta"], device=dev, k_max=k)
+        g = P.Grid(cfg["q"], cfg["r"], cfg["delta"], cfg["seed"], cfg["eta"], device=dev, k_max=k,
+                   shard=(N, rank) if N > 1 else None)
         g.set_stream(stream.cuda_stream)
         g.set_shard(table.data_ptr(), N, rank, cap)
         return g
@@ -71,8 +73,6 @@ def main():
         return e
 
     r0 = grid(0)
-    full = P.Grid(cfg["q"], cfg["r"], cfg["delta"], cfg["seed"], cfg["eta"], device=dev, k_max=k)
-    full.set_stream(stream.cuda_stream)
     rows = []
     for slot in range(args.slots):
         # the other routers' scans, one at a time, pushing into router 0's inbox
@@ -90,47 +90,39 @@ def main():
         a = ev()
         r0.scan_device(buf.data_ptr(), n)
         b = ev()
-        box = inboxes[0].view(N, cap, 2)
-        for src in range(1, N):
-            assert sent_to_0[src] <= cap
-            r0.shard_receive(box[src].data_ptr(), sent_to_0[src])
+        counts = torch.tensor(sent_to_0, dtype=torch.int64, device="cuda")
+        r0.shard_receive_regions_dev(inboxes[0].data_ptr(), cap, counts.data_ptr(), 1, N, 0)
         c = ev()
         r0.shard_hot(k, theta)
         ns, mptr, words = r0.shard_select(k, theta)
         reps = r0.shard_finish(theta)
         d = ev()
-        # the single-router reference point: the same shard into the full table
-        full.scan_device(buf.data_ptr(), n)
-        e = ev()
-        full.reconstruct_leveled(k, theta)
-        f = ev()
         torch.cuda.synchronize()
+        assert not r0.shard_overflow(), "a region ran past its capacity"
         own, recv, rec = a.elapsed_time(b), b.elapsed_time(c), c.elapsed_time(d)
-        rows.append((slot, own, recv, rec, sum(sent_to_0), d.elapsed_time(e)))
+        rows.append((slot, own, recv, rec, sum(sent_to_0)))
         r0.advance_slot()
-        full.advance_slot()
         inboxes[0].zero_()
         print(f"slot {slot}: own {own:.3f} ms, receive {recv:.3f} ms ({sum(sent_to_0) / 1e6:.1f}M pairs), "
-              f"reconstruct {rec:.3f} ms, single-router scan {d.elapsed_time(e):.3f} ms", file=sys.stderr, flush=True)
+              f"reconstruct {rec:.3f} ms", file=sys.stderr, flush=True)
     rows = rows[1:]  # first slot: cold
     own = np.mean([r[1] for r in rows])
     recv = np.mean([r[2] for r in rows])
     rec = np.mean([r[3] for r in rows])
     got = np.mean([r[4] for r in rows]) / 1e6
-    single = np.mean([r[5] for r in rows])
     per_router = own + recv + rec
-    print(f"# One router of {N} under the SHARD exchange, timed on one B200 (`tools/sim_shard_router.py`)\n")
-    print(f"C2 trace (1e8 Zipf pairs per router per slot, sharded by j % {N}), table q16 r5 delta6 eta 2^15 "
-          f"(40 GiB), k={k}; mean of slots 1..{args.slots - 1}.\n")
+    print(f"# One router of {N} under the ONE-HOP SHARD exchange, partial grids, timed on one B200 "
+          f"(`tools/sim_shard_router.py`)\n")
+    print(f"C2 trace (1e8 Zipf pairs per router per slot), table q16 r5 delta6 eta {cfg['eta']}, k={k}; "
+          f"mean of slots 1..{args.slots - 1}.\n")
     print("| phase | ms per slot |\n|---|---|")
     print(f"| own scan: dedup, stamp owned cells (1/{N} of them), push new pairs to owners | {own:.3f} |")
-    print(f"| receive: stamp the {got:.1f}M pairs the other {N - 1} routers pushed here | {recv:.3f} |")
+    print(f"| receive: dedup and stamp the {got:.1f}M pairs the other {N - 1} routers pushed here | {recv:.3f} |")
     print(f"| reconstruction on this router's hot bits (the merged sets are larger; collectives not included) "
           f"| {rec:.3f} |")
     print(f"| **router slot** | **{per_router:.3f}** |")
-    print(f"| single router, same shard into the full table (scan only) | {single:.3f} |")
     print(f"\nPredicted aggregate at N={N} (no collective time): {N} x 1e8 / {per_router:.3f} ms = "
-          f"{N * 1e8 / per_router / 1e6:.0f} Gpkt/s, against {1e8 / single / 1e6:.1f} Gpkt/s for one router's scan.")
+          f"{N * 1e8 / per_router / 1e6:.0f} Gpkt/s.")
 
 
 if __name__ == "__main__":
