@@ -954,21 +954,23 @@ __global__ void __launch_bounds__(256, SSPD_PIPE_MINB) scan_dedup_pipe_kernel(
 //    stamps are (row, col_row(cip), bucket) (rsea.cpp:31-36), so two pairs
 //    with one key stamp the same recorders and the second is redundant.
 //    With eta <= 2^16 the key has 48 bits.
-//  * x = perm48(key) is a bijection of 48-bit values.  Its top lg bits are
-//    the key's home slot in a 2^lg-entry table; the other 48 - lg <= 24
-//    bits (the remainder) are stored with the probe distance d in one u32:
-//    entry = (d + 1) << 24 | remainder, 0 = empty.  An entry at slot s
-//    therefore names exactly one key (home = s - d, remainder), so a match
-//    is exact: "seen" is never wrong, and every miss path (probe limit)
-//    reads as fresh, which only costs redundant stamps.
-//  * 4 B per entry instead of 8: at lg = 24 the table is 64 MiB, and the
-//    ~9.4M keys of a C2 slot load it to 0.56.  The table plus the stamp
-//    atomics' own L2 footprint fit the 126 MB L2, where the 256 MiB table of
-//    8-byte keys did not (~52M of its 100M probes per slot missed L2 to
-//    DRAM, profiles/r02_ab_scan.md).  Linear probing walks 8 entries per 32 B
-//    sector, so a collision rarely costs a second line.
+//  * x = perm48(key) is a bijection of 48-bit values.  Its top bits pick
+//    the key's home bucket (BW = 4 u32 entries, one 16 B load; BUCKETS
+//    below); the remaining rb bits (the remainder) are stored with the
+//    bucket displacement d: entry = (d + 1) << rb | remainder, 0 = empty.
+//    An entry in bucket b therefore names exactly one key (home b - d,
+//    remainder), so a match is exact: "seen" is never wrong, and every miss
+//    path (the walk limit) reads as fresh, which only costs redundant stamps.
+//  * 4 B per entry instead of 8: at 2^24 entries the table is 64 MiB, and
+//    the ~9.4M keys of a C2 slot load it to 0.56.  On its own such a table
+//    is served from L2 (random 16 B probes run at the L2 rate up to 96 MiB,
+//    profiles/r02_l2_probe.txt); beside the slot's 47M stamp atomics about
+//    half its probe sectors still miss, against ~52M misses per 100M probes
+//    for the 256 MiB table of 8-byte keys (profiles/r02_ab_keyset.md).
 // Concurrent inserters of one key walk the same slots and compare the same
 // expected entry: one CAS wins, the others read it back as "seen".
+// BW = 1 (linear probing by slot, entry = (d + 1) << 24 | remainder) and
+// BW = 8 remain as compile-time A/B variants (SSPD_CSET_BW).
 #ifndef SSPD_CSET_PROBE_LIMIT
 #define SSPD_CSET_PROBE_LIMIT 32
 #endif
