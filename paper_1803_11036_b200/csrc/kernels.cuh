@@ -982,13 +982,15 @@ __global__ void __launch_bounds__(256, SSPD_PIPE_MINB) scan_dedup_pipe_kernel(
 #endif
 constexpr uint32_t kCsetMinLog2 = 24, kCsetMaxLog2 = 30;
 // first size 2^24 (64 MiB); the host grows it while a slot's keys load it
-// past kCsetMaxLoad (sspd_cuda.cu cset_slot_end_locked).  With 4-entry
+// past kCsetMaxLoad, and shrinks it again below kCsetMinLoad (sspd_cuda.cu
+// cset_slot_end_locked).  With 4-entry
 // buckets the smallest set that holds the keys is the fastest (C2: 2^24 at
 // load 0.56 beat 2^25 and 2^26; C2 with 64-entry pools: 2^24 at 0.92 still
 // beat 2^25, profiles/r02_ab_keyset.md), so growth only keeps the table
 // clear of the overflow cliff.
 constexpr uint32_t kCsetStartLog2 = 24;
 constexpr double kCsetMaxLoad = 0.75;
+constexpr double kCsetMinLoad = 0.15;  // below it the host halves the set (never under kCsetStartLog2)
 
 #ifndef SSPD_CSET_PERM
 #define SSPD_CSET_PERM 0  // 1: one odd multiply (Fibonacci hashing: the home is the product's top bits)

@@ -853,9 +853,15 @@ sspd_status cset_slot_end_locked(sspd_grid* g) {
     if (g->cset_seen_now && g->cset_pin_now > g->cset_seen_now) {
       const uint64_t per_slot = (total - g->cset_seen_total) / (g->cset_pin_now - g->cset_seen_now);
       const uint64_t cap = 1ull << g->cset_lg;
-      if ((double)per_slot > kCsetMaxLoad * (double)cap && g->cset_lg < kCsetMaxLog2) {
-        uint32_t lg = g->cset_lg;
+      uint32_t lg = g->cset_lg;
+      if ((double)per_slot > kCsetMaxLoad * (double)cap) {
         while (lg < kCsetMaxLog2 && (double)per_slot > kCsetMaxLoad * (double)(1ull << lg)) ++lg;
+      } else {
+        // shrink back (to at most 4x the load) once slots need far less: the
+        // per-slot clear and the L2 footprint scale with the table
+        while (lg > kCsetStartLog2 && (double)per_slot < kCsetMinLoad * (double)(1ull << lg)) --lg;
+      }
+      if (lg != g->cset_lg) {
         g->cset.release();
         g->cset_lg = lg;
         g->cset_dirty = false;

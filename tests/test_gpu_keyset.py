@@ -156,8 +156,8 @@ def test_keyset_survives_cells_writes_and_slot_reset(gpu):
 @pytest.mark.slow
 def test_keyset_grows_with_the_slot_keys(gpu):
     """Slots with more keys than 0.75 x the 2^24 starting entries make the
-    host grow the set at a later slot end (reallocated, starting empty); the
-    grid stays exact across the change.  Before the growth some probes may
+    host grow the set at a later slot end (reallocated, starting empty), and
+    small slots shrink it back; the grid stays exact across both changes.  Before the growth some probes may
     hit the bucket limit and count as fresh; after it (slot 3 on: the count
     of slot 1 is read at the end of slot 2) the count is the slot's distinct
     keys."""
@@ -178,8 +178,19 @@ def test_keyset_grows_with_the_slot_keys(gpu):
         got, d = decode_table(g.keyset())
         assert len(np.unique(got)) == len(got), (s, "duplicate keys in the set")
         assert fresh == want if s >= 3 else fresh >= want, (s, fresh, want, len(got), int(d.max()))
+        assert g.keyset().size == (1 << 24 if s < 3 else 1 << 25), s
         assert np.array_equal(g.cells(), o.cells()), s
         assert np.array_equal(g.active_counts(3), o.active_counts(3)), s
+        g.advance_slot()
+        o.advance()
+    # small slots after the burst: the set shrinks back to 2^24 (the count of
+    # slot j is read at the end of slot j + 1) and stays exact
+    for s in range(4):
+        p = rng.pairs(300_000)
+        g.scan_batch(p)
+        o.scan(p)
+        assert g.keyset().size == (1 << 25 if s < 2 else 1 << 24), ("shrink", s)
+        assert np.array_equal(g.cells(), o.cells()), ("shrink", s)
         g.advance_slot()
         o.advance()
 
