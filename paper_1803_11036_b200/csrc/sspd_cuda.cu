@@ -832,6 +832,18 @@ sspd_status ensure_cset_locked(sspd_grid* g) {
   if (g->cset.ensure(4ull << g->cset_lg) != cudaSuccess)
     return fail(SSPD_CUDA_ERROR, "CUDA error: out of memory (key set)");
   CU(cudaMemsetAsync(g->cset.p, 0, 4ull << g->cset_lg, g->stream));
+  // $SSPD_L2_SETASIDE_MIB: the device's persisting-L2 set-aside, the
+  // carve-out the set's evict_last probes may occupy (A/B knob; the driver
+  // default is 0, capped at persistingL2CacheMaxSize)
+  if (const char* e = std::getenv("SSPD_L2_SETASIDE_MIB")) {
+    int maxb = 0;
+    CU(cudaDeviceGetAttribute(&maxb, cudaDevAttrMaxPersistingL2CacheSize, g->device));
+    const size_t want = std::min<size_t>((size_t)std::max(0, std::atoi(e)) << 20, (size_t)maxb);
+    CU(cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, want));
+    size_t got = 0;
+    CU(cudaDeviceGetLimit(&got, cudaLimitPersistingL2CacheSize));
+    std::fprintf(stderr, "[sspd] L2 set-aside %zu B (max %d B)\n", got, maxb);
+  }
   return SSPD_OK;
 }
 
