@@ -611,7 +611,13 @@ def main():
                       "source": "fresh pairs: device counter of the pipelined dedup scan (sspd_grid_fresh_pairs); "
                                 "DRAM accesses: ncu dram__bytes_read/64 + dram__bytes_write/32 of the same kernel "
                                 f"({tsrc}); ceiling: tools/fetch_probe.cu best random-load rate "
-                                "(profiles/r01_access_probe.txt)"}
+                                "(profiles/r01_access_probe.txt); stamp atomic ceiling: tools/tlb_probe.cu random "
+                                "atom.max into 80 GiB (profiles/r02_tlb_probe.txt)"}
+                # the stamps are returning atomics: tools/tlb_probe.cu (profiles/r02_tlb_probe.txt)
+                # measured random atom.max on an 80 GiB table at 21.0 G/s (best CTAs/SM; 20-21 G/s
+                # at any footprint), so 47M stamps per slot cannot take less than ~2.2 ms
+                ra["stamp_atomic_ceiling_per_s"] = 21.0
+                ra["stamp_atomic_frac"] = round(fresh_pl * r / launch_s / 21.0e9, 3)
                 if traffic:
                     acc = traffic["dram_read"] / 64 + traffic["dram_write"] / 32
                     ra["dram_accesses_per_s"] = round(acc / launch_s / 1e9, 3)
