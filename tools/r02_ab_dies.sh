@@ -1,4 +1,4 @@
-# Round-2 A/B #11 of the key-set scan: the set split between the B200's two dies ($SSPD_CSET_DIES=1:
+# Round-2 A/B #11 of the key-set scan (rejected; the kernels are in profiles/r02_ab_dies.patch -- apply it first): the set split between the B200's two dies ($SSPD_CSET_DIES=1:
 # cset_bin_kernel puts each pair on the list of the die owning its key's part of the set, and each die's
 # CTAs scan their own list) against the default scan.  Die probe and parity first.
 #   /usr/local/graft/bin/gpurun --timeout 2400 -- 'bash tools/r02_ab_dies.sh'
