@@ -971,6 +971,12 @@ __global__ void __launch_bounds__(256, SSPD_PIPE_MINB) scan_dedup_pipe_kernel(
 // expected entry: one CAS wins, the others read it back as "seen".
 // BW = 1 (linear probing by slot, entry = (d + 1) << 24 | remainder) and
 // BW = 8 remain as compile-time A/B variants (SSPD_CSET_BW).
+// A/B diagnostics of the key-set scan's cost split (never the product build;
+// their results are wrong): 1 = no window-ring moves (the stamps compile to non-returning
+// reds), 2 = non-returning red.max stamps without a cache hint, 3 = returning stamps, no ring moves
+#ifndef SSPD_AB_DIAG
+#define SSPD_AB_DIAG 0
+#endif
 #ifndef SSPD_CSET_PROBE_LIMIT
 #define SSPD_CSET_PROBE_LIMIT 32
 #endif
@@ -1208,8 +1214,13 @@ __global__ void __launch_bounds__(256, SSPD_PIPE_MINB) scan_cset_kernel(
           const uint32_t cell = row << geo.q | row_col(geo, row, pc[u], p0[u]);
           uint32_t* sp = stamps + (uint64_t)cell * geo.eta + pb[u];
           old[u][row] = now;
+#if SSPD_AB_DIAG == 2
+          // DIAGNOSTIC BUILD ONLY (wrong results): non-returning stamps, no ring
+          asm volatile("red.relaxed.gpu.global.max.u32 [%0], %1;" ::"l"(sp), "r"(now) : "memory");
+#else
           if (SSPD_OK_OR_SKIP(rec_ok(geo, cell, pb[u])))
             old[u][row] = HINT ? atom_max_hint(sp, now, pol_first) : atomicMax(sp, now);
+#endif
         }
     }
     bool fresh[P];
@@ -1226,7 +1237,11 @@ __global__ void __launch_bounds__(256, SSPD_PIPE_MINB) scan_cset_kernel(
       if (!pv[u]) continue;
 #pragma unroll
       for (uint32_t row = 0; row < RM; ++row) {
-        if (row >= nr || old[u][row] >= now) continue;
+#if SSPD_AB_DIAG == 3
+        n_fresh += (row < nr && old[u][row] == 0x7fffffffu);  // consume the returned stamps, no ring moves
+        continue;
+#endif
+        if (SSPD_AB_DIAG || row >= nr || old[u][row] >= now) continue;  // diagnostic builds: no ring moves
         const uint32_t cell = row << geo.q | row_col(geo, row, pc[u], p0[u]);
         ring_add(hist, now_slot, geo.ncells, cell, K, __LINE__);
         if (old[u][row] + K > now)
