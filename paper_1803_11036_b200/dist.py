@@ -21,6 +21,10 @@ router uses.  Three exchange formats give the same grid:
           at reconstruction.  Per-router stamping then scales with 1/N of the
           routers' union of pairs.
 
+SHARD, the default at N > 1, keeps the per-router counts on the device
+(relay and receive kernels read them there); PUSH and PAIRS read them on the
+host once per slot to size their receive scans.
+
 merge_stamps_max is the literal all-reduce(max) of the full stamp grid, kept as
 the baseline.  Every variant equals merge_rseas(node grids, kUnionMin) of the
 reference bit for bit (tests/test_dist_gloo.py on CPU, tests/test_gpu_parity.py
