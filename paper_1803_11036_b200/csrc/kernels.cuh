@@ -1121,16 +1121,51 @@ __device__ __forceinline__ bool cset_resolve_bucket(uint32_t* __restrict__ table
   return cset_resolve_far<BW, HINT>(table, bmask, hb, rem, rb, pol);
 }
 
+// Narrow-stamp touch and ring helpers (see NARROW STAMPS below); here so
+// that the key-set scan can run on 16-bit grids too.
+struct NarrowCodes {
+  uint32_t now;     // code(now)
+  uint32_t lo;      // smallest live code
+};
+
+__device__ __forceinline__ uint32_t narrow_max(uint16_t* p, uint32_t code) {
+  uint32_t* w = reinterpret_cast<uint32_t*>(reinterpret_cast<uintptr_t>(p) & ~uintptr_t(3));
+  const bool upper = (reinterpret_cast<uintptr_t>(p) & 2u) != 0;
+  const unsigned short a = upper ? 0 : (unsigned short)code, b = upper ? (unsigned short)code : 0;
+  unsigned short oa, ob;
+  asm volatile("atom.global.max.noftz.v2.bf16 {%0, %1}, [%2], {%3, %4};"
+               : "=h"(oa), "=h"(ob)
+               : "l"(w), "h"(a), "h"(b)
+               : "memory");
+  return upper ? ob : oa;
+}
+
+// Ring bookkeeping of one touch whose previous code was `old`.
+__device__ __forceinline__ void narrow_ring(uint32_t old, uint32_t cell, const NarrowCodes& nc, uint32_t now,
+                                           uint32_t now_slot, const Geo& geo, uint32_t* __restrict__ hist,
+                                           uint32_t K) {
+  if (old >= nc.now) return;  // already stamped this slot
+  ring_add(hist, now_slot, geo.ncells, cell, K, __LINE__);
+  if (old >= nc.lo) {
+    const uint32_t age = nc.now - old;
+    if (age < K) ring_sub(hist, ring_back(now_slot, age, K), geo.ncells, cell, K, __LINE__);
+  }
+}
+
 // Pipelined exactly like scan_dedup_pipe_kernel: iteration i loads and
 // probes group i while group i-1's stamp atomics are in flight.
 // HINT 1: the set's probes evict_last, the stamps and the pair stream
 // evict_first.
-template <int H1MODE, int HINT, int R, int BW>
+// CT = uint16_t: a 16-bit grid (NARROW STAMPS), each touch one packed-bf16
+// max atomic of code(now) = nc.now and the ring moved by narrow_ring.
+template <int H1MODE, int HINT, int R, int BW, class CT = uint32_t>
 __global__ void __launch_bounds__(256, SSPD_PIPE_MINB) scan_cset_kernel(
     const uint32_t* __restrict__ pairs, uint64_t n, const HashTabs* __restrict__ tabs, Geo geo,
-    uint32_t* __restrict__ table, uint32_t lg, uint32_t* __restrict__ stamps, uint32_t now,
+    uint32_t* __restrict__ table, uint32_t lg, CT* __restrict__ stamps, uint32_t now,
     uint32_t* __restrict__ hist, uint32_t K, unsigned long long* __restrict__ fresh_count, uint32_t part = 0,
-    uint32_t part_shift = 31) {
+    uint32_t part_shift = 31, NarrowCodes nc = {}) {
+  constexpr bool kNarrow = sizeof(CT) == 2;
+  const uint32_t cnow = kNarrow ? nc.now : now;  // the value a touch writes
   __shared__ ScanTables t;
   load_scan_tables(t, tabs);
   const uint32_t now_slot = now % K;
@@ -1212,14 +1247,17 @@ __global__ void __launch_bounds__(256, SSPD_PIPE_MINB) scan_cset_kernel(
       for (uint32_t row = 0; row < RM; ++row)
         if (row < nr) {
           const uint32_t cell = row << geo.q | row_col(geo, row, pc[u], p0[u]);
-          uint32_t* sp = stamps + (uint64_t)cell * geo.eta + pb[u];
-          old[u][row] = now;
+          CT* sp = stamps + (uint64_t)cell * geo.eta + pb[u];
+          old[u][row] = cnow;
 #if SSPD_AB_DIAG == 2
           // DIAGNOSTIC BUILD ONLY (wrong results): non-returning stamps, no ring
-          asm volatile("red.relaxed.gpu.global.max.u32 [%0], %1;" ::"l"(sp), "r"(now) : "memory");
+          if constexpr (!kNarrow)
+            asm volatile("red.relaxed.gpu.global.max.u32 [%0], %1;" ::"l"(sp), "r"(now) : "memory");
 #else
-          if (SSPD_OK_OR_SKIP(rec_ok(geo, cell, pb[u])))
-            old[u][row] = HINT ? atom_max_hint(sp, now, pol_first) : atomicMax(sp, now);
+          if (SSPD_OK_OR_SKIP(rec_ok(geo, cell, pb[u]))) {
+            if constexpr (kNarrow) old[u][row] = narrow_max(sp, nc.now);
+            else old[u][row] = HINT ? atom_max_hint(sp, now, pol_first) : atomicMax(sp, now);
+          }
 #endif
         }
     }
@@ -1241,8 +1279,12 @@ __global__ void __launch_bounds__(256, SSPD_PIPE_MINB) scan_cset_kernel(
         n_fresh += (row < nr && old[u][row] == 0x7fffffffu);  // consume the returned stamps, no ring moves
         continue;
 #endif
-        if (SSPD_AB_DIAG || row >= nr || old[u][row] >= now) continue;  // diagnostic builds: no ring moves
+        if (SSPD_AB_DIAG || row >= nr || old[u][row] >= cnow) continue;  // diagnostic builds: no ring moves
         const uint32_t cell = row << geo.q | row_col(geo, row, pc[u], p0[u]);
+        if constexpr (kNarrow) {
+          narrow_ring(old[u][row], cell, nc, now, now_slot, geo, hist, K);
+          continue;
+        }
         ring_add(hist, now_slot, geo.ncells, cell, K, __LINE__);
         if (old[u][row] + K > now)
           ring_sub(hist, ring_back(now_slot, now - old[u][row], K), geo.ncells, cell, K, __LINE__);
@@ -2297,23 +2339,6 @@ __global__ void shard_popcount_kernel(const uint32_t* __restrict__ masks, const 
 //   w = 8:  lo = 1, hi = 255; no 8-bit atomic exists, so a touch is a load
 //           of the 32-bit word and a CAS on it (retried if a neighbour moved).
 // The old code drives the window ring exactly as in the 32-bit scan.
-struct NarrowCodes {
-  uint32_t now;     // code(now)
-  uint32_t lo;      // smallest live code
-};
-
-__device__ __forceinline__ uint32_t narrow_max(uint16_t* p, uint32_t code) {
-  uint32_t* w = reinterpret_cast<uint32_t*>(reinterpret_cast<uintptr_t>(p) & ~uintptr_t(3));
-  const bool upper = (reinterpret_cast<uintptr_t>(p) & 2u) != 0;
-  const unsigned short a = upper ? 0 : (unsigned short)code, b = upper ? (unsigned short)code : 0;
-  unsigned short oa, ob;
-  asm volatile("atom.global.max.noftz.v2.bf16 {%0, %1}, [%2], {%3, %4};"
-               : "=h"(oa), "=h"(ob)
-               : "l"(w), "h"(a), "h"(b)
-               : "memory");
-  return upper ? ob : oa;
-}
-
 // u8: CAS on the containing word, starting from the value `cur` read earlier.
 __device__ __forceinline__ uint32_t narrow_max_from(uint8_t* p, uint32_t code, uint32_t cur) {
   uint32_t* w = reinterpret_cast<uint32_t*>(reinterpret_cast<uintptr_t>(p) & ~uintptr_t(3));
@@ -2329,18 +2354,6 @@ __device__ __forceinline__ uint32_t narrow_max_from(uint8_t* p, uint32_t code, u
 
 __device__ __forceinline__ uint32_t word_of(const uint8_t* p) {
   return __ldcg(reinterpret_cast<const uint32_t*>(reinterpret_cast<uintptr_t>(p) & ~uintptr_t(3)));
-}
-
-// Ring bookkeeping of one touch whose previous code was `old`.
-__device__ __forceinline__ void narrow_ring(uint32_t old, uint32_t cell, const NarrowCodes& nc, uint32_t now,
-                                           uint32_t now_slot, const Geo& geo, uint32_t* __restrict__ hist,
-                                           uint32_t K) {
-  if (old >= nc.now) return;  // already stamped this slot
-  ring_add(hist, now_slot, geo.ncells, cell, K, __LINE__);
-  if (old >= nc.lo) {
-    const uint32_t age = nc.now - old;
-    if (age < K) ring_sub(hist, ring_back(now_slot, age, K), geo.ncells, cell, K, __LINE__);
-  }
 }
 
 // Scan into a narrow grid: direct stamping, optionally behind the per-slot

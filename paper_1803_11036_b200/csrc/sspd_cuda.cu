@@ -1360,7 +1360,10 @@ sspd_status scan_locked(sspd_grid* g, const uint32_t* pairs, uint64_t n, int pai
   const bool pipe = dedup && !g->shard && !g->export_pairs && hist && !bits && g->width == 32 && g->geo.r <= 8 &&
                     (g->dedup_pipe == 0 || g->dedup_pipe == 1);
   const bool cset = pipe && g->use_cset && g->geo.eta <= 65536u;
-  if (cset) {
+  // 16-bit grids' dedup scan: the same pipelined key-set kernel on bf16 codes
+  const bool ncset = dedup && g->width == 16 && !g->shard && !g->export_pairs && g->K && g->geo.r <= 8 &&
+                     g->use_cset && g->geo.eta <= 65536u;
+  if (cset || ncset) {
     if (sspd_status cs = ensure_cset_locked(g)) return cs;
   } else if (dedup || g->shard) {
     sspd_status ps = ensure_pairset_locked(g);
@@ -1384,6 +1387,24 @@ sspd_status scan_locked(sspd_grid* g, const uint32_t* pairs, uint64_t n, int pai
       else SSPD_SHARD(1, 0, kShardOwn);
 #undef SSPD_SHARD
       g->pairset_dirty = true;
+      return;
+    }
+    if (ncset) {
+      const NarrowCodes nc{g->code_now(), g->code_lo};
+      const unsigned pblocks = grid_blocks(g, (cnt + 3) / 4, 256, SSPD_PIPE_MINB);
+      auto* ct = g->cset.as<uint32_t>();
+      auto* fc = g->fresh_count.as<unsigned long long>();
+      auto* codes = static_cast<uint16_t*>(g->codes);
+#define SSPD_CSETN(H1, R)                                                                                        \
+  scan_cset_kernel<H1, 1, R, SSPD_CSET_BW, uint16_t><<<pblocks, 256, 0, g->stream>>>(                            \
+      dp, cnt, g->d_tabs, g->geo, ct, g->cset_lg, codes, g->now, g->hist, g->K, fc, 0u, 31u, nc)
+      const bool r5 = g->geo.r == 5;
+      if (pow2 && r5) SSPD_CSETN(0, 5);
+      else if (pow2) SSPD_CSETN(0, 0);
+      else if (r5) SSPD_CSETN(1, 5);
+      else SSPD_CSETN(1, 0);
+#undef SSPD_CSETN
+      g->cset_dirty = true;
       return;
     }
     if (g->width != 32) {

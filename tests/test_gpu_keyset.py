@@ -249,3 +249,27 @@ def test_keyset_table_holds_each_key_once(gpu, n, dup):
         else:
             assert np.isin(got, want).all(), s
         g.advance_slot()
+
+
+@pytest.mark.parametrize("geo", [DESK, PAPER, E16], ids=["desk", "paper", "eta65536"])
+def test_keyset_scan_on_16bit_grids(gpu, geo):
+    """A 16-bit grid's dedup scan is the pipelined key-set kernel on bf16
+    codes: in-window counts and reports equal the oracle's over bucket-colliding
+    traffic, and the fresh-key counter equals the distinct keys."""
+    g = gpu.Grid(seed=0x5eed, width=16, k_max=4, **geo)
+    g.scan_mode(2, -1)
+    o = O.OracleGrid(seed=0x5eed, **geo)
+    bucket = bucket_fn(0x5eed, geo["eta"])
+    rng = O.Mt64(13)
+    for s in range(4):
+        p = colliding_traffic(rng, 0x5eed, geo["eta"], 2000, 3 * geo["eta"] // 2 + 1, 120_000)
+        u = rng.pairs(30_000)
+        before = g.fresh_pairs()
+        for part in (p[:70_000], u, p[70_000:], p[:20_000]):
+            g.scan_batch(part)
+            o.scan(part)
+        assert g.fresh_pairs() - before == distinct_keys(np.concatenate([p, u]), bucket), s
+        for k in (1, 3, 4):
+            assert np.array_equal(g.active_counts(k), o.active_counts(k)), (s, k)
+        g.advance_slot()
+        o.advance()

@@ -83,11 +83,16 @@ def test_width8_counts_and_reports_across_wraps(gpu, geo, mode):
         o.advance()
 
 
-@pytest.mark.parametrize("mode", [1, 2], ids=["direct", "dedup"])
-def test_width16_counts_across_a_wrap(gpu, mode):
+@pytest.mark.parametrize("mode", [1, 2, "pairset"], ids=["direct", "dedup", "dedup_pairset"])
+def test_width16_counts_across_a_wrap(gpu, mode, monkeypatch):
     """w=16 (bf16-ordered codes, epochs of ~32K slots): bulk advances carry
-    the grid across several rebases while recorders of every age are kept."""
+    the grid across several rebases while recorders of every age are kept.
+    dedup: the pipelined key-set scan on bf16 codes; dedup_pairset: the
+    narrow scan behind the 8-byte pair set ($SSPD_CSET=0)."""
     k_max = 64
+    if mode == "pairset":
+        monkeypatch.setenv("SSPD_CSET", "0")
+        mode = 2
     g = gpu.Grid(seed=0x77, width=16, k_max=k_max, **DESK)
     g.scan_mode(mode, -1)
     o = O.OracleGrid(seed=0x77, **DESK)
