@@ -1140,6 +1140,23 @@ __device__ __forceinline__ uint32_t narrow_max(uint16_t* p, uint32_t code) {
   return upper ? ob : oa;
 }
 
+// u8: CAS on the containing word, starting from the value `cur` read earlier.
+__device__ __forceinline__ uint32_t narrow_max_from(uint8_t* p, uint32_t code, uint32_t cur) {
+  uint32_t* w = reinterpret_cast<uint32_t*>(reinterpret_cast<uintptr_t>(p) & ~uintptr_t(3));
+  const uint32_t sh = (uint32_t)(reinterpret_cast<uintptr_t>(p) & 3u) * 8u;
+  for (;;) {
+    const uint32_t old = (cur >> sh) & 0xffu;
+    if (old >= code) return old;
+    const uint32_t prev = atomicCAS(w, cur, (cur & ~(0xffu << sh)) | (code << sh));
+    if (prev == cur) return old;
+    cur = prev;
+  }
+}
+
+__device__ __forceinline__ uint32_t word_of(const uint8_t* p) {
+  return __ldcg(reinterpret_cast<const uint32_t*>(reinterpret_cast<uintptr_t>(p) & ~uintptr_t(3)));
+}
+
 // Ring bookkeeping of one touch whose previous code was `old`.
 __device__ __forceinline__ void narrow_ring(uint32_t old, uint32_t cell, const NarrowCodes& nc, uint32_t now,
                                            uint32_t now_slot, const Geo& geo, uint32_t* __restrict__ hist,
@@ -1164,7 +1181,7 @@ __global__ void __launch_bounds__(256, SSPD_PIPE_MINB) scan_cset_kernel(
     uint32_t* __restrict__ table, uint32_t lg, CT* __restrict__ stamps, uint32_t now,
     uint32_t* __restrict__ hist, uint32_t K, unsigned long long* __restrict__ fresh_count, uint32_t part = 0,
     uint32_t part_shift = 31, NarrowCodes nc = {}) {
-  constexpr bool kNarrow = sizeof(CT) == 2;
+  constexpr bool kNarrow = sizeof(CT) < 4;
   const uint32_t cnow = kNarrow ? nc.now : now;  // the value a touch writes
   __shared__ ScanTables t;
   load_scan_tables(t, tabs);
@@ -1255,7 +1272,8 @@ __global__ void __launch_bounds__(256, SSPD_PIPE_MINB) scan_cset_kernel(
             asm volatile("red.relaxed.gpu.global.max.u32 [%0], %1;" ::"l"(sp), "r"(now) : "memory");
 #else
           if (SSPD_OK_OR_SKIP(rec_ok(geo, cell, pb[u]))) {
-            if constexpr (kNarrow) old[u][row] = narrow_max(sp, nc.now);
+            if constexpr (sizeof(CT) == 1) old[u][row] = narrow_max_from(sp, nc.now, word_of(sp));
+            else if constexpr (kNarrow) old[u][row] = narrow_max(sp, nc.now);
             else old[u][row] = HINT ? atom_max_hint(sp, now, pol_first) : atomicMax(sp, now);
           }
 #endif
@@ -2339,22 +2357,6 @@ __global__ void shard_popcount_kernel(const uint32_t* __restrict__ masks, const 
 //   w = 8:  lo = 1, hi = 255; no 8-bit atomic exists, so a touch is a load
 //           of the 32-bit word and a CAS on it (retried if a neighbour moved).
 // The old code drives the window ring exactly as in the 32-bit scan.
-// u8: CAS on the containing word, starting from the value `cur` read earlier.
-__device__ __forceinline__ uint32_t narrow_max_from(uint8_t* p, uint32_t code, uint32_t cur) {
-  uint32_t* w = reinterpret_cast<uint32_t*>(reinterpret_cast<uintptr_t>(p) & ~uintptr_t(3));
-  const uint32_t sh = (uint32_t)(reinterpret_cast<uintptr_t>(p) & 3u) * 8u;
-  for (;;) {
-    const uint32_t old = (cur >> sh) & 0xffu;
-    if (old >= code) return old;
-    const uint32_t prev = atomicCAS(w, cur, (cur & ~(0xffu << sh)) | (code << sh));
-    if (prev == cur) return old;
-    cur = prev;
-  }
-}
-
-__device__ __forceinline__ uint32_t word_of(const uint8_t* p) {
-  return __ldcg(reinterpret_cast<const uint32_t*>(reinterpret_cast<uintptr_t>(p) & ~uintptr_t(3)));
-}
 
 // Scan into a narrow grid: direct stamping, optionally behind the per-slot
 // pair set (DEDUP) of scan_dedup_kernel; 2 pairs per thread, every touch's

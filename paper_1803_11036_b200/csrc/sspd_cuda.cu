@@ -468,6 +468,7 @@ struct sspd_grid {
   // eta <= 2^16.  $SSPD_CSET=0 turns it off, $SSPD_CSET_LOG2 sizes it.
   int use_cset = 1;
   int cset_hint = 1;            // L2 priorities in the key-set scan ($SSPD_CSET_HINT=0: off)
+  int cset8 = 1;                // 8-bit grids' dedup on the key-set scan too ($SSPD_CSET8=0: the narrow scan)
   uint32_t cset_pass_log2 = 0;  // 2^k passes per batch, each over 1/2^k of the set ($SSPD_CSET_PASSES)
   DevBuf cset;
   uint32_t cset_lg = 0;         // log2 entries of the (next) allocation
@@ -1040,6 +1041,7 @@ sspd_status create_impl(int device, uint32_t q, uint32_t r, uint32_t delta, uint
   if (const char* f = std::getenv("SSPD_DEDUP_PIPE")) g->dedup_pipe = std::atoi(f);
   if (const char* f = std::getenv("SSPD_CSET")) g->use_cset = std::atoi(f);
   if (const char* f = std::getenv("SSPD_CSET_HINT")) g->cset_hint = std::atoi(f);
+  if (const char* f = std::getenv("SSPD_CSET8")) g->cset8 = std::atoi(f);
   if (const char* f = std::getenv("SSPD_CSET_PASSES")) {
     const int v = std::atoi(f);
     g->cset_pass_log2 = v >= 4 ? 2 : v >= 2 ? 1 : 0;
@@ -1360,8 +1362,8 @@ sspd_status scan_locked(sspd_grid* g, const uint32_t* pairs, uint64_t n, int pai
   const bool pipe = dedup && !g->shard && !g->export_pairs && hist && !bits && g->width == 32 && g->geo.r <= 8 &&
                     (g->dedup_pipe == 0 || g->dedup_pipe == 1);
   const bool cset = pipe && g->use_cset && g->geo.eta <= 65536u;
-  // 16-bit grids' dedup scan: the same pipelined key-set kernel on bf16 codes
-  const bool ncset = dedup && g->width == 16 && !g->shard && !g->export_pairs && g->K && g->geo.r <= 8 &&
+  // narrow grids' dedup scan: the same pipelined key-set kernel on bf16 / byte codes
+  const bool ncset = dedup && (g->width == 16 || (g->width == 8 && g->cset8)) && !g->shard && !g->export_pairs && g->K && g->geo.r <= 8 &&
                      g->use_cset && g->geo.eta <= 65536u;
   if (cset || ncset) {
     if (sspd_status cs = ensure_cset_locked(g)) return cs;
@@ -1394,15 +1396,21 @@ sspd_status scan_locked(sspd_grid* g, const uint32_t* pairs, uint64_t n, int pai
       const unsigned pblocks = grid_blocks(g, (cnt + 3) / 4, 256, SSPD_PIPE_MINB);
       auto* ct = g->cset.as<uint32_t>();
       auto* fc = g->fresh_count.as<unsigned long long>();
-      auto* codes = static_cast<uint16_t*>(g->codes);
-#define SSPD_CSETN(H1, R)                                                                                        \
-  scan_cset_kernel<H1, 1, R, SSPD_CSET_BW, uint16_t><<<pblocks, 256, 0, g->stream>>>(                            \
-      dp, cnt, g->d_tabs, g->geo, ct, g->cset_lg, codes, g->now, g->hist, g->K, fc, 0u, 31u, nc)
+#define SSPD_CSETN(T, H1, R)                                                                                     \
+  scan_cset_kernel<H1, 1, R, SSPD_CSET_BW, T><<<pblocks, 256, 0, g->stream>>>(                                   \
+      dp, cnt, g->d_tabs, g->geo, ct, g->cset_lg, static_cast<T*>(g->codes), g->now, g->hist, g->K, fc, 0u, 31u, nc)
       const bool r5 = g->geo.r == 5;
-      if (pow2 && r5) SSPD_CSETN(0, 5);
-      else if (pow2) SSPD_CSETN(0, 0);
-      else if (r5) SSPD_CSETN(1, 5);
-      else SSPD_CSETN(1, 0);
+      if (g->width == 8) {
+        if (pow2 && r5) SSPD_CSETN(uint8_t, 0, 5);
+        else if (pow2) SSPD_CSETN(uint8_t, 0, 0);
+        else if (r5) SSPD_CSETN(uint8_t, 1, 5);
+        else SSPD_CSETN(uint8_t, 1, 0);
+      } else {
+        if (pow2 && r5) SSPD_CSETN(uint16_t, 0, 5);
+        else if (pow2) SSPD_CSETN(uint16_t, 0, 0);
+        else if (r5) SSPD_CSETN(uint16_t, 1, 5);
+        else SSPD_CSETN(uint16_t, 1, 0);
+      }
 #undef SSPD_CSETN
       g->cset_dirty = true;
       return;

@@ -251,12 +251,14 @@ def test_keyset_table_holds_each_key_once(gpu, n, dup):
         g.advance_slot()
 
 
+@pytest.mark.parametrize("width", [16, 8])
 @pytest.mark.parametrize("geo", [DESK, PAPER, E16], ids=["desk", "paper", "eta65536"])
-def test_keyset_scan_on_16bit_grids(gpu, geo):
-    """A 16-bit grid's dedup scan is the pipelined key-set kernel on bf16
-    codes: in-window counts and reports equal the oracle's over bucket-colliding
-    traffic, and the fresh-key counter equals the distinct keys."""
-    g = gpu.Grid(seed=0x5eed, width=16, k_max=4, **geo)
+def test_keyset_scan_on_narrow_grids(gpu, geo, width):
+    """A narrow grid's dedup scan is the pipelined key-set kernel on its codes
+    (bf16 max atomics at 16 bits, load + CAS at 8): in-window counts equal the
+    oracle's over bucket-colliding traffic, and the fresh-key counter equals
+    the distinct keys."""
+    g = gpu.Grid(seed=0x5eed, width=width, k_max=4, **geo)
     g.scan_mode(2, -1)
     o = O.OracleGrid(seed=0x5eed, **geo)
     bucket = bucket_fn(0x5eed, geo["eta"])

@@ -53,12 +53,16 @@ def slot_traffic(rng, hosts, fanout, noise):
     return np.concatenate(parts)
 
 
-@pytest.mark.parametrize("mode", [1, 2, -1], ids=["direct", "dedup", "auto"])
+@pytest.mark.parametrize("mode", [1, 2, "pairset", -1], ids=["direct", "dedup", "dedup_pairset", "auto"])
 @pytest.mark.parametrize("geo", [DESK, ODD, TINY], ids=["desk", "odd_eta", "tiny_q"])
-def test_width8_counts_and_reports_across_wraps(gpu, geo, mode):
+def test_width8_counts_and_reports_across_wraps(gpu, geo, mode, monkeypatch):
     """600 slots at w=8: epochs of 255 then 226 slots (K = 30), so two rebase
-    passes; a recurring host that keeps cells hot, then goes quiet."""
+    passes; a recurring host that keeps cells hot, then goes quiet.  dedup:
+    the key-set scan on byte codes; dedup_pairset: the narrow pair-set scan."""
     k_max = 30
+    if mode == "pairset":
+        monkeypatch.setenv("SSPD_CSET", "0")
+        mode = 2
     g = gpu.Grid(seed=0x5eed, width=8, k_max=k_max, **geo)
     g.scan_mode(mode, -1)
     o = O.OracleGrid(seed=0x5eed, **geo)
