@@ -2361,9 +2361,9 @@ __global__ void shard_popcount_kernel(const uint32_t* __restrict__ masks, const 
 // Scan into a narrow grid: direct stamping, optionally behind the per-slot
 // pair set (DEDUP) of scan_dedup_kernel; 2 pairs per thread, every touch's
 // atomic issued before any old code is consumed.  The window ring is always
-// kept.  (A 16-bit grid's dedup scan normally runs scan_cset_kernel on its
-// codes instead -- profiles/r02_ab_keyset.md A/B 16; this kernel is its
-// $SSPD_CSET=0 path and the 8-bit grids' scan.)
+// kept.  (A narrow grid's dedup scan normally runs scan_cset_kernel on its
+// codes instead -- profiles/r02_ab_keyset.md A/Bs 16-17; this kernel is the
+// direct scan and the $SSPD_CSET=0 / $SSPD_CSET8=0 dedup path.)
 template <class T, int H1MODE, int DEDUP, int PRELOAD = 0>
 __global__ void __launch_bounds__(256) scan_narrow_kernel(const uint32_t* __restrict__ pairs, uint64_t n,
                                                           const HashTabs* __restrict__ tabs, Geo geo,
